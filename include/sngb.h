@@ -1,0 +1,142 @@
+/*
+ * sngb.h -- C ABI of the B200-native SNG-DBSCAN hot path (libsngb.so).
+ *
+ * The reference (arXiv 2006.06743 companion library, C++20) has no C ABI and
+ * no GPU path; its hot path is the C++ call
+ *
+ *     Clustering sng::sng_dbscan(const Dataset&, const SngParams&, ClusterRunInfo*)
+ *         -- proj/include/sng/clusterer.hpp:42, proj/src/clusterer.cpp:54-65
+ *
+ * which builds the subsampled eps-graph (sng::build_sampled_graph,
+ * graph.hpp:65-66, graph.cpp:133-189) and clusters it (sng::cluster_graph,
+ * clusterer.hpp:38, clusterer.cpp:7-52).  The entry points below are what a
+ * binding of that path binds: plain pointers and sizes, no C++ or torch types.
+ * The C++ mirror (paper_2006_06743_b200/cpp/include/sngb/sng.hpp) and the
+ * Python mirror (paper_2006_06743_b200/__init__.py) sit on top of them and
+ * map status codes back to the reference's exception types and messages.
+ *
+ * Semantics are the reference's, bit for bit: the same per-vertex Floyd
+ * partner sets from the same (seed, vertex) counter streams (rng.hpp), the
+ * same fp64 eps decision (distance.hpp:75-83; fp32 is used only where the
+ * decision is provably identical, every other pair is re-evaluated in the
+ * reference's exact fp64 order), the same core mask, components, border ties
+ * and relabelling (clusterer.cpp:7-52).  Points are fp32 row-major n x d
+ * (the reference widens to fp64; fp32 -> fp64 widening is exact).
+ *
+ * There is no CPU fallback: every entry point returns SNGB_ERR_NO_DEVICE when
+ * no CUDA device is usable.
+ */
+#ifndef SNGB_H
+#define SNGB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNGB_ABI_VERSION 1
+
+/* Status codes.  1..6 carry the reference's std::invalid_argument messages. */
+enum {
+    SNGB_OK = 0,
+    SNGB_ERR_EPS = 1,        /* "eps must be > 0"                 clusterer.hpp:20, graph.cpp:19 */
+    SNGB_ERR_MINPTS = 2,     /* "min_pts must be >= 1"            clusterer.hpp:21, clusterer.cpp:8 */
+    SNGB_ERR_RATE = 3,       /* "rate must lie in (0, 1]"         clusterer.hpp:22, graph.cpp:136 */
+    SNGB_ERR_EMPTY = 4,      /* "dataset is empty"                graph.cpp:18 */
+    SNGB_ERR_DIM = 5,        /* "dataset dimension must be >= 1"  dataset.hpp:22 */
+    SNGB_ERR_NONFINITE = 6,  /* "dataset contains a non-finite value" dataset.hpp:26 */
+    SNGB_ERR_TOO_LARGE = 7,  /* n must fit u32 vertex ids (graph.cpp:147) */
+    SNGB_ERR_ARG = 8,        /* null pointer / bad row range */
+    SNGB_ERR_NO_DEVICE = 9,  /* no usable CUDA device (there is no CPU fallback) */
+    SNGB_ERR_CUDA = 10,      /* CUDA runtime error; see sngb_last_error_detail() */
+    SNGB_ERR_CAPACITY = 11   /* caller-provided output buffer too small; *count_out = needed */
+};
+
+/* opts.flags */
+#define SNGB_FLAG_TIMING 0x1u /* record per-stage CUDA-event times into sngb_info */
+
+typedef struct sngb_opts {
+    int32_t device;     /* CUDA ordinal; -1 = current device */
+    uint32_t flags;     /* SNGB_FLAG_* */
+    void* stream;       /* cudaStream_t to run on; NULL = library-owned stream */
+    uint64_t row_begin; /* sampled-edge entry only: query rows [row_begin, row_end) */
+    uint64_t row_end;   /*   (row_end == 0 means n) -- the multi-GPU row shard */
+} sngb_opts;
+
+/* ClusterRunInfo (clusterer.hpp:27-31) + BuildStats (graph.hpp:56-58) + GPU counters. */
+typedef struct sngb_info {
+    /* reference fields */
+    uint64_t distance_evals; /* n * draws, exactly as graph.cpp:153,176,179 count them */
+    uint64_t edges;          /* unique undirected edges (SampledGraph::edge_count) */
+    uint64_t graph_bytes;    /* (n+1)*8 + 2*edges*4 (SampledGraph::storage_bytes) */
+    int32_t cluster_count;   /* Clustering::cluster_count */
+    uint32_t core_count, border_count, noise_count;
+    /* sampling */
+    uint64_t draws;              /* min(ceil(rate*n), n-1) */
+    uint64_t collisions;         /* Floyd replacement draws (t already chosen -> j) */
+    uint64_t irregular_vertices; /* vertices whose stream hit the Lemire reject test */
+    /* eps-test exactness accounting (north star: traceability of fp32 decisions) */
+    uint64_t pairs_evaluated;  /* pairs the GPU actually tested (incl. duplicate t draws) */
+    uint64_t band_rechecks;    /* fp32 sum inside the guard band -> exact fp64 recheck */
+    uint64_t band_1e6;         /* of those, |s32 - eps^2| <= 1e-6 * eps^2 */
+    uint64_t fp32_flips;       /* pairs where a bare fp32 test would have decided wrongly */
+    uint64_t directed_accepts; /* accepted (u,v) emissions before symmetrise/dedup */
+    /* stage times in ms (only with SNGB_FLAG_TIMING; CUDA events on the run stream) */
+    float ms_total, ms_upload, ms_sample, ms_gather, ms_extras, ms_sort, ms_cluster, ms_download;
+    uint64_t gather_pairs; /* pairs evaluated by the dominant gather kernel */
+    uint64_t gather_bytes; /* its algorithmic bytes: gather_pairs * 4 * d */
+} sngb_info;
+
+/* sng::sng_dbscan (clusterer.hpp:42) on HOST buffers: pts[n*d] fp32 row-major,
+ * labels_out[n] (cluster id or -1 = kNoiseLabel), roles_out[n] (PointRole:
+ * 0 Core, 1 Border, 2 Noise; dataset.hpp:74).  Upload, compute and download
+ * run on opts->stream; returns when labels are on the host. */
+int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                    double rate, uint64_t seed, const sngb_opts* opts, int32_t* labels_out,
+                    uint8_t* roles_out, sngb_info* info_out);
+
+/* Same with DEVICE buffers (d_pts[n*d], d_labels[n], d_roles[n] on opts->device).
+ * Returns after the work on opts->stream has completed. */
+int sngb_dbscan_f32_device(const float* d_pts, uint64_t n, uint32_t d, double eps,
+                           int32_t min_pts, double rate, uint64_t seed, const sngb_opts* opts,
+                           int32_t* d_labels, uint8_t* d_roles, sngb_info* info_out);
+
+/* sng::build_sampled_graph (graph.hpp:65-66) restricted to query rows
+ * [opts->row_begin, opts->row_end): the sorted unique canonical edge keys
+ * (u << 32 | v, u < v) of every accepted pair sampled BY those rows, written
+ * to d_keys_out (device).  With the full row range this is exactly
+ * SampledGraph::edges() (graph.cpp:104-111).  If *count_out > capacity the
+ * call returns SNGB_ERR_CAPACITY and writes nothing. */
+int sngb_sampled_edges_f32_device(const float* d_pts, uint64_t n, uint32_t d, double eps,
+                                  double rate, uint64_t seed, const sngb_opts* opts,
+                                  uint64_t* d_keys_out, uint64_t capacity, uint64_t* count_out,
+                                  sngb_info* info_out);
+
+/* Host-buffer variant of the above (keys_out on the host). */
+int sngb_sampled_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps, double rate,
+                           uint64_t seed, const sngb_opts* opts, uint64_t* keys_out,
+                           uint64_t capacity, uint64_t* count_out, sngb_info* info_out);
+
+/* sng::cluster_graph (clusterer.hpp:38) over canonical edge keys on the device
+ * (any order, duplicates allowed -- they are sorted and deduplicated first,
+ * graph.cpp:34-40).  This is the merge step of the multi-GPU path: every rank
+ * all-gathers the shard keys and clusters them. */
+int sngb_cluster_edges_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n,
+                              int32_t min_pts, const sngb_opts* opts, int32_t* d_labels,
+                              uint8_t* d_roles, sngb_info* info_out);
+
+/* Status code -> message (the reference's exception text for codes 1..6). */
+const char* sngb_strerror(int code);
+/* Thread-local detail of the last SNGB_ERR_CUDA (CUDA error string + site). */
+const char* sngb_last_error_detail(void);
+int sngb_abi_version(void);
+/* Number of usable CUDA devices (0 on a host without a GPU). */
+int sngb_device_count(void);
+/* Free the library-owned device pools of every device. */
+void sngb_release_pools(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNGB_H */

@@ -1,0 +1,365 @@
+"""sngdbscan on B200 -- Python mirror of the reference's SNG-DBSCAN entry point.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(proj/include/sng/clusterer.hpp, graph.hpp, dataset.hpp):
+
+    from paper_2006_06743_b200 import Dataset, SngParams, ClusterRunInfo, sng_dbscan
+    c = sng_dbscan(Dataset(points), SngParams(eps=0.03, min_pts=10, rate=0.1, seed=1), info)
+    c.assignment, c.role, c.cluster_count
+
+Every call runs on the GPU through the C ABI (include/sngb.h, libsngb.so).
+``std::invalid_argument`` maps to :class:`InvalidArgument` (a ValueError)
+with the reference's message.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import SNGB_FLAG_TIMING, SngbInfo, SngbOpts
+
+__all__ = [
+    "InvalidArgument", "GpuError", "kNoiseLabel", "PointRole", "Dataset", "Distance",
+    "SngParams", "ClusterRunInfo", "BuildStats", "Clustering", "SampledGraph",
+    "sng_dbscan", "build_sampled_graph", "cluster_graph", "sng_dbscan_device",
+    "sampled_edges_device", "cluster_edges_device", "device_count",
+]
+
+kNoiseLabel = -1  # dataset.hpp:13
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument of the reference (same messages)."""
+
+
+class GpuError(RuntimeError):
+    """CUDA failure or no usable GPU (the library has no CPU fallback)."""
+
+
+class PointRole(enum.IntEnum):  # dataset.hpp:74
+    Core = 0
+    Border = 1
+    Noise = 2
+
+
+def _check(rc: int) -> None:
+    if rc == _lib.SNGB_OK:
+        return
+    msg = _lib.strerror(rc)
+    if rc in (_lib.SNGB_ERR_EPS, _lib.SNGB_ERR_MINPTS, _lib.SNGB_ERR_RATE, _lib.SNGB_ERR_EMPTY,
+              _lib.SNGB_ERR_DIM, _lib.SNGB_ERR_NONFINITE, _lib.SNGB_ERR_TOO_LARGE,
+              _lib.SNGB_ERR_ARG):
+        raise InvalidArgument(msg)
+    if rc == _lib.SNGB_ERR_CUDA:
+        msg = f"{msg}: {_lib.last_error_detail()}"
+    raise GpuError(msg)
+
+
+def device_count() -> int:
+    return int(_lib.lib().sngb_device_count())
+
+
+class Distance:
+    """distance.hpp: only the Euclidean metric runs on the GPU path."""
+
+    def __init__(self, kind: str = "euclidean"):
+        if kind != "euclidean":
+            raise NotImplementedError(
+                f"distance '{kind}' is not on the B200 hot path (Euclidean only)")
+        self.kind = kind
+
+    @staticmethod
+    def euclidean() -> "Distance":
+        return Distance("euclidean")
+
+    @staticmethod
+    def parse(name: str) -> "Distance":  # distance.hpp:37-43
+        if name not in ("euclidean", "manhattan", "cosine"):
+            raise InvalidArgument(
+                f"unknown distance '{name}' (expected euclidean, manhattan, or cosine)")
+        return Distance(name)
+
+
+class Dataset:
+    """Row-major n x dim matrix of finite reals (dataset.hpp:16-71).
+
+    Stored as fp32 on the way to the device.  fp64 input must be exactly
+    representable in fp32 (widening back is then exact and the results are
+    the reference's); other fp64 input is rejected rather than rounded.
+    """
+
+    def __init__(self, values, dim: int | None = None):
+        a = np.asarray(values)
+        if dim is not None:
+            if dim == 0:
+                raise InvalidArgument("dataset dimension must be >= 1")
+            flat = a.reshape(-1)
+            if flat.size == 0 or flat.size % dim != 0:
+                raise InvalidArgument("dataset values do not form n x dim rows")
+            a = flat.reshape(-1, dim)
+        if a.ndim != 2:
+            raise InvalidArgument("dataset values do not form n x dim rows")
+        if a.shape[1] == 0:
+            raise InvalidArgument("dataset dimension must be >= 1")
+        if a.shape[0] == 0:
+            raise InvalidArgument("dataset values do not form n x dim rows")
+        if a.dtype == np.float32:
+            f = np.ascontiguousarray(a)
+        else:
+            a64 = np.asarray(a, np.float64)
+            f = np.ascontiguousarray(a64.astype(np.float32))
+            if not np.array_equal(f.astype(np.float64), a64, equal_nan=True):
+                raise NotImplementedError(
+                    "fp64 data that is not exactly representable in fp32 is not supported "
+                    "by the fp32 GPU path")
+        if not np.isfinite(f).all():
+            raise InvalidArgument("dataset contains a non-finite value")
+        self.values = f
+        self.truth = None
+
+    def size(self) -> int:
+        return self.values.shape[0]
+
+    def dim(self) -> int:
+        return self.values.shape[1]
+
+    def empty(self) -> bool:
+        return self.values.size == 0
+
+    def row(self, i: int) -> np.ndarray:
+        return self.values[i]
+
+
+@dataclass
+class SngParams:  # clusterer.hpp:11-24
+    eps: float = 0.0
+    min_pts: int = 1
+    rate: float = 1.0
+    seed: int = 0
+    dist: Distance = field(default_factory=Distance.euclidean)
+    threads: int = 0  # CPU worker count in the reference; ignored by the GPU path
+    device: int = -1  # extension: CUDA ordinal (-1 = current)
+
+    def validate(self) -> None:
+        if not (self.eps > 0.0):
+            raise InvalidArgument("eps must be > 0")
+        if self.min_pts < 1:
+            raise InvalidArgument("min_pts must be >= 1")
+        if not (self.rate > 0.0) or self.rate > 1.0:
+            raise InvalidArgument("rate must lie in (0, 1]")
+
+
+@dataclass
+class ClusterRunInfo:  # clusterer.hpp:27-31 (+ GPU counters in .gpu)
+    distance_evals: int = 0
+    edges: int = 0
+    graph_bytes: int = 0
+    gpu: dict = field(default_factory=dict)
+
+
+@dataclass
+class BuildStats:  # graph.hpp:56-58
+    distance_evals: int = 0
+
+
+@dataclass
+class Clustering:  # dataset.hpp:78-91
+    assignment: np.ndarray
+    role: np.ndarray
+    cluster_count: int = 0
+
+    def size(self) -> int:
+        return len(self.assignment)
+
+    def count_role(self, r: PointRole) -> int:
+        return int(np.count_nonzero(self.role == int(r)))
+
+
+class SampledGraph:
+    """Canonical edge set of the sampled graph (graph.hpp:17-54), CSR on demand."""
+
+    def __init__(self, n: int, keys: np.ndarray):
+        self.n = n
+        self.keys = np.asarray(keys, np.uint64)  # sorted unique u<<32|v, u < v
+        self._deg = None
+
+    def vertex_count(self) -> int:
+        return self.n
+
+    def edge_count(self) -> int:
+        return int(self.keys.size)
+
+    def edges(self) -> list[tuple[int, int]]:
+        return [(int(k >> np.uint64(32)), int(k & np.uint64(0xFFFFFFFF))) for k in self.keys]
+
+    def edge_array(self) -> np.ndarray:
+        u = (self.keys >> np.uint64(32)).astype(np.int64)
+        v = (self.keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        return np.stack([u, v], axis=1)
+
+    def degree(self, v: int | None = None):
+        if self._deg is None:
+            e = self.edge_array()
+            self._deg = np.bincount(e.reshape(-1), minlength=self.n).astype(np.int64)
+        return self._deg if v is None else int(self._deg[v])
+
+    def storage_bytes(self) -> int:  # graph.hpp:41-43
+        return (self.n + 1) * 8 + 2 * self.edge_count() * 4
+
+
+def _opts(device: int = -1, timing: bool = False, stream: int = 0, row_begin: int = 0,
+          row_end: int = 0) -> SngbOpts:
+    return SngbOpts(device, SNGB_FLAG_TIMING if timing else 0, C.c_void_p(stream or None),
+                    row_begin, row_end)
+
+
+def sng_dbscan(data: Dataset, params: SngParams, info: ClusterRunInfo | None = None,
+               timing: bool = False) -> Clustering:
+    """sng::sng_dbscan (clusterer.hpp:42, clusterer.cpp:54-65) on the GPU."""
+    if not isinstance(data, Dataset):
+        data = Dataset(data)
+    params.validate()
+    if not isinstance(params.dist, Distance) or params.dist.kind != "euclidean":
+        raise NotImplementedError("only the Euclidean metric is on the GPU path")
+    pts = data.values
+    n, d = pts.shape
+    labels = np.empty(n, np.int32)
+    roles = np.empty(n, np.uint8)
+    gi = SngbInfo()
+    o = _opts(params.device, timing)
+    rc = _lib.lib().sngb_dbscan_f32(
+        pts.ctypes.data_as(C.POINTER(C.c_float)), n, d, float(params.eps), int(params.min_pts),
+        float(params.rate), int(params.seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o),
+        labels.ctypes.data_as(C.POINTER(C.c_int32)), roles.ctypes.data_as(C.POINTER(C.c_uint8)),
+        C.byref(gi))
+    _check(rc)
+    if info is not None:
+        info.distance_evals = gi.distance_evals
+        info.edges = gi.edges
+        info.graph_bytes = gi.graph_bytes
+        info.gpu = gi.as_dict()
+    return Clustering(labels, roles, int(gi.cluster_count))
+
+
+def build_sampled_graph(data: Dataset, eps: float, rate: float, dist: Distance | None = None,
+                        seed: int = 0, threads: int = 0, stats: BuildStats | None = None,
+                        device: int = -1) -> SampledGraph:
+    """sng::build_sampled_graph (graph.hpp:65-66, graph.cpp:133-189) on the GPU."""
+    if not isinstance(data, Dataset):
+        data = Dataset(data)
+    if dist is not None and dist.kind != "euclidean":
+        raise NotImplementedError("only the Euclidean metric is on the GPU path")
+    pts = data.values
+    n, d = pts.shape
+    L = _lib.lib()
+    gi = SngbInfo()
+    o = _opts(device)
+    cnt = C.c_uint64(0)
+    f32p = pts.ctypes.data_as(C.POINTER(C.c_float))
+    cap = 1 << 20
+    while True:
+        keys = np.empty(cap, np.uint64)
+        rc = L.sngb_sampled_edges_f32(f32p, n, d, float(eps), float(rate),
+                                      int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o),
+                                      keys.ctypes.data_as(C.POINTER(C.c_uint64)), cap,
+                                      C.byref(cnt), C.byref(gi))
+        if rc == _lib.SNGB_ERR_CAPACITY:
+            cap = int(cnt.value)
+            continue
+        _check(rc)
+        break
+    if stats is not None:
+        stats.distance_evals = gi.distance_evals
+    return SampledGraph(n, keys[: cnt.value].copy())
+
+
+def cluster_graph(g: SampledGraph, min_pts: int, device: int = -1) -> Clustering:
+    """sng::cluster_graph (clusterer.hpp:38, clusterer.cpp:7-52) on the GPU."""
+    if min_pts < 1:
+        raise InvalidArgument("min_pts must be >= 1")
+    import torch
+
+    dev = torch.device("cuda", device if device >= 0 else torch.cuda.current_device())
+    keys = torch.from_numpy(g.keys.view(np.int64)).to(dev)
+    labels, roles, gi = cluster_edges_device(keys, g.n, min_pts)
+    return Clustering(labels.cpu().numpy(), roles.cpu().numpy(), int(gi.cluster_count))
+
+
+# ---------------------------------------------------------------------------
+# Device-tensor entry points (torch is plumbing only: memory + streams).
+# ---------------------------------------------------------------------------
+def _stream_handle(t) -> int:
+    import torch
+
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def sng_dbscan_device(points, eps: float, min_pts: int, rate: float, seed: int,
+                      labels=None, roles=None, timing: bool = False):
+    """sng_dbscan over a CUDA float32 [n, d] tensor on torch's current stream.
+
+    Returns (labels int32[n], roles uint8[n], SngbInfo) as CUDA tensors."""
+    import torch
+
+    if points.dtype != torch.float32 or not points.is_cuda or points.dim() != 2:
+        raise InvalidArgument("points must be a CUDA float32 [n, d] tensor")
+    points = points.contiguous()
+    n, d = points.shape
+    if labels is None:
+        labels = torch.empty(n, dtype=torch.int32, device=points.device)
+    if roles is None:
+        roles = torch.empty(n, dtype=torch.uint8, device=points.device)
+    gi = SngbInfo()
+    o = _opts(points.device.index, timing, _stream_handle(points))
+    rc = _lib.lib().sngb_dbscan_f32_device(points.data_ptr(), n, d, float(eps), int(min_pts),
+                                           float(rate), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                           C.byref(o), labels.data_ptr(), roles.data_ptr(),
+                                           C.byref(gi))
+    _check(rc)
+    return labels, roles, gi
+
+
+def sampled_edges_device(points, eps: float, rate: float, seed: int, row_begin: int = 0,
+                         row_end: int = 0, timing: bool = False):
+    """Canonical edge keys (int64 view of u<<32|v) sampled by rows [row_begin, row_end)."""
+    import torch
+
+    points = points.contiguous()
+    n, d = points.shape
+    L = _lib.lib()
+    gi = SngbInfo()
+    o = _opts(points.device.index, timing, _stream_handle(points), row_begin, row_end)
+    cnt = C.c_uint64(0)
+    rc = L.sngb_sampled_edges_f32_device(points.data_ptr(), n, d, float(eps), float(rate),
+                                         int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o), None, 0,
+                                         C.byref(cnt), C.byref(gi))
+    if rc not in (_lib.SNGB_OK, _lib.SNGB_ERR_CAPACITY):
+        _check(rc)
+    keys = torch.empty(max(int(cnt.value), 1), dtype=torch.int64, device=points.device)
+    if cnt.value:
+        rc = L.sngb_sampled_edges_f32_device(points.data_ptr(), n, d, float(eps), float(rate),
+                                             int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o),
+                                             keys.data_ptr(), keys.numel(), C.byref(cnt),
+                                             C.byref(gi))
+        _check(rc)
+    return keys[: cnt.value], gi
+
+
+def cluster_edges_device(keys, n: int, min_pts: int, timing: bool = False):
+    """cluster_graph over CUDA int64 keys (u<<32|v, any order, duplicates allowed)."""
+    import torch
+
+    keys = keys.contiguous()
+    labels = torch.empty(n, dtype=torch.int32, device=keys.device)
+    roles = torch.empty(n, dtype=torch.uint8, device=keys.device)
+    gi = SngbInfo()
+    o = _opts(keys.device.index, timing, _stream_handle(keys))
+    rc = _lib.lib().sngb_cluster_edges_device(keys.data_ptr() if keys.numel() else None,
+                                              keys.numel(), n, int(min_pts), C.byref(o),
+                                              labels.data_ptr(), roles.data_ptr(), C.byref(gi))
+    _check(rc)
+    return labels, roles, gi

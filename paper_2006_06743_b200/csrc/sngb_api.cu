@@ -1,0 +1,699 @@
+// sngb_api.cu -- the C ABI (include/sngb.h): validation, device pools,
+// stage orchestration on one CUDA stream.
+//
+// Orchestration of sng::sng_dbscan (clusterer.cpp:54-65):
+//   validate (clusterer.hpp:19-23, graph.cpp:17-21, dataset.hpp:21-27)
+//   -> prepare points (padded fp32 layout, non-finite check)        [sync #1]
+//   -> k_sampler (Floyd collisions)  -> k_gather (hot) -> k_extras
+//   -> read cursors, retry with larger pools on overflow            [sync #2]
+//   -> sort + unique (graph.cpp:34-40) -> cluster (clusterer.cpp:7-52)
+//   -> read counters                                                [sync #3]
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sngb.h"
+#include "sngb_internal.cuh"
+#include "sngb_rng.cuh"
+
+using namespace sngb;
+
+namespace {
+
+thread_local std::string g_detail;
+
+struct CudaFail {
+    cudaError_t err;
+};
+
+#define CK(expr)                                                                      \
+    do {                                                                              \
+        cudaError_t _e = (expr);                                                      \
+        if (_e != cudaSuccess) {                                                      \
+            char _b[512];                                                             \
+            snprintf(_b, sizeof(_b), "%s at %s:%d (%s)", cudaGetErrorString(_e),      \
+                     __FILE__, __LINE__, #expr);                                      \
+            g_detail = _b;                                                            \
+            throw CudaFail{_e};                                                       \
+        }                                                                             \
+    } while (0)
+
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    void ensure(size_t want) {
+        if (want == 0) want = 16;
+        if (bytes >= want) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        CK(cudaMalloc(&p, want));
+        bytes = want;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct DevCtx {
+    int dev = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
+        flags, rank, temp, labels, roles;
+    unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
+    cudaEvent_t ev[10] = {};
+    uint64_t edge_hint = 0;  // last needed edge capacity for this context
+
+    void release() {
+        for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
+                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles})
+            b->release();
+    }
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<DevCtx>> g_ctx;
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int device_count() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+DevCtx& get_ctx(int dev) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if ((int)g_ctx.size() <= dev) g_ctx.resize(dev + 1);
+    if (!g_ctx[dev]) {
+        auto c = std::make_unique<DevCtx>();
+        c->dev = dev;
+        CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaMallocHost(&c->h_counters, C_COUNT * sizeof(unsigned long long)));
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+        g_ctx[dev] = std::move(c);
+    }
+    return *g_ctx[dev];
+}
+
+int resolve_device(const sngb_opts* o) {
+    if (o && o->device >= 0) return o->device;
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+uint32_t bits_for(uint64_t x) {  // bits needed to represent x (>= 1)
+    uint32_t b = 1;
+    while (b < 64 && (x >> b) != 0) ++b;
+    return b;
+}
+
+// graph.cpp:139-140, same double expression.
+uint64_t draws_for(uint64_t n, double rate) {
+    const uint64_t c = static_cast<uint64_t>(std::ceil(rate * static_cast<double>(n)));
+    return std::min<uint64_t>(c, n - 1);
+}
+
+float f32_down(double x) {
+    float f = (float)x;
+    if ((double)f > x) f = nextafterf(f, -INFINITY);
+    return f;
+}
+float f32_up(double x) {
+    float f = (float)x;
+    if ((double)f < x) f = nextafterf(f, INFINITY);
+    return f;
+}
+
+// Guard band for the fp32 eps test.  With u = 2^-24, every pair's fp32 sum
+// s32 (diff rounding + at most d+5 rounded accumulations, fused or not)
+// satisfies |s32 - S| <= ((1+u)^(2d+12) - 1) S + (2d+16) 2^-149 for the exact
+// S; the reference's fp64 sum is within (d+1) 2^-53 S of S.  rel below
+// over-covers both, so s32 < lo => ref accepts, s32 > hi => ref rejects.
+TestParams make_test(const float* pts, uint32_t stride, uint32_t d, double eps) {
+    TestParams tp{};
+    tp.pts = pts;
+    tp.stride = stride;
+    tp.d = d;
+    tp.eps2 = eps * eps;
+    const double rel = (2.0 * d + 16.0) * std::ldexp(1.0, -24) * 1.25 + 1e-12;
+    const double abs_ = (2.0 * d + 16.0) * std::ldexp(1.0, -148);
+    const double lo = tp.eps2 * (1.0 - rel) - abs_;
+    const double hi = tp.eps2 * (1.0 + rel) + abs_;
+    tp.lo_thr = lo > 0 ? f32_down(lo) : 0.0f;
+    tp.hi_thr = hi < (double)FLT_MAX / 4 ? f32_up(hi) : INFINITY;
+    tp.eps2f = (float)tp.eps2;
+    return tp;
+}
+
+int validate(uint64_t n, uint32_t d, double eps, int32_t min_pts, double rate, bool need_minpts) {
+    // clusterer.hpp:19-23 order, then graph.cpp:17-21, then dataset shape.
+    if (!(eps > 0.0)) return SNGB_ERR_EPS;
+    if (need_minpts && min_pts < 1) return SNGB_ERR_MINPTS;
+    if (!(rate > 0.0) || rate > 1.0) return SNGB_ERR_RATE;
+    if (n == 0) return SNGB_ERR_EMPTY;
+    if (d == 0) return SNGB_ERR_DIM;
+    if (n >= 0xffffff00ull) return SNGB_ERR_TOO_LARGE;
+    return SNGB_OK;
+}
+
+struct Timer {
+    DevCtx& c;
+    cudaStream_t s;
+    bool on;
+    int next = 0;
+    void mark(int i) {
+        if (on) CK(cudaEventRecord(c.ev[i], s));
+    }
+    float between(int a, int b) {
+        if (!on) return 0.f;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c.ev[a], c.ev[b]) != cudaSuccess) {
+            cudaGetLastError();
+            return 0.f;
+        }
+        return ms;
+    }
+};
+
+enum Ev { E_START = 0, E_UPLOADED, E_PREPARED, E_SAMPLED, E_GATHERED, E_EXTRAS, E_SORTED,
+          E_CLUSTERED, E_DOWNLOADED, E_END };
+
+struct GraphResult {
+    unsigned long long* ukeys = nullptr;  // device, compact keys
+    uint64_t m = 0;                       // unique count (valid after sync)
+    uint32_t nb = 1;
+    uint64_t draws = 0;
+    bool exhaustive = false;
+    uint64_t raw = 0;
+};
+
+// Prepare points and run the graph build for rows [rb, re).  Leaves sorted
+// unique compact keys in c.keys/keys_alt and their count in
+// counters[C_UNIQUE] (device); returns after sync #2 with the raw count.
+int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64_t n, uint32_t d,
+                double eps, double rate, uint64_t seed, uint64_t rb, uint64_t re,
+                GraphResult& gr) {
+    unsigned long long* dc = nullptr;
+    c.counters.ensure(C_COUNT * sizeof(unsigned long long));
+    dc = c.counters.as<unsigned long long>();
+    CK(cudaMemsetAsync(dc, 0, C_COUNT * sizeof(unsigned long long), s));
+
+    // ---- points: padded device layout + finiteness (dataset.hpp:24-26) ----
+    const uint32_t stride = d <= 2 ? 2u : ((d + 3u) & ~3u);
+    const size_t align = stride == 2 ? 8 : 16;
+    const float* pts = d_pts;
+    if (stride != d || (reinterpret_cast<uintptr_t>(d_pts) % align) != 0) {
+        c.pts.ensure(n * stride * sizeof(float));
+        CK(launch_prepare_points(d_pts, c.pts.as<float>(), n, d, stride, dc, s));
+        pts = c.pts.as<float>();
+    } else {
+        CK(launch_prepare_points(d_pts, nullptr, n, d, stride, dc, s));
+    }
+    CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (c.h_counters[C_NONFINITE]) return SNGB_ERR_NONFINITE;
+    tm.mark(E_PREPARED);
+
+    // ---- sampling geometry (graph.cpp:138-140) ----
+    const uint64_t draws = draws_for(n, rate);
+    const bool exhaustive = draws >= n - 1;
+    const uint64_t rows = re - rb;
+    const uint32_t nb = bits_for(n - 1);
+    const uint64_t base = (n - 1) - draws;
+    gr.draws = draws;
+    gr.exhaustive = exhaustive;
+    gr.nb = nb;
+
+    // ---- capacities ----
+    uint64_t pairs;
+    if (exhaustive) {
+        // rows [rb, re) pair with all v > u
+        const double sum = (double)rows * (double)(n - 1) - ((double)re * (re - 1) - (double)rb * (rb - 1)) / 2.0;
+        pairs = (uint64_t)std::max(0.0, sum);
+    } else {
+        pairs = rows * draws;
+    }
+    double exp_col = 0.0;
+    if (!exhaustive)
+        for (uint64_t i = 0; i < draws; ++i) exp_col += (double)i / (double)(base + i + 1);
+    uint64_t extras_cap =
+        exhaustive ? 0 : (uint64_t)(1.5 * exp_col * (double)rows) + 4096 + 4 * draws;
+    uint64_t edge_cap = std::min<uint64_t>(pairs + extras_cap + 1, std::max<uint64_t>(1ull << 24, pairs / 8));
+    edge_cap = std::min<uint64_t>(edge_cap, 1ull << 28);
+    edge_cap = std::max<uint64_t>(edge_cap, std::min<uint64_t>(c.edge_hint, pairs + extras_cap + 1));
+
+    // sampler table (per warp): bitmap over [0, n-1) or hash of 2*draws slots
+    const size_t bitmap_bytes = (((n - 1 + 31) / 32) * 4 + 15) / 16 * 16;
+    uint32_t slots = 64;
+    while (slots < 2 * draws) slots <<= 1;
+    const size_t hash_bytes = (size_t)slots * 4;
+    const bool bitmap = bitmap_bytes <= hash_bytes;
+    const size_t table_bytes = bitmap ? bitmap_bytes : hash_bytes;
+
+    const TestParams tp = make_test(pts, stride, d, eps);
+    const uint64_t seed_mixed = seed_part(seed);
+
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        c.keys.ensure(edge_cap * 8);
+        c.extras.ensure(std::max<uint64_t>(extras_cap, 1) * 8);
+        if (attempt > 0)
+            CK(cudaMemsetAsync(dc, 0, C_UNIQUE * sizeof(unsigned long long), s));
+        tm.mark(E_PREPARED);
+        if (!exhaustive) {
+            SamplerArgs sa{};
+            sa.n = n;
+            sa.row_begin = rb;
+            sa.row_end = re;
+            sa.draws = (uint32_t)draws;
+            sa.base = (uint32_t)base;
+            sa.seed_mixed = seed_mixed;
+            sa.table_words = (uint32_t)(table_bytes / 4);
+            sa.hash_mask = slots - 1;
+            sa.hash_shift = 32 - bits_for(slots - 1);
+            const size_t scratch = sampler_scratch_bytes(table_bytes, c.num_sms);
+            if (scratch) c.scratch.ensure(scratch);
+            sa.scratch = scratch ? c.scratch.as<uint32_t>() : nullptr;
+            sa.extras = c.extras.as<unsigned long long>();
+            sa.extras_capacity = extras_cap;
+            sa.counters = dc;
+            CK(launch_sampler(sa, bitmap, table_bytes, s, c.num_sms));
+        }
+        tm.mark(E_SAMPLED);
+        GatherArgs ga{};
+        ga.tp = tp;
+        ga.sink = EdgeSink{c.keys.as<unsigned long long>(), edge_cap, &dc[C_EDGE_CURSOR], nb};
+        ga.counters = dc;
+        ga.n = n;
+        ga.row_begin = rb;
+        ga.row_end = re;
+        ga.draws = (uint32_t)draws;
+        ga.base = (uint32_t)base;
+        ga.seed_mixed = seed_mixed;
+        CK(launch_gather(ga, exhaustive, s, c.num_sms));
+        tm.mark(E_GATHERED);
+        if (!exhaustive) {
+            ExtrasArgs ea{};
+            ea.tp = tp;
+            ea.sink = ga.sink;
+            ea.counters = dc;
+            ea.extras = c.extras.as<unsigned long long>();
+            ea.count_ptr = &dc[C_EXTRA_CURSOR];
+            ea.capacity = extras_cap;
+            CK(launch_extras(ea, s, c.num_sms));
+        }
+        tm.mark(E_EXTRAS);
+        CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t need_e = c.h_counters[C_EDGE_CURSOR];
+        const uint64_t need_x = c.h_counters[C_EXTRA_CURSOR];
+        const bool ok = need_e <= edge_cap && (exhaustive || need_x <= extras_cap);
+        if (ok) {
+            gr.raw = need_e;
+            c.edge_hint = std::max<uint64_t>(c.edge_hint, need_e);
+            break;
+        }
+        if (attempt == 3) {
+            g_detail = "edge buffer overflow after retries";
+            throw CudaFail{cudaErrorMemoryAllocation};
+        }
+        if (need_e > edge_cap) edge_cap = need_e + need_e / 8 + 1024;
+        if (need_x > extras_cap) extras_cap = need_x + need_x / 8 + 1024;
+        c.edge_hint = std::max<uint64_t>(c.edge_hint, edge_cap);
+    }
+
+    // ---- symmetrise + dedup (graph.cpp:181-188, 34-40) ----
+    c.keys_alt.ensure(std::max<uint64_t>(gr.raw, 1) * 8);
+    const size_t tb = std::max(sort_unique_temp_bytes(std::max<uint64_t>(gr.raw, 1), nb),
+                               cluster_temp_bytes(n));
+    c.temp.ensure(tb);
+    CK(sort_unique(c.keys.as<unsigned long long>(), c.keys_alt.as<unsigned long long>(), gr.raw,
+                   nb, c.temp.p, c.temp.bytes, dc, &gr.ukeys, s));
+    tm.mark(E_SORTED);
+    return SNGB_OK;
+}
+
+void ensure_cluster_bufs(DevCtx& c, uint64_t n, ClusterBuffers& b) {
+    c.deg.ensure(n * 4);
+    c.core.ensure(n);
+    c.parent.ensure(n * 4);
+    c.broot.ensure(n * 4);
+    c.first.ensure(n * 4);
+    c.flags.ensure((n + 1) * 4);
+    c.rank.ensure((n + 1) * 4);
+    c.temp.ensure(cluster_temp_bytes(n));
+    b.deg = c.deg.as<uint32_t>();
+    b.core = c.core.as<uint8_t>();
+    b.parent = c.parent.as<uint32_t>();
+    b.broot = c.broot.as<uint32_t>();
+    b.first = c.first.as<uint32_t>();
+    b.flags = c.flags.as<uint32_t>();
+    b.rank = c.rank.as<uint32_t>();
+    b.temp = c.temp.p;
+    b.temp_bytes = c.temp.bytes;
+}
+
+void fill_info(sngb_info* info, const unsigned long long* hc, uint64_t n, uint32_t d,
+               const GraphResult& gr, uint64_t rows, Timer& tm, bool clustered, bool host) {
+    if (!info) return;
+    std::memset(info, 0, sizeof(*info));
+    info->draws = gr.draws;
+    info->distance_evals = gr.exhaustive ? rows * (n - 1) : rows * gr.draws;  // graph.cpp:153,179
+    info->edges = hc[C_UNIQUE];
+    info->graph_bytes = (n + 1) * 8 + 2 * info->edges * 4;  // graph.hpp:41-43
+    info->collisions = hc[C_COLLISIONS];
+    info->irregular_vertices = hc[C_IRREGULAR];
+    info->pairs_evaluated = hc[C_PAIRS];
+    info->band_rechecks = hc[C_BAND];
+    info->band_1e6 = hc[C_BAND6];
+    info->fp32_flips = hc[C_FLIPS];
+    info->directed_accepts = hc[C_EDGE_CURSOR];
+    info->gather_pairs = hc[C_GATHER_PAIRS];
+    info->gather_bytes = hc[C_GATHER_PAIRS] * 4ull * d;
+    if (clustered) {
+        info->cluster_count = (int32_t)hc[C_CLUSTERS];
+        info->core_count = (uint32_t)hc[C_CORE];
+        info->border_count = (uint32_t)hc[C_BORDER];
+        info->noise_count = (uint32_t)hc[C_NOISE];
+    }
+    if (tm.on) {
+        info->ms_upload = host ? tm.between(E_START, E_UPLOADED) : 0.f;
+        info->ms_sample = tm.between(E_PREPARED, E_SAMPLED);
+        info->ms_gather = tm.between(E_SAMPLED, E_GATHERED);
+        info->ms_extras = tm.between(E_GATHERED, E_EXTRAS);
+        info->ms_sort = tm.between(E_EXTRAS, E_SORTED);
+        info->ms_cluster = clustered ? tm.between(E_SORTED, E_CLUSTERED) : 0.f;
+        info->ms_download = host ? tm.between(E_CLUSTERED, E_DOWNLOADED) : 0.f;
+        info->ms_total = tm.between(E_START, E_END);
+    }
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const CudaFail&) {
+        cudaGetLastError();
+        return SNGB_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        g_detail = "host allocation failed";
+        return SNGB_ERR_CUDA;
+    }
+}
+
+// Full pipeline on device buffers; labels/roles device pointers.
+int dbscan_device(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64_t n, uint32_t d,
+                  double eps, int32_t min_pts, double rate, uint64_t seed, int32_t* d_labels,
+                  uint8_t* d_roles, GraphResult& gr) {
+    int rc = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, 0, n, gr);
+    if (rc) return rc;
+    ClusterBuffers b{};
+    ensure_cluster_bufs(c, n, b);
+    unsigned long long* dc = c.counters.as<unsigned long long>();
+    CK(cluster_unique_edges(gr.ukeys, &dc[C_UNIQUE], gr.raw, n, gr.nb, min_pts, b, dc, d_labels,
+                            d_roles, s, c.num_sms));
+    tm.mark(E_CLUSTERED);
+    return SNGB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sngb_abi_version(void) { return SNGB_ABI_VERSION; }
+
+int sngb_device_count(void) { return device_count(); }
+
+const char* sngb_last_error_detail(void) { return g_detail.c_str(); }
+
+const char* sngb_strerror(int code) {
+    switch (code) {
+        case SNGB_OK: return "ok";
+        case SNGB_ERR_EPS: return "eps must be > 0";
+        case SNGB_ERR_MINPTS: return "min_pts must be >= 1";
+        case SNGB_ERR_RATE: return "rate must lie in (0, 1]";
+        case SNGB_ERR_EMPTY: return "dataset is empty";
+        case SNGB_ERR_DIM: return "dataset dimension must be >= 1";
+        case SNGB_ERR_NONFINITE: return "dataset contains a non-finite value";
+        case SNGB_ERR_TOO_LARGE: return "dataset has too many points for u32 vertex ids";
+        case SNGB_ERR_ARG: return "invalid argument (null pointer, bad row range or key)";
+        case SNGB_ERR_NO_DEVICE: return "no CUDA device available (the GPU path has no CPU fallback)";
+        case SNGB_ERR_CUDA: return "CUDA error";
+        case SNGB_ERR_CAPACITY: return "output buffer too small";
+        default: return "unknown error";
+    }
+}
+
+void sngb_release_pools(void) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (auto& c : g_ctx)
+        if (c) {
+            std::lock_guard<std::mutex> l2(c->mu);
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(c->dev);
+            c->release();
+            cudaSetDevice(prev);
+        }
+}
+
+int sngb_dbscan_f32_device(const float* d_pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                           double rate, uint64_t seed, const sngb_opts* opts, int32_t* d_labels,
+                           uint8_t* d_roles, sngb_info* info) {
+    int rc = validate(n, d, eps, min_pts, rate, true);
+    if (rc) return rc;
+    if (!d_pts || !d_labels || !d_roles) return SNGB_ERR_ARG;
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    return guarded([&]() -> int {
+        const int dev = resolve_device(opts);
+        DeviceGuard dg(dev);
+        DevCtx& c = get_ctx(dev);
+        std::lock_guard<std::mutex> lk(c.mu);
+        cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
+        Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
+        tm.mark(E_START);
+        tm.mark(E_UPLOADED);
+        GraphResult gr;
+        int r = dbscan_device(c, s, tm, d_pts, n, d, eps, min_pts, rate, seed, d_labels, d_roles, gr);
+        if (r) return r;
+        tm.mark(E_DOWNLOADED);
+        tm.mark(E_END);
+        CK(cudaMemcpyAsync(c.h_counters, c.counters.p, C_COUNT * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fill_info(info, c.h_counters, n, d, gr, n, tm, true, false);
+        return SNGB_OK;
+    });
+}
+
+int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                    double rate, uint64_t seed, const sngb_opts* opts, int32_t* labels_out,
+                    uint8_t* roles_out, sngb_info* info) {
+    int rc = validate(n, d, eps, min_pts, rate, true);
+    if (rc) return rc;
+    if (!pts || !labels_out || !roles_out) return SNGB_ERR_ARG;
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    return guarded([&]() -> int {
+        const int dev = resolve_device(opts);
+        DeviceGuard dg(dev);
+        DevCtx& c = get_ctx(dev);
+        std::lock_guard<std::mutex> lk(c.mu);
+        cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
+        Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
+        tm.mark(E_START);
+        c.upload.ensure(n * d * sizeof(float));
+        CK(cudaMemcpyAsync(c.upload.p, pts, n * d * sizeof(float), cudaMemcpyHostToDevice, s));
+        tm.mark(E_UPLOADED);
+        c.labels.ensure(n * 4);
+        c.roles.ensure(n);
+        GraphResult gr;
+        int r = dbscan_device(c, s, tm, c.upload.as<float>(), n, d, eps, min_pts, rate, seed,
+                              c.labels.as<int32_t>(), c.roles.as<uint8_t>(), gr);
+        if (r) return r;
+        CK(cudaMemcpyAsync(labels_out, c.labels.p, n * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(roles_out, c.roles.p, n, cudaMemcpyDeviceToHost, s));
+        tm.mark(E_DOWNLOADED);
+        tm.mark(E_END);
+        CK(cudaMemcpyAsync(c.h_counters, c.counters.p, C_COUNT * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fill_info(info, c.h_counters, n, d, gr, n, tm, true, true);
+        return SNGB_OK;
+    });
+}
+
+int sngb_sampled_edges_f32_device(const float* d_pts, uint64_t n, uint32_t d, double eps,
+                                  double rate, uint64_t seed, const sngb_opts* opts,
+                                  uint64_t* d_keys_out, uint64_t capacity, uint64_t* count_out,
+                                  sngb_info* info) {
+    int rc = validate(n, d, eps, 1, rate, false);
+    if (rc) return rc;
+    if (!d_pts || !count_out) return SNGB_ERR_ARG;
+    const uint64_t rb = opts ? opts->row_begin : 0;
+    const uint64_t re = (opts && opts->row_end) ? opts->row_end : n;
+    if (rb > re || re > n) return SNGB_ERR_ARG;
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    return guarded([&]() -> int {
+        const int dev = resolve_device(opts);
+        DeviceGuard dg(dev);
+        DevCtx& c = get_ctx(dev);
+        std::lock_guard<std::mutex> lk(c.mu);
+        cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
+        Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
+        tm.mark(E_START);
+        tm.mark(E_UPLOADED);
+        GraphResult gr;
+        int r = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, rb, re, gr);
+        if (r) return r;
+        tm.mark(E_CLUSTERED);
+        tm.mark(E_DOWNLOADED);
+        tm.mark(E_END);
+        unsigned long long* dc = c.counters.as<unsigned long long>();
+        CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t m = c.h_counters[C_UNIQUE];
+        *count_out = m;
+        fill_info(info, c.h_counters, n, d, gr, re - rb, tm, false, false);
+        if (m > capacity) return SNGB_ERR_CAPACITY;
+        if (m && !d_keys_out) return SNGB_ERR_ARG;
+        CK(launch_convert_keys(gr.ukeys, reinterpret_cast<unsigned long long*>(d_keys_out), m,
+                               gr.nb, false, n, dc, s, c.num_sms));
+        CK(cudaStreamSynchronize(s));
+        return SNGB_OK;
+    });
+}
+
+int sngb_sampled_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps, double rate,
+                           uint64_t seed, const sngb_opts* opts, uint64_t* keys_out,
+                           uint64_t capacity, uint64_t* count_out, sngb_info* info) {
+    int rc = validate(n, d, eps, 1, rate, false);
+    if (rc) return rc;
+    if (!pts || !count_out) return SNGB_ERR_ARG;
+    const uint64_t rb = opts ? opts->row_begin : 0;
+    const uint64_t re = (opts && opts->row_end) ? opts->row_end : n;
+    if (rb > re || re > n) return SNGB_ERR_ARG;
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    return guarded([&]() -> int {
+        const int dev = resolve_device(opts);
+        DeviceGuard dg(dev);
+        DevCtx& c = get_ctx(dev);
+        std::lock_guard<std::mutex> lk(c.mu);
+        cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
+        Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
+        tm.mark(E_START);
+        c.upload.ensure(n * d * sizeof(float));
+        CK(cudaMemcpyAsync(c.upload.p, pts, n * d * sizeof(float), cudaMemcpyHostToDevice, s));
+        tm.mark(E_UPLOADED);
+        GraphResult gr;
+        int r = build_graph(c, s, tm, c.upload.as<float>(), n, d, eps, rate, seed, rb, re, gr);
+        if (r) return r;
+        tm.mark(E_CLUSTERED);
+        unsigned long long* dc = c.counters.as<unsigned long long>();
+        CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t m = c.h_counters[C_UNIQUE];
+        *count_out = m;
+        if (m > capacity) {
+            fill_info(info, c.h_counters, n, d, gr, re - rb, tm, false, true);
+            return SNGB_ERR_CAPACITY;
+        }
+        if (m && !keys_out) return SNGB_ERR_ARG;
+        unsigned long long* conv = (gr.ukeys == c.keys.as<unsigned long long>())
+                                       ? c.keys_alt.as<unsigned long long>()
+                                       : c.keys.as<unsigned long long>();
+        CK(launch_convert_keys(gr.ukeys, conv, m, gr.nb, false, n, dc, s, c.num_sms));
+        if (m) CK(cudaMemcpyAsync(keys_out, conv, m * 8, cudaMemcpyDeviceToHost, s));
+        tm.mark(E_DOWNLOADED);
+        tm.mark(E_END);
+        CK(cudaStreamSynchronize(s));
+        fill_info(info, c.h_counters, n, d, gr, re - rb, tm, false, true);
+        return SNGB_OK;
+    });
+}
+
+int sngb_cluster_edges_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n, int32_t min_pts,
+                              const sngb_opts* opts, int32_t* d_labels, uint8_t* d_roles,
+                              sngb_info* info) {
+    if (min_pts < 1) return SNGB_ERR_MINPTS;
+    if (n == 0) return SNGB_ERR_EMPTY;
+    if (n >= 0xffffff00ull) return SNGB_ERR_TOO_LARGE;
+    if ((nkeys && !d_keys) || !d_labels || !d_roles) return SNGB_ERR_ARG;
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    return guarded([&]() -> int {
+        const int dev = resolve_device(opts);
+        DeviceGuard dg(dev);
+        DevCtx& c = get_ctx(dev);
+        std::lock_guard<std::mutex> lk(c.mu);
+        cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
+        Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
+        tm.mark(E_START);
+        tm.mark(E_UPLOADED);
+        tm.mark(E_PREPARED);
+        tm.mark(E_SAMPLED);
+        tm.mark(E_GATHERED);
+        tm.mark(E_EXTRAS);
+        c.counters.ensure(C_COUNT * 8);
+        unsigned long long* dc = c.counters.as<unsigned long long>();
+        CK(cudaMemsetAsync(dc, 0, C_COUNT * 8, s));
+        const uint32_t nb = bits_for(n - 1);
+        c.keys.ensure(std::max<uint64_t>(nkeys, 1) * 8);
+        c.keys_alt.ensure(std::max<uint64_t>(nkeys, 1) * 8);
+        CK(launch_convert_keys(reinterpret_cast<const unsigned long long*>(d_keys),
+                               c.keys.as<unsigned long long>(), nkeys, nb, true, n, dc, s,
+                               c.num_sms));
+        c.temp.ensure(std::max(sort_unique_temp_bytes(std::max<uint64_t>(nkeys, 1), nb),
+                               cluster_temp_bytes(n)));
+        GraphResult gr;
+        gr.nb = nb;
+        gr.raw = nkeys;
+        CK(sort_unique(c.keys.as<unsigned long long>(), c.keys_alt.as<unsigned long long>(), nkeys,
+                       nb, c.temp.p, c.temp.bytes, dc, &gr.ukeys, s));
+        tm.mark(E_SORTED);
+        ClusterBuffers b{};
+        ensure_cluster_bufs(c, n, b);
+        CK(cluster_unique_edges(gr.ukeys, &dc[C_UNIQUE], nkeys, n, nb, min_pts, b, dc, d_labels,
+                                d_roles, s, c.num_sms));
+        tm.mark(E_CLUSTERED);
+        tm.mark(E_DOWNLOADED);
+        tm.mark(E_END);
+        CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (c.h_counters[C_BADKEY]) return SNGB_ERR_ARG;
+        fill_info(info, c.h_counters, n, 0, gr, 0, tm, true, false);
+        return SNGB_OK;
+    });
+}
+
+}  // extern "C"

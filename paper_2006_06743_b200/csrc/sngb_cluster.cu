@@ -1,0 +1,286 @@
+// sngb_cluster.cu -- symmetrise/dedup, degrees, core mask, union-find,
+// border attachment and canonical relabelling on the device.
+//
+// Reference being replaced:
+//   csr_from_pairs / SampledGraph::from_edges   graph.cpp:34-40, 67-102
+//   core mask                                   clusterer.cpp:12-13
+//   connected_components + UnionFind            graph.cpp:222-247, union_find.hpp
+//   core / border / noise                       clusterer.cpp:17-39
+//   relabel by smallest member                  clusterer.cpp:41-51
+//
+// Order-equivalences that make the edge-centric GPU form exact:
+//   * Union-find always hooks the larger root under the smaller one, so every
+//     component's final root is its smallest core vertex.  The reference
+//     numbers components by first appearance of the root in vertex order,
+//     i.e. by smallest member -- the same order as our roots.
+//   * "smallest component id over core neighbours" (clusterer.cpp:31-35) is
+//     therefore "smallest root", an atomicMin over incident core edges.
+//   * relabel by smallest member: first[r] = atomicMin over members; the
+//     vertices that are some cluster's first member, in vertex order, are the
+//     clusters in the reference's final order -> exclusive scan of flags.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sngb_internal.cuh"
+
+namespace sngb {
+
+namespace {
+
+constexpr uint32_t kNone = 0xffffffffu;
+
+__device__ __forceinline__ void decode(unsigned long long k, uint32_t nb, uint32_t& a, uint32_t& b) {
+    a = (uint32_t)(k >> nb);
+    b = (uint32_t)(k & ((1ull << nb) - 1));
+}
+
+__global__ void k_degrees(const unsigned long long* __restrict__ keys, const unsigned long long* m_ptr,
+                          uint32_t nb, uint32_t* deg) {
+    const uint64_t m = *m_ptr;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t a, b;
+        decode(keys[e], nb, a, b);
+        atomicAdd(&deg[a], 1u);
+        atomicAdd(&deg[b], 1u);
+    }
+}
+
+// core mask (clusterer.cpp:12-13) + union-find init + border init.
+__global__ void k_init(const uint32_t* __restrict__ deg, uint64_t n, uint32_t min_pts, uint8_t* core,
+                       uint32_t* parent, uint32_t* broot, uint32_t* first) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        core[v] = deg[v] >= min_pts ? 1 : 0;
+        parent[v] = (uint32_t)v;
+        broot[v] = kNone;
+        first[v] = kNone;
+    }
+}
+
+__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x) {
+    // pointer jumping with path halving; parent[x] <= x always, so the
+    // benign races only ever shorten paths.
+    uint32_t p = parent[x];
+    while (p != x) {
+        const uint32_t gp = parent[p];
+        if (gp != p) parent[x] = gp;
+        x = p;
+        p = gp;
+    }
+    return x;
+}
+
+// union over core-core edges (graph.cpp:228-235): hook larger root under smaller.
+__global__ void k_union(const unsigned long long* __restrict__ keys, const unsigned long long* m_ptr,
+                        uint32_t nb, const uint8_t* __restrict__ core, uint32_t* parent) {
+    const uint64_t m = *m_ptr;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t a, b;
+        decode(keys[e], nb, a, b);
+        if (!core[a] || !core[b]) continue;
+        for (;;) {
+            uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
+            if (ra == rb) break;
+            if (ra > rb) {
+                const uint32_t t = ra;
+                ra = rb;
+                rb = t;
+            }
+            if (atomicCAS(&parent[rb], rb, ra) == rb) break;
+        }
+    }
+}
+
+__global__ void k_compress(uint64_t n, const uint8_t* __restrict__ core, uint32_t* parent) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        if (!core[v]) continue;
+        uint32_t r = (uint32_t)v;
+        while (parent[r] != r) r = parent[r];
+        parent[v] = r;
+    }
+}
+
+// border: non-core endpoint adjacent to a core vertex takes the minimum root.
+__global__ void k_border(const unsigned long long* __restrict__ keys, const unsigned long long* m_ptr,
+                         uint32_t nb, const uint8_t* __restrict__ core,
+                         const uint32_t* __restrict__ parent, uint32_t* broot) {
+    const uint64_t m = *m_ptr;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t a, b;
+        decode(keys[e], nb, a, b);
+        const bool ca = core[a], cb = core[b];
+        if (ca && !cb) atomicMin(&broot[b], parent[a]);
+        else if (cb && !ca) atomicMin(&broot[a], parent[b]);
+    }
+}
+
+__device__ __forceinline__ uint32_t cluster_root(uint64_t v, const uint8_t* core,
+                                                 const uint32_t* parent, const uint32_t* broot) {
+    return core[v] ? parent[v] : broot[v];
+}
+
+__global__ void k_first(uint64_t n, const uint8_t* __restrict__ core,
+                        const uint32_t* __restrict__ parent, const uint32_t* __restrict__ broot,
+                        uint32_t* first) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = cluster_root(v, core, parent, broot);
+        if (r != kNone) atomicMin(&first[r], (uint32_t)v);
+    }
+}
+
+__global__ void k_flags(uint64_t n, const uint8_t* __restrict__ core,
+                        const uint32_t* __restrict__ parent, const uint32_t* __restrict__ broot,
+                        const uint32_t* __restrict__ first, uint32_t* flags) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t f = 0;
+        if (v < n) {
+            const uint32_t r = cluster_root(v, core, parent, broot);
+            f = (r != kNone && first[r] == (uint32_t)v) ? 1u : 0u;
+        }
+        flags[v] = f;
+    }
+}
+
+__global__ void k_labels(uint64_t n, const uint8_t* __restrict__ core,
+                         const uint32_t* __restrict__ parent, const uint32_t* __restrict__ broot,
+                         const uint32_t* __restrict__ first, const uint32_t* __restrict__ rank,
+                         int32_t* labels, uint8_t* roles, unsigned long long* counters) {
+    unsigned nc = 0, nbd = 0, nn = 0;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const bool c = core[v];
+        const uint32_t r = c ? parent[v] : broot[v];
+        if (r == kNone) {
+            labels[v] = -1;  // kNoiseLabel (dataset.hpp:13)
+            roles[v] = 2;    // PointRole::Noise
+            ++nn;
+        } else {
+            labels[v] = (int32_t)rank[first[r]];
+            roles[v] = c ? 0 : 1;  // Core / Border
+            if (c) ++nc; else ++nbd;
+        }
+    }
+    nc = __reduce_add_sync(kFull, nc);
+    nbd = __reduce_add_sync(kFull, nbd);
+    nn = __reduce_add_sync(kFull, nn);
+    if ((threadIdx.x & 31) == 0) {
+        if (nc) atomicAdd(&counters[C_CORE], (unsigned long long)nc);
+        if (nbd) atomicAdd(&counters[C_BORDER], (unsigned long long)nbd);
+        if (nn) atomicAdd(&counters[C_NOISE], (unsigned long long)nn);
+    }
+}
+
+__global__ void k_store_clusters(const uint32_t* rank, uint64_t n, unsigned long long* counters) {
+    counters[C_CLUSTERS] = rank[n];
+}
+
+__global__ void k_convert(const unsigned long long* __restrict__ in, unsigned long long* out,
+                          uint64_t m, uint32_t nb, bool to_compact, uint64_t n,
+                          unsigned long long* counters) {
+    const unsigned long long mask = (1ull << nb) - 1;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = in[e];
+        if (to_compact) {
+            uint64_t a = k >> 32, b = k & 0xffffffffull;
+            if (a > b) {
+                const uint64_t t = a;
+                a = b;
+                b = t;
+            }
+            // self loops / out-of-range endpoints are rejected like graph.cpp:78-80
+            if (a == b || b >= n) atomicAdd(&counters[C_BADKEY], 1ull);
+            out[e] = (a << nb) | b;
+        } else {
+            out[e] = ((k >> nb) << 32) | (k & mask);
+        }
+    }
+}
+
+unsigned grid_for(uint64_t items, int num_sms) {
+    uint64_t b = (items + 255) / 256;
+    const uint64_t cap = (uint64_t)num_sms * 8;
+    if (b > cap) b = cap;
+    return (unsigned)(b ? b : 1);
+}
+
+}  // namespace
+
+size_t sort_unique_temp_bytes(uint64_t count, uint32_t nb) {
+    size_t a = 0, b = 0;
+    cub::DoubleBuffer<unsigned long long> db(nullptr, nullptr);
+    cub::DeviceRadixSort::SortKeys(nullptr, a, db, (int64_t)count, 0, (int)(2 * nb));
+    cub::DeviceSelect::Unique(nullptr, b, (unsigned long long*)nullptr,
+                              (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                              (int64_t)count);
+    return (a > b ? a : b) + 256;
+}
+
+size_t cluster_temp_bytes(uint64_t n) {
+    size_t a = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (int64_t)(n + 1));
+    return a + 256;
+}
+
+cudaError_t sort_unique(unsigned long long* keys, unsigned long long* alt, uint64_t count,
+                        uint32_t nb, void* temp, size_t temp_bytes, unsigned long long* counters,
+                        unsigned long long** unique_out, cudaStream_t s) {
+    if (count == 0) {
+        *unique_out = keys;
+        return cudaMemsetAsync(&counters[C_UNIQUE], 0, sizeof(unsigned long long), s);
+    }
+    cub::DoubleBuffer<unsigned long long> db(keys, alt);
+    size_t tb = temp_bytes;
+    cudaError_t e =
+        cub::DeviceRadixSort::SortKeys(temp, tb, db, (int64_t)count, 0, (int)(2 * nb), s);
+    if (e != cudaSuccess) return e;
+    unsigned long long* sorted = db.Current();
+    unsigned long long* out = (sorted == keys) ? alt : keys;
+    tb = temp_bytes;
+    e = cub::DeviceSelect::Unique(temp, tb, sorted, out, &counters[C_UNIQUE], (int64_t)count, s);
+    *unique_out = out;
+    return e;
+}
+
+cudaError_t launch_convert_keys(const unsigned long long* in, unsigned long long* out, uint64_t m,
+                                uint32_t nb, bool to_compact, uint64_t n,
+                                unsigned long long* counters, cudaStream_t s, int num_sms) {
+    if (m == 0) return cudaSuccess;
+    k_convert<<<grid_for(m, num_sms), 256, 0, s>>>(in, out, m, nb, to_compact, n, counters);
+    return cudaGetLastError();
+}
+
+cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned long long* m_ptr,
+                                 uint64_t m, uint64_t n,
+                                 uint32_t nb, int32_t min_pts, const ClusterBuffers& b,
+                                 unsigned long long* counters, int32_t* labels, uint8_t* roles,
+                                 cudaStream_t s, int num_sms) {
+    cudaError_t e = cudaMemsetAsync(b.deg, 0, n * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    const unsigned ge = grid_for(m, num_sms), gn = grid_for(n + 1, num_sms);
+    if (m) k_degrees<<<ge, 256, 0, s>>>(ukeys, m_ptr, nb, b.deg);
+    k_init<<<gn, 256, 0, s>>>(b.deg, n, (uint32_t)min_pts, b.core, b.parent, b.broot, b.first);
+    if (m) k_union<<<ge, 256, 0, s>>>(ukeys, m_ptr, nb, b.core, b.parent);
+    k_compress<<<gn, 256, 0, s>>>(n, b.core, b.parent);
+    if (m) k_border<<<ge, 256, 0, s>>>(ukeys, m_ptr, nb, b.core, b.parent, b.broot);
+    k_first<<<gn, 256, 0, s>>>(n, b.core, b.parent, b.broot, b.first);
+    k_flags<<<gn, 256, 0, s>>>(n, b.core, b.parent, b.broot, b.first, b.flags);
+    size_t tb = b.temp_bytes;
+    e = cub::DeviceScan::ExclusiveSum(b.temp, tb, b.flags, b.rank, (int64_t)(n + 1), s);
+    if (e != cudaSuccess) return e;
+    k_labels<<<gn, 256, 0, s>>>(n, b.core, b.parent, b.broot, b.first, b.rank, labels, roles,
+                                counters);
+    k_store_clusters<<<1, 1, 0, s>>>(b.rank, n, counters);
+    return cudaGetLastError();
+}
+
+}  // namespace sngb

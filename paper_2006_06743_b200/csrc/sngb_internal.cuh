@@ -1,0 +1,132 @@
+// sngb_internal.cuh -- shared device types of libsngb (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sngb {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kEmpty = 0xffffffffu;
+
+// Slots of the device counter block (u64 each).
+enum Counter : int {
+    C_EDGE_CURSOR = 0,   // emitted directed-accept keys (may exceed capacity)
+    C_EXTRA_CURSOR,      // sampler extras (collision replacements, irregular partners)
+    C_PAIRS,             // pairs evaluated on the GPU
+    C_BAND,              // fp32 sum inside guard band -> exact fp64 recheck
+    C_BAND6,             // |s32 - eps2| <= 1e-6 eps2
+    C_FLIPS,             // bare-fp32 decision would differ from the exact one
+    C_COLLISIONS,        // Floyd replacements
+    C_IRREGULAR,         // vertices with a Lemire reject pre-condition
+    C_GATHER_PAIRS,      // pairs evaluated by the gather kernel
+    C_NONFINITE,         // non-finite input values seen
+    C_UNIQUE,            // unique undirected edges (DeviceSelect output)
+    C_CORE,
+    C_BORDER,
+    C_NOISE,
+    C_CLUSTERS,
+    C_BADKEY,            // self loop / out-of-range endpoint in caller keys
+    C_COUNT
+};
+
+// The eps-test: fp32 accumulate with a rigorous guard band, exact fp64
+// recheck (distance.hpp:75-83 order) inside the band.
+struct TestParams {
+    const float* pts;  // device rows, `stride` floats each, zero padded past d
+    uint32_t stride;   // 2 (d <= 2) or a multiple of 4
+    uint32_t d;        // true dimension
+    float lo_thr;      // s32 <  lo_thr  => exact s64 <= eps2 (accept)
+    float hi_thr;      // s32 >  hi_thr  => exact s64 >  eps2 (reject)
+    float eps2f;       // (float)eps2, for the bare-fp32 comparison statistics
+    double eps2;       // eps * eps in fp64, as distance.hpp:82 computes it
+};
+
+// Canonical undirected edge keys: (min << nb) | max with nb = bits(n-1).
+struct EdgeSink {
+    unsigned long long* keys;
+    unsigned long long capacity;
+    unsigned long long* cursor;
+    uint32_t nb;
+};
+
+struct GatherArgs {
+    TestParams tp;
+    EdgeSink sink;
+    unsigned long long* counters;
+    uint64_t n;
+    uint64_t row_begin, row_end;
+    uint32_t draws;       // per-vertex draws (sampled mode)
+    uint32_t base;        // pool - draws, pool = n - 1
+    uint64_t seed_mixed;  // mix(seed + gamma)
+};
+
+struct SamplerArgs {
+    uint64_t n;
+    uint64_t row_begin, row_end;
+    uint32_t draws, base;
+    uint64_t seed_mixed;
+    uint32_t table_words;      // u32 words per warp table
+    uint32_t hash_mask;        // hash mode: slots - 1
+    uint32_t hash_shift;       // hash mode: 32 - log2(slots)
+    uint32_t* scratch;         // global tables (when not in shared memory)
+    unsigned long long* extras;  // (u << 32) | v ordered pairs to evaluate
+    unsigned long long extras_capacity;
+    unsigned long long* counters;
+};
+
+struct ExtrasArgs {
+    TestParams tp;
+    EdgeSink sink;
+    unsigned long long* counters;
+    const unsigned long long* extras;
+    const unsigned long long* count_ptr;  // device: number of extras written (may exceed capacity)
+    unsigned long long capacity;
+};
+
+// ---- launchers (sngb_kernels.cu) ----
+cudaError_t launch_prepare_points(const float* src, float* dst, uint64_t n, uint32_t d,
+                                  uint32_t stride, unsigned long long* counters, cudaStream_t s);
+cudaError_t launch_sampler(const SamplerArgs& a, bool bitmap, size_t table_bytes,
+                           cudaStream_t s, int num_sms);
+size_t sampler_scratch_bytes(size_t table_bytes, int num_sms);
+bool sampler_uses_shared(size_t table_bytes);
+cudaError_t launch_gather(const GatherArgs& a, bool exhaustive, cudaStream_t s, int num_sms);
+cudaError_t launch_extras(const ExtrasArgs& a, cudaStream_t s, int num_sms);
+
+// ---- cluster stage (sngb_cluster.cu) ----
+struct ClusterBuffers {
+    unsigned long long* keys;     // in: raw keys (count), sorted in place via alt
+    unsigned long long* keys_alt; // scratch of the same size
+    uint32_t* deg;                // n
+    uint8_t* core;                // n
+    uint32_t* parent;             // n
+    uint32_t* broot;              // n
+    uint32_t* first;              // n
+    uint32_t* flags;              // n + 1
+    uint32_t* rank;               // n + 1
+    void* temp;
+    size_t temp_bytes;
+};
+
+// Sort + unique raw keys; returns pointer to the unique keys (one of the two
+// buffers) and writes the unique count to counters[C_UNIQUE].
+cudaError_t sort_unique(unsigned long long* keys, unsigned long long* alt, uint64_t count,
+                        uint32_t nb, void* temp, size_t temp_bytes,
+                        unsigned long long* counters, unsigned long long** unique_out,
+                        cudaStream_t s);
+size_t sort_unique_temp_bytes(uint64_t count, uint32_t nb);
+size_t cluster_temp_bytes(uint64_t n);
+
+// m_ptr: device pointer to the unique count (DeviceSelect output); m_max bounds it.
+cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned long long* m_ptr,
+                                 uint64_t m_max, uint64_t n,
+                                 uint32_t nb, int32_t min_pts, const ClusterBuffers& b,
+                                 unsigned long long* counters, int32_t* labels, uint8_t* roles,
+                                 cudaStream_t s, int num_sms);
+
+cudaError_t launch_convert_keys(const unsigned long long* in, unsigned long long* out, uint64_t m,
+                                uint32_t nb, bool to_compact, uint64_t n,
+                                unsigned long long* counters, cudaStream_t s, int num_sms);
+
+}  // namespace sngb

@@ -1,0 +1,74 @@
+// sngb_rng.cuh -- device restatement of the reference's counter-based RNG.
+//
+// Bit-exact with proj/include/sng/rng.hpp:
+//   mix                 rng.hpp:9-13   (SplitMix64 finalizer)
+//   Stream key          rng.hpp:23-24  key = mix(seed + gamma) ^ mix(id * C1 + C2)
+//   next()              rng.hpp:26     mix(key + (++counter) * gamma)
+//   next_below(bound)   rng.hpp:35-48  Lemire multiply-reject
+//
+// Data-parallel form: while no Lemire rejection has
+// happened, draw i of a stream uses counter i+1, so every draw is computable
+// independently.  `fire` flags the (necessary) pre-condition of a rejection,
+// lo < bound; a vertex with any fired draw is resolved by the exact
+// sequential path (sampler kernel), so the fast paths never need to know how
+// many extra counters a rejection consumed.
+#pragma once
+#include <cstdint>
+
+namespace sngb {
+
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
+constexpr uint64_t kIdMul = 0xda942042e4dd58b5ULL;
+constexpr uint64_t kIdAdd = 0x8bb84b93962eacc9ULL;
+
+__host__ __device__ __forceinline__ uint64_t mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// mix(seed + gamma): the seed half of every vertex key, computed once on the host.
+__host__ __device__ __forceinline__ uint64_t seed_part(uint64_t seed) { return mix(seed + kGamma); }
+
+__host__ __device__ __forceinline__ uint64_t vertex_key(uint64_t seed_mixed, uint64_t u) {
+    return seed_mixed ^ mix(u * kIdMul + kIdAdd);
+}
+
+// Output of the counter-th next() (counter >= 1) of a stream with `key`.
+__device__ __forceinline__ uint64_t stream_at(uint64_t key, uint64_t counter) {
+    return mix(key + counter * kGamma);
+}
+
+// Lemire step for a 32-bit bound: t = floor(x * b / 2^64); fire = (lo < b)
+// where lo = x * b mod 2^64.  Two 32x32->64 products instead of a 64x64 high
+// multiply (b < 2^32 because b <= n-1 and vertex ids are u32).
+__device__ __forceinline__ uint32_t lemire32(uint64_t x, uint32_t b, bool& fire) {
+    const uint64_t p1 = (uint64_t)(uint32_t)x * b;
+    const uint64_t s = (uint64_t)(uint32_t)(x >> 32) * b + (p1 >> 32);
+    // lo = (s << 32) | (uint32)p1  <  b  (< 2^32)  <=>  (uint32)s == 0 && (uint32)p1 < b
+    fire = ((uint32_t)s == 0u) && ((uint32_t)p1 < b);
+    return (uint32_t)(s >> 32);
+}
+
+// Exact sequential Stream (rng.hpp:21-48) for the rare irregular vertices.
+struct SeqStream {
+    uint64_t key;
+    uint64_t counter;
+    __device__ __forceinline__ uint64_t next() { return mix(key + (++counter) * kGamma); }
+    __device__ uint64_t next_below(uint64_t bound) {
+        uint64_t x = next();
+        uint64_t hi = __umul64hi(x, bound);
+        uint64_t lo = x * bound;
+        if (lo < bound) {
+            const uint64_t threshold = (0 - bound) % bound;
+            while (lo < threshold) {
+                x = next();
+                hi = __umul64hi(x, bound);
+                lo = x * bound;
+            }
+        }
+        return hi;
+    }
+};
+
+}  // namespace sngb

@@ -1,0 +1,117 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bit-exact bar: edge sets, degrees/core masks, labels, roles, cluster counts
+and the reference counters (distance_evals, edges, graph_bytes) must be
+identical to the oracle on the same inputs and seed.  The oracle itself is
+pinned to the compiled reference in tests/test_oracle.py.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_2006_06743_b200 as sng  # noqa: E402
+from paper_2006_06743_b200 import synthetic  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if sng.device_count() < 1:
+        pytest.fail("no CUDA device: the GPU path has no CPU fallback")
+
+
+def _run_both(oracle, pts, eps, min_pts, rate, seed):
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=eps, min_pts=min_pts, rate=rate,
+                                                       seed=seed), info)
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, min_pts, rate, seed)
+    return c, info, labels, roles, oinfo, keys
+
+
+def _assert_same(c, info, labels, roles, oinfo):
+    assert info.distance_evals == oinfo["distance_evals"]
+    assert info.edges == oinfo["edges"]
+    assert info.graph_bytes == oinfo["graph_bytes"]
+    assert c.cluster_count == oinfo["cluster_count"]
+    np.testing.assert_array_equal(c.role, roles)
+    np.testing.assert_array_equal(c.assignment, labels)
+
+
+def test_kat_line_graph():
+    """SURVEY Appendix A KAT (computed from the compiled reference)."""
+    pts = np.arange(12, dtype=np.float32).reshape(12, 1)
+    st = sng.BuildStats()
+    g = sng.build_sampled_graph(sng.Dataset(pts), 1e9, 0.25, seed=1, stats=st)
+    want = ("0-1 0-2 0-4 0-6 0-8 0-9 0-11 1-4 1-6 1-7 1-8 2-5 2-7 2-8 2-10 3-7 3-10 3-11 "
+            "4-5 4-10 5-10 6-8 6-9 6-10 6-11 7-9 7-11 8-11 9-10 10-11")
+    assert g.edges() == [tuple(map(int, e.split("-"))) for e in want.split()]
+    assert st.distance_evals == 36
+    assert list(g.degree()) == [7, 5, 5, 3, 4, 3, 6, 5, 5, 4, 7, 6]
+
+
+@pytest.mark.parametrize("n,d,eps,rate,seed", [
+    (3, 1, 1.0, 0.5, 0),
+    (50, 2, 0.2, 0.3, 7),
+    (500, 3, 0.15, 0.1, 3),
+    (2000, 16, 1.5, 0.05, 11),
+    (3000, 33, 2.0, 0.02, 5),
+    (1500, 784, 4.5, 0.03, 2),
+    (4000, 2, 0.05, 0.5, 42),
+])
+def test_edges_match_oracle(oracle, n, d, eps, rate, seed):
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, d), dtype=np.float32) * np.float32(1.0 + d ** 0.5 / 2)
+    keys, evals = oracle.sampled_edges(pts, eps, rate, seed)
+    st = sng.BuildStats()
+    g = sng.build_sampled_graph(sng.Dataset(pts), eps, rate, seed=seed, stats=st)
+    assert st.distance_evals == evals
+    np.testing.assert_array_equal(g.keys, keys)
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 20_000), (2, 4_000), (3, 30_000), (4, 40_000), (5, 30_000)])
+def test_configs_reduced_match_oracle(oracle, cfg, n):
+    w = synthetic.CONFIGS[cfg]
+    pts = synthetic.generate(cfg, n=n)
+    # keep the per-vertex draw count of the full config where possible
+    rate = min(1.0, w.draws / n) if cfg != 1 else w.rate
+    c, info, labels, roles, oinfo, _ = _run_both(oracle, pts, w.eps, w.min_pts, rate, w.seed)
+    _assert_same(c, info, labels, roles, oinfo)
+
+
+@pytest.mark.parametrize("n,d,eps,min_pts", [(1, 2, 0.5, 1), (2, 2, 0.5, 1), (300, 2, 0.08, 4),
+                                              (700, 5, 0.6, 6)])
+def test_exhaustive_rate1_matches_oracle(oracle, n, d, eps, min_pts):
+    rng = np.random.default_rng(n)
+    pts = rng.random((n, d), dtype=np.float32)
+    c, info, labels, roles, oinfo, _ = _run_both(oracle, pts, eps, min_pts, 1.0, 9)
+    _assert_same(c, info, labels, roles, oinfo)
+
+
+def test_spec_line_example():
+    """SPEC.md clusterer example: {0, 0.5, 10, 10.5}, eps=1, min_pts=1, rate=1."""
+    pts = np.array([[0.0], [0.5], [10.0], [10.5]], np.float32)
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=1.0, min_pts=1, rate=1.0))
+    assert list(c.assignment) == [0, 0, 1, 1]
+    assert c.cluster_count == 2
+
+
+def test_errors_match_reference_messages():
+    pts = np.zeros((4, 2), np.float32)
+    with pytest.raises(sng.InvalidArgument, match=r"eps must be > 0"):
+        sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=0.0, min_pts=1, rate=1.0))
+    with pytest.raises(sng.InvalidArgument, match=r"min_pts must be >= 1"):
+        sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=1.0, min_pts=0, rate=1.0))
+    with pytest.raises(sng.InvalidArgument, match=r"rate must lie in \(0, 1\]"):
+        sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=1.0, min_pts=1, rate=1.5))
+
+
+def test_device_api_matches_host_api(oracle):
+    import torch
+    pts = synthetic.generate(1, n=5000)
+    t = torch.from_numpy(pts).cuda()
+    labels, roles, gi = sng.sng_dbscan_device(t, 0.03, 10, 0.1, 1)
+    torch.cuda.synchronize()
+    ol, orl, oinfo, _ = oracle.sng_dbscan(pts, 0.03, 10, 0.1, 1)
+    np.testing.assert_array_equal(labels.cpu().numpy(), ol)
+    np.testing.assert_array_equal(roles.cpu().numpy(), orl)
+    assert gi.edges == oinfo["edges"]
