@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py -- SNG-DBSCAN hot path on B200 (sampled pairs/s, e2e, roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (rows sharded over N GPUs)
+
+A "step" is one full sng::sng_dbscan (clusterer.cpp:54-65) over one synthetic
+workload: sample + eps-test every vertex's draws, symmetrise/dedup, degrees,
+core mask, union-find, border, relabel.  The metric is BASELINE.json's:
+sampled pairs per second (pairs = n * draws, the reference's distance_evals),
+end-to-end clustering time, and the gather kernel's fraction of roofline.
+
+  value     device-resident: points already in HBM, labels left in HBM;
+            CUDA events per step on the launching stream, L2 flushed (256 MB
+            write) before every timed step, max over ranks.
+  e2e       the public host API (sngb_dbscan_f32 through the C ABI) from
+            pinned host memory: H2D of the points and D2H of labels+roles
+            inside the timed region.
+  roofline  gather kernel: algorithmic bytes (4*d per evaluated pair) over its
+            CUDA-event duration measured inside the library on the same stream,
+            against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline  the reference's own graph.cpp/clusterer.cpp (oracle/_ref,
+            compiled unmodified) on this host's cores, rank 0, N=1 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "sampled_pairs_per_sec"
+UNIT = "pairs/s"
+DEFAULT_CONFIG = 2  # BASELINE.json configs[1]
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-budget-s", type=float, default=25.0,
+                   help="CPU seconds allowed for the cpu_baseline sample")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(workload: str):
+    """dram bytes per gather launch from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm = float(f[1])
+                mx = float(f[2])
+            except ValueError:
+                continue
+            sms.append(sm)
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def cpu_baseline(pts, w, budget_s: float):
+    """The reference's own sng_dbscan (oracle/_ref) on all host cores, bounded sample."""
+    from oracle import Reference
+    ref = Reference()
+    cores = ref.hw_threads()
+    n = pts.shape[0]
+    draws = w.draws
+    # full workload if it fits the budget at ~5e6 pairs/s/8 cores per 784-d..., else a
+    # row-prefix sample with the same per-vertex draws (same d, same work per pair).
+    est_rate = 1.5e9 / max(w.d, 1) * cores / 8.0  # rough pairs/s of the reference
+    m = n
+    if n * draws / est_rate > budget_s:
+        m = max(draws + 2, int(budget_s * est_rate / draws))
+    if m >= n:
+        sample_pts, rate, desc = pts, w.rate, f"full workload (n={n}, draws={draws})"
+    else:
+        sample_pts = np.ascontiguousarray(pts[:m])
+        rate = draws / m
+        desc = (f"first {m} rows of the workload, rate={rate:.6g} so each vertex keeps "
+                f"draws={draws} (same d, same per-pair work)")
+    ds = ref.dataset(sample_pts)
+    labels, roles, info = ref.sng_dbscan(ds, w.eps, w.min_pts, rate, w.seed, threads=0)
+    pairs = info["distance_evals"]
+    return {"value": pairs / (info["ms"] / 1e3), "unit": UNIT, "cores": cores,
+            "kind": "reference", "sample": desc, "ms": info["ms"], "pairs": pairs}
+
+
+def run_reference_arm(args, w, pts):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import Reference
+    ref = Reference()
+    cores = ref.hw_threads()
+    # Bound each step so (warmup + steps) finishes in a few minutes.
+    probe = cpu_baseline(pts, w, budget_s=max(1.0, 150.0 / max(1, args.steps + args.warmup)))
+    times = []
+    m_desc = probe["sample"]
+    # reuse the sample choice: rebuild it the same way
+    n = pts.shape[0]
+    draws = w.draws
+    if probe["pairs"] == n * draws:
+        sample_pts, rate = pts, w.rate
+    else:
+        m = probe["pairs"] // draws
+        sample_pts, rate = np.ascontiguousarray(pts[:m]), draws / m
+    ds = ref.dataset(sample_pts)
+    pairs = None
+    for i in range(args.warmup + args.steps):
+        _, _, info = ref.sng_dbscan(ds, w.eps, w.min_pts, rate, w.seed, threads=0)
+        pairs = info["distance_evals"]
+        if i >= args.warmup:
+            times.append(info["ms"])
+    ms = sum(times) / len(times)
+    value = pairs / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": w.name, "n": w.n, "d": w.d, "eps": w.eps, "rate": w.rate,
+                       "min_pts": w.min_pts, "seed": w.seed, "draws": draws,
+                       "parallelism": f"{cores} host threads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": m_desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    from paper_2006_06743_b200 import synthetic
+    w = synthetic.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank == 0:
+            pts = synthetic.generate(args.config)
+            run_reference_arm(args, w, pts)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2006_06743_b200 as sng
+    from paper_2006_06743_b200 import _lib
+    from paper_2006_06743_b200.distributed import sng_dbscan_sharded
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    pts = synthetic.generate(args.config)  # same seeded bytes on every rank
+    n, d = pts.shape
+    pairs = n * w.draws
+    host = torch.from_numpy(pts).pin_memory()
+    points = host.to(dev, non_blocking=False)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step_device():
+        if world == 1:
+            return sng.sng_dbscan_device(points, w.eps, w.min_pts, w.rate, w.seed, timing=True)
+        labels, roles, st = sng_dbscan_sharded(points, w.eps, w.min_pts, w.rate, w.seed)
+        return labels, roles, st["edge_info"]
+
+    # ---- warmup ----
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize(dev)
+
+    # ---- timed device-resident steps ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    gather_ms, gather_bytes, gather_pairs, launches, lib_launches = [], 0, 0, 0, 0
+    stage = {}
+    info = None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for k in range(args.steps):
+        flush.zero_()  # L2 flush (outside the events)
+        ev[k][0].record(stream)
+        _, _, info = step_device()
+        ev[k][1].record(stream)
+        gather_ms.append(info.ms_gather)
+        gather_bytes = info.gather_bytes
+        gather_pairs = info.gather_pairs
+        launches += info.kernel_launches
+        lib_launches += info.library_launches
+        for nm in ("ms_sample", "ms_gather", "ms_extras", "ms_sort", "ms_cluster", "ms_total"):
+            stage.setdefault(nm, []).append(getattr(info, nm))
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = pairs / (ms_per_step / 1e3)
+
+    # ---- e2e through the public host API (pinned host buffers) ----
+    e2e = None
+    if not args.no_e2e:
+        labels_h = torch.empty(n, dtype=torch.int32).pin_memory()
+        roles_h = torch.empty(n, dtype=torch.uint8).pin_memory()
+        import ctypes as C
+        L = _lib.lib()
+        o = _lib.SngbOpts(local, 0, C.c_void_p(stream.cuda_stream), 0, 0)
+        gi = _lib.SngbInfo()
+
+        def step_e2e():
+            if world == 1:
+                rc = L.sngb_dbscan_f32(C.cast(host.data_ptr(), C.POINTER(C.c_float)), n, d,
+                                       w.eps, w.min_pts, w.rate, w.seed, C.byref(o),
+                                       C.cast(labels_h.data_ptr(), C.POINTER(C.c_int32)),
+                                       C.cast(roles_h.data_ptr(), C.POINTER(C.c_uint8)),
+                                       C.byref(gi))
+                sng._check(rc)
+            else:
+                pts_d = host.to(dev, non_blocking=True)
+                lab, rol, _ = sng_dbscan_sharded(pts_d, w.eps, w.min_pts, w.rate, w.seed)
+                if rank == 0:
+                    labels_h.copy_(lab, non_blocking=True)
+                    roles_h.copy_(rol, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+
+        for _ in range(max(1, args.warmup)):
+            step_e2e()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e_ms = []
+        for _ in range(max(3, args.steps // 2)):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step_e2e()
+            b.record(stream)
+            b.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        e_tot = sum(e_ms)
+        if world > 1:
+            t = torch.tensor([e_tot], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_tot = float(t.item())
+        e_step = e_tot / len(e_ms)
+        e2e = {"value": pairs / (e_step / 1e3), "unit": UNIT, "ms_per_step": e_step,
+               "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": n * 4 + n * 1}
+
+    # ---- roofline of the gather kernel ----
+    peak, peak_kind = load_peaks()
+    g_ms = statistics.mean(gather_ms) if gather_ms else 0.0
+    achieved = gather_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else None
+    roofline = {"bound": "hbm", "kernel": "k_gather", "achieved": achieved, "peak": peak,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": load_traffic(w.name),
+                "algorithmic_bytes_per_launch": gather_bytes,
+                "bytes_per_pair": 4 * d, "pairs_per_launch": gather_pairs,
+                "kernel_ms": g_ms,
+                "kernel_share_of_step": (g_ms / ms_per_step) if ms_per_step else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(pts, w, args.cpu_budget_s)
+        except Exception as e:  # the checker is optional; report why
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generator, BASELINE.json shape)",
+            "config": {"workload": w.name, "n": n, "d": d, "eps": w.eps, "rate": w.rate,
+                       "min_pts": w.min_pts, "seed": w.seed, "draws": w.draws, "pairs": pairs,
+                       "parallelism": f"rows sharded x{world}" if world > 1 else "1 GPU",
+                       "l2": "256 MB L2 flush before every timed step"},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "library_launches": lib_launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "stages_ms": {k: statistics.mean(v) for k, v in stage.items()},
+            "result": {"edges": info.edges, "clusters": info.cluster_count,
+                       "core": info.core_count, "border": info.border_count,
+                       "noise": info.noise_count, "band_rechecks": info.band_rechecks,
+                       "band_1e6": info.band_1e6, "fp32_flips": info.fp32_flips,
+                       "collisions": info.collisions,
+                       "irregular_vertices": info.irregular_vertices} if world == 1 else None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -86,6 +86,8 @@ typedef struct sngb_info {
     float ms_total, ms_upload, ms_sample, ms_gather, ms_extras, ms_sort, ms_cluster, ms_download;
     uint64_t gather_pairs; /* pairs evaluated by the dominant gather kernel */
     uint64_t gather_bytes; /* its algorithmic bytes: gather_pairs * 4 * d */
+    uint64_t kernel_launches; /* hand-written kernels launched by this call (CUB not counted) */
+    uint64_t library_launches; /* CUB radix-sort / select / scan kernels launched by this call */
 } sngb_info;
 
 /* sng::sng_dbscan (clusterer.hpp:42) on HOST buffers: pts[n*d] fp32 row-major,

@@ -334,18 +334,19 @@ def sampled_edges_device(points, eps: float, rate: float, seed: int, row_begin: 
     gi = SngbInfo()
     o = _opts(points.device.index, timing, _stream_handle(points), row_begin, row_end)
     cnt = C.c_uint64(0)
-    rc = L.sngb_sampled_edges_f32_device(points.data_ptr(), n, d, float(eps), float(rate),
-                                         int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o), None, 0,
-                                         C.byref(cnt), C.byref(gi))
-    if rc not in (_lib.SNGB_OK, _lib.SNGB_ERR_CAPACITY):
-        _check(rc)
-    keys = torch.empty(max(int(cnt.value), 1), dtype=torch.int64, device=points.device)
-    if cnt.value:
+    rows = (row_end or n) - row_begin
+    draws = min(int(np.ceil(rate * float(n))), n - 1)
+    cap = int(min(max(rows * draws // 64, 1 << 20), 1 << 27))
+    while True:
+        keys = torch.empty(cap, dtype=torch.int64, device=points.device)
         rc = L.sngb_sampled_edges_f32_device(points.data_ptr(), n, d, float(eps), float(rate),
                                              int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o),
-                                             keys.data_ptr(), keys.numel(), C.byref(cnt),
-                                             C.byref(gi))
+                                             keys.data_ptr(), cap, C.byref(cnt), C.byref(gi))
+        if rc == _lib.SNGB_ERR_CAPACITY:
+            cap = int(cnt.value)
+            continue
         _check(rc)
+        break
     return keys[: cnt.value], gi
 
 

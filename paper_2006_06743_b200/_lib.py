@@ -53,6 +53,7 @@ class SngbInfo(C.Structure):
         ("ms_gather", C.c_float), ("ms_extras", C.c_float), ("ms_sort", C.c_float),
         ("ms_cluster", C.c_float), ("ms_download", C.c_float),
         ("gather_pairs", C.c_uint64), ("gather_bytes", C.c_uint64),
+        ("kernel_launches", C.c_uint64), ("library_launches", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

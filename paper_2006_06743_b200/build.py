@@ -19,8 +19,8 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libsngb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["sngb_api.cu", "sngb_kernels.cu", "sngb_cluster.cu"]
-HEADERS = ["sngb_internal.cuh", "sngb_rng.cuh"]
+SOURCES = ["sngb_api.cu", "sngb_kernels.cu", "sngb_sampler.cu", "sngb_cluster.cu"]
+HEADERS = ["sngb_internal.cuh", "sngb_rng.cuh", "sngb_device.cuh"]
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

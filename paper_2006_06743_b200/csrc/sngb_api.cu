@@ -14,6 +14,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -25,6 +26,13 @@
 #include "sngb_rng.cuh"
 
 using namespace sngb;
+
+static thread_local uint64_t sngb_t_launch_hand = 0, sngb_t_launch_lib = 0;
+
+void sngb::note_launch(int hand_written, int library) {
+    sngb_t_launch_hand += hand_written;
+    sngb_t_launch_lib += library;
+}
 
 namespace {
 
@@ -132,6 +140,11 @@ int resolve_device(const sngb_opts* o) {
     int d = 0;
     cudaGetDevice(&d);
     return d;
+}
+
+uint32_t test_force_mod() {  // see test_fire() in sngb_internal.cuh
+    const char* v = std::getenv("SNGB_TEST_FORCE_IRREGULAR");
+    return v ? (uint32_t)std::strtoul(v, nullptr, 10) : 0u;
 }
 
 uint32_t bits_for(uint64_t x) {  // bits needed to represent x (>= 1)
@@ -276,13 +289,9 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     edge_cap = std::min<uint64_t>(edge_cap, 1ull << 28);
     edge_cap = std::max<uint64_t>(edge_cap, std::min<uint64_t>(c.edge_hint, pairs + extras_cap + 1));
 
-    // sampler table (per warp): bitmap over [0, n-1) or hash of 2*draws slots
-    const size_t bitmap_bytes = (((n - 1 + 31) / 32) * 4 + 15) / 16 * 16;
-    uint32_t slots = 64;
-    while (slots < 2 * draws) slots <<= 1;
-    const size_t hash_bytes = (size_t)slots * 4;
-    const bool bitmap = bitmap_bytes <= hash_bytes;
-    const size_t table_bytes = bitmap ? bitmap_bytes : hash_bytes;
+    // Floyd tables (k_floyd, one block per vertex)
+    uint32_t slots = 64, col_words = 4;
+    if (!exhaustive) floyd_geometry((uint32_t)draws, slots, col_words);
 
     const TestParams tp = make_test(pts, stride, d, eps);
     const uint64_t seed_mixed = seed_part(seed);
@@ -301,16 +310,14 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             sa.draws = (uint32_t)draws;
             sa.base = (uint32_t)base;
             sa.seed_mixed = seed_mixed;
-            sa.table_words = (uint32_t)(table_bytes / 4);
-            sa.hash_mask = slots - 1;
-            sa.hash_shift = 32 - bits_for(slots - 1);
-            const size_t scratch = sampler_scratch_bytes(table_bytes, c.num_sms);
+            sa.force_mod = test_force_mod();
+            const size_t scratch = floyd_scratch_bytes((uint32_t)draws, c.num_sms);
             if (scratch) c.scratch.ensure(scratch);
-            sa.scratch = scratch ? c.scratch.as<uint32_t>() : nullptr;
+            sa.scratch64 = scratch ? c.scratch.as<unsigned long long>() : nullptr;
             sa.extras = c.extras.as<unsigned long long>();
             sa.extras_capacity = extras_cap;
             sa.counters = dc;
-            CK(launch_sampler(sa, bitmap, table_bytes, s, c.num_sms));
+            CK(launch_sampler(sa, s, c.num_sms));
         }
         tm.mark(E_SAMPLED);
         GatherArgs ga{};
@@ -323,6 +330,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         ga.draws = (uint32_t)draws;
         ga.base = (uint32_t)base;
         ga.seed_mixed = seed_mixed;
+        ga.force_mod = test_force_mod();
         CK(launch_gather(ga, exhaustive, s, c.num_sms));
         tm.mark(E_GATHERED);
         if (!exhaustive) {
@@ -391,6 +399,8 @@ void fill_info(sngb_info* info, const unsigned long long* hc, uint64_t n, uint32
                const GraphResult& gr, uint64_t rows, Timer& tm, bool clustered, bool host) {
     if (!info) return;
     std::memset(info, 0, sizeof(*info));
+    info->kernel_launches = sngb_t_launch_hand;
+    info->library_launches = sngb_t_launch_lib;
     info->draws = gr.draws;
     info->distance_evals = gr.exhaustive ? rows * (n - 1) : rows * gr.draws;  // graph.cpp:153,179
     info->edges = hc[C_UNIQUE];
@@ -424,6 +434,8 @@ void fill_info(sngb_info* info, const unsigned long long* hc, uint64_t n, uint32
 
 template <typename F>
 int guarded(F&& f) {
+    sngb_t_launch_hand = 0;
+    sngb_t_launch_lib = 0;
     try {
         return f();
     } catch (const CudaFail&) {

@@ -247,6 +247,8 @@ cudaError_t sort_unique(unsigned long long* keys, unsigned long long* alt, uint6
     unsigned long long* out = (sorted == keys) ? alt : keys;
     tb = temp_bytes;
     e = cub::DeviceSelect::Unique(temp, tb, sorted, out, &counters[C_UNIQUE], (int64_t)count, s);
+    // onesweep: 1 histogram + 1 exclusive-sum + ceil(bits/8) passes; select: init + sweep
+    note_launch(0, 2 + (int)((2 * nb + 7) / 8) + 2);
     *unique_out = out;
     return e;
 }
@@ -256,6 +258,7 @@ cudaError_t launch_convert_keys(const unsigned long long* in, unsigned long long
                                 unsigned long long* counters, cudaStream_t s, int num_sms) {
     if (m == 0) return cudaSuccess;
     k_convert<<<grid_for(m, num_sms), 256, 0, s>>>(in, out, m, nb, to_compact, n, counters);
+    note_launch(1);
     return cudaGetLastError();
 }
 
@@ -280,6 +283,7 @@ cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned
     k_labels<<<gn, 256, 0, s>>>(n, b.core, b.parent, b.broot, b.first, b.rank, labels, roles,
                                 counters);
     k_store_clusters<<<1, 1, 0, s>>>(b.rank, n, counters);
+    note_launch(m ? 9 : 6, 2);  // + CUB scan (init + sweep)
     return cudaGetLastError();
 }
 

@@ -59,17 +59,30 @@ struct GatherArgs {
     uint32_t draws;       // per-vertex draws (sampled mode)
     uint32_t base;        // pool - draws, pool = n - 1
     uint64_t seed_mixed;  // mix(seed + gamma)
+    uint32_t force_mod;   // test hook (0 = off), see test_fire()
 };
+
+// Test hook (env SNGB_TEST_FORCE_IRREGULAR=m): pretend the Lemire reject
+// pre-condition fired at draw draws/2 of every vertex u with u % m == 0, so
+// the exact sequential replay of irregular vertices is exercised by the
+// parity tests.  The pre-condition is a superset test, so forcing it never
+// changes results -- only which path produces them.
+__device__ __forceinline__ bool test_fire(uint32_t force_mod, uint64_t u, uint32_t i,
+                                          uint32_t draws) {
+    return force_mod != 0 && (u % force_mod) == 0 && i == draws / 2;
+}
 
 struct SamplerArgs {
     uint64_t n;
     uint64_t row_begin, row_end;
     uint32_t draws, base;
     uint64_t seed_mixed;
-    uint32_t table_words;      // u32 words per warp table
-    uint32_t hash_mask;        // hash mode: slots - 1
-    uint32_t hash_shift;       // hash mode: 32 - log2(slots)
-    uint32_t* scratch;         // global tables (when not in shared memory)
+    uint32_t force_mod;        // test hook, see test_fire()
+    uint32_t hash_mask;        // slots - 1 (slots: power of two >= 1.6 * draws)
+    uint32_t hash_shift;       // 32 - log2(slots)
+    uint32_t col_words;        // u32 words of a draws-bit bitmap (multiple of 4)
+    uint32_t key_bits;         // bits of a draw value t (fast path epoch tags)
+    unsigned long long* scratch64;  // global tables when they do not fit shared memory
     unsigned long long* extras;  // (u << 32) | v ordered pairs to evaluate
     unsigned long long extras_capacity;
     unsigned long long* counters;
@@ -84,13 +97,16 @@ struct ExtrasArgs {
     unsigned long long capacity;
 };
 
+// Host-side launch accounting (thread-local; read back into sngb_info).
+void note_launch(int hand_written, int library = 0);
+
 // ---- launchers (sngb_kernels.cu) ----
 cudaError_t launch_prepare_points(const float* src, float* dst, uint64_t n, uint32_t d,
                                   uint32_t stride, unsigned long long* counters, cudaStream_t s);
-cudaError_t launch_sampler(const SamplerArgs& a, bool bitmap, size_t table_bytes,
-                           cudaStream_t s, int num_sms);
-size_t sampler_scratch_bytes(size_t table_bytes, int num_sms);
-bool sampler_uses_shared(size_t table_bytes);
+// sngb_sampler.cu
+void floyd_geometry(uint32_t draws, uint32_t& slots, uint32_t& col_words);
+size_t floyd_scratch_bytes(uint32_t draws, int num_sms);
+cudaError_t launch_sampler(const SamplerArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_gather(const GatherArgs& a, bool exhaustive, cudaStream_t s, int num_sms);
 cudaError_t launch_extras(const ExtrasArgs& a, cudaStream_t s, int num_sms);
 

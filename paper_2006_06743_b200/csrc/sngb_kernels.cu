@@ -31,16 +31,11 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "sngb_device.cuh"
 #include "sngb_internal.cuh"
 #include "sngb_rng.cuh"
 
 namespace sngb {
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned r;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
-    return r;
-}
 
 __device__ __forceinline__ float4 ldg_row(const float4* p) { return __ldg(p); }
 __device__ __forceinline__ float2 ldg_row(const float2* p) { return __ldg(p); }
@@ -111,44 +106,6 @@ __device__ __forceinline__ bool decide(float s, bool ok, bool leader, int leader
         if (need) acc = ex;
     }
     return acc;
-}
-
-// Per-warp shared-memory staging of 64-bit records with batched flushes
-// (one global atomic per flush instead of one per record).
-template <int STAGE>
-struct WarpStage {
-    unsigned long long* buf;
-    int count;
-
-    __device__ __forceinline__ void flush(const EdgeSink& s, int lane) {
-        __syncwarp();
-        if (count == 0) return;
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(s.cursor, (unsigned long long)count);
-        base = __shfl_sync(kFull, base, 0);
-        for (int j = lane; j < count; j += 32)
-            if (base + j < s.capacity) s.keys[base + j] = buf[j];
-        __syncwarp();
-        count = 0;
-    }
-
-    __device__ __forceinline__ void push(bool has, unsigned long long rec, const EdgeSink& s,
-                                         int lane) {
-        const unsigned m = __ballot_sync(kFull, has);
-        if (!m) return;
-        if (has) buf[count + __popc(m & lanemask_lt())] = rec;
-        count += __popc(m);
-        if (count > STAGE - 32) flush(s, lane);
-    }
-};
-
-constexpr int kStage = 128;
-constexpr int kWarpsPerBlock = 8;
-
-__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    return v;
 }
 
 __device__ __forceinline__ void flush_stats(const TestStats& st, unsigned long long gpairs,
@@ -226,7 +183,10 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
                     const bool valid = i < limit;
                     bool fire = false;
                     uint32_t t = 0;
-                    if (valid) t = lemire32(stream_at(key, (uint64_t)i + 1), a.base + i + 1, fire);
+                    if (valid) {
+                        t = lemire32(stream_at(key, (uint64_t)i + 1), a.base + i + 1, fire);
+                        fire |= test_fire(a.force_mod, u, i, a.draws);
+                    }
                     pv[k] = t + (t >= (uint32_t)u ? 1u : 0u);
                     const unsigned fm = __ballot_sync(kFull, valid && fire);
                     if (fm && first_fire == 0xffffffffu) first_fire = i0 + 32 * k + __ffs(fm) - 1;
@@ -318,150 +278,6 @@ __global__ void __launch_bounds__(256) k_extras(const ExtrasArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_sampler: Floyd bookkeeping (graph.cpp:164-170), one warp per vertex,
-// draws processed 32 at a time in order with a per-warp membership table
-// (bitmap over [0, n-1) when that is smaller, else an open-addressing hash of
-// the chosen values).  Membership is "value already chosen by an earlier
-// draw": earlier chunks via the table, earlier lanes of this chunk via
-// match.any, and the rare j-chain (t equal to the replacement j of an earlier
-// collided lane of the same chunk) by an in-order lane scan.
-// ---------------------------------------------------------------------------
-template <bool BITMAP>
-__device__ __forceinline__ bool table_contains(const uint32_t* tab, uint32_t x,
-                                               const SamplerArgs& a) {
-    if (BITMAP) return (tab[x >> 5] >> (x & 31)) & 1u;
-    uint32_t h = (x * 0x9E3779B1u) >> a.hash_shift;
-    for (;;) {
-        const uint32_t v = tab[h];
-        if (v == x) return true;
-        if (v == kEmpty) return false;
-        h = (h + 1) & a.hash_mask;
-    }
-}
-
-// Insert a value known to be absent (concurrent inserts of distinct values).
-template <bool BITMAP>
-__device__ __forceinline__ void table_insert(uint32_t* tab, uint32_t x, const SamplerArgs& a) {
-    if (BITMAP) {
-        atomicOr(&tab[x >> 5], 1u << (x & 31));
-        return;
-    }
-    uint32_t h = (x * 0x9E3779B1u) >> a.hash_shift;
-    for (;;) {
-        if (atomicCAS(&tab[h], kEmpty, x) == kEmpty) return;
-        h = (h + 1) & a.hash_mask;
-    }
-}
-
-// Single-thread insert-if-absent (exact sequential fallback).
-template <bool BITMAP>
-__device__ bool table_insert_seq(uint32_t* tab, uint32_t x, const SamplerArgs& a) {
-    if (BITMAP) {
-        const uint32_t bit = 1u << (x & 31);
-        if (tab[x >> 5] & bit) return false;
-        tab[x >> 5] |= bit;
-        return true;
-    }
-    uint32_t h = (x * 0x9E3779B1u) >> a.hash_shift;
-    for (;;) {
-        const uint32_t v = tab[h];
-        if (v == x) return false;
-        if (v == kEmpty) {
-            tab[h] = x;
-            return true;
-        }
-        h = (h + 1) & a.hash_mask;
-    }
-}
-
-template <bool BITMAP>
-__device__ __forceinline__ void table_clear(uint32_t* tab, uint32_t words, int lane) {
-    const uint32_t fill = BITMAP ? 0u : kEmpty;
-    uint4* t4 = reinterpret_cast<uint4*>(tab);
-    for (uint32_t w = lane; w < words / 4; w += 32) t4[w] = make_uint4(fill, fill, fill, fill);
-    __syncwarp();
-}
-
-template <bool BITMAP, bool SHARED>
-__global__ void __launch_bounds__(256) k_sampler(const SamplerArgs a) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int wpb = blockDim.x >> 5;
-    const uint64_t gw = (uint64_t)blockIdx.x * wpb + wib;
-    const uint64_t nw = (uint64_t)gridDim.x * wpb;
-    uint32_t* tab = SHARED ? smem + (size_t)wib * a.table_words
-                           : a.scratch + gw * (uint64_t)a.table_words;
-    unsigned long long* sbuf =
-        reinterpret_cast<unsigned long long*>(smem + (SHARED ? (size_t)wpb * a.table_words : 0)) +
-        (size_t)wib * kStage;
-    const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
-    WarpStage<kStage> stage{sbuf, 0};
-    unsigned long long ncol = 0, nirr = 0;
-    const uint32_t D = a.draws, base = a.base;
-
-    for (uint64_t u = a.row_begin + gw; u < a.row_end; u += nw) {
-        table_clear<BITMAP>(tab, a.table_words, lane);
-        const uint64_t key = vertex_key(a.seed_mixed, u);
-        bool irregular = false;
-        for (uint32_t c0 = 0; c0 < D; c0 += 32) {
-            const uint32_t i = c0 + lane;
-            const bool valid = i < D;
-            bool fire = false;
-            uint32_t t = 0;
-            if (valid) t = lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fire);
-            if (__ballot_sync(kFull, valid && fire)) {
-                irregular = true;
-                break;
-            }
-            const bool in_prev = valid && table_contains<BITMAP>(tab, t, a);
-            const unsigned mm = __match_any_sync(kFull, valid ? t : (0xffffffffu - lane));
-            const bool dup = (mm & lanemask_lt()) != 0;
-            bool col = valid && (in_prev || dup);
-            const uint32_t j = base + i;  // Floyd's replacement value for draw i
-            if (__ballot_sync(kFull, valid && !col && t >= base + c0 && t < j)) {
-                for (int l = 0; l < 31; ++l) {
-                    const bool cl = __shfl_sync(kFull, col, l);
-                    if (cl && lane > l && valid && !col && t == base + c0 + l) col = true;
-                }
-            }
-            if (valid) table_insert<BITMAP>(tab, col ? j : t, a);
-            __syncwarp();
-            const unsigned cm = __ballot_sync(kFull, col);
-            ncol += (lane == 0) ? __popc(cm) : 0;
-            const uint32_t pj = j + (j >= (uint32_t)u ? 1u : 0u);
-            stage.push(col, ((unsigned long long)u << 32) | pj, xs, lane);
-        }
-        if (irregular) {
-            // Exact replay of graph.cpp:163-174 with the true Stream (rejections
-            // consume extra counters); every partner of u becomes an extra.
-            table_clear<BITMAP>(tab, a.table_words, lane);
-            if (lane == 0) {
-                ++nirr;
-                SeqStream s{key, 0};
-                const uint64_t pool = a.n - 1;
-                for (uint64_t jj = base; jj < pool; ++jj) {
-                    const uint32_t t = (uint32_t)s.next_below(jj + 1);
-                    uint32_t e = t;
-                    if (!table_insert_seq<BITMAP>(tab, t, a)) {
-                        table_insert_seq<BITMAP>(tab, (uint32_t)jj, a);
-                        e = (uint32_t)jj;
-                    }
-                    const uint32_t pe = e + (e >= (uint32_t)u ? 1u : 0u);
-                    const unsigned long long slot = atomicAdd(xs.cursor, 1ull);
-                    if (slot < xs.capacity) xs.keys[slot] = ((unsigned long long)u << 32) | pe;
-                }
-            }
-            __syncwarp();
-        }
-    }
-    stage.flush(xs, lane);
-    if (lane == 0) {
-        if (ncol) atomicAdd(&a.counters[C_COLLISIONS], ncol);
-        if (nirr) atomicAdd(&a.counters[C_IRREGULAR], nirr);
-    }
-}
-
-// ---------------------------------------------------------------------------
 // k_prepare: copy n x d rows into the padded device layout (stride floats)
 // and count non-finite values (dataset.hpp:24-26).  With dst == nullptr the
 // kernel only checks.
@@ -499,6 +315,7 @@ cudaError_t launch_prepare_points(const float* src, float* dst, uint64_t n, uint
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     if (blocks == 0) blocks = 1;
     k_prepare<<<(unsigned)blocks, 256, 0, s>>>(src, dst, n, d, stride, counters);
+    note_launch(1);
     return cudaGetLastError();
 }
 
@@ -520,6 +337,7 @@ cudaError_t gather_one(const GatherArgs& a, cudaStream_t s, int num_sms) {
     auto k = k_gather<G, V, R, F2, EXH>;
     unsigned grid = persistent_grid(k, a.row_end - a.row_begin, num_sms);
     k<<<grid, 256, 0, s>>>(a);
+    note_launch(1);
     return cudaGetLastError();
 }
 
@@ -551,6 +369,7 @@ cudaError_t extras_one(const ExtrasArgs& a, cudaStream_t s, int num_sms) {
     constexpr int NG = 32 / G;
     unsigned grid = persistent_grid(k, (a.capacity + NG - 1) / NG, num_sms);
     k<<<grid, 256, 0, s>>>(a);
+    note_launch(1);
     return cudaGetLastError();
 }
 
@@ -581,51 +400,6 @@ cudaError_t launch_extras(const ExtrasArgs& a, cudaStream_t s, int num_sms) {
         case 8: return extras_one<32, 8, false>(a, s, num_sms);
         default: return cudaErrorInvalidValue;
     }
-}
-
-// Shared-memory budget for the sampler's per-warp tables.
-constexpr size_t kSamplerSmemBudget = 200 * 1024;
-constexpr size_t kStageBytes = kStage * sizeof(unsigned long long);
-
-bool sampler_uses_shared(size_t table_bytes) { return table_bytes + kStageBytes <= 96 * 1024; }
-
-static int sampler_warps_per_block(size_t table_bytes) {
-    int w = (int)(kSamplerSmemBudget / (table_bytes + kStageBytes));
-    if (w > kWarpsPerBlock) w = kWarpsPerBlock;
-    if (w < 1) w = 1;
-    return w;
-}
-
-size_t sampler_scratch_bytes(size_t table_bytes, int num_sms) {
-    if (sampler_uses_shared(table_bytes)) return 0;
-    return (size_t)num_sms * 4 * kWarpsPerBlock * table_bytes;
-}
-
-cudaError_t launch_sampler(const SamplerArgs& a, bool bitmap, size_t table_bytes, cudaStream_t s,
-                           int num_sms) {
-    const uint64_t rows = a.row_end - a.row_begin;
-    if (rows == 0 || a.draws == 0) return cudaSuccess;
-    if (sampler_uses_shared(table_bytes)) {
-        const int wpb = sampler_warps_per_block(table_bytes);
-        const size_t smem = (size_t)wpb * (table_bytes + kStageBytes);
-        auto k = bitmap ? k_sampler<true, true> : k_sampler<false, true>;
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * 32, smem);
-        if (per_sm < 1) per_sm = 1;
-        uint64_t want = (rows + wpb - 1) / wpb, cap = (uint64_t)num_sms * per_sm;
-        unsigned grid = (unsigned)(want < cap ? want : cap);
-        k<<<grid, wpb * 32, smem, s>>>(a);
-    } else {
-        // Tables in global memory (L2-resident scratch), fixed warp count.
-        auto k = bitmap ? k_sampler<true, false> : k_sampler<false, false>;
-        const size_t smem = (size_t)kWarpsPerBlock * kStageBytes;
-        uint64_t want = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock, cap = (uint64_t)num_sms * 4;
-        unsigned grid = (unsigned)(want < cap ? want : cap);
-        k<<<grid, kWarpsPerBlock * 32, smem, s>>>(a);
-    }
-    return cudaGetLastError();
 }
 
 }  // namespace sngb

@@ -1,0 +1,303 @@
+// sngb_sampler.cu -- Floyd bookkeeping of the sampled eps-graph (k_floyd).
+//
+// Reference: graph.cpp:161-174 (Floyd's algorithm over [0, n-2] with the
+// rng.hpp:35-48 Lemire draw), run one vertex at a time with an
+// std::unordered_set.  The draw values t_i need no state (counter i+1, SURVEY
+// Appendix C); only the Floyd replacements need bookkeeping:
+//
+//     draw i collides  <=>  t_i in S_{i-1} = {t_0..t_{i-1}} U {j_k : k < i collided}
+//     (j_k = base + k is draw k's replacement, base = n-1-draws)
+//
+// which splits into an ORDER-FREE part and a short ordered chain:
+//
+//   dupT_i  = t_i equals an earlier t_k          -> first occurrence via a
+//             shared-memory hash of (t, min index), all draws in parallel;
+//   chain_i = t_i = j_k for a collided k < i     -> only possible when
+//             t_i >= base; k = t_i - base; resolved in index order.
+//
+// One thread block per vertex (all draws of the vertex in flight at once),
+// four block-wide phases: insert (min-index) -> classify -> resolve chains
+// (thread 0, rare) -> emit the replacement partner j_i + (j_i >= u) of every
+// collided draw as an "extra" pair for k_extras.  Vertices whose stream meets
+// the Lemire reject pre-condition are replayed exactly by one thread with the
+// sequential Stream (all of their partners become extras).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sngb_device.cuh"
+#include "sngb_internal.cuh"
+#include "sngb_rng.cuh"
+
+namespace sngb {
+
+namespace {
+
+constexpr int kFloydThreads = 256;
+constexpr int kFloydWarps = kFloydThreads / 32;
+constexpr int kFloydStage = 64;
+constexpr unsigned long long kEmpty64 = ~0ull;  // t < n-1 < 2^32-1, never a real key
+
+__device__ __forceinline__ uint32_t hslot(uint32_t t, uint32_t shift) {
+    return (t * 0x9E3779B1u) >> shift;
+}
+
+// The table is bucketized: 4 entries (t << 32 | first index) per 32-byte
+// bucket, read with two 16-byte shared loads, linear probing over buckets.
+// Load factor <= 0.5, so a probe almost always ends in the home bucket and
+// the lanes of a warp stay converged (a slot-wise linear probe at 0.6 load
+// left warps iterating at 2-4 active lanes).  Entries are filled in slot
+// order and never emptied within a vertex, so the first slot holding t is
+// unique and every draw of t meets it.
+struct Bucket {
+    unsigned long long e[4];
+};
+
+__device__ __forceinline__ Bucket load_bucket(const unsigned long long* tab, uint32_t b) {
+    const unsigned long long* p = tab + 4 * (size_t)b;
+    Bucket r;
+    asm volatile("ld.volatile.v2.u64 {%0, %1}, [%2];" : "=l"(r.e[0]), "=l"(r.e[1]) : "l"(p));
+    asm volatile("ld.volatile.v2.u64 {%0, %1}, [%2];" : "=l"(r.e[2]), "=l"(r.e[3]) : "l"(p + 2));
+    return r;
+}
+
+// Insert (t, i); the entry of t keeps the minimum index (first occurrence).
+__device__ __forceinline__ void insert_min(unsigned long long* tab, uint32_t t, uint32_t i,
+                                           uint32_t mask, uint32_t shift) {
+    const unsigned long long mine = ((unsigned long long)t << 32) | i;
+    uint32_t b = hslot(t, shift);
+    for (;;) {
+        const Bucket bk = load_bucket(tab, b);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            unsigned long long cur = bk.e[k];
+            if (cur == kEmpty64) {
+                cur = atomicCAS(&tab[4 * (size_t)b + k], kEmpty64, mine);
+                if (cur == kEmpty64) return;
+            }
+            if ((uint32_t)(cur >> 32) == t) {
+                if ((uint32_t)cur > i) atomicMin(&tab[4 * (size_t)b + k], mine);
+                return;
+            }
+        }
+        b = (b + 1) & mask;
+    }
+}
+
+__device__ __forceinline__ uint32_t first_index(const unsigned long long* tab, uint32_t t,
+                                                uint32_t mask, uint32_t shift) {
+    uint32_t b = hslot(t, shift);
+    for (;;) {
+        const Bucket bk = load_bucket(tab, b);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((uint32_t)(bk.e[k] >> 32) == t) return (uint32_t)bk.e[k];
+        b = (b + 1) & mask;
+    }
+}
+
+// Single-thread insert-if-absent for the exact sequential replay.
+__device__ bool insert_seq(unsigned long long* tab, uint32_t t, uint32_t mask, uint32_t shift) {
+    uint32_t b = hslot(t, shift);
+    for (;;) {
+        for (int k = 0; k < 4; ++k) {
+            unsigned long long& cur = tab[4 * (size_t)b + k];
+            if (cur == kEmpty64) {
+                cur = (unsigned long long)t << 32;
+                return true;
+            }
+            if ((uint32_t)(cur >> 32) == t) return false;
+        }
+        b = (b + 1) & mask;
+    }
+}
+
+__device__ __forceinline__ uint32_t draw_t(uint64_t key, uint32_t i, uint32_t base, bool& fire) {
+    return lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fire);
+}
+
+template <bool SHARED>
+__global__ void __launch_bounds__(kFloydThreads) k_floyd(const SamplerArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t P = 4 * (a.hash_mask + 1);  // entries (4 per bucket)
+    const uint32_t W = a.col_words;  // words of one D-bit bitmap (multiple of 4)
+    unsigned long long* tab = SHARED ? reinterpret_cast<unsigned long long*>(smem)
+                                     : a.scratch64 + (uint64_t)blockIdx.x * P;
+    uint32_t* colbits = reinterpret_cast<uint32_t*>(smem + (SHARED ? (size_t)P * 8 : 0));
+    uint32_t* cbits = colbits + W;
+    unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(cbits + W);
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    WarpStage<kFloydStage> stage{sbuf + wib * kFloydStage, 0};
+    const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
+    const uint32_t D = a.draws, base = a.base, mask = a.hash_mask, shift = a.hash_shift;
+    unsigned long long ncol = 0, nirr = 0;
+
+    for (uint64_t u = a.row_begin + blockIdx.x; u < a.row_end; u += gridDim.x) {
+        // ---- clear (table + both bitmaps) ----
+        {
+            ulonglong2* t2 = reinterpret_cast<ulonglong2*>(tab);
+            for (uint32_t s = tid; s < P / 2; s += kFloydThreads) t2[s] = make_ulonglong2(kEmpty64, kEmpty64);
+            uint4* b4 = reinterpret_cast<uint4*>(colbits);
+            for (uint32_t s = tid; s < (2 * W) / 4; s += kFloydThreads) b4[s] = make_uint4(0, 0, 0, 0);
+        }
+        __syncthreads();
+        const uint64_t key = vertex_key(a.seed_mixed, u);
+
+        // ---- phase 1: every draw inserts (t, i); slot keeps the first index ----
+        bool fired = false;
+        for (uint32_t i = tid; i < D; i += kFloydThreads) {
+            bool f;
+            const uint32_t t = draw_t(key, i, base, f);
+            fired |= f || test_fire(a.force_mod, u, i, D);
+            insert_min(tab, t, i, mask, shift);
+        }
+        if (__syncthreads_or(fired)) {
+            // ---- irregular vertex: exact sequential replay (graph.cpp:163-174) ----
+            for (uint32_t s = tid; s < P; s += kFloydThreads) tab[s] = kEmpty64;
+            __syncthreads();
+            if (tid == 0) {
+                ++nirr;
+                SeqStream st{key, 0};
+                const uint64_t pool = a.n - 1;
+                for (uint64_t jj = base; jj < pool; ++jj) {
+                    const uint32_t t = (uint32_t)st.next_below(jj + 1);
+                    uint32_t e = t;
+                    if (!insert_seq(tab, t, mask, shift)) {
+                        insert_seq(tab, (uint32_t)jj, mask, shift);
+                        e = (uint32_t)jj;
+                    }
+                    const uint32_t pe = e + (e >= (uint32_t)u ? 1u : 0u);
+                    const unsigned long long slot = atomicAdd(xs.cursor, 1ull);
+                    if (slot < xs.capacity) xs.keys[slot] = ((unsigned long long)u << 32) | pe;
+                }
+            }
+            __syncthreads();
+            continue;
+        }
+
+        // ---- phase 2: classify: dupT -> collided; possible chain -> candidate ----
+        bool anycand = false;
+        for (uint32_t i = tid; i < D; i += kFloydThreads) {
+            bool f;
+            const uint32_t t = draw_t(key, i, base, f);
+            if (first_index(tab, t, mask, shift) != i) {
+                atomicOr(&colbits[i >> 5], 1u << (i & 31));
+            } else if (t >= base && t - base < i) {
+                atomicOr(&cbits[i >> 5], 1u << (i & 31));
+                anycand = true;
+            }
+        }
+        // ---- phase 3: chains t_i = j_k (k collided, k < i), in index order ----
+        if (__syncthreads_or(anycand)) {
+            if (tid == 0) {
+                for (uint32_t w = 0; w < W; ++w) {
+                    uint32_t bits = cbits[w];
+                    while (bits) {
+                        const uint32_t b = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const uint32_t i = 32 * w + b;
+                        bool f;
+                        const uint32_t k = draw_t(key, i, base, f) - base;
+                        if ((colbits[k >> 5] >> (k & 31)) & 1u) colbits[i >> 5] |= 1u << (i & 31);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // ---- phase 4: emit Floyd replacements j_i of collided draws ----
+        for (uint32_t i0 = 0; i0 < D; i0 += kFloydThreads) {
+            const uint32_t i = i0 + tid;
+            const bool col = i < D && ((colbits[i >> 5] >> (i & 31)) & 1u);
+            const unsigned cm = __ballot_sync(kFull, col);
+            if (lane == 0) ncol += __popc(cm);
+            const uint32_t j = base + i;
+            const uint32_t pj = j + (j >= (uint32_t)u ? 1u : 0u);
+            stage.push(col, ((unsigned long long)u << 32) | pj, xs, lane);
+        }
+        __syncthreads();
+    }
+    stage.flush(xs, lane);
+    if (lane == 0) {
+        if (ncol) atomicAdd(&a.counters[C_COLLISIONS], ncol);
+        if (nirr && wib == 0) atomicAdd(&a.counters[C_IRREGULAR], nirr);
+    }
+}
+
+#include "sngb_floyd_fast.cuh"
+
+}  // namespace
+
+// Geometry of the per-vertex tables.
+void floyd_geometry(uint32_t draws, uint32_t& slots, uint32_t& col_words) {
+    uint32_t buckets = 16;
+    while (20 * buckets < 8 * draws) buckets <<= 1;  // 4 * buckets >= 1.6 * draws: load <= 0.625
+    slots = 4 * buckets;
+    col_words = ((draws + 31) / 32 + 3) & ~3u;
+}
+
+size_t floyd_smem_bytes(uint32_t draws, bool shared_table) {
+    uint32_t slots, cw;
+    floyd_geometry(draws, slots, cw);
+    return (shared_table ? (size_t)slots * 8 : 0) + (size_t)cw * 8 +
+           (size_t)kFloydWarps * kFloydStage * 8;
+}
+
+bool floyd_shared(uint32_t draws) { return floyd_smem_bytes(draws, true) <= 200 * 1024; }
+
+size_t floyd_scratch_bytes(uint32_t draws, int num_sms) {
+    if (floyd_shared(draws)) return 0;
+    uint32_t slots, cw;
+    floyd_geometry(draws, slots, cw);
+    return (size_t)num_sms * 2 * slots * 8;
+}
+
+cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
+    const uint64_t rows = in.row_end - in.row_begin;
+    if (rows == 0 || in.draws == 0) return cudaSuccess;
+    SamplerArgs a = in;
+    const uint32_t D = a.draws;
+    uint32_t fb = 16;  // fast path: buckets of 4 u32 keys, load <= 0.625
+    while (10 * fb < 4 * D) fb <<= 1;
+    const uint32_t cw = ((D + 31) / 32 + 3) & ~3u;
+    const size_t fast_smem = floyd_fast_smem_bytes(fb, cw);
+    uint32_t tb = 1;  // bits of a draw value t <= n - 2
+    while (tb < 32 && ((uint64_t)(a.n - 2) >> tb) != 0) ++tb;
+    if (D <= 4096 && tb < 30 && fast_smem <= 200 * 1024) {
+        a.hash_mask = fb - 1;
+        a.hash_shift = 32 - __builtin_ctz(fb);
+        a.col_words = cw;
+        a.key_bits = tb;
+        auto k = D <= 1024 ? k_floyd_fast<4> : D <= 2048 ? k_floyd_fast<8> : D <= 3072 ? k_floyd_fast<12> : k_floyd_fast<16>;
+        cudaError_t e =
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFastThreads, fast_smem);
+        if (per_sm < 1) per_sm = 1;
+        const uint64_t cap = (uint64_t)num_sms * per_sm;
+        k<<<(unsigned)(rows < cap ? rows : cap), kFastThreads, fast_smem, s>>>(a);
+        note_launch(1);
+        return cudaGetLastError();
+    }
+    // generic path: 64-bit (t, first index) entries, any draws
+    uint32_t slots, cw64;
+    floyd_geometry(D, slots, cw64);
+    a.hash_mask = slots / 4 - 1;
+    a.hash_shift = 32 - __builtin_ctz(slots / 4);
+    a.col_words = cw64;
+    const bool sh = floyd_shared(D);
+    const size_t smem = floyd_smem_bytes(D, sh);
+    auto k = sh ? k_floyd<true> : k_floyd<false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFloydThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    if (!sh) per_sm = 2;  // scratch holds num_sms * 2 tables
+    const uint64_t cap = (uint64_t)num_sms * per_sm;
+    k<<<(unsigned)(rows < cap ? rows : cap), kFloydThreads, smem, s>>>(a);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
+}  // namespace sngb

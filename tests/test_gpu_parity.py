@@ -115,3 +115,34 @@ def test_device_api_matches_host_api(oracle):
     np.testing.assert_array_equal(labels.cpu().numpy(), ol)
     np.testing.assert_array_equal(roles.cpu().numpy(), orl)
     assert gi.edges == oinfo["edges"]
+
+
+@pytest.mark.parametrize("n,d,eps,rate,seed", [(6000, 3, 0.1, 0.8, 4), (9000, 2, 0.02, 0.5, 8)])
+def test_large_draws_generic_sampler(oracle, n, d, eps, rate, seed):
+    """draws > 4096 takes the generic (regenerating) Floyd kernel."""
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, d), dtype=np.float32)
+    keys, evals = oracle.sampled_edges(pts, eps, rate, seed)
+    st = sng.BuildStats()
+    g = sng.build_sampled_graph(sng.Dataset(pts), eps, rate, seed=seed, stats=st)
+    assert st.distance_evals == evals
+    np.testing.assert_array_equal(g.keys, keys)
+
+
+@pytest.mark.parametrize("n,d,eps,rate,seed", [(3000, 2, 0.05, 0.3, 1), (20000, 16, 1.0, 0.02, 3),
+                                               (6000, 3, 0.1, 0.8, 4)])
+def test_forced_irregular_vertices_exact(oracle, monkeypatch, n, d, eps, rate, seed):
+    """Force the Lemire-reject pre-condition on every 7th vertex: those vertices
+    go through the exact sequential replay; the edge set must not change."""
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, d), dtype=np.float32)
+    keys, _ = oracle.sampled_edges(pts, eps, rate, seed)
+    monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", "7")
+    info = sng.ClusterRunInfo()
+    g = sng.build_sampled_graph(sng.Dataset(pts), eps, rate, seed=seed)
+    np.testing.assert_array_equal(g.keys, keys)
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=eps, min_pts=3, rate=rate, seed=seed),
+                       info)
+    assert info.gpu["irregular_vertices"] == (n + 6) // 7
+    ol, orl, _, _ = oracle.sng_dbscan(pts, eps, 3, rate, seed)
+    np.testing.assert_array_equal(c.assignment, ol)
