@@ -66,6 +66,11 @@ class Oracle:
         L.orc_sampled_edges.argtypes = [C.POINTER(C.c_float), C.c_uint64, C.c_uint32, C.c_double,
                                         C.c_double, C.c_uint64, C.c_int, C.POINTER(_u64p),
                                         _u64p, _u64p]
+        L.orc_sampled_edges_rows.restype = C.c_int
+        L.orc_sampled_edges_rows.argtypes = [C.POINTER(C.c_float), C.c_uint64, C.c_uint32,
+                                             C.c_double, C.c_double, C.c_uint64, C.c_int,
+                                             C.c_uint64, C.c_uint64, C.POINTER(_u64p), _u64p,
+                                             _u64p]
         L.orc_cluster_edges.restype = C.c_int
         L.orc_cluster_edges.argtypes = [_u64p, C.c_uint64, C.c_uint64, C.c_int32,
                                         C.POINTER(C.c_int32), C.POINTER(C.c_uint8),
@@ -103,6 +108,24 @@ class Oracle:
         ev = C.c_uint64()
         rc = self.L.orc_sampled_edges(_ptr(pts, C.c_float), n, d, eps, rate, seed, threads,
                                       C.byref(kp), C.byref(nk), C.byref(ev))
+        if rc:
+            raise ValueError(self.ERRORS.get(rc, f"oracle error {rc}"))
+        keys = np.ctypeslib.as_array(kp, shape=(nk.value,)).copy() if nk.value else \
+            np.empty(0, np.uint64)
+        self.L.orc_free(kp)
+        return keys, int(ev.value)
+
+    def sampled_edges_rows(self, pts: np.ndarray, eps: float, rate: float, seed: int,
+                           row_begin: int, row_end: int, threads: int = 0):
+        """Edges sampled by the query rows [row_begin, row_end) (a row shard)."""
+        pts = np.ascontiguousarray(pts, np.float32)
+        n, d = pts.shape
+        kp = _u64p()
+        nk = C.c_uint64()
+        ev = C.c_uint64()
+        rc = self.L.orc_sampled_edges_rows(_ptr(pts, C.c_float), n, d, eps, rate, seed, threads,
+                                           row_begin, row_end, C.byref(kp), C.byref(nk),
+                                           C.byref(ev))
         if rc:
             raise ValueError(self.ERRORS.get(rc, f"oracle error {rc}"))
         keys = np.ctypeslib.as_array(kp, shape=(nk.value,)).copy() if nk.value else \

@@ -245,17 +245,26 @@ static int resolve_threads(int threads, uint64_t n) { /* graph.cpp:23-31 */
 int orc_sampled_edges(const float* pts, uint64_t n, uint32_t d, double eps, double rate,
                       uint64_t seed, int threads, uint64_t** keys_out, uint64_t* nkeys,
                       uint64_t* distance_evals) {
+    return orc_sampled_edges_rows(pts, n, d, eps, rate, seed, threads, 0, n, keys_out, nkeys,
+                                  distance_evals);
+}
+
+int orc_sampled_edges_rows(const float* pts, uint64_t n, uint32_t d, double eps, double rate,
+                           uint64_t seed, int threads, uint64_t row_begin, uint64_t row_end,
+                           uint64_t** keys_out, uint64_t* nkeys, uint64_t* distance_evals) {
     if (n == 0) return -4;
     if (!(eps > 0.0)) return -1;
     if (!(rate > 0.0) || rate > 1.0) return -3;
+    if (row_begin > row_end || row_end > n) return -7;
     const uint64_t draws = orc_draws(n, rate);
-    int workers = resolve_threads(threads, n);
+    const uint64_t rows = row_end - row_begin;
+    int workers = resolve_threads(threads, rows ? rows : 1);
     worker_arg* args = (worker_arg*)calloc((size_t)workers, sizeof(worker_arg));
     pthread_t* tids = (pthread_t*)calloc((size_t)workers, sizeof(pthread_t));
-    const uint64_t chunk = (n + workers - 1) / workers; /* graph.cpp:52 */
+    const uint64_t chunk = (rows + workers - 1) / workers; /* graph.cpp:52 */
     int used = 0;
     for (int t = 0; t < workers; ++t) {
-        uint64_t b = t * chunk, e = b + chunk < n ? b + chunk : n;
+        uint64_t b = row_begin + t * chunk, e = b + chunk < row_end ? b + chunk : row_end;
         if (b >= e) break;
         args[t] = (worker_arg){pts, n, d, eps, draws, seed, b, e, NULL, 0, 0, 0};
         ++used;

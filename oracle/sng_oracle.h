@@ -61,6 +61,12 @@ int orc_sampled_edges(const float* pts, uint64_t n, uint32_t d, double eps, doub
                       uint64_t seed, int threads, uint64_t** keys_out, uint64_t* nkeys,
                       uint64_t* distance_evals);
 
+/* The same restricted to the query rows [row_begin, row_end) -- the edges a
+ * row shard of the multi-GPU path produces (graph.cpp:146-177 per vertex). */
+int orc_sampled_edges_rows(const float* pts, uint64_t n, uint32_t d, double eps, double rate,
+                           uint64_t seed, int threads, uint64_t row_begin, uint64_t row_end,
+                           uint64_t** keys_out, uint64_t* nkeys, uint64_t* distance_evals);
+
 /* clusterer.cpp:7-52 cluster_graph over canonical sorted unique keys. */
 int orc_cluster_edges(const uint64_t* keys, uint64_t nkeys, uint64_t n, int32_t min_pts,
                       int32_t* labels, uint8_t* roles, int32_t* cluster_count);
