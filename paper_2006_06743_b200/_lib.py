@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libsngb.so")
+LIB_PATH = os.environ.get("SNGB_LIBRARY") or os.path.join(PKG, "lib", "libsngb.so")
 
 SNGB_OK = 0
 SNGB_ERR_EPS = 1

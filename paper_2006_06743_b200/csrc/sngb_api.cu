@@ -80,6 +80,7 @@ struct Buf {
 struct DevCtx {
     int dev = 0;
     int num_sms = 148;
+    uint64_t l2_bytes = 126ull << 20;
     cudaStream_t stream = nullptr;
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
@@ -127,6 +128,9 @@ DevCtx& get_ctx(int dev) {
         auto c = std::make_unique<DevCtx>();
         c->dev = dev;
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
+        int l2 = 0;
+        CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+        c->l2_bytes = (uint64_t)l2;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         CK(cudaMallocHost(&c->h_counters, C_COUNT * sizeof(unsigned long long)));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
@@ -145,6 +149,11 @@ int resolve_device(const sngb_opts* o) {
 uint32_t test_force_mod() {  // see test_fire() in sngb_internal.cuh
     const char* v = std::getenv("SNGB_TEST_FORCE_IRREGULAR");
     return v ? (uint32_t)std::strtoul(v, nullptr, 10) : 0u;
+}
+
+uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* v = std::getenv(name);
+    return v ? (uint64_t)std::strtoull(v, nullptr, 10) : dflt;
 }
 
 uint32_t bits_for(uint64_t x) {  // bits needed to represent x (>= 1)
@@ -223,6 +232,21 @@ struct Timer {
 
 enum Ev { E_START = 0, E_UPLOADED, E_PREPARED, E_SAMPLED, E_GATHERED, E_EXTRAS, E_SORTED,
           E_CLUSTERED, E_DOWNLOADED, E_END };
+
+// Number of L2-blocked gather phases.  A phase re-generates every draw
+// (~0.35 SM-cycles each) and re-streams the query rows, and in exchange turns
+// the partner gather into L2 hits; it pays while the row table is a small
+// multiple of L2 and the rows are wide (cfg2: 219.5 MB of 3136-byte rows).
+// Env SNGB_GATHER_PHASES forces a count; SNGB_L2_PHASE_BYTES sets the slice.
+uint32_t gather_phases(const DevCtx& c, uint64_t n, uint32_t stride, uint64_t draws) {
+    const uint64_t forced = env_u64("SNGB_GATHER_PHASES", 0);
+    if (forced) return (uint32_t)std::min<uint64_t>(forced, std::max<uint64_t>(n, 1));
+    const uint64_t table = n * stride * 4ull;
+    const uint64_t slice = env_u64("SNGB_L2_PHASE_BYTES", (uint64_t)(0.5 * c.l2_bytes));
+    if (slice == 0 || table <= slice || stride < 64 || draws == 0) return 1;
+    const uint64_t p = (table + slice - 1) / slice;
+    return p <= 4 ? (uint32_t)p : 1u;
+}
 
 struct GraphResult {
     unsigned long long* ukeys = nullptr;  // device, compact keys
@@ -331,7 +355,15 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         ga.base = (uint32_t)base;
         ga.seed_mixed = seed_mixed;
         ga.force_mod = test_force_mod();
-        CK(launch_gather(ga, exhaustive, s, c.num_sms));
+        // L2-blocked phases: each launch tests only partners in one slice of
+        // the rows, small enough to stay L2-resident while every vertex's
+        // draws are regenerated (cheap) and its query row streamed.
+        const uint32_t phases = gather_phases(c, n, stride, draws);
+        for (uint32_t ph = 0; ph < phases; ++ph) {
+            ga.part_lo = (uint32_t)(n * ph / phases);
+            ga.part_hi = (uint32_t)(n * (ph + 1) / phases);
+            CK(launch_gather(ga, exhaustive, s, c.num_sms));
+        }
         tm.mark(E_GATHERED);
         if (!exhaustive) {
             ExtrasArgs ea{};

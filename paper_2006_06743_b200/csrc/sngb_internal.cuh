@@ -60,6 +60,7 @@ struct GatherArgs {
     uint32_t base;        // pool - draws, pool = n - 1
     uint64_t seed_mixed;  // mix(seed + gamma)
     uint32_t force_mod;   // test hook (0 = off), see test_fire()
+    uint32_t part_lo, part_hi;  // partner rows tested by this launch (L2-blocked phases)
 };
 
 // Test hook (env SNGB_TEST_FORCE_IRREGULAR=m): pretend the Lemire reject

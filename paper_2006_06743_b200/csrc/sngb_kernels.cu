@@ -39,6 +39,25 @@ namespace sngb {
 
 __device__ __forceinline__ float4 ldg_row(const float4* p) { return __ldg(p); }
 __device__ __forceinline__ float2 ldg_row(const float2* p) { return __ldg(p); }
+// Query rows are read once per vertex (per phase): keep them out of L1 and
+// mark them evict-first in L2 so they do not displace partner rows.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(evict_first_policy()));
+    return r;
+}
+__device__ __forceinline__ float2 ldg_stream(const float2* p) {
+    float2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+                 : "=f"(r.x), "=f"(r.y) : "l"(p), "l"(evict_first_policy()));
+    return r;
+}
 template <typename Vec>
 __device__ __forceinline__ Vec vzero();
 template <>
@@ -108,6 +127,20 @@ __device__ __forceinline__ bool decide(float s, bool ok, bool leader, int leader
     return acc;
 }
 
+// Same decision when every lane owns one pair (no group broadcast needed).
+__device__ __forceinline__ bool decide_lane(float s, bool ok, const TestParams& tp, uint64_t u,
+                                            uint64_t v, TestStats& st) {
+    const bool need = ok && !(s < tp.lo_thr) && !(s > tp.hi_thr);
+    bool acc = ok && (s < tp.lo_thr);
+    if (need) {
+        acc = exact_within(tp, u, v);
+        st.band++;
+        if (fabsf(s - tp.eps2f) <= 1e-6f * tp.eps2f) st.band6++;
+        if ((s <= tp.eps2f) != acc) st.flips++;
+    }
+    return acc;
+}
+
 __device__ __forceinline__ void flush_stats(const TestStats& st, unsigned long long gpairs,
                                             unsigned long long* counters, int lane) {
     const unsigned long long p = warp_sum(st.pairs), b = warp_sum(st.band),
@@ -123,9 +156,10 @@ __device__ __forceinline__ void flush_stats(const TestStats& st, unsigned long l
 }
 
 // Pairs per group issued back to back (loads in flight per lane = U * V).
-template <int G, int V>
+// G < 32: a group takes R*G pairs of each 32*R-draw chunk in one go.
+template <int G, int V, int R>
 struct Unroll {
-    static constexpr int value = G < 32 ? G : (V == 1 ? 8 : (V == 2 ? 4 : 2));
+    static constexpr int value = G < 32 ? R * G : (V == 1 ? 8 : (V == 2 ? 4 : 2));
 };
 
 // ---------------------------------------------------------------------------
@@ -134,13 +168,19 @@ struct Unroll {
 //   EXH = false: partners are the Floyd draws t_i (graph.cpp:167-174)
 //   EXH = true : partners are all v > u (draws >= n-1, graph.cpp:157-159;
 //                each unordered pair once -- same edge set)
+// Each chunk of 32*R draws is compacted (ballot + popc into a per-warp
+// shared list) to the pairs that are live: below the irregular cut and with
+// the partner row inside [part_lo, part_hi).  The partner range lets the host
+// run the gather as L2-blocked phases (one slice of the rows per launch) when
+// the row table is a small multiple of L2; a single phase covers [0, n).
 // ---------------------------------------------------------------------------
 template <int G, int V, int R, bool F2, bool EXH>
 __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
     using Vec = typename std::conditional<F2, float2, float4>::type;
     constexpr int NG = 32 / G;
-    constexpr int U = Unroll<G, V>::value;
+    constexpr int U = Unroll<G, V, R>::value;
     __shared__ unsigned long long s_stage[kWarpsPerBlock][kStage];
+    __shared__ uint32_t s_list[kWarpsPerBlock][32 * R];
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int q = lane % G, g = lane / G;
@@ -150,6 +190,8 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
     const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerBlock;
     const Vec* __restrict__ P = reinterpret_cast<const Vec*>(a.tp.pts);
     const uint32_t W = a.tp.stride / (F2 ? 2 : 4);
+    const uint32_t plo = a.part_lo, phi = a.part_hi;
+    uint32_t* list = s_list[wib];
 
     WarpStage<kStage> stage{s_stage[wib], 0};
     TestStats st;
@@ -160,22 +202,15 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
 #pragma unroll
         for (int vv = 0; vv < V; ++vv) {
             const uint32_t c = q + G * vv;
-            qv[vv] = (c < W) ? ldg_row(P + u * W + c) : vzero<Vec>();
+            qv[vv] = (c < W) ? (G == 32 ? ldg_stream(P + u * W + c) : ldg_row(P + u * W + c))
+                             : vzero<Vec>();
         }
         uint32_t limit = EXH ? (uint32_t)(a.n - 1 - u) : a.draws;
         const uint64_t key = EXH ? 0ull : vertex_key(a.seed_mixed, u);
 
         for (uint32_t i0 = 0; i0 < limit; i0 += 32 * R) {
             uint32_t pv[R];
-            unsigned vm[R];
-            if (EXH) {
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const uint32_t i = i0 + 32 * k + lane;
-                    pv[k] = (uint32_t)u + 1 + i;
-                    vm[k] = __ballot_sync(kFull, i < limit);
-                }
-            } else {
+            if (!EXH) {
                 uint32_t first_fire = 0xffffffffu;
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
@@ -192,43 +227,107 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
                     if (fm && first_fire == 0xffffffffu) first_fire = i0 + 32 * k + __ffs(fm) - 1;
                 }
                 if (first_fire != 0xffffffffu) limit = first_fire;  // irregular: cut here
-#pragma unroll
-                for (int k = 0; k < R; ++k) vm[k] = __ballot_sync(kFull, i0 + 32 * k + lane < limit);
             }
-
+            if (G < 32) {
+                // narrow rows: every lane's draw is one pair; group g takes the
+                // pairs of lanes g + NG*m straight from registers (no staging)
 #pragma unroll
-            for (int k = 0; k < R; ++k) {
-                if (vm[k] == 0) continue;
-#pragma unroll 1
-                for (int m0 = 0; m0 < G; m0 += U) {
-                    Vec rows[U][V];
-                    uint32_t pvv[U];
-                    bool ok[U];
+                for (int k = 0; k < R; ++k) {
+                    const uint32_t i = i0 + 32 * k + lane;
+                    const uint32_t p = EXH ? (uint32_t)u + 1 + i : pv[k];
+                    const unsigned vm = __ballot_sync(kFull, i < limit && p >= plo && p < phi);
+                    if (vm == 0) continue;
+                    constexpr int UG = G < 32 ? G : 1;
+                    Vec rows[UG][V];
+                    uint32_t pvv[UG];
+                    bool ok[UG];
 #pragma unroll
-                    for (int uu = 0; uu < U; ++uu) {
-                        const int src = (G == 1) ? lane : (g + NG * (m0 + uu));
-                        pvv[uu] = (G == 1) ? pv[k] : __shfl_sync(kFull, pv[k], src);
-                        ok[uu] = (vm[k] >> src) & 1u;
+                    for (int uu = 0; uu < UG; ++uu) {
+                        const int src = (G == 1) ? lane : (g + NG * uu);
+                        pvv[uu] = (G == 1) ? p : __shfl_sync(kFull, p, src);
+                        ok[uu] = (vm >> src) & 1u;
 #pragma unroll
                         for (int vv = 0; vv < V; ++vv) {
                             const uint32_t c = q + G * vv;
-                            rows[uu][vv] = (ok[uu] && c < W) ? ldg_row(P + (uint64_t)pvv[uu] * W + c)
-                                                             : vzero<Vec>();
+                            rows[uu][vv] = (ok[uu] && c < W)
+                                               ? ldg_row(P + (uint64_t)pvv[uu] * W + c)
+                                               : vzero<Vec>();
                         }
                     }
+                    // partial sums of the G pairs of this group, then a
+                    // transposed reduce-scatter (G-1 shuffles for G pairs instead
+                    // of log2(G) per pair): lane q ends with the total of pair q,
+                    // so decision, recheck and emission are one lane per pair.
+                    float ps[UG];
 #pragma unroll
-                    for (int uu = 0; uu < U; ++uu) {
+                    for (int uu = 0; uu < UG; ++uu) {
                         float s = 0.f;
 #pragma unroll
                         for (int vv = 0; vv < V; ++vv) s = diff2(qv[vv], rows[uu][vv], s);
+                        ps[uu] = s;
+                    }
 #pragma unroll
-                        for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-                        const bool acc = decide(s, ok[uu], leader, leader_lane, a.tp, u, pvv[uu], st);
-                        if (ok[uu] && leader) ++gpairs;
-                        stage.push(leader && acc, edge_key(u, pvv[uu], a.sink.nb), a.sink, lane);
+                    for (int o = UG / 2; o > 0; o >>= 1) {
+                        const bool hi = (q & o) != 0;
+#pragma unroll
+                        for (int j = 0; j < o; ++j) {
+                            const float mine = hi ? ps[j + o] : ps[j];
+                            const float other = hi ? ps[j] : ps[j + o];
+                            ps[j] = mine + __shfl_xor_sync(kFull, other, o);
+                        }
+                    }
+                    const int src = (G == 1) ? lane : (g + NG * q);  // my pair's draw lane
+                    const uint32_t pm = (G == 1) ? p : __shfl_sync(kFull, p, src);
+                    const bool okm = (vm >> src) & 1u;
+                    const bool acc = decide_lane(ps[0], okm, a.tp, u, pm, st);
+                    gpairs += okm ? 1u : 0u;
+                    stage.push(acc, edge_key(u, pm, a.sink.nb), a.sink, lane);
+                }
+                continue;
+            }
+            // ---- wide rows: compact the live pairs of this chunk ----
+            uint32_t nlive = 0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const uint32_t i = i0 + 32 * k + lane;
+                const uint32_t p = EXH ? (uint32_t)u + 1 + i : pv[k];
+                const bool live = i < limit && p >= plo && p < phi;
+                const unsigned m = __ballot_sync(kFull, live);
+                if (live) list[nlive + __popc(m & lanemask_lt())] = p;
+                nlive += __popc(m);
+            }
+            __syncwarp();
+            // ---- eps-test the live pairs, NG groups x U pairs per step ----
+#pragma unroll 1
+            for (uint32_t j0 = 0; j0 < nlive; j0 += NG * U) {
+                Vec rows[U][V];
+                uint32_t pvv[U];
+                bool ok[U];
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    const uint32_t j = j0 + NG * uu + g;
+                    ok[uu] = j < nlive;
+                    pvv[uu] = ok[uu] ? list[j] : 0u;
+#pragma unroll
+                    for (int vv = 0; vv < V; ++vv) {
+                        const uint32_t c = q + G * vv;
+                        rows[uu][vv] = (ok[uu] && c < W) ? ldg_row(P + (uint64_t)pvv[uu] * W + c)
+                                                         : vzero<Vec>();
                     }
                 }
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    float s = 0.f;
+#pragma unroll
+                    for (int vv = 0; vv < V; ++vv) s = diff2(qv[vv], rows[uu][vv], s);
+#pragma unroll
+                    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+                    const bool acc = decide(s, ok[uu], leader, leader_lane, a.tp, u, pvv[uu], st);
+                    if (ok[uu] && leader) ++gpairs;
+                    stage.push(leader && acc, edge_key(u, pvv[uu], a.sink.nb), a.sink, lane);
+                }
             }
+            __syncwarp();
         }
     }
     stage.flush(a.sink, lane);
