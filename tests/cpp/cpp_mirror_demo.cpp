@@ -1,0 +1,39 @@
+// Builds against the C++ mirror (sngb/sng.hpp) exactly as a reference user
+// would against sng/clusterer.hpp.  Exit codes: 0 ok, 2 wrong result,
+// 3 no GPU (std::runtime_error), 4 unexpected exception text.
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sngb/sng.hpp"
+
+int main() {
+    // argument errors come first, with the reference's messages
+    try {
+        sng::SngParams bad;
+        bad.eps = 0.0;
+        sng::sng_dbscan(sng::Dataset(std::vector<double>{0.0, 1.0}, 1), bad);
+        return 4;
+    } catch (const std::invalid_argument& e) {
+        if (std::string(e.what()) != "eps must be > 0") return 4;
+    }
+    // SPEC.md clusterer example: {0, 0.5, 10, 10.5}, eps=1, min_pts=1, rate=1
+    sng::Dataset ds(std::vector<double>{0.0, 0.5, 10.0, 10.5}, 1);
+    sng::SngParams p;
+    p.eps = 1.0;
+    p.min_pts = 1;
+    p.rate = 1.0;
+    sng::ClusterRunInfo info;
+    try {
+        sng::Clustering c = sng::sng_dbscan(ds, p, &info);
+        const bool ok = c.cluster_count == 2 && c.assignment == std::vector<int>{0, 0, 1, 1} &&
+                        info.edges == 2 && info.distance_evals == 12;
+        std::printf("clusters=%d edges=%zu evals=%llu\n", c.cluster_count, info.edges,
+                    (unsigned long long)info.distance_evals);
+        return ok ? 0 : 2;
+    } catch (const std::runtime_error& e) {
+        std::printf("runtime_error: %s\n", e.what());
+        return 3;
+    }
+}
