@@ -73,6 +73,30 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def load_gather_peaks(row_bytes: int, table_bytes: int):
+    """Measured random-row gather ceilings for this row size (tools/microbench.cu,
+    profiles/r01_microbench.jsonl): from L2 (table resident) and from HBM."""
+    path = os.path.join(ROOT, "profiles", "r01_microbench.jsonl")
+    try:
+        m = {}
+        for ln in open(path):
+            ln = ln.strip()
+            if ln.startswith("{"):
+                j = json.loads(ln)
+                m[j["bench"]] = j.get("GB_per_s")
+    except Exception:
+        return None, None
+    if row_bytes <= 16:
+        l2, hbm = m.get("gather_l2_row16B_80MB"), m.get("gather_hbm_row16B_2GB")
+    elif row_bytes <= 64:
+        l2, hbm = m.get("gather_l2_row64B_64MB"), None
+    elif row_bytes <= 128:
+        l2, hbm = m.get("gather_l2_row128B_64MB"), m.get("gather_hbm_row128B_2.5GB")
+    else:
+        l2, hbm = m.get("gather_l2_row3136B_55MB"), m.get("gather_hbm_row3136B_2GB")
+    return l2, hbm
+
+
 def load_traffic(workload: str):
     """dram bytes per gather launch from the committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -345,6 +369,18 @@ def main():
                 "bytes_per_pair": 4 * d, "pairs_per_launch": gather_pairs,
                 "kernel_ms": g_ms,
                 "kernel_share_of_step": (g_ms / ms_per_step) if ms_per_step else None}
+    # The gather's real ceiling is the memory level the partner rows come from:
+    # L2 when the (padded) row table, or one L2-blocked phase of it, is resident.
+    row_bytes = 16 if d == 3 else 4 * d
+    l2_peak, hbm_gather_peak = load_gather_peaks(row_bytes, n * row_bytes)
+    resident = n * row_bytes <= 100 * 2**20 or (d >= 256 and n * row_bytes <= 4 * 63 * 2**20)
+    roofline.update({
+        "effective_bound": "l2" if resident else "hbm (random rows)",
+        "l2_gather_peak": l2_peak, "hbm_gather_peak": hbm_gather_peak,
+        "frac_of_effective_peak": (achieved / (l2_peak if resident else (hbm_gather_peak or peak)))
+        if achieved and (l2_peak or hbm_gather_peak) else None,
+        "peaks_source": "tools/microbench.cu random-row gather of this row size "
+                        "(profiles/r01_microbench.jsonl)"})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

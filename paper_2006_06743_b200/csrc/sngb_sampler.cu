@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "sngb_device.cuh"
 #include "sngb_internal.cuh"
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(kFloydThreads) k_floyd(const SamplerArgs a) {
 }
 
 #include "sngb_floyd_fast.cuh"
+#include "sngb_floyd_bitmap.cuh"
 
 }  // namespace
 
@@ -256,8 +258,27 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
     if (rows == 0 || in.draws == 0) return cudaSuccess;
     SamplerArgs a = in;
     const uint32_t D = a.draws;
+    // small n: exact per-warp bitmap of the chosen values, draws in reference order
+    const uint64_t bm_words = (((a.n - 1) + 31) / 32 + 3) & ~3ull;
+    if (bm_words * 4 <= 4096 && !std::getenv("SNGB_FLOYD_NO_BITMAP")) {
+        a.col_words = (uint32_t)bm_words;
+        const int wpb = 8;
+        const size_t smem = (size_t)wpb * (bm_words * 4 + kBitmapStage * 8);
+        cudaError_t e = cudaFuncSetAttribute(k_floyd_bitmap,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_floyd_bitmap, wpb * 32, smem);
+        if (per_sm < 1) per_sm = 1;
+        const uint64_t want = (rows + wpb - 1) / wpb, cap = (uint64_t)num_sms * per_sm;
+        k_floyd_bitmap<<<(unsigned)(want < cap ? want : cap), wpb * 32, smem, s>>>(a);
+        note_launch(1);
+        return cudaGetLastError();
+    }
     uint32_t fb = 16;  // fast path: buckets of 4 u32 keys, load <= 0.625
-    while (10 * fb < 4 * D) fb <<= 1;
+    const char* lf_env = std::getenv("SNGB_FLOYD_SLOTS_PER_DRAW_X10");  // tuning knob
+    const uint32_t lf10 = lf_env ? (uint32_t)std::strtoul(lf_env, nullptr, 10) : 32u;
+    while (40 * fb < lf10 * D) fb <<= 1;  // 4 * buckets >= lf10/10 * draws
     const uint32_t cw = ((D + 31) / 32 + 3) & ~3u;
     const size_t fast_smem = floyd_fast_smem_bytes(fb, cw);
     uint32_t tb = 1;  // bits of a draw value t <= n - 2

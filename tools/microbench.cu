@@ -98,6 +98,19 @@ __global__ void k_gather_rows(const float4* __restrict__ tab, uint64_t rows, uin
     if (acc == 1234.5f) sink[0] = 1;
 }
 
+// Coalesced re-reads of an L2-resident buffer: `passes` sweeps, grid-stride.
+__global__ void k_stream(const float4* __restrict__ tab, uint64_t n4, int passes,
+                         unsigned long long* sink) {
+    float acc = 0.f;
+    for (int p = 0; p < passes; ++p)
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+             i += (uint64_t)gridDim.x * blockDim.x) {
+            const float4 v = __ldg(tab + i);
+            acc += v.x + v.y + v.z + v.w;
+        }
+    if (acc == 1234.5f) sink[0] = 1;
+}
+
 template <typename F>
 float time_ms(F&& f, int reps = 5) {
     cudaEvent_t a, b;
@@ -165,6 +178,7 @@ int main() {
         {"l2_row64B_64MB", 64ull << 20, 4},    {"l2_row128B_64MB", 64ull << 20, 8},
         {"hbm_row16B_2GB", 2ull << 30, 1},     {"hbm_row128B_2.5GB", 2560ull << 20, 8},
         {"hbm_row3136B_2GB", 2ull << 30, 196}, {"mixed_row3136B_220MB", 220ull << 20, 196},
+        {"l2_row3136B_55MB", 55ull << 20, 196}, {"l2_row3136B_32MB", 32ull << 20, 196},
     };
     float4* tab;
     CK(cudaMalloc(&tab, 2560ull << 20));
@@ -186,6 +200,19 @@ int main() {
         const double bytes = nrows * c.vec * 16;
         printf("{\"bench\": \"gather_%s\", \"rows_per_s\": %.4g, \"GB_per_s\": %.1f}\n", c.name,
                nrows / (ms * 1e-3), bytes / (ms * 1e-3) / 1e9);
+    }
+    // L2 streaming read: every warp reads a 32 MB L2-resident buffer with
+    // coalesced 16-byte loads (the L2 -> SM bandwidth ceiling)
+    {
+        const size_t bytes = 32ull << 20;
+        const uint64_t n4 = bytes / 16;
+        const int b = sms * 8;
+        auto launch = [&] { k_stream<<<b, 256>>>(tab, n4, 8, sink); };
+        const float ms = time_ms(launch);
+        const double total = (double)b * 256 * 8 * (n4 / ((double)b * 256)) * 16;
+        printf("{\"bench\": \"l2_stream_read_32MB\", \"GB_per_s\": %.1f}\n",
+               (double)n4 * 16 * 8 / (ms * 1e-3) / 1e9);
+        (void)total;
     }
     return 0;
 }
