@@ -32,128 +32,11 @@
 #include <type_traits>
 
 #include "sngb_device.cuh"
+#include "sngb_epstest.cuh"
 #include "sngb_internal.cuh"
 #include "sngb_rng.cuh"
 
 namespace sngb {
-
-__device__ __forceinline__ float4 ldg_row(const float4* p) { return __ldg(p); }
-__device__ __forceinline__ float2 ldg_row(const float2* p) { return __ldg(p); }
-// Query rows are read once per vertex (per phase): keep them out of L1 and
-// mark them evict-first in L2 so they do not displace partner rows.
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ float4 ldg_stream(const float4* p) {
-    float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(evict_first_policy()));
-    return r;
-}
-__device__ __forceinline__ float2 ldg_stream(const float2* p) {
-    float2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
-                 : "=f"(r.x), "=f"(r.y) : "l"(p), "l"(evict_first_policy()));
-    return r;
-}
-template <typename Vec>
-__device__ __forceinline__ Vec vzero();
-template <>
-__device__ __forceinline__ float4 vzero<float4>() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-template <>
-__device__ __forceinline__ float2 vzero<float2>() { return make_float2(0.f, 0.f); }
-
-__device__ __forceinline__ float diff2(float4 a, float4 b, float acc) {
-    float t = a.x - b.x;
-    acc = fmaf(t, t, acc);
-    t = a.y - b.y;
-    acc = fmaf(t, t, acc);
-    t = a.z - b.z;
-    acc = fmaf(t, t, acc);
-    t = a.w - b.w;
-    return fmaf(t, t, acc);
-}
-__device__ __forceinline__ float diff2(float2 a, float2 b, float acc) {
-    float t = a.x - b.x;
-    acc = fmaf(t, t, acc);
-    t = a.y - b.y;
-    return fmaf(t, t, acc);
-}
-
-// Canonical key of the undirected edge {u, v} (graph.cpp:183-186: min, max).
-__device__ __forceinline__ unsigned long long edge_key(uint64_t u, uint64_t v, uint32_t nb) {
-    const uint64_t a = u < v ? u : v, b = u < v ? v : u;
-    return (a << nb) | b;
-}
-
-// distance.hpp:75-83 verbatim in fp64: s += (a_k - b_k)^2 sequentially in k,
-// no contraction (explicit _rn intrinsics), then s <= eps*eps.
-__device__ __noinline__ bool exact_within(const TestParams tp, uint64_t u, uint64_t v) {
-    const float* a = tp.pts + u * tp.stride;
-    const float* b = tp.pts + v * tp.stride;
-    double s = 0.0;
-    for (uint32_t k = 0; k < tp.d; ++k) {
-        const double t = __dsub_rn((double)a[k], (double)b[k]);
-        s = __dadd_rn(s, __dmul_rn(t, t));
-    }
-    return s <= tp.eps2;
-}
-
-struct TestStats {
-    unsigned long long pairs = 0, band = 0, band6 = 0, flips = 0;
-};
-
-// Decide one pair per G-lane group.  `s` is group-uniform.  Returns the exact
-// reference decision to every lane.  Must be called by all 32 lanes.
-__device__ __forceinline__ bool decide(float s, bool ok, bool leader, int leader_lane,
-                                       const TestParams& tp, uint64_t u, uint64_t v,
-                                       TestStats& st) {
-    const bool need = ok && !(s < tp.lo_thr) && !(s > tp.hi_thr);
-    bool acc = ok && (s < tp.lo_thr);
-    const unsigned nm = __ballot_sync(kFull, need);
-    if (nm) {
-        bool ex = false;
-        if (need && leader) {
-            ex = exact_within(tp, u, v);
-            st.band++;
-            if (fabsf(s - tp.eps2f) <= 1e-6f * tp.eps2f) st.band6++;
-            if ((s <= tp.eps2f) != ex) st.flips++;
-        }
-        ex = __shfl_sync(kFull, ex, leader_lane);
-        if (need) acc = ex;
-    }
-    return acc;
-}
-
-// Same decision when every lane owns one pair (no group broadcast needed).
-__device__ __forceinline__ bool decide_lane(float s, bool ok, const TestParams& tp, uint64_t u,
-                                            uint64_t v, TestStats& st) {
-    const bool need = ok && !(s < tp.lo_thr) && !(s > tp.hi_thr);
-    bool acc = ok && (s < tp.lo_thr);
-    if (need) {
-        acc = exact_within(tp, u, v);
-        st.band++;
-        if (fabsf(s - tp.eps2f) <= 1e-6f * tp.eps2f) st.band6++;
-        if ((s <= tp.eps2f) != acc) st.flips++;
-    }
-    return acc;
-}
-
-__device__ __forceinline__ void flush_stats(const TestStats& st, unsigned long long gpairs,
-                                            unsigned long long* counters, int lane) {
-    const unsigned long long p = warp_sum(st.pairs), b = warp_sum(st.band),
-                             b6 = warp_sum(st.band6), f = warp_sum(st.flips),
-                             gp = warp_sum(gpairs);
-    if (lane == 0) {
-        if (p) atomicAdd(&counters[C_PAIRS], p);
-        if (b) atomicAdd(&counters[C_BAND], b);
-        if (b6) atomicAdd(&counters[C_BAND6], b6);
-        if (f) atomicAdd(&counters[C_FLIPS], f);
-        if (gp) atomicAdd(&counters[C_GATHER_PAIRS], gp);
-    }
-}
 
 // Pairs per group issued back to back (loads in flight per lane = U * V).
 // G < 32: a group takes R*G pairs of each 32*R-draw chunk in one go.
