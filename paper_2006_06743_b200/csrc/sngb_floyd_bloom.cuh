@@ -1,0 +1,275 @@
+// sngb_floyd_bloom.cuh -- k_floyd_bloom, Floyd bookkeeping for large n and
+// draws <= 4096 (cfg2-cfg5).  Included by sngb_sampler.cu.
+//
+// k_floyd_fast claims every draw value in a CAS-built key set; profiling
+// showed it issue/latency bound on divergent claim loops (CAS races, probes)
+// and barrier waits.  For large n a vertex's draws are almost all distinct
+// (about D^2/2n duplicates), so exact membership is only needed for the few
+// draws that can collide.  Per vertex (one block, draws in registers):
+//
+//   P1  every draw ORs bit h(t) into a 2^B-bit filter (atomicOr never fails,
+//       no loops); a draw that finds its bit already set also marks it in a
+//       second "shared bit" filter.  Draws with t in [base, base + i) (may
+//       equal an earlier replacement j_k) go to a small chain list.
+//   P2  every draw whose bit is shared (true duplicates + ~D/2^B false
+//       positives) appends (t, i) to a small group list.
+//   P3  warp 0: a group-list draw collides iff another entry has the same t and
+//       a smaller index (first occurrence = minimum index); chain candidates
+//       are then resolved in index order against the collided bitmap.  Every
+//       collided draw emits its replacement j_i as an extra.
+//
+// Filters and lists are double-buffered by vertex parity and each thread
+// clears the filter words its previous-vertex draws touched, so there are two
+// barriers per vertex and no table clears.  A list overflow or a Lemire reject
+// pre-condition replays the vertex exactly and sequentially.
+#pragma once
+
+constexpr int kBloomThreads = 256;
+constexpr int kGroupCap = 512;
+constexpr int kHashLog2 = 10;
+constexpr int kHashSlots = 1 << kHashLog2;
+constexpr int kChainCap = 256;
+
+struct BloomGeom {
+    uint32_t bits_log2;   // B
+    uint32_t words;       // 2^B / 32
+    uint32_t col_words;   // draws-bit bitmap words
+};
+
+inline BloomGeom bloom_geometry(uint32_t draws) {
+    uint32_t lg = 0;
+    while ((1u << lg) < draws) ++lg;
+    BloomGeom g;
+    g.bits_log2 = lg + 4 < 12 ? 12 : lg + 4;  // false-positive rate ~ draws / 2^B <= 1/16
+    if (g.bits_log2 > 17) g.bits_log2 = 17;
+    g.words = (1u << g.bits_log2) / 32;
+    g.col_words = ((draws + 31) / 32 + 3) & ~3u;
+    return g;
+}
+
+inline size_t bloom_smem_bytes(const BloomGeom& g) {
+    return 4ull * g.words * 4                    // filter + shared-bit filter, x2 parity
+           + (size_t)g.col_words * 4             // collided bitmap
+           + 2ull * kGroupCap * 8                // group lists (t << 32 | i), x2 parity
+           + 2ull * kChainCap * 4                // chain lists, x2 parity
+           + (size_t)kHashSlots * 8;             // warp 0's first-occurrence hash
+}
+
+// Exact sequential replay (graph.cpp:163-174) with a u32 open-addressing set
+// in `tab` (cap slots, power of two); every partner becomes an extra.
+__device__ void bloom_replay(uint64_t key, uint64_t u, uint64_t n, uint32_t base, uint32_t* tab,
+                             uint32_t cap, const EdgeSink& xs) {
+    for (uint32_t s = 0; s < cap; ++s) tab[s] = kEmpty;
+    const uint32_t mask = cap - 1;
+    auto insert = [&](uint32_t t) -> bool {
+        uint32_t h = (t * 0x9E3779B1u) & mask;
+        for (;;) {
+            if (tab[h] == kEmpty) {
+                tab[h] = t;
+                return true;
+            }
+            if (tab[h] == t) return false;
+            h = (h + 1) & mask;
+        }
+    };
+    SeqStream st{key, 0};
+    for (uint64_t jj = base; jj < n - 1; ++jj) {
+        const uint32_t t = (uint32_t)st.next_below(jj + 1);
+        uint32_t e = t;
+        if (!insert(t)) {
+            insert((uint32_t)jj);
+            e = (uint32_t)jj;
+        }
+        const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
+        if (s2 < xs.capacity)
+            xs.keys[s2] = ((unsigned long long)u << 32) | (e + (e >= (uint32_t)u ? 1u : 0u));
+    }
+}
+
+template <int MAXR>
+__global__ void __launch_bounds__(kBloomThreads) k_floyd_bloom(const SamplerArgs a) {
+    constexpr int kT = kBloomThreads;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t WB = a.hash_mask;  // filter words (2^B / 32)
+    const uint32_t shift = 32 - a.key_bits;
+    const uint32_t W = a.col_words;
+    uint32_t* filt = reinterpret_cast<uint32_t*>(smem);          // [2][WB]
+    uint32_t* shared_bits = filt + 2 * WB;                         // [2][WB]
+    uint32_t* colbits = shared_bits + 2 * WB;                      // [W]
+    unsigned long long* glist =
+        reinterpret_cast<unsigned long long*>(colbits + W);       // [2][kGroupCap]
+    uint32_t* clist = reinterpret_cast<uint32_t*>(glist + 2 * kGroupCap);  // [2][kChainCap]
+    unsigned long long* htab =
+        reinterpret_cast<unsigned long long*>(clist + 2 * kChainCap);  // [kHashSlots]
+    __shared__ uint32_t s_cnt[2][2];  // [parity][group, chain]
+
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
+    const uint32_t D = a.draws, base = a.base;
+    unsigned long long ncol = 0, nrep = 0;
+    uint32_t prevw[MAXR];  // filter words touched by the previous vertex (parity 1-p)
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r) prevw[r] = 0xffffffffu;
+
+    for (uint32_t s = tid; s < 4 * WB + W; s += kT) filt[s] = 0;
+    for (uint32_t s = tid; s < kHashSlots; s += kT) htab[s] = ~0ull;
+    if (tid < 4) (&s_cnt[0][0])[tid] = 0;
+    __syncthreads();
+
+    auto emit = [&](uint64_t u, uint32_t e) {  // extra pair (u, partner of value e)
+        const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
+        if (s2 < xs.capacity)
+            xs.keys[s2] = ((unsigned long long)u << 32) | (e + (e >= (uint32_t)u ? 1u : 0u));
+    };
+
+    uint32_t par = 0;
+    for (uint64_t u = a.row_begin + blockIdx.x; u < a.row_end; u += gridDim.x) {
+        par ^= 1u;
+        uint32_t* f = filt + par * WB;
+        uint32_t* sb = shared_bits + par * WB;
+        uint32_t* fo = filt + (par ^ 1u) * WB;
+        uint32_t* sbo = shared_bits + (par ^ 1u) * WB;
+        unsigned long long* gl = glist + par * kGroupCap;
+        uint32_t* cl = clist + par * kChainCap;
+        uint32_t* cnt = s_cnt[par];
+        const uint64_t key = vertex_key(a.seed_mixed, u);
+
+        // ---- P1: draws, filter bits, chain candidates; clear last vertex's words ----
+        uint32_t tr[MAXR];
+        bool fired = false;
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) {
+            const uint32_t i = tid + kT * r;
+            bool fi = false;
+            tr[r] = (i < D) ? lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fi) : 0u;
+            fired |= (i < D) && (fi || test_fire(a.force_mod, u, i, D));
+        }
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) {
+            if (prevw[r] != 0xffffffffu) {
+                fo[prevw[r]] = 0;
+                sbo[prevw[r]] = 0;
+            }
+            const uint32_t i = tid + kT * r;
+            prevw[r] = 0xffffffffu;
+            if (i < D) {
+                const uint32_t t = tr[r];
+                const uint32_t h = (t * 0x9E3779B1u) >> shift;
+                const uint32_t w = h >> 5, bit = 1u << (h & 31);
+                prevw[r] = w;
+                if (atomicOr(&f[w], bit) & bit) atomicOr(&sb[w], bit);
+                if (t >= base && t - base < i) {
+                    const uint32_t p = atomicAdd(&cnt[1], 1u);
+                    if (p < kChainCap) cl[p] = i;
+                }
+            }
+        }
+        // exact sequential replay of one vertex (rare); the filter memory
+        // (4 * WB >= 4 * draws words) serves as its hash set, then is re-zeroed
+        auto replay = [&]() {
+            __syncthreads();
+            if (tid == 0) {
+                ++nrep;
+                bloom_replay(key, u, a.n, base, filt, 4 * WB, xs);
+                cnt[0] = cnt[1] = 0;
+            }
+            __syncthreads();
+            for (uint32_t s = tid; s < 4 * WB; s += kT) filt[s] = 0;
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r) prevw[r] = 0xffffffffu;
+            __syncthreads();
+        };
+        if (__syncthreads_or(fired)) {  // (block-uniform)
+            replay();
+            continue;
+        }
+        // ---- P2: draws whose filter bit is shared join the group list ----
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) {
+            const uint32_t i = tid + kT * r;
+            if (i < D) {
+                const uint32_t h = (tr[r] * 0x9E3779B1u) >> shift;
+                if ((sb[h >> 5] >> (h & 31)) & 1u) {
+                    const uint32_t p = atomicAdd(&cnt[0], 1u);
+                    if (p < kGroupCap) gl[p] = ((unsigned long long)tr[r] << 32) | i;
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t ng = cnt[0], nc = cnt[1];
+        if (ng == 0 && nc == 0) continue;  // (block-uniform)
+        if (ng > kGroupCap || nc > kChainCap) {  // list overflow: exact replay
+            replay();
+            continue;
+        }
+        // ---- P3 (warp 0): duplicates, then chains in index order ----
+        if (wib == 0) {
+            // first occurrence per value: (t, min index) in a small warp-private
+            // hash (the list holds ~D^2/2^B entries; kGroupCap <= kHashSlots/2)
+            for (uint32_t p = lane; p < ng; p += 32) {
+                const unsigned long long e = gl[p];
+                const uint32_t t = (uint32_t)(e >> 32);
+                uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
+                for (;;) {
+                    const unsigned long long old = atomicCAS(&htab[h], ~0ull, e);
+                    if (old == ~0ull) break;
+                    if ((uint32_t)(old >> 32) == t) {
+                        atomicMin(&htab[h], e);
+                        break;
+                    }
+                    h = (h + 1) & (kHashSlots - 1);
+                }
+            }
+            __syncwarp();
+            for (uint32_t p = lane; p < ng; p += 32) {
+                const unsigned long long e = gl[p];
+                const uint32_t t = (uint32_t)(e >> 32), i = (uint32_t)e;
+                uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
+                while ((uint32_t)(htab[h] >> 32) != t) h = (h + 1) & (kHashSlots - 1);
+                if ((uint32_t)htab[h] != i) {  // an earlier draw has the same value
+                    atomicOr(&colbits[i >> 5], 1u << (i & 31));
+                    emit(u, base + i);
+                    ++ncol;
+                }
+            }
+            __syncwarp();  // all lookups done: reset the whole (8 KB) hash
+            for (uint32_t s2 = lane; s2 < kHashSlots; s2 += 32) htab[s2] = ~0ull;
+            __syncwarp();
+            if (lane == 0 && nc) {
+                for (uint32_t x = 1; x < nc; ++x) {  // insertion sort (tiny list)
+                    const uint32_t v = cl[x];
+                    uint32_t y = x;
+                    while (y > 0 && cl[y - 1] > v) {
+                        cl[y] = cl[y - 1];
+                        --y;
+                    }
+                    cl[y] = v;
+                }
+                for (uint32_t x = 0; x < nc; ++x) {
+                    const uint32_t i = cl[x];
+                    if ((colbits[i >> 5] >> (i & 31)) & 1u) continue;  // already collided
+                    bool fi;
+                    const uint32_t k =
+                        lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fi) - base;
+                    if ((colbits[k >> 5] >> (k & 31)) & 1u) {
+                        colbits[i >> 5] |= 1u << (i & 31);
+                        emit(u, base + i);
+                        ++ncol;
+                    }
+                }
+            }
+            __syncwarp();
+            for (uint32_t p = lane; p < ng + nc; p += 32) {  // clear the touched words
+                const uint32_t i = p < ng ? (uint32_t)gl[p] : cl[p - ng];
+                colbits[i >> 5] = 0;
+            }
+            __syncwarp();
+            if (lane == 0) cnt[0] = cnt[1] = 0;
+        }
+    }
+    ncol = warp_sum(ncol);
+    if (lane == 0) {
+        if (ncol) atomicAdd(&a.counters[C_COLLISIONS], ncol);
+        if (nrep && wib == 0) atomicAdd(&a.counters[C_IRREGULAR], nrep);
+    }
+}

@@ -25,6 +25,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <string>
 
 #include "sngb_device.cuh"
 #include "sngb_internal.cuh"
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(kFloydThreads) k_floyd(const SamplerArgs a) {
 
 #include "sngb_floyd_fast.cuh"
 #include "sngb_floyd_bitmap.cuh"
+#include "sngb_floyd_bloom.cuh"
 
 }  // namespace
 
@@ -272,6 +274,28 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
         if (per_sm < 1) per_sm = 1;
         const uint64_t want = (rows + wpb - 1) / wpb, cap = (uint64_t)num_sms * per_sm;
         k_floyd_bitmap<<<(unsigned)(want < cap ? want : cap), wpb * 32, smem, s>>>(a);
+        note_launch(1);
+        return cudaGetLastError();
+    }
+    // large n, draws <= 4096: filter + exact resolution of the few shared bits
+    const char* fk = std::getenv("SNGB_FLOYD_KERNEL");
+    if (D <= 4096 && a.n - 2 < 0xffffffffull && !(fk && std::string(fk) == "fast")) {
+        const BloomGeom bg = bloom_geometry(D);
+        a.hash_mask = bg.words;
+        a.key_bits = bg.bits_log2;
+        a.col_words = bg.col_words;
+        const size_t smem = bloom_smem_bytes(bg);
+        auto k = D <= 1024   ? k_floyd_bloom<4>
+                 : D <= 2048 ? k_floyd_bloom<8>
+                 : D <= 3072 ? k_floyd_bloom<12>
+                             : k_floyd_bloom<16>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBloomThreads, smem);
+        if (per_sm < 1) per_sm = 1;
+        const uint64_t cap = (uint64_t)num_sms * per_sm;
+        k<<<(unsigned)(rows < cap ? rows : cap), kBloomThreads, smem, s>>>(a);
         note_launch(1);
         return cudaGetLastError();
     }
