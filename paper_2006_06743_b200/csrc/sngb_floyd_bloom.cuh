@@ -86,8 +86,33 @@ __device__ void bloom_replay(uint64_t key, uint64_t u, uint64_t n, uint32_t base
     }
 }
 
+// Named barriers (bar.sync/arrive with a thread count): the 8 worker warps
+// synchronise among themselves and hand each vertex's lists to a resolver warp
+// producer/consumer style, so the resolver's work never stalls the workers.
+__device__ __forceinline__ void bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ bool bar_or(int id, int count, bool pred) {
+    unsigned r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+        "bar.red.or.pred q, %2, %3, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+        : "=r"(r)
+        : "r"((unsigned)pred), "r"(id), "r"(count)
+        : "memory");
+    return r != 0;
+}
+
+constexpr int kBarWorkers = 1;  // 256 worker threads
+constexpr int kBarReady = 2;    // + parity: lists of a vertex are complete (288)
+constexpr int kBarFree = 4;     // + parity: resolver is done with that parity (288)
+constexpr int kBloomBlock = kBloomThreads + 32;
+
 template <int MAXR>
-__global__ void __launch_bounds__(kBloomThreads) k_floyd_bloom(const SamplerArgs a) {
+__global__ void __launch_bounds__(kBloomBlock) k_floyd_bloom(const SamplerArgs a) {
     constexpr int kT = kBloomThreads;
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t WB = a.hash_mask;  // filter words (2^B / 32)
@@ -104,15 +129,13 @@ __global__ void __launch_bounds__(kBloomThreads) k_floyd_bloom(const SamplerArgs
     __shared__ uint32_t s_cnt[2][2];  // [parity][group, chain]
 
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    const bool resolver = tid >= kT;
     const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
     const uint32_t D = a.draws, base = a.base;
     unsigned long long ncol = 0, nrep = 0;
-    uint32_t prevw[MAXR];  // filter words touched by the previous vertex (parity 1-p)
-#pragma unroll
-    for (int r = 0; r < MAXR; ++r) prevw[r] = 0xffffffffu;
 
-    for (uint32_t s = tid; s < 4 * WB + W; s += kT) filt[s] = 0;
-    for (uint32_t s = tid; s < kHashSlots; s += kT) htab[s] = ~0ull;
+    for (uint32_t s = tid; s < 4 * WB + W; s += kBloomBlock) filt[s] = 0;
+    for (uint32_t s = tid; s < kHashSlots; s += kBloomBlock) htab[s] = ~0ull;
     if (tid < 4) (&s_cnt[0][0])[tid] = 0;
     __syncthreads();
 
@@ -122,154 +145,172 @@ __global__ void __launch_bounds__(kBloomThreads) k_floyd_bloom(const SamplerArgs
             xs.keys[s2] = ((unsigned long long)u << 32) | (e + (e >= (uint32_t)u ? 1u : 0u));
     };
 
-    uint32_t par = 0;
-    for (uint64_t u = a.row_begin + blockIdx.x; u < a.row_end; u += gridDim.x) {
-        par ^= 1u;
-        uint32_t* f = filt + par * WB;
-        uint32_t* sb = shared_bits + par * WB;
-        uint32_t* fo = filt + (par ^ 1u) * WB;
-        uint32_t* sbo = shared_bits + (par ^ 1u) * WB;
-        unsigned long long* gl = glist + par * kGroupCap;
-        uint32_t* cl = clist + par * kChainCap;
-        uint32_t* cnt = s_cnt[par];
-        const uint64_t key = vertex_key(a.seed_mixed, u);
-
-        // ---- P1: draws, filter bits, chain candidates; clear last vertex's words ----
-        uint32_t tr[MAXR];
-        bool fired = false;
-#pragma unroll
-        for (int r = 0; r < MAXR; ++r) {
-            const uint32_t i = tid + kT * r;
-            bool fi = false;
-            tr[r] = (i < D) ? lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fi) : 0u;
-            fired |= (i < D) && (fi || test_fire(a.force_mod, u, i, D));
-        }
-#pragma unroll
-        for (int r = 0; r < MAXR; ++r) {
-            if (prevw[r] != 0xffffffffu) {
-                fo[prevw[r]] = 0;
-                sbo[prevw[r]] = 0;
-            }
-            const uint32_t i = tid + kT * r;
-            prevw[r] = 0xffffffffu;
-            if (i < D) {
-                const uint32_t t = tr[r];
-                const uint32_t h = (t * 0x9E3779B1u) >> shift;
-                const uint32_t w = h >> 5, bit = 1u << (h & 31);
-                prevw[r] = w;
-                if (atomicOr(&f[w], bit) & bit) atomicOr(&sb[w], bit);
-                if (t >= base && t - base < i) {
-                    const uint32_t p = atomicAdd(&cnt[1], 1u);
-                    if (p < kChainCap) cl[p] = i;
-                }
-            }
-        }
-        // exact sequential replay of one vertex (rare); the filter memory
-        // (4 * WB >= 4 * draws words) serves as its hash set, then is re-zeroed
-        auto replay = [&]() {
-            __syncthreads();
-            if (tid == 0) {
-                ++nrep;
-                bloom_replay(key, u, a.n, base, filt, 4 * WB, xs);
-                cnt[0] = cnt[1] = 0;
-            }
-            __syncthreads();
-            for (uint32_t s = tid; s < 4 * WB; s += kT) filt[s] = 0;
-#pragma unroll
-            for (int r = 0; r < MAXR; ++r) prevw[r] = 0xffffffffu;
-            __syncthreads();
-        };
-        if (__syncthreads_or(fired)) {  // (block-uniform)
-            replay();
-            continue;
-        }
-        // ---- P2: draws whose filter bit is shared join the group list ----
-#pragma unroll
-        for (int r = 0; r < MAXR; ++r) {
-            const uint32_t i = tid + kT * r;
-            if (i < D) {
-                const uint32_t h = (tr[r] * 0x9E3779B1u) >> shift;
-                if ((sb[h >> 5] >> (h & 31)) & 1u) {
-                    const uint32_t p = atomicAdd(&cnt[0], 1u);
-                    if (p < kGroupCap) gl[p] = ((unsigned long long)tr[r] << 32) | i;
-                }
-            }
-        }
-        __syncthreads();
-        const uint32_t ng = cnt[0], nc = cnt[1];
-        if (ng == 0 && nc == 0) continue;  // (block-uniform)
-        if (ng > kGroupCap || nc > kChainCap) {  // list overflow: exact replay
-            replay();
-            continue;
-        }
-        // ---- P3 (warp 0): duplicates, then chains in index order ----
-        if (wib == 0) {
-            // first occurrence per value: (t, min index) in a small warp-private
-            // hash (the list holds ~D^2/2^B entries; kGroupCap <= kHashSlots/2)
-            for (uint32_t p = lane; p < ng; p += 32) {
-                const unsigned long long e = gl[p];
-                const uint32_t t = (uint32_t)(e >> 32);
-                uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
-                for (;;) {
-                    const unsigned long long old = atomicCAS(&htab[h], ~0ull, e);
-                    if (old == ~0ull) break;
-                    if ((uint32_t)(old >> 32) == t) {
-                        atomicMin(&htab[h], e);
-                        break;
+    if (resolver) {
+        // ---- P3 (resolver warp), one vertex behind the workers ----
+        uint32_t par = 0;
+        for (uint64_t u = a.row_begin + blockIdx.x; u < a.row_end; u += gridDim.x) {
+            par ^= 1u;
+            bar_sync(kBarReady + par, kBloomBlock);
+            unsigned long long* gl = glist + par * kGroupCap;
+            uint32_t* cl = clist + par * kChainCap;
+            uint32_t* cnt = s_cnt[par];
+            const uint32_t ng = cnt[0], nc = cnt[1];
+            if (ng || nc) {
+                // first occurrence per value: (t, min index) in a small hash
+                for (uint32_t p = lane; p < ng; p += 32) {
+                    const unsigned long long e = gl[p];
+                    const uint32_t t = (uint32_t)(e >> 32);
+                    uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
+                    for (;;) {
+                        const unsigned long long old = atomicCAS(&htab[h], ~0ull, e);
+                        if (old == ~0ull) break;
+                        if ((uint32_t)(old >> 32) == t) {
+                            atomicMin(&htab[h], e);
+                            break;
+                        }
+                        h = (h + 1) & (kHashSlots - 1);
                     }
-                    h = (h + 1) & (kHashSlots - 1);
                 }
-            }
-            __syncwarp();
-            for (uint32_t p = lane; p < ng; p += 32) {
-                const unsigned long long e = gl[p];
-                const uint32_t t = (uint32_t)(e >> 32), i = (uint32_t)e;
-                uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
-                while ((uint32_t)(htab[h] >> 32) != t) h = (h + 1) & (kHashSlots - 1);
-                if ((uint32_t)htab[h] != i) {  // an earlier draw has the same value
-                    atomicOr(&colbits[i >> 5], 1u << (i & 31));
-                    emit(u, base + i);
-                    ++ncol;
-                }
-            }
-            __syncwarp();  // all lookups done: reset the whole (8 KB) hash
-            for (uint32_t s2 = lane; s2 < kHashSlots; s2 += 32) htab[s2] = ~0ull;
-            __syncwarp();
-            if (lane == 0 && nc) {
-                for (uint32_t x = 1; x < nc; ++x) {  // insertion sort (tiny list)
-                    const uint32_t v = cl[x];
-                    uint32_t y = x;
-                    while (y > 0 && cl[y - 1] > v) {
-                        cl[y] = cl[y - 1];
-                        --y;
-                    }
-                    cl[y] = v;
-                }
-                for (uint32_t x = 0; x < nc; ++x) {
-                    const uint32_t i = cl[x];
-                    if ((colbits[i >> 5] >> (i & 31)) & 1u) continue;  // already collided
-                    bool fi;
-                    const uint32_t k =
-                        lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fi) - base;
-                    if ((colbits[k >> 5] >> (k & 31)) & 1u) {
-                        colbits[i >> 5] |= 1u << (i & 31);
+                __syncwarp();
+                for (uint32_t p = lane; p < ng; p += 32) {
+                    const unsigned long long e = gl[p];
+                    const uint32_t t = (uint32_t)(e >> 32), i = (uint32_t)e;
+                    uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
+                    while ((uint32_t)(htab[h] >> 32) != t) h = (h + 1) & (kHashSlots - 1);
+                    if ((uint32_t)htab[h] != i) {  // an earlier draw has the same value
+                        atomicOr(&colbits[i >> 5], 1u << (i & 31));
                         emit(u, base + i);
                         ++ncol;
                     }
                 }
+                __syncwarp();  // all lookups done: reset the whole (8 KB) hash
+                for (uint32_t s2 = lane; s2 < kHashSlots; s2 += 32) htab[s2] = ~0ull;
+                __syncwarp();
+                if (lane == 0 && nc) {
+                    const uint64_t key = vertex_key(a.seed_mixed, u);
+                    for (uint32_t x = 1; x < nc; ++x) {  // insertion sort (tiny list)
+                        const uint32_t v = cl[x];
+                        uint32_t y = x;
+                        while (y > 0 && cl[y - 1] > v) {
+                            cl[y] = cl[y - 1];
+                            --y;
+                        }
+                        cl[y] = v;
+                    }
+                    for (uint32_t x = 0; x < nc; ++x) {
+                        const uint32_t i = cl[x];
+                        if ((colbits[i >> 5] >> (i & 31)) & 1u) continue;  // already collided
+                        bool fi;
+                        const uint32_t k =
+                            lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fi) - base;
+                        if ((colbits[k >> 5] >> (k & 31)) & 1u) {
+                            colbits[i >> 5] |= 1u << (i & 31);
+                            emit(u, base + i);
+                            ++ncol;
+                        }
+                    }
+                }
+                __syncwarp();
+                for (uint32_t p = lane; p < ng + nc; p += 32) {  // clear the touched words
+                    const uint32_t i = p < ng ? (uint32_t)gl[p] : cl[p - ng];
+                    colbits[i >> 5] = 0;
+                }
+                __syncwarp();
+                if (lane == 0) cnt[0] = cnt[1] = 0;
             }
             __syncwarp();
-            for (uint32_t p = lane; p < ng + nc; p += 32) {  // clear the touched words
-                const uint32_t i = p < ng ? (uint32_t)gl[p] : cl[p - ng];
-                colbits[i >> 5] = 0;
+            bar_arrive(kBarFree + par, kBloomBlock);
+        }
+    } else {
+        // ---- workers: P1 filter bits + chain candidates, P2 group list ----
+        uint32_t prevw[MAXR];  // filter words touched by the previous vertex (parity 1-p)
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) prevw[r] = 0xffffffffu;
+        uint32_t par = 0, vcount = 0;
+        for (uint64_t u = a.row_begin + blockIdx.x; u < a.row_end; u += gridDim.x) {
+            par ^= 1u;
+            if (++vcount > 2) bar_sync(kBarFree + par, kBloomBlock);  // parity par reusable
+            uint32_t* f = filt + par * WB;
+            uint32_t* sb = shared_bits + par * WB;
+            uint32_t* fo = filt + (par ^ 1u) * WB;
+            uint32_t* sbo = shared_bits + (par ^ 1u) * WB;
+            unsigned long long* gl = glist + par * kGroupCap;
+            uint32_t* cl = clist + par * kChainCap;
+            uint32_t* cnt = s_cnt[par];
+            const uint64_t key = vertex_key(a.seed_mixed, u);
+
+            uint32_t tr[MAXR];
+            bool fired = false;
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r) {
+                const uint32_t i = tid + kT * r;
+                bool fi = false;
+                tr[r] = (i < D) ? lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fi) : 0u;
+                fired |= (i < D) && (fi || test_fire(a.force_mod, u, i, D));
             }
-            __syncwarp();
-            if (lane == 0) cnt[0] = cnt[1] = 0;
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r) {
+                if (prevw[r] != 0xffffffffu) {
+                    fo[prevw[r]] = 0;
+                    sbo[prevw[r]] = 0;
+                }
+                const uint32_t i = tid + kT * r;
+                prevw[r] = 0xffffffffu;
+                if (i < D) {
+                    const uint32_t t = tr[r];
+                    const uint32_t h = (t * 0x9E3779B1u) >> shift;
+                    const uint32_t w = h >> 5, bit = 1u << (h & 31);
+                    prevw[r] = w;
+                    if (atomicOr(&f[w], bit) & bit) atomicOr(&sb[w], bit);
+                    if (t >= base && t - base < i) {
+                        const uint32_t p = atomicAdd(&cnt[1], 1u);
+                        if (p < kChainCap) cl[p] = i;
+                    }
+                }
+            }
+            // exact sequential replay of one vertex (rare); the filter memory
+            // (4 * WB >= 4 * draws words) serves as its hash set, then is re-zeroed;
+            // the resolver then sees empty lists for this vertex
+            auto replay = [&]() {
+                bar_sync(kBarWorkers, kT);
+                if (tid == 0) {
+                    ++nrep;
+                    bloom_replay(key, u, a.n, base, filt, 4 * WB, xs);
+                    cnt[0] = cnt[1] = 0;
+                }
+                bar_sync(kBarWorkers, kT);
+                for (uint32_t s = tid; s < 4 * WB; s += kT) filt[s] = 0;
+#pragma unroll
+                for (int r = 0; r < MAXR; ++r) prevw[r] = 0xffffffffu;
+                bar_sync(kBarWorkers, kT);
+                bar_arrive(kBarReady + par, kBloomBlock);
+            };
+            if (bar_or(kBarWorkers, kT, fired)) {
+                replay();
+                continue;
+            }
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r) {
+                const uint32_t i = tid + kT * r;
+                if (i < D) {
+                    const uint32_t h = (tr[r] * 0x9E3779B1u) >> shift;
+                    if ((sb[h >> 5] >> (h & 31)) & 1u) {
+                        const uint32_t p = atomicAdd(&cnt[0], 1u);
+                        if (p < kGroupCap) gl[p] = ((unsigned long long)tr[r] << 32) | i;
+                    }
+                }
+            }
+            bar_sync(kBarWorkers, kT);
+            if (cnt[0] > kGroupCap || cnt[1] > kChainCap) {  // list overflow: exact replay
+                replay();
+                continue;
+            }
+            bar_arrive(kBarReady + par, kBloomBlock);
         }
     }
     ncol = warp_sum(ncol);
     if (lane == 0) {
         if (ncol) atomicAdd(&a.counters[C_COLLISIONS], ncol);
-        if (nrep && wib == 0) atomicAdd(&a.counters[C_IRREGULAR], nrep);
+        if (nrep) atomicAdd(&a.counters[C_IRREGULAR], nrep);
     }
 }

@@ -292,10 +292,10 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBloomThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBloomBlock, smem);
         if (per_sm < 1) per_sm = 1;
         const uint64_t cap = (uint64_t)num_sms * per_sm;
-        k<<<(unsigned)(rows < cap ? rows : cap), kBloomThreads, smem, s>>>(a);
+        k<<<(unsigned)(rows < cap ? rows : cap), kBloomBlock, smem, s>>>(a);
         note_launch(1);
         return cudaGetLastError();
     }
