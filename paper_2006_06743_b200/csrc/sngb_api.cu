@@ -82,11 +82,13 @@ struct DevCtx {
     int num_sms = 148;
     uint64_t l2_bytes = 126ull << 20;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;          // sampler runs here, concurrently with the gather
+    cudaEvent_t fork = nullptr, join = nullptr;
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
         flags, rank, temp, labels, roles;
     unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
-    cudaEvent_t ev[10] = {};
+    cudaEvent_t ev[12] = {};
     uint64_t edge_hint = 0;  // last needed edge capacity for this context
 
     void release() {
@@ -132,6 +134,9 @@ DevCtx& get_ctx(int dev) {
         CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
         c->l2_bytes = (uint64_t)l2;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         CK(cudaMallocHost(&c->h_counters, C_COUNT * sizeof(unsigned long long)));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
         g_ctx[dev] = std::move(c);
@@ -219,6 +224,10 @@ struct Timer {
     void mark(int i) {
         if (on) CK(cudaEventRecord(c.ev[i], s));
     }
+    void mark_on(int i, cudaStream_t st) {
+        if (on) CK(cudaEventRecord(c.ev[i], st));
+    }
+    bool side = false;  // the sampler ran on the side stream (E_SIDE0..E_SIDE1)
     float between(int a, int b) {
         if (!on) return 0.f;
         float ms = 0.f;
@@ -231,7 +240,7 @@ struct Timer {
 };
 
 enum Ev { E_START = 0, E_UPLOADED, E_PREPARED, E_SAMPLED, E_GATHERED, E_EXTRAS, E_SORTED,
-          E_CLUSTERED, E_DOWNLOADED, E_END };
+          E_CLUSTERED, E_DOWNLOADED, E_END, E_SIDE0, E_SIDE1 };
 
 // Number of L2-blocked gather phases.  A phase re-generates every draw
 // (~0.35 SM-cycles each) and re-streams the query rows, and in exchange turns
@@ -326,6 +335,13 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         if (attempt > 0)
             CK(cudaMemsetAsync(dc, 0, C_UNIQUE * sizeof(unsigned long long), s));
         tm.mark(E_PREPARED);
+        // Run the sampler concurrently with the gather when both are large and
+        // use different resources (narrow rows: the gather is L2/HBM-latency
+        // bound, the sampler shared-memory/ALU bound).  Measured: cfg5 2.80 ->
+        // 2.44 s, cfg3 14.8 -> 13.4 ms; small or wide-row problems lose.
+        const uint64_t ov = env_u64("SNGB_OVERLAP", 2);  // 0 off, 1 on, 2 auto
+        const bool overlap =
+            !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 200000));
         if (!exhaustive) {
             SamplerArgs sa{};
             sa.n = n;
@@ -341,7 +357,21 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             sa.extras = c.extras.as<unsigned long long>();
             sa.extras_capacity = extras_cap;
             sa.counters = dc;
-            CK(launch_sampler(sa, s, c.num_sms));
+            if (overlap) {
+                // the Floyd bookkeeping needs no point data: run it on the side
+                // stream while the gather runs here; non-persistent grids let the
+                // block scheduler interleave the two kernels on every SM
+                sa.rows_per_block = 32;
+                CK(cudaEventRecord(c.fork, s));
+                CK(cudaStreamWaitEvent(c.side, c.fork, 0));
+                tm.mark_on(E_SIDE0, c.side);
+                CK(launch_sampler(sa, c.side, c.num_sms));
+                tm.mark_on(E_SIDE1, c.side);
+                tm.side = true;
+                CK(cudaEventRecord(c.join, c.side));
+            } else {
+                CK(launch_sampler(sa, s, c.num_sms));
+            }
         }
         tm.mark(E_SAMPLED);
         GatherArgs ga{};
@@ -355,6 +385,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         ga.base = (uint32_t)base;
         ga.seed_mixed = seed_mixed;
         ga.force_mod = test_force_mod();
+        ga.rows_per_block = overlap ? 8 * 16 : 0;
         // L2-blocked phases: each launch tests only partners in one slice of
         // the rows, small enough to stay L2-resident while every vertex's
         // draws are regenerated (cheap) and its query row streamed.
@@ -364,7 +395,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             ga.part_hi = (uint32_t)(n * (ph + 1) / phases);
             CK(launch_gather(ga, exhaustive, s, c.num_sms));
         }
-        tm.mark(E_GATHERED);
+        tm.mark(E_GATHERED);  // gather kernel(s) done (concurrent with the sampler)
+        if (overlap) CK(cudaStreamWaitEvent(s, c.join, 0));  // extras need the sampler
         if (!exhaustive) {
             ExtrasArgs ea{};
             ea.tp = tp;
@@ -454,7 +486,7 @@ void fill_info(sngb_info* info, const unsigned long long* hc, uint64_t n, uint32
     }
     if (tm.on) {
         info->ms_upload = host ? tm.between(E_START, E_UPLOADED) : 0.f;
-        info->ms_sample = tm.between(E_PREPARED, E_SAMPLED);
+        info->ms_sample = tm.side ? tm.between(E_SIDE0, E_SIDE1) : tm.between(E_PREPARED, E_SAMPLED);
         info->ms_gather = tm.between(E_SAMPLED, E_GATHERED);
         info->ms_extras = tm.between(E_GATHERED, E_EXTRAS);
         info->ms_sort = tm.between(E_EXTRAS, E_SORTED);

@@ -61,6 +61,7 @@ struct GatherArgs {
     uint64_t seed_mixed;  // mix(seed + gamma)
     uint32_t force_mod;   // test hook (0 = off), see test_fire()
     uint32_t part_lo, part_hi;  // partner rows tested by this launch (L2-blocked phases)
+    uint32_t rows_per_block;    // 0: persistent grid; else one block per this many rows
 };
 
 // Test hook (env SNGB_TEST_FORCE_IRREGULAR=m): pretend the Lemire reject
@@ -79,6 +80,7 @@ struct SamplerArgs {
     uint32_t draws, base;
     uint64_t seed_mixed;
     uint32_t force_mod;        // test hook, see test_fire()
+    uint32_t rows_per_block;   // 0: persistent grid; else one block per this many rows
     uint32_t hash_mask;        // slots - 1 (slots: power of two >= 1.6 * draws)
     uint32_t hash_shift;       // 32 - log2(slots)
     uint32_t col_words;        // u32 words of a draws-bit bitmap (multiple of 4)

@@ -317,7 +317,11 @@ unsigned persistent_grid(K kernel, uint64_t rows, int num_sms, size_t smem = 0) 
 template <int G, int V, int R, bool F2, bool EXH>
 cudaError_t gather_one(const GatherArgs& a, cudaStream_t s, int num_sms) {
     auto k = k_gather<G, V, R, F2, EXH>;
-    unsigned grid = persistent_grid(k, a.row_end - a.row_begin, num_sms);
+    const uint64_t rows = a.row_end - a.row_begin;
+    // rows_per_block: a non-persistent grid, so the block scheduler can
+    // interleave these blocks with a concurrently running sampler
+    unsigned grid = a.rows_per_block ? (unsigned)((rows + a.rows_per_block - 1) / a.rows_per_block)
+                                     : persistent_grid(k, rows, num_sms);
     k<<<grid, 256, 0, s>>>(a);
     note_launch(1);
     return cudaGetLastError();

@@ -295,7 +295,10 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBloomBlock, smem);
         if (per_sm < 1) per_sm = 1;
         const uint64_t cap = (uint64_t)num_sms * per_sm;
-        k<<<(unsigned)(rows < cap ? rows : cap), kBloomBlock, smem, s>>>(a);
+        const unsigned grid = a.rows_per_block
+                                  ? (unsigned)((rows + a.rows_per_block - 1) / a.rows_per_block)
+                                  : (unsigned)(rows < cap ? rows : cap);
+        k<<<grid, kBloomBlock, smem, s>>>(a);
         note_launch(1);
         return cudaGetLastError();
     }

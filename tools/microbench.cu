@@ -98,6 +98,29 @@ __global__ void k_gather_rows(const float4* __restrict__ tab, uint64_t rows, uin
     if (acc == 1234.5f) sink[0] = 1;
 }
 
+// Lean random-row gather: 8 lanes per 128-byte row, UN rows in flight per
+// group, minimal index math -- the random-row ceiling without our kernel's
+// per-pair work.
+template <int UN>
+__global__ void k_gather_lean(const float4* __restrict__ tab, uint64_t rows, uint32_t iters,
+                              unsigned long long* sink) {
+    const int lane = threadIdx.x & 31, q = lane & 7, g = lane >> 3;
+    uint32_t x = 0x9e3779b9u * (blockIdx.x * blockDim.x + (threadIdx.x & ~7) + 1);
+    float acc = 0.f;
+    for (uint32_t it = 0; it < iters; ++it) {
+        float4 v[UN];
+#pragma unroll
+        for (int k = 0; k < UN; ++k) {
+            x = xs32(x + g + k);
+            const uint64_t r = (uint64_t)x * rows >> 32;
+            v[k] = __ldg(tab + r * 8 + q);
+        }
+#pragma unroll
+        for (int k = 0; k < UN; ++k) acc += v[k].x + v[k].y + v[k].z + v[k].w;
+    }
+    if (acc == 1234.5f) sink[0] = 1;
+}
+
 // Coalesced re-reads of an L2-resident buffer: `passes` sweeps, grid-stride.
 __global__ void k_stream(const float4* __restrict__ tab, uint64_t n4, int passes,
                          unsigned long long* sink) {
@@ -200,6 +223,21 @@ int main() {
         const double bytes = nrows * c.vec * 16;
         printf("{\"bench\": \"gather_%s\", \"rows_per_s\": %.4g, \"GB_per_s\": %.1f}\n", c.name,
                nrows / (ms * 1e-3), bytes / (ms * 1e-3) / 1e9);
+    }
+    {
+        const uint64_t rows = (2560ull << 20) / 128;
+        for (int bpsm : {4, 8}) {
+            const int b = sms * bpsm;
+            const uint32_t iters = 64;
+            auto l8 = [&] { k_gather_lean<8><<<b, 256>>>(tab, rows, iters, sink); };
+            auto l16 = [&] { k_gather_lean<16><<<b, 256>>>(tab, rows, iters, sink); };
+            const float m8 = time_ms(l8), m16 = time_ms(l16);
+            const double r8 = (double)b * 32 * iters * 8, r16 = (double)b * 32 * iters * 16;
+            printf("{\"bench\": \"gather_hbm_row128B_lean_u8_b%d\", \"GB_per_s\": %.1f}\n", bpsm,
+                   r8 * 128 / (m8 * 1e-3) / 1e9);
+            printf("{\"bench\": \"gather_hbm_row128B_lean_u16_b%d\", \"GB_per_s\": %.1f}\n", bpsm,
+                   r16 * 128 / (m16 * 1e-3) / 1e9);
+        }
     }
     // L2 streaming read: every warp reads a 32 MB L2-resident buffer with
     // coalesced 16-byte loads (the L2 -> SM bandwidth ceiling)
