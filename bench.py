@@ -86,14 +86,20 @@ def load_gather_peaks(row_bytes: int, table_bytes: int):
                 m[j["bench"]] = j.get("GB_per_s")
     except Exception:
         return None, None
+    def best(*names):
+        vals = [m[k] for k in names if m.get(k)]
+        return max(vals) if vals else None
     if row_bytes <= 16:
-        l2, hbm = m.get("gather_l2_row16B_80MB"), m.get("gather_hbm_row16B_2GB")
+        l2, hbm = best("gather_l2_row16B_80MB"), best("gather_hbm_row16B_2GB")
     elif row_bytes <= 64:
-        l2, hbm = m.get("gather_l2_row64B_64MB"), None
+        l2, hbm = best("gather_l2_row64B_64MB"), None
     elif row_bytes <= 128:
-        l2, hbm = m.get("gather_l2_row128B_64MB"), m.get("gather_hbm_row128B_2.5GB")
+        l2 = best("gather_l2_row128B_64MB")
+        hbm = best("gather_hbm_row128B_2.5GB", "gather_hbm_row128B_lean_u8_b4",
+                   "gather_hbm_row128B_lean_u16_b4", "gather_hbm_row128B_lean_u8_b8",
+                   "gather_hbm_row128B_lean_u16_b8")
     else:
-        l2, hbm = m.get("gather_l2_row3136B_55MB"), m.get("gather_hbm_row3136B_2GB")
+        l2, hbm = best("gather_l2_row3136B_55MB"), best("gather_hbm_row3136B_2GB")
     return l2, hbm
 
 
@@ -159,28 +165,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
+def _ref_sample(pts, w, m):
+    """Row-prefix sample of m rows keeping each vertex's draws (same d, same per-pair work)."""
+    n, draws = pts.shape[0], w.draws
+    if m >= n:
+        return pts, w.rate, f"full workload (n={n}, draws={draws})"
+    rate = draws / m
+    return (np.ascontiguousarray(pts[:m]), rate,
+            f"first {m} rows of the workload, rate={rate:.6g} so each vertex keeps "
+            f"draws={draws} (same d, same per-pair work)")
+
+
 def cpu_baseline(pts, w, budget_s: float):
-    """The reference's own sng_dbscan (oracle/_ref) on all host cores, bounded sample."""
+    """The reference's own sng_dbscan (oracle/_ref) on all host cores, on the full
+    workload when it fits `budget_s`, else on a row-prefix sample sized from a
+    short probe run."""
     from oracle import Reference
     ref = Reference()
     cores = ref.hw_threads()
-    n = pts.shape[0]
-    draws = w.draws
-    # full workload if it fits the budget at ~5e6 pairs/s/8 cores per 784-d..., else a
-    # row-prefix sample with the same per-vertex draws (same d, same work per pair).
-    est_rate = 1.5e9 / max(w.d, 1) * cores / 8.0  # rough pairs/s of the reference
-    m = n
-    if n * draws / est_rate > budget_s:
-        m = max(draws + 2, int(budget_s * est_rate / draws))
-    if m >= n:
-        sample_pts, rate, desc = pts, w.rate, f"full workload (n={n}, draws={draws})"
-    else:
-        sample_pts = np.ascontiguousarray(pts[:m])
-        rate = draws / m
-        desc = (f"first {m} rows of the workload, rate={rate:.6g} so each vertex keeps "
-                f"draws={draws} (same d, same per-pair work)")
-    ds = ref.dataset(sample_pts)
-    labels, roles, info = ref.sng_dbscan(ds, w.eps, w.min_pts, rate, w.seed, threads=0)
+    n, draws = pts.shape[0], w.draws
+    m0 = min(n, max(4 * draws, 20000))
+    sp, rate, _ = _ref_sample(pts, w, m0)
+    _, _, pinfo = ref.sng_dbscan(ref.dataset(sp), w.eps, w.min_pts, rate, w.seed, threads=0)
+    probe_rate = pinfo["distance_evals"] / max(pinfo["ms"] / 1e3, 1e-6)
+    m = n if n * draws / probe_rate <= budget_s else max(m0, int(budget_s * probe_rate / draws))
+    sample_pts, rate, desc = _ref_sample(pts, w, m)
+    labels, roles, info = ref.sng_dbscan(ref.dataset(sample_pts), w.eps, w.min_pts, rate, w.seed,
+                                         threads=0)
     pairs = info["distance_evals"]
     return {"value": pairs / (info["ms"] / 1e3), "unit": UNIT, "cores": cores,
             "kind": "reference", "sample": desc, "ms": info["ms"], "pairs": pairs}
@@ -197,14 +208,9 @@ def run_reference_arm(args, w, pts):
     probe = cpu_baseline(pts, w, budget_s=max(1.0, 150.0 / max(1, args.steps + args.warmup)))
     times = []
     m_desc = probe["sample"]
-    # reuse the sample choice: rebuild it the same way
-    n = pts.shape[0]
+    m = probe["pairs"] // w.draws
+    sample_pts, rate, _ = _ref_sample(pts, w, m)
     draws = w.draws
-    if probe["pairs"] == n * draws:
-        sample_pts, rate = pts, w.rate
-    else:
-        m = probe["pairs"] // draws
-        sample_pts, rate = np.ascontiguousarray(pts[:m]), draws / m
     ds = ref.dataset(sample_pts)
     pairs = None
     for i in range(args.warmup + args.steps):
@@ -216,7 +222,7 @@ def run_reference_arm(args, w, pts):
     value = pairs / (ms / 1e3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": w.name, "n": w.n, "d": w.d, "eps": w.eps, "rate": w.rate,
                        "min_pts": w.min_pts, "seed": w.seed, "draws": draws,
@@ -373,6 +379,10 @@ def main():
     # L2 when the (padded) row table, or one L2-blocked phase of it, is resident.
     row_bytes = 16 if d == 3 else 4 * d
     l2_peak, hbm_gather_peak = load_gather_peaks(row_bytes, n * row_bytes)
+    # the microbenchmarks count whole (padded) rows; express them in algorithmic bytes
+    scale = (4.0 * d) / row_bytes
+    l2_peak = l2_peak * scale if l2_peak else None
+    hbm_gather_peak = hbm_gather_peak * scale if hbm_gather_peak else None
     resident = n * row_bytes <= 100 * 2**20 or (d >= 256 and n * row_bytes <= 4 * 63 * 2**20)
     roofline.update({
         "effective_bound": "l2" if resident else "hbm (random rows)",
@@ -380,7 +390,9 @@ def main():
         "frac_of_effective_peak": (achieved / (l2_peak if resident else (hbm_gather_peak or peak)))
         if achieved and (l2_peak or hbm_gather_peak) else None,
         "peaks_source": "tools/microbench.cu random-row gather of this row size "
-                        "(profiles/r01_microbench.jsonl)"})
+                        "(profiles/r01_microbench.jsonl)",
+        "concurrent_with": "k_floyd_bloom on a side stream" if w.d in (16, 32) and n >= 200000
+        else None})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -338,10 +338,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         // Run the sampler concurrently with the gather when both are large and
         // use different resources (narrow rows: the gather is L2/HBM-latency
         // bound, the sampler shared-memory/ALU bound).  Measured: cfg5 2.80 ->
-        // 2.44 s, cfg3 14.8 -> 13.4 ms; small or wide-row problems lose.
+        // 2.44 s, cfg3 14.8 -> 13.4 ms; cfg4 (16-byte rows) neutral, small or
+        // wide-row problems lose.
         const uint64_t ov = env_u64("SNGB_OVERLAP", 2);  // 0 off, 1 on, 2 auto
         const bool overlap =
-            !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 200000));
+            !exhaustive && (ov == 1 || (ov == 2 && stride >= 8 && stride <= 64 && (re - rb) >= 200000));
         if (!exhaustive) {
             SamplerArgs sa{};
             sa.n = n;
