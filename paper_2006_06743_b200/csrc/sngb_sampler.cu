@@ -15,17 +15,23 @@
 //   chain_i = t_i = j_k for a collided k < i     -> only possible when
 //             t_i >= base; k = t_i - base; resolved in index order.
 //
-// One thread block per vertex (all draws of the vertex in flight at once),
-// four block-wide phases: insert (min-index) -> classify -> resolve chains
-// (thread 0, rare) -> emit the replacement partner j_i + (j_i >= u) of every
-// collided draw as an "extra" pair for k_extras.  Vertices whose stream meets
-// the Lemire reject pre-condition are replayed exactly by one thread with the
-// sequential Stream (all of their partners become extras).
+// Three kernels, chosen by launch_sampler:
+//   k_floyd_bitmap (sngb_floyd_bitmap.cuh)  n <= 32 k: exact per-warp bitmap,
+//                                           draws in reference order;
+//   k_floyd_bloom  (sngb_floyd_bloom.cuh)   draws <= 4096: conflict-free bit
+//                                           filter + resolver warp (the
+//                                           BASELINE configs 2-5);
+//   k_floyd        (this file)              anything else: one block per
+//                                           vertex, (t, min index) hash in
+//                                           shared memory or L2 scratch.
+// Every kernel emits the replacement partner j_i + (j_i >= u) of every
+// collided draw as an "extra" pair for k_extras, and replays a vertex whose
+// stream meets the Lemire reject pre-condition exactly and sequentially (all
+// of its partners become extras).
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <cstdlib>
-#include <string>
 
 #include "sngb_device.cuh"
 #include "sngb_internal.cuh"
@@ -225,7 +231,6 @@ __global__ void __launch_bounds__(kFloydThreads) k_floyd(const SamplerArgs a) {
     }
 }
 
-#include "sngb_floyd_fast.cuh"
 #include "sngb_floyd_bitmap.cuh"
 #include "sngb_floyd_bloom.cuh"
 
@@ -278,8 +283,7 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
         return cudaGetLastError();
     }
     // large n, draws <= 4096: filter + exact resolution of the few shared bits
-    const char* fk = std::getenv("SNGB_FLOYD_KERNEL");
-    if (D <= 4096 && a.n - 2 < 0xffffffffull && !(fk && std::string(fk) == "fast")) {
+    if (D <= 4096 && a.n - 2 < 0xffffffffull) {
         const BloomGeom bg = bloom_geometry(D);
         a.hash_mask = bg.words;
         a.key_bits = bg.bits_log2;
@@ -299,31 +303,6 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
                                   ? (unsigned)((rows + a.rows_per_block - 1) / a.rows_per_block)
                                   : (unsigned)(rows < cap ? rows : cap);
         k<<<grid, kBloomBlock, smem, s>>>(a);
-        note_launch(1);
-        return cudaGetLastError();
-    }
-    uint32_t fb = 16;  // fast path: buckets of 4 u32 keys, load <= 0.625
-    const char* lf_env = std::getenv("SNGB_FLOYD_SLOTS_PER_DRAW_X10");  // tuning knob
-    const uint32_t lf10 = lf_env ? (uint32_t)std::strtoul(lf_env, nullptr, 10) : 32u;
-    while (40 * fb < lf10 * D) fb <<= 1;  // 4 * buckets >= lf10/10 * draws
-    const uint32_t cw = ((D + 31) / 32 + 3) & ~3u;
-    const size_t fast_smem = floyd_fast_smem_bytes(fb, cw);
-    uint32_t tb = 1;  // bits of a draw value t <= n - 2
-    while (tb < 32 && ((uint64_t)(a.n - 2) >> tb) != 0) ++tb;
-    if (D <= 4096 && tb < 30 && fast_smem <= 200 * 1024) {
-        a.hash_mask = fb - 1;
-        a.hash_shift = 32 - __builtin_ctz(fb);
-        a.col_words = cw;
-        a.key_bits = tb;
-        auto k = D <= 1024 ? k_floyd_fast<4> : D <= 2048 ? k_floyd_fast<8> : D <= 3072 ? k_floyd_fast<12> : k_floyd_fast<16>;
-        cudaError_t e =
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem);
-        if (e != cudaSuccess) return e;
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFastThreads, fast_smem);
-        if (per_sm < 1) per_sm = 1;
-        const uint64_t cap = (uint64_t)num_sms * per_sm;
-        k<<<(unsigned)(rows < cap ? rows : cap), kFastThreads, fast_smem, s>>>(a);
         note_launch(1);
         return cudaGetLastError();
     }
