@@ -323,6 +323,12 @@ def main():
         L = _lib.lib()
         o = _lib.SngbOpts(local, 0, C.c_void_p(stream.cuda_stream), 0, 0)
         gi = _lib.SngbInfo()
+        if world > 1:
+            from paper_2006_06743_b200.distributed import shard_bounds
+            chunk = (n + world - 1) // world
+            rb_, re_ = shard_bounds(n, world, rank)
+            shard_in = torch.zeros((chunk, d), dtype=torch.float32, device=dev)
+            replica = torch.empty((chunk * world, d), dtype=torch.float32, device=dev)
 
         def step_e2e():
             if world == 1:
@@ -333,8 +339,11 @@ def main():
                                        C.byref(gi))
                 sng._check(rc)
             else:
-                pts_d = host.to(dev, non_blocking=True)
-                lab, rol, _ = sng_dbscan_sharded(pts_d, w.eps, w.min_pts, w.rate, w.seed)
+                # replica: every rank uploads its own row shard over its PCIe link,
+                # then one NCCL all-gather over NVLink assembles the full table
+                shard_in[: re_ - rb_].copy_(host[rb_:re_], non_blocking=True)
+                dist.all_gather_into_tensor(replica, shard_in)
+                lab, rol, _ = sng_dbscan_sharded(replica[:n], w.eps, w.min_pts, w.rate, w.seed)
                 if rank == 0:
                     labels_h.copy_(lab, non_blocking=True)
                     roles_h.copy_(rol, non_blocking=True)
@@ -411,6 +420,9 @@ def main():
             "config": {"workload": w.name, "n": n, "d": d, "eps": w.eps, "rate": w.rate,
                        "min_pts": w.min_pts, "seed": w.seed, "draws": w.draws, "pairs": pairs,
                        "parallelism": f"rows sharded x{world}" if world > 1 else "1 GPU",
+                       "merge": "fixed-point union-find over NCCL all-reduce" if world > 1
+                       else None,
+                       "replica": "row-shard upload + NCCL all-gather" if world > 1 else None,
                        "l2": "256 MB L2 flush before every timed step"},
             "e2e": e2e,
             "gpu_launches": launches,

@@ -128,6 +128,52 @@ int sngb_cluster_edges_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n
                               int32_t min_pts, const sngb_opts* opts, int32_t* d_labels,
                               uint8_t* d_roles, sngb_info* info_out);
 
+/* ---- Multi-GPU merge steps: local union-find per GPU, then a
+ * fixed-point merge by NCCL all-reduce of full-length vertex arrays.
+ *
+ * Query rows are sharded; rank r owns the canonical keys (a<<32 | b, a < b)
+ * whose smaller endpoint a lies in its row shard (after an all-to-all of the
+ * keys its edge builder produced).  Vertex arrays are full length n < 2^31
+ * and int32, so the caller can SUM / MIN all-reduce them between the steps.
+ * Every call is synchronous on opts->stream (or the library stream), and a
+ * key with a >= b or b >= n fails it with SNGB_ERR_ARG before any write.
+ * Together they replace connected_components + core/border/relabel
+ * (graph.cpp:222-247, clusterer.cpp:7-52) for an edge set split over ranks. */
+
+/* Sort + deduplicate canonical keys (any order, duplicates allowed) into d_out
+ * (capacity >= nkeys, must not alias d_keys); *count_out = unique count
+ * (graph.cpp:34-40). */
+int sngb_unique_keys_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n,
+                            const sngb_opts* opts, uint64_t* d_out, uint64_t* count_out);
+
+/* d_degree[v] += number of keys incident to v: the owned part of deg(v)
+ * (graph.hpp:28); SUM-all-reduce over ranks gives the sampled degree. */
+int sngb_degrees_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n, const sngb_opts* opts,
+                        int32_t* d_degree);
+
+/* Union-find over the keys whose endpoints are both core (degree >= min_pts,
+ * clusterer.cpp:12-13; graph.cpp:228-235).  d_parent in: a forest with
+ * parent[v] <= v (the identity on the first call, the MIN-all-reduced array
+ * afterwards); out: every core vertex holds its root, the smallest vertex of
+ * its set.  *changed_out = vertices whose entry changed; the merge has reached
+ * its fixed point when that is 0 on every rank. */
+int sngb_components_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n,
+                           const int32_t* d_degree, int32_t min_pts, const sngb_opts* opts,
+                           int32_t* d_parent, uint64_t* changed_out);
+
+/* Border attachment over the keys (clusterer.cpp:26-37): for a non-core
+ * endpoint b of a core vertex a, d_border[b] = min(d_border[b], d_parent[a]).
+ * Initialise d_border to INT32_MAX ("no core neighbour"); MIN-all-reduce it. */
+int sngb_border_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n, const int32_t* d_degree,
+                       int32_t min_pts, const int32_t* d_parent, const sngb_opts* opts,
+                       int32_t* d_border);
+
+/* Labels and roles from the merged arrays (clusterer.cpp:17-51): identical on
+ * every rank.  info (optional): cluster/core/border/noise counts. */
+int sngb_relabel_device(uint64_t n, const int32_t* d_degree, int32_t min_pts,
+                        const int32_t* d_parent, const int32_t* d_border, const sngb_opts* opts,
+                        int32_t* d_labels, uint8_t* d_roles, sngb_info* info_out);
+
 /* Status code -> message (the reference's exception text for codes 1..6). */
 const char* sngb_strerror(int code);
 /* Thread-local detail of the last SNGB_ERR_CUDA (CUDA error string + site). */

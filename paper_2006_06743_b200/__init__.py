@@ -364,3 +364,69 @@ def cluster_edges_device(keys, n: int, min_pts: int, timing: bool = False):
                                               labels.data_ptr(), roles.data_ptr(), C.byref(gi))
     _check(rc)
     return labels, roles, gi
+
+
+# ---- multi-GPU merge steps (include/sngb.h; used by distributed.py) --------
+def _ptr(t):
+    return t.data_ptr() if t.numel() else None
+
+
+def unique_keys_device(keys, n: int):
+    """Sorted unique canonical keys (graph.cpp:34-40) of CUDA int64 keys."""
+    import torch
+
+    keys = keys.contiguous()
+    out = torch.empty(max(keys.numel(), 1), dtype=torch.int64, device=keys.device)
+    cnt = C.c_uint64(0)
+    o = _opts(keys.device.index, False, _stream_handle(keys))
+    _check(_lib.lib().sngb_unique_keys_device(_ptr(keys), keys.numel(), n, C.byref(o),
+                                              out.data_ptr(), C.byref(cnt)))
+    return out[: cnt.value]
+
+
+def degrees_device(keys, n: int, degree=None):
+    """degree[v] += keys incident to v (int32[n], created zeroed when None)."""
+    import torch
+
+    keys = keys.contiguous()
+    if degree is None:
+        degree = torch.zeros(n, dtype=torch.int32, device=keys.device)
+    o = _opts(keys.device.index, False, _stream_handle(keys))
+    _check(_lib.lib().sngb_degrees_device(_ptr(keys), keys.numel(), n, C.byref(o),
+                                          degree.data_ptr()))
+    return degree
+
+
+def components_device(keys, n: int, degree, min_pts: int, parent) -> int:
+    """Union-find step over core-core keys into `parent` (in place); returns
+    the number of vertices whose entry changed."""
+    keys = keys.contiguous()
+    changed = C.c_uint64(0)
+    o = _opts(keys.device.index, False, _stream_handle(parent))
+    _check(_lib.lib().sngb_components_device(_ptr(keys), keys.numel(), n, degree.data_ptr(),
+                                             int(min_pts), C.byref(o), parent.data_ptr(),
+                                             C.byref(changed)))
+    return int(changed.value)
+
+
+def border_device(keys, n: int, degree, min_pts: int, parent, border) -> None:
+    """border[b] = min(border[b], parent[a]) for core a -- non-core b edges."""
+    keys = keys.contiguous()
+    o = _opts(parent.device.index, False, _stream_handle(parent))
+    _check(_lib.lib().sngb_border_device(_ptr(keys), keys.numel(), n, degree.data_ptr(),
+                                         int(min_pts), parent.data_ptr(), C.byref(o),
+                                         border.data_ptr()))
+
+
+def relabel_device(n: int, degree, min_pts: int, parent, border):
+    """(labels int32[n], roles uint8[n], SngbInfo) from the merged arrays."""
+    import torch
+
+    labels = torch.empty(n, dtype=torch.int32, device=parent.device)
+    roles = torch.empty(n, dtype=torch.uint8, device=parent.device)
+    gi = SngbInfo()
+    o = _opts(parent.device.index, False, _stream_handle(parent))
+    _check(_lib.lib().sngb_relabel_device(n, degree.data_ptr(), int(min_pts), parent.data_ptr(),
+                                          border.data_ptr(), C.byref(o), labels.data_ptr(),
+                                          roles.data_ptr(), C.byref(gi)))
+    return labels, roles, gi

@@ -33,6 +33,8 @@ EXPORTS = [
     "sngb_dbscan_f32", "sngb_dbscan_f32_device", "sngb_sampled_edges_f32_device",
     "sngb_sampled_edges_f32", "sngb_cluster_edges_device", "sngb_strerror",
     "sngb_last_error_detail", "sngb_abi_version", "sngb_device_count", "sngb_release_pools",
+    "sngb_unique_keys_device", "sngb_degrees_device", "sngb_components_device",
+    "sngb_border_device", "sngb_relabel_device",
 ]
 
 
@@ -93,6 +95,17 @@ def lib() -> C.CDLL:
         L.sngb_cluster_edges_device.restype = C.c_int
         L.sngb_cluster_edges_device.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_int32, optp, vp,
                                                 vp, infop]
+        L.sngb_unique_keys_device.restype = C.c_int
+        L.sngb_unique_keys_device.argtypes = [vp, C.c_uint64, C.c_uint64, optp, vp, u64p]
+        L.sngb_degrees_device.restype = C.c_int
+        L.sngb_degrees_device.argtypes = [vp, C.c_uint64, C.c_uint64, optp, vp]
+        L.sngb_components_device.restype = C.c_int
+        L.sngb_components_device.argtypes = [vp, C.c_uint64, C.c_uint64, vp, C.c_int32, optp, vp,
+                                             u64p]
+        L.sngb_border_device.restype = C.c_int
+        L.sngb_border_device.argtypes = [vp, C.c_uint64, C.c_uint64, vp, C.c_int32, vp, optp, vp]
+        L.sngb_relabel_device.restype = C.c_int
+        L.sngb_relabel_device.argtypes = [C.c_uint64, vp, C.c_int32, vp, vp, optp, vp, vp, infop]
         L.sngb_strerror.restype = C.c_char_p
         L.sngb_strerror.argtypes = [C.c_int]
         L.sngb_last_error_detail.restype = C.c_char_p

@@ -527,6 +527,37 @@ int dbscan_device(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint
     return SNGB_OK;
 }
 
+// ---- multi-GPU merge steps -----------------------------------
+// Shared frame: device + context lock + zeroed counters; `f` enqueues on `s`;
+// the counters come back synchronously and bad caller keys fail the call.
+template <class F>
+int merge_step(const sngb_opts* opts, uint64_t n, F&& f) {
+    if (n == 0) return SNGB_ERR_EMPTY;
+    if (n > 0x7fffffffull) return SNGB_ERR_TOO_LARGE;  // int32 vertex arrays
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    return guarded([&]() -> int {
+        const int dev = resolve_device(opts);
+        DeviceGuard dg(dev);
+        DevCtx& c = get_ctx(dev);
+        std::lock_guard<std::mutex> lk(c.mu);
+        cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
+        sngb_t_launch_hand = 0;
+        sngb_t_launch_lib = 0;
+        c.counters.ensure(C_COUNT * 8);
+        unsigned long long* dc = c.counters.as<unsigned long long>();
+        CK(cudaMemsetAsync(dc, 0, C_COUNT * 8, s));
+        CK(f(c, s, dc));
+        CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (c.h_counters[C_BADKEY]) return SNGB_ERR_ARG;
+        return SNGB_OK;
+    });
+}
+
+const unsigned long long* ull(const uint64_t* p) {
+    return reinterpret_cast<const unsigned long long*>(p);
+}
+
 }  // namespace
 
 extern "C" {
@@ -771,6 +802,132 @@ int sngb_cluster_edges_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n
         fill_info(info, c.h_counters, n, 0, gr, 0, tm, true, false);
         return SNGB_OK;
     });
+}
+
+int sngb_unique_keys_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n,
+                            const sngb_opts* opts, uint64_t* d_out, uint64_t* count_out) {
+    if ((nkeys && (!d_keys || !d_out)) || !count_out) return SNGB_ERR_ARG;
+    if (nkeys && d_keys == d_out) return SNGB_ERR_ARG;
+    uint64_t count = 0;
+    const int rc = merge_step(opts, n, [&](DevCtx& c, cudaStream_t s, unsigned long long* dc) {
+        if (nkeys == 0) return cudaSuccess;
+        const uint32_t nb = bits_for(n - 1);
+        c.keys.ensure(nkeys * 8);
+        c.keys_alt.ensure(nkeys * 8);
+        cudaError_t e = launch_convert_keys(ull(d_keys), c.keys.as<unsigned long long>(), nkeys, nb,
+                                            true, n, dc, s, c.num_sms);
+        if (e != cudaSuccess) return e;
+        c.temp.ensure(sort_unique_temp_bytes(nkeys, nb));
+        unsigned long long* u = nullptr;
+        e = sort_unique(c.keys.as<unsigned long long>(), c.keys_alt.as<unsigned long long>(), nkeys,
+                        nb, c.temp.p, c.temp.bytes, dc, &u, s);
+        if (e != cudaSuccess) return e;
+        // back to a<<32|b; unique <= nkeys, the tail beyond the count is scratch
+        e = launch_convert_keys(u, reinterpret_cast<unsigned long long*>(d_out), nkeys, nb, false,
+                                n, dc, s, c.num_sms);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return e;
+        return cudaMemcpy(&count, &dc[C_UNIQUE], 8, cudaMemcpyDeviceToHost);
+    });
+    if (rc == SNGB_OK) *count_out = count;
+    return rc;
+}
+
+int sngb_degrees_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n, const sngb_opts* opts,
+                        int32_t* d_degree) {
+    if ((nkeys && !d_keys) || !d_degree) return SNGB_ERR_ARG;
+    return merge_step(opts, n, [&](DevCtx& c, cudaStream_t s, unsigned long long* dc) {
+        cudaError_t e = merge_check_keys(ull(d_keys), nkeys, n, dc, s, c.num_sms);
+        if (e != cudaSuccess) return e;
+        // a bad key is counted before any write: skip the pass and fail below
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return e;
+        unsigned long long bad = 0;
+        e = cudaMemcpy(&bad, &dc[C_BADKEY], 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess || bad) return e;
+        return merge_degrees(ull(d_keys), nkeys, reinterpret_cast<uint32_t*>(d_degree), s,
+                             c.num_sms);
+    });
+}
+
+int sngb_components_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n,
+                           const int32_t* d_degree, int32_t min_pts, const sngb_opts* opts,
+                           int32_t* d_parent, uint64_t* changed_out) {
+    if (min_pts < 1) return SNGB_ERR_MINPTS;
+    if ((nkeys && !d_keys) || !d_degree || !d_parent) return SNGB_ERR_ARG;
+    uint64_t changed = 0;
+    const int rc = merge_step(opts, n, [&](DevCtx& c, cudaStream_t s, unsigned long long* dc) {
+        cudaError_t e = merge_check_keys(ull(d_keys), nkeys, n, dc, s, c.num_sms);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return e;
+        unsigned long long bad = 0;
+        e = cudaMemcpy(&bad, &dc[C_BADKEY], 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess || bad) return e;
+        c.core.ensure(n);
+        c.first.ensure(n * 4);  // snapshot of the incoming forest
+        e = merge_components(ull(d_keys), nkeys, n, reinterpret_cast<const uint32_t*>(d_degree),
+                             min_pts, reinterpret_cast<uint32_t*>(d_parent), c.core.as<uint8_t>(),
+                             c.first.as<uint32_t>(), dc, s, c.num_sms);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return e;
+        return cudaMemcpy(&changed, &dc[C_CHANGED], 8, cudaMemcpyDeviceToHost);
+    });
+    if (rc == SNGB_OK && changed_out) *changed_out = changed;
+    return rc;
+}
+
+int sngb_border_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n, const int32_t* d_degree,
+                       int32_t min_pts, const int32_t* d_parent, const sngb_opts* opts,
+                       int32_t* d_border) {
+    if (min_pts < 1) return SNGB_ERR_MINPTS;
+    if ((nkeys && !d_keys) || !d_degree || !d_parent || !d_border) return SNGB_ERR_ARG;
+    return merge_step(opts, n, [&](DevCtx& c, cudaStream_t s, unsigned long long* dc) {
+        cudaError_t e = merge_check_keys(ull(d_keys), nkeys, n, dc, s, c.num_sms);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return e;
+        unsigned long long bad = 0;
+        e = cudaMemcpy(&bad, &dc[C_BADKEY], 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess || bad) return e;
+        c.core.ensure(n);
+        return merge_border(ull(d_keys), nkeys, n, reinterpret_cast<const uint32_t*>(d_degree),
+                            min_pts, reinterpret_cast<const uint32_t*>(d_parent),
+                            reinterpret_cast<uint32_t*>(d_border), c.core.as<uint8_t>(), s,
+                            c.num_sms);
+    });
+}
+
+int sngb_relabel_device(uint64_t n, const int32_t* d_degree, int32_t min_pts,
+                        const int32_t* d_parent, const int32_t* d_border, const sngb_opts* opts,
+                        int32_t* d_labels, uint8_t* d_roles, sngb_info* info) {
+    if (min_pts < 1) return SNGB_ERR_MINPTS;
+    if (!d_degree || !d_parent || !d_border || !d_labels || !d_roles) return SNGB_ERR_ARG;
+    unsigned long long hc[C_COUNT] = {};
+    const int rc = merge_step(opts, n, [&](DevCtx& c, cudaStream_t s, unsigned long long* dc) {
+        ClusterBuffers b{};
+        ensure_cluster_bufs(c, n, b);
+        cudaError_t e = merge_relabel(n, reinterpret_cast<const uint32_t*>(d_degree), min_pts,
+                                      reinterpret_cast<const uint32_t*>(d_parent),
+                                      reinterpret_cast<const uint32_t*>(d_border), b, dc, d_labels,
+                                      d_roles, s, c.num_sms);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return e;
+        return cudaMemcpy(hc, dc, sizeof(hc), cudaMemcpyDeviceToHost);
+    });
+    if (rc == SNGB_OK && info) {
+        std::memset(info, 0, sizeof(*info));
+        info->cluster_count = (int32_t)hc[C_CLUSTERS];
+        info->core_count = (uint32_t)hc[C_CORE];
+        info->border_count = (uint32_t)hc[C_BORDER];
+        info->noise_count = (uint32_t)hc[C_NOISE];
+        info->kernel_launches = sngb_t_launch_hand;
+        info->library_launches = sngb_t_launch_lib;
+    }
+    return rc;
 }
 
 }  // extern "C"

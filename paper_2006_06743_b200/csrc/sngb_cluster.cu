@@ -36,9 +36,11 @@ __device__ __forceinline__ void decode(unsigned long long k, uint32_t nb, uint32
     b = (uint32_t)(k & ((1ull << nb) - 1));
 }
 
+// Edge-centric kernels read the edge count from the device (m_ptr: the
+// DeviceSelect output, no host round trip) or, when m_ptr is null, take m_host.
 __global__ void k_degrees(const unsigned long long* __restrict__ keys, const unsigned long long* m_ptr,
-                          uint32_t nb, uint32_t* deg) {
-    const uint64_t m = *m_ptr;
+                          uint64_t m_host, uint32_t nb, uint32_t* deg) {
+    const uint64_t m = m_ptr ? *m_ptr : m_host;
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
          e += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t a, b;
@@ -75,8 +77,9 @@ __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x) {
 
 // union over core-core edges (graph.cpp:228-235): hook larger root under smaller.
 __global__ void k_union(const unsigned long long* __restrict__ keys, const unsigned long long* m_ptr,
-                        uint32_t nb, const uint8_t* __restrict__ core, uint32_t* parent) {
-    const uint64_t m = *m_ptr;
+                        uint64_t m_host, uint32_t nb, const uint8_t* __restrict__ core,
+                        uint32_t* parent) {
+    const uint64_t m = m_ptr ? *m_ptr : m_host;
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
          e += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t a, b;
@@ -107,9 +110,9 @@ __global__ void k_compress(uint64_t n, const uint8_t* __restrict__ core, uint32_
 
 // border: non-core endpoint adjacent to a core vertex takes the minimum root.
 __global__ void k_border(const unsigned long long* __restrict__ keys, const unsigned long long* m_ptr,
-                         uint32_t nb, const uint8_t* __restrict__ core,
+                         uint64_t m_host, uint32_t nb, const uint8_t* __restrict__ core,
                          const uint32_t* __restrict__ parent, uint32_t* broot) {
-    const uint64_t m = *m_ptr;
+    const uint64_t m = m_ptr ? *m_ptr : m_host;
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
          e += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t a, b;
@@ -205,6 +208,58 @@ __global__ void k_convert(const unsigned long long* __restrict__ in, unsigned lo
     }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU merge steps.  Every rank owns the canonical keys
+// (a<<32 | b, a < b) whose smaller endpoint lies in its row shard; vertex
+// arrays are full length, int32 on the caller side so NCCL can SUM / MIN-
+// reduce them; "no core neighbour" in the border array is INT32_MAX.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kNoneI32 = 0x7fffffffu;
+
+__global__ void k_check_keys(const unsigned long long* __restrict__ keys, uint64_t m, uint64_t n,
+                             unsigned long long* counters) {
+    unsigned bad = 0;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[e];
+        const uint64_t a = k >> 32, b = k & 0xffffffffull;
+        bad += (a >= b || b >= n) ? 1u : 0u;
+    }
+    bad = __reduce_add_sync(kFull, bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&counters[C_BADKEY], (unsigned long long)bad);
+}
+
+__global__ void k_coremask(const uint32_t* __restrict__ deg, uint64_t n, uint32_t min_pts,
+                           uint8_t* core) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        core[v] = deg[v] >= min_pts ? 1 : 0;
+}
+
+__global__ void k_count_changed(uint64_t n, const uint32_t* __restrict__ now,
+                                const uint32_t* __restrict__ before, unsigned long long* counters) {
+    unsigned c = 0;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        c += now[v] != before[v] ? 1u : 0u;
+    c = __reduce_add_sync(kFull, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&counters[C_CHANGED], (unsigned long long)c);
+}
+
+// relabel inputs from the merged arrays: core mask, border roots (INT32_MAX ->
+// kNone), first-member init.
+__global__ void k_import(const uint32_t* __restrict__ deg, const uint32_t* __restrict__ border,
+                         uint64_t n, uint32_t min_pts, uint8_t* core, uint32_t* broot,
+                         uint32_t* first) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        core[v] = deg[v] >= min_pts ? 1 : 0;
+        const uint32_t r = border[v];
+        broot[v] = r == kNoneI32 ? kNone : r;
+        first[v] = kNone;
+    }
+}
+
 unsigned grid_for(uint64_t items, int num_sms) {
     uint64_t b = (items + 255) / 256;
     const uint64_t cap = (uint64_t)num_sms * 8;
@@ -270,11 +325,11 @@ cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned
     cudaError_t e = cudaMemsetAsync(b.deg, 0, n * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
     const unsigned ge = grid_for(m, num_sms), gn = grid_for(n + 1, num_sms);
-    if (m) k_degrees<<<ge, 256, 0, s>>>(ukeys, m_ptr, nb, b.deg);
+    if (m) k_degrees<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.deg);
     k_init<<<gn, 256, 0, s>>>(b.deg, n, (uint32_t)min_pts, b.core, b.parent, b.broot, b.first);
-    if (m) k_union<<<ge, 256, 0, s>>>(ukeys, m_ptr, nb, b.core, b.parent);
+    if (m) k_union<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.core, b.parent);
     k_compress<<<gn, 256, 0, s>>>(n, b.core, b.parent);
-    if (m) k_border<<<ge, 256, 0, s>>>(ukeys, m_ptr, nb, b.core, b.parent, b.broot);
+    if (m) k_border<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.core, b.parent, b.broot);
     k_first<<<gn, 256, 0, s>>>(n, b.core, b.parent, b.broot, b.first);
     k_flags<<<gn, 256, 0, s>>>(n, b.core, b.parent, b.broot, b.first, b.flags);
     size_t tb = b.temp_bytes;
@@ -284,6 +339,64 @@ cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned
                                 counters);
     k_store_clusters<<<1, 1, 0, s>>>(b.rank, n, counters);
     note_launch(m ? 9 : 6, 2);  // + CUB scan (init + sweep)
+    return cudaGetLastError();
+}
+
+cudaError_t merge_check_keys(const unsigned long long* keys, uint64_t m, uint64_t n,
+                             unsigned long long* counters, cudaStream_t s, int num_sms) {
+    if (m == 0) return cudaSuccess;
+    k_check_keys<<<grid_for(m, num_sms), 256, 0, s>>>(keys, m, n, counters);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
+cudaError_t merge_degrees(const unsigned long long* keys, uint64_t m, uint32_t* deg, cudaStream_t s,
+                          int num_sms) {
+    if (m == 0) return cudaSuccess;
+    k_degrees<<<grid_for(m, num_sms), 256, 0, s>>>(keys, nullptr, m, 32, deg);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
+cudaError_t merge_components(const unsigned long long* keys, uint64_t m, uint64_t n,
+                             const uint32_t* deg, int32_t min_pts, uint32_t* parent, uint8_t* core,
+                             uint32_t* before, unsigned long long* counters, cudaStream_t s,
+                             int num_sms) {
+    const unsigned gn = grid_for(n, num_sms);
+    k_coremask<<<gn, 256, 0, s>>>(deg, n, (uint32_t)min_pts, core);
+    cudaError_t e = cudaMemcpyAsync(before, parent, n * 4, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+    if (m) k_union<<<grid_for(m, num_sms), 256, 0, s>>>(keys, nullptr, m, 32, core, parent);
+    k_compress<<<gn, 256, 0, s>>>(n, core, parent);
+    k_count_changed<<<gn, 256, 0, s>>>(n, parent, before, counters);
+    note_launch(m ? 4 : 3);
+    return cudaGetLastError();
+}
+
+cudaError_t merge_border(const unsigned long long* keys, uint64_t m, uint64_t n, const uint32_t* deg,
+                         int32_t min_pts, const uint32_t* parent, uint32_t* border, uint8_t* core,
+                         cudaStream_t s, int num_sms) {
+    k_coremask<<<grid_for(n, num_sms), 256, 0, s>>>(deg, n, (uint32_t)min_pts, core);
+    if (m) k_border<<<grid_for(m, num_sms), 256, 0, s>>>(keys, nullptr, m, 32, core, parent, border);
+    note_launch(m ? 2 : 1);
+    return cudaGetLastError();
+}
+
+cudaError_t merge_relabel(uint64_t n, const uint32_t* deg, int32_t min_pts, const uint32_t* parent,
+                          const uint32_t* border, const ClusterBuffers& b,
+                          unsigned long long* counters, int32_t* labels, uint8_t* roles,
+                          cudaStream_t s, int num_sms) {
+    const unsigned gn = grid_for(n + 1, num_sms);
+    k_import<<<gn, 256, 0, s>>>(deg, border, n, (uint32_t)min_pts, b.core, b.broot, b.first);
+    k_first<<<gn, 256, 0, s>>>(n, b.core, parent, b.broot, b.first);
+    k_flags<<<gn, 256, 0, s>>>(n, b.core, parent, b.broot, b.first, b.flags);
+    size_t tb = b.temp_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(b.temp, tb, b.flags, b.rank, (int64_t)(n + 1), s);
+    if (e != cudaSuccess) return e;
+    k_labels<<<gn, 256, 0, s>>>(n, b.core, parent, b.broot, b.first, b.rank, labels, roles,
+                                counters);
+    k_store_clusters<<<1, 1, 0, s>>>(b.rank, n, counters);
+    note_launch(5, 2);
     return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@ enum Counter : int {
     C_NOISE,
     C_CLUSTERS,
     C_BADKEY,            // self loop / out-of-range endpoint in caller keys
+    C_CHANGED,           // merge step: vertices whose component root moved
     C_COUNT
 };
 
@@ -144,6 +145,22 @@ cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned
                                  unsigned long long* counters, int32_t* labels, uint8_t* roles,
                                  cudaStream_t s, int num_sms);
 
+// multi-GPU merge steps (sngb_cluster.cu); keys are canonical a<<32|b
+cudaError_t merge_check_keys(const unsigned long long* keys, uint64_t m, uint64_t n,
+                             unsigned long long* counters, cudaStream_t s, int num_sms);
+cudaError_t merge_degrees(const unsigned long long* keys, uint64_t m, uint32_t* deg, cudaStream_t s,
+                          int num_sms);
+cudaError_t merge_components(const unsigned long long* keys, uint64_t m, uint64_t n,
+                             const uint32_t* deg, int32_t min_pts, uint32_t* parent, uint8_t* core,
+                             uint32_t* before, unsigned long long* counters, cudaStream_t s,
+                             int num_sms);
+cudaError_t merge_border(const unsigned long long* keys, uint64_t m, uint64_t n, const uint32_t* deg,
+                         int32_t min_pts, const uint32_t* parent, uint32_t* border, uint8_t* core,
+                         cudaStream_t s, int num_sms);
+cudaError_t merge_relabel(uint64_t n, const uint32_t* deg, int32_t min_pts, const uint32_t* parent,
+                          const uint32_t* border, const ClusterBuffers& b,
+                          unsigned long long* counters, int32_t* labels, uint8_t* roles,
+                          cudaStream_t s, int num_sms);
 cudaError_t launch_convert_keys(const unsigned long long* in, unsigned long long* out, uint64_t m,
                                 uint32_t nb, bool to_compact, uint64_t n,
                                 unsigned long long* counters, cudaStream_t s, int num_sms);
