@@ -84,6 +84,12 @@ struct DevCtx {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;          // sampler runs here, concurrently with the gather
     cudaEvent_t fork = nullptr, join = nullptr;
+    // host-buffer calls: the points are uploaded in row chunks on `copy`,
+    // chunk k's arrival is up_ev[k]; compute starts on the first chunk
+    static constexpr int kMaxChunks = 8;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t up_start = nullptr;
+    cudaEvent_t up_ev[kMaxChunks] = {};
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
         flags, rank, temp, labels, roles;
@@ -137,6 +143,9 @@ DevCtx& get_ctx(int dev) {
         CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->up_start, cudaEventDisableTiming));
+        for (auto& e : c->up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaMallocHost(&c->h_counters, C_COUNT * sizeof(unsigned long long)));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
         g_ctx[dev] = std::move(c);
@@ -268,31 +277,32 @@ struct GraphResult {
 
 // Prepare points and run the graph build for rows [rb, re).  Leaves sorted
 // unique compact keys in c.keys/keys_alt and their count in
-// counters[C_UNIQUE] (device); returns after sync #2 with the raw count.
+// counters[C_UNIQUE] (device); one host sync (edge/extras counts, non-finite
+// check).  With h_src, d_pts is an uninitialised device buffer of n x d floats
+// that this call fills from the host in row chunks on c.copy, overlapped with
+// the sampler and (L2-blocked case) with the gather of the chunks already in.
 int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64_t n, uint32_t d,
                 double eps, double rate, uint64_t seed, uint64_t rb, uint64_t re,
-                GraphResult& gr) {
+                GraphResult& gr, const float* h_src = nullptr) {
     unsigned long long* dc = nullptr;
     c.counters.ensure(C_COUNT * sizeof(unsigned long long));
     dc = c.counters.as<unsigned long long>();
     CK(cudaMemsetAsync(dc, 0, C_COUNT * sizeof(unsigned long long), s));
 
     // ---- points: padded device layout + finiteness (dataset.hpp:24-26) ----
+    // The non-finite count is checked at the one host sync below (a rejected
+    // dataset costs a wasted graph build, never a wrong answer: NaN rows fail
+    // every eps-test).
     const uint32_t stride = d <= 2 ? 2u : ((d + 3u) & ~3u);
     const size_t align = stride == 2 ? 8 : 16;
-    const float* pts = d_pts;
-    if (stride != d || (reinterpret_cast<uintptr_t>(d_pts) % align) != 0) {
-        c.pts.ensure(n * stride * sizeof(float));
-        CK(launch_prepare_points(d_pts, c.pts.as<float>(), n, d, stride, dc, s));
-        pts = c.pts.as<float>();
-    } else {
-        CK(launch_prepare_points(d_pts, nullptr, n, d, stride, dc, s));
-    }
-    CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (c.h_counters[C_NONFINITE]) return SNGB_ERR_NONFINITE;
-    tm.mark(E_PREPARED);
+    const bool pad = stride != d || (reinterpret_cast<uintptr_t>(d_pts) % align) != 0;
+    if (pad) c.pts.ensure(n * stride * sizeof(float));
+    const float* pts = pad ? c.pts.as<float>() : d_pts;
+    auto prepare_rows = [&](uint64_t lo, uint64_t hi) {
+        if (hi > lo)
+            CK(launch_prepare_points(d_pts + lo * d, pad ? c.pts.as<float>() + lo * stride : nullptr,
+                                     hi - lo, d, stride, dc, s));
+    };
 
     // ---- sampling geometry (graph.cpp:138-140) ----
     const uint64_t draws = draws_for(n, rate);
@@ -328,6 +338,26 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
 
     const TestParams tp = make_test(pts, stride, d, eps);
     const uint64_t seed_mixed = seed_part(seed);
+    const uint32_t phases = gather_phases(c, n, stride, draws);
+
+    // ---- host upload in row chunks (chunk k = L2 phase k when phased) ----
+    const uint32_t chunks = h_src ? std::min<uint32_t>(phases, DevCtx::kMaxChunks) : 1;
+    auto chunk_lo = [&](uint32_t k) { return n * k / chunks; };
+    // issued after the sampler launch: a pageable source blocks the host while
+    // it is staged, and the sampler should already be running by then
+    auto start_upload = [&]() {
+        CK(cudaEventRecord(c.up_start, s));  // after the caller's prior work on s
+        CK(cudaStreamWaitEvent(c.copy, c.up_start, 0));
+        for (uint32_t k = 0; k < chunks; ++k) {
+            const uint64_t lo = chunk_lo(k), hi = chunk_lo(k + 1);
+            CK(cudaMemcpyAsync(const_cast<float*>(d_pts) + lo * d, h_src + lo * d,
+                               (hi - lo) * d * sizeof(float), cudaMemcpyHostToDevice, c.copy));
+            CK(cudaEventRecord(c.up_ev[k], c.copy));
+        }
+        tm.mark_on(E_UPLOADED, c.copy);
+    };
+    if (!h_src) prepare_rows(0, n);
+    tm.mark(E_PREPARED);
 
     for (int attempt = 0; attempt < 4; ++attempt) {
         c.keys.ensure(edge_cap * 8);
@@ -343,6 +373,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         const uint64_t ov = env_u64("SNGB_OVERLAP", 2);  // 0 off, 1 on, 2 auto
         const bool overlap =
             !exhaustive && (ov == 1 || (ov == 2 && stride >= 8 && stride <= 64 && (re - rb) >= 200000));
+        // host upload: the sampler reads no points, so it also runs while they arrive
+        const bool side = !exhaustive && (overlap || (h_src && attempt == 0));
         if (!exhaustive) {
             SamplerArgs sa{};
             sa.n = n;
@@ -358,11 +390,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             sa.extras = c.extras.as<unsigned long long>();
             sa.extras_capacity = extras_cap;
             sa.counters = dc;
-            if (overlap) {
+            if (side) {
                 // the Floyd bookkeeping needs no point data: run it on the side
                 // stream while the gather runs here; non-persistent grids let the
                 // block scheduler interleave the two kernels on every SM
-                sa.rows_per_block = 32;
+                sa.rows_per_block = overlap ? 32 : 0;
                 CK(cudaEventRecord(c.fork, s));
                 CK(cudaStreamWaitEvent(c.side, c.fork, 0));
                 tm.mark_on(E_SIDE0, c.side);
@@ -374,6 +406,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 CK(launch_sampler(sa, s, c.num_sms));
             }
         }
+        if (h_src && attempt == 0) start_upload();
         tm.mark(E_SAMPLED);
         GatherArgs ga{};
         ga.tp = tp;
@@ -390,14 +423,34 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         // L2-blocked phases: each launch tests only partners in one slice of
         // the rows, small enough to stay L2-resident while every vertex's
         // draws are regenerated (cheap) and its query row streamed.
-        const uint32_t phases = gather_phases(c, n, stride, draws);
-        for (uint32_t ph = 0; ph < phases; ++ph) {
-            ga.part_lo = (uint32_t)(n * ph / phases);
-            ga.part_hi = (uint32_t)(n * (ph + 1) / phases);
-            CK(launch_gather(ga, exhaustive, s, c.num_sms));
+        auto part = [&](uint32_t ph) { return (uint32_t)(n * ph / phases); };
+        auto gather = [&](uint64_t qlo, uint64_t qhi, uint32_t plo, uint32_t phi) {
+            ga.row_begin = std::max(rb, qlo);
+            ga.row_end = std::min(re, qhi);
+            ga.part_lo = plo;
+            ga.part_hi = phi;
+            if (ga.row_end > ga.row_begin) CK(launch_gather(ga, exhaustive, s, c.num_sms));
+        };
+        if (h_src && attempt == 0 && chunks == phases && phases > 1) {
+            // triangular schedule over (query chunk, partner slice) blocks:
+            // once chunk k is in, every block it completes can run -- queries
+            // <= k against slice k, then chunk k against the earlier slices
+            for (uint32_t k = 0; k < phases; ++k) {
+                CK(cudaStreamWaitEvent(s, c.up_ev[k], 0));
+                prepare_rows(chunk_lo(k), chunk_lo(k + 1));
+                gather(0, part(k + 1), part(k), part(k + 1));
+                for (uint32_t j = 0; j < k; ++j) gather(part(k), part(k + 1), part(j), part(j + 1));
+            }
+        } else {
+            if (h_src && attempt == 0)
+                for (uint32_t k = 0; k < chunks; ++k) {
+                    CK(cudaStreamWaitEvent(s, c.up_ev[k], 0));
+                    prepare_rows(chunk_lo(k), chunk_lo(k + 1));
+                }
+            for (uint32_t ph = 0; ph < phases; ++ph) gather(rb, re, part(ph), part(ph + 1));
         }
         tm.mark(E_GATHERED);  // gather kernel(s) done (concurrent with the sampler)
-        if (overlap) CK(cudaStreamWaitEvent(s, c.join, 0));  // extras need the sampler
+        if (side) CK(cudaStreamWaitEvent(s, c.join, 0));  // extras need the sampler
         if (!exhaustive) {
             ExtrasArgs ea{};
             ea.tp = tp;
@@ -412,6 +465,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        if (c.h_counters[C_NONFINITE]) return SNGB_ERR_NONFINITE;
         const uint64_t need_e = c.h_counters[C_EDGE_CURSOR];
         const uint64_t need_x = c.h_counters[C_EXTRA_CURSOR];
         const bool ok = need_e <= edge_cap && (exhaustive || need_x <= extras_cap);
@@ -515,8 +569,8 @@ int guarded(F&& f) {
 // Full pipeline on device buffers; labels/roles device pointers.
 int dbscan_device(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64_t n, uint32_t d,
                   double eps, int32_t min_pts, double rate, uint64_t seed, int32_t* d_labels,
-                  uint8_t* d_roles, GraphResult& gr) {
-    int rc = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, 0, n, gr);
+                  uint8_t* d_roles, GraphResult& gr, const float* h_src = nullptr) {
+    int rc = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, 0, n, gr, h_src);
     if (rc) return rc;
     ClusterBuffers b{};
     ensure_cluster_bufs(c, n, b);
@@ -643,13 +697,12 @@ int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_
         Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
         tm.mark(E_START);
         c.upload.ensure(n * d * sizeof(float));
-        CK(cudaMemcpyAsync(c.upload.p, pts, n * d * sizeof(float), cudaMemcpyHostToDevice, s));
-        tm.mark(E_UPLOADED);
         c.labels.ensure(n * 4);
         c.roles.ensure(n);
         GraphResult gr;
+        // the upload is chunked and overlapped inside build_graph
         int r = dbscan_device(c, s, tm, c.upload.as<float>(), n, d, eps, min_pts, rate, seed,
-                              c.labels.as<int32_t>(), c.roles.as<uint8_t>(), gr);
+                              c.labels.as<int32_t>(), c.roles.as<uint8_t>(), gr, pts);
         if (r) return r;
         CK(cudaMemcpyAsync(labels_out, c.labels.p, n * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(roles_out, c.roles.p, n, cudaMemcpyDeviceToHost, s));
@@ -722,10 +775,9 @@ int sngb_sampled_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps,
         Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
         tm.mark(E_START);
         c.upload.ensure(n * d * sizeof(float));
-        CK(cudaMemcpyAsync(c.upload.p, pts, n * d * sizeof(float), cudaMemcpyHostToDevice, s));
-        tm.mark(E_UPLOADED);
         GraphResult gr;
-        int r = build_graph(c, s, tm, c.upload.as<float>(), n, d, eps, rate, seed, rb, re, gr);
+        int r = build_graph(c, s, tm, c.upload.as<float>(), n, d, eps, rate, seed, rb, re, gr,
+                            pts);
         if (r) return r;
         tm.mark(E_CLUSTERED);
         unsigned long long* dc = c.counters.as<unsigned long long>();

@@ -152,3 +152,56 @@ def test_forced_irregular_vertices_exact(oracle, monkeypatch, n, d, eps, rate, s
     assert info.gpu["irregular_vertices"] >= (n + 6) // 7  # + list-overflow replays
     ol, orl, _, _ = oracle.sng_dbscan(pts, eps, 3, rate, seed)
     np.testing.assert_array_equal(c.assignment, ol)
+
+
+def _host_edges_rows(pts, eps, rate, seed, rb, re):
+    """sngb_sampled_edges_f32 (host buffers) over the query rows [rb, re)."""
+    import ctypes as C
+    from paper_2006_06743_b200 import _lib
+    n, d = pts.shape
+    cap = 1 << 22
+    keys = np.empty(cap, np.uint64)
+    cnt = C.c_uint64(0)
+    o = _lib.SngbOpts(-1, 0, None, rb, re)
+    rc = _lib.lib().sngb_sampled_edges_f32(pts.ctypes.data_as(C.POINTER(C.c_float)), n, d, eps,
+                                           rate, seed, C.byref(o),
+                                           keys.ctypes.data_as(C.POINTER(C.c_uint64)), cap,
+                                           C.byref(cnt), None)
+    sng._check(rc)
+    return keys[: cnt.value]
+
+
+@pytest.mark.parametrize("phases", [1, 2, 3, 4])
+@pytest.mark.parametrize("cfg,n,d", [(2, 3000, 784), (3, 20000, 16)])
+def test_chunked_host_upload_matches_oracle(oracle, monkeypatch, phases, cfg, n, d):
+    """Host-buffer calls upload the points in row chunks on a copy stream; with
+    L2 phases forced, the gather runs as the triangular (query chunk x
+    partner slice) schedule as chunks arrive.  Same results as the oracle."""
+    monkeypatch.setenv("SNGB_GATHER_PHASES", str(phases))
+    w = synthetic.CONFIGS[cfg]
+    pts = synthetic.generate(cfg, n=n)
+    rate = min(1.0, 4 * w.draws / n)
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=w.eps, min_pts=w.min_pts, rate=rate,
+                                                       seed=w.seed), info)
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, w.eps, w.min_pts, rate, w.seed)
+    _assert_same(c, info, labels, roles, oinfo)
+    rb, re = n // 3, 2 * n // 3 + 5
+    okeys, _ = oracle.sampled_edges_rows(pts, w.eps, rate, w.seed, rb, re)
+    np.testing.assert_array_equal(_host_edges_rows(pts, w.eps, rate, w.seed, rb, re), okeys)
+
+
+def test_nonfinite_rejected_after_deferred_check():
+    """The finiteness check is read at the one host sync; the error is still
+    the reference's (dataset.hpp:24-26), on both the host and device paths."""
+    import torch
+    pts = synthetic.generate(1, n=2000)
+    pts[1234, 1] = np.nan
+    with pytest.raises(sng.InvalidArgument, match="non-finite"):
+        _host_edges_rows(pts, 0.03, 0.1, 1, 0, 0)  # raw C ABI, host buffers
+    with pytest.raises(sng.InvalidArgument, match="non-finite"):
+        sng.sng_dbscan_device(torch.from_numpy(pts).cuda(), 0.03, 10, 0.1, 1)
+    # the library is still usable afterwards
+    pts[1234, 1] = 0.5
+    labels, _, _ = sng.sng_dbscan_device(torch.from_numpy(pts).cuda(), 0.03, 10, 0.1, 1)
+    assert labels.numel() == 2000
