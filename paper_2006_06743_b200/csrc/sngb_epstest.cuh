@@ -56,6 +56,41 @@ __device__ __forceinline__ float diff2(float2 a, float2 b, float acc) {
     return fmaf(t, t, acc);
 }
 
+// Packed-pair variant (sm_100 FADD2/FFMA2): a 16-byte row chunk as two
+// f32x2 registers; half the FP instructions of diff2 and two independent
+// accumulator pairs instead of one serial chain.  Any summation order and
+// fusing is inside the guard band (make_test).
+struct F4x2 {
+    unsigned long long lo, hi;  // {x, y}, {z, w}
+};
+__device__ __forceinline__ F4x2 ldg_row2(const float4* p) {
+    F4x2 r;
+    asm("ld.global.nc.v2.b64 {%0, %1}, [%2];" : "=l"(r.lo), "=l"(r.hi) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ F4x2 to_x2(float4 v) {
+    F4x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.lo) : "f"(v.x), "f"(v.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.hi) : "f"(v.z), "f"(v.w));
+    return r;
+}
+struct Acc2 {
+    unsigned long long xy = 0, zw = 0;  // two f32x2 accumulators (+0.0f each)
+};
+__device__ __forceinline__ void diff2x2(const F4x2& a, const F4x2& b, Acc2& acc) {
+    unsigned long long d0, d1;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d0) : "l"(a.lo), "l"(b.lo));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d1) : "l"(a.hi), "l"(b.hi));
+    asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc.xy) : "l"(d0));
+    asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc.zw) : "l"(d1));
+}
+__device__ __forceinline__ float acc2_sum(const Acc2& acc) {
+    float x, y, z, w;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(acc.xy));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(z), "=f"(w) : "l"(acc.zw));
+    return (x + y) + (z + w);
+}
+
 // Canonical key of the undirected edge {u, v} (graph.cpp:183-186: min, max).
 __device__ __forceinline__ unsigned long long edge_key(uint64_t u, uint64_t v, uint32_t nb) {
     const uint64_t a = u < v ? u : v, b = u < v ? v : u;

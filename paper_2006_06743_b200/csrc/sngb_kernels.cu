@@ -180,35 +180,62 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
                 nlive += __popc(m);
             }
             __syncwarp();
-            // ---- eps-test the live pairs, NG groups x U pairs per step ----
+            // ---- eps-test the live pairs, U per step (G = 32: a warp per row) ----
+            // Loads are unconditional except the last float4 column (V =
+            // ceil(W/32), so columns < V-1 are always inside the row); a tail
+            // step re-reads a live partner and ignores the result.  The U
+            // partial sums are reduce-scattered (transposed butterfly: U-1 +
+            // log2(32/U) shuffles for U pairs), leaving pair k's total in lane
+            // k*32/U, which alone decides and emits it.
+            if constexpr (G == 32 && !F2) {
+            constexpr int SPAN = 32 / U;  // lanes per pair after the scatter
+            F4x2 q2[V];
+#pragma unroll
+            for (int vv = 0; vv < V; ++vv) q2[vv] = to_x2(qv[vv]);
 #pragma unroll 1
-            for (uint32_t j0 = 0; j0 < nlive; j0 += NG * U) {
-                Vec rows[U][V];
-                uint32_t pvv[U];
-                bool ok[U];
+            for (uint32_t j0 = 0; j0 < nlive; j0 += U) {
+                F4x2 rows[U][V];
 #pragma unroll
                 for (int uu = 0; uu < U; ++uu) {
-                    const uint32_t j = j0 + NG * uu + g;
-                    ok[uu] = j < nlive;
-                    pvv[uu] = ok[uu] ? list[j] : 0u;
+                    const uint32_t j = j0 + uu;
+                    const uint32_t pv = list[j < nlive ? j : j0];
+                    const Vec* row = P + (uint64_t)pv * W + lane;
 #pragma unroll
                     for (int vv = 0; vv < V; ++vv) {
-                        const uint32_t c = q + G * vv;
-                        rows[uu][vv] = (ok[uu] && c < W) ? ldg_row(P + (uint64_t)pvv[uu] * W + c)
-                                                         : vzero<Vec>();
+                        if (vv < V - 1 || lane + 32 * vv < W) rows[uu][vv] = ldg_row2(row + 32 * vv);
+                        else rows[uu][vv] = q2[vv];  // outside the row: contributes 0
+                    }
+                }
+                // scheduling fence: keeps all U*V loads in flight together
+                // (ptxas otherwise sinks each next to its use to save registers)
+                __syncwarp();
+                float ps[U];
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    Acc2 acc;
+#pragma unroll
+                    for (int vv = 0; vv < V; ++vv) diff2x2(q2[vv], rows[uu][vv], acc);
+                    ps[uu] = acc2_sum(acc);
+                }
+#pragma unroll
+                for (int o = 16, m = U; m > 1; o >>= 1, m >>= 1) {
+                    const bool hi = (lane & o) != 0;
+#pragma unroll
+                    for (int k = 0; k < m / 2; ++k) {
+                        const float mine = hi ? ps[k + m / 2] : ps[k];
+                        const float other = hi ? ps[k] : ps[k + m / 2];
+                        ps[k] = mine + __shfl_xor_sync(kFull, other, o);
                     }
                 }
 #pragma unroll
-                for (int uu = 0; uu < U; ++uu) {
-                    float s = 0.f;
-#pragma unroll
-                    for (int vv = 0; vv < V; ++vv) s = diff2(qv[vv], rows[uu][vv], s);
-#pragma unroll
-                    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-                    const bool acc = decide(s, ok[uu], leader, leader_lane, a.tp, u, pvv[uu], st);
-                    if (ok[uu] && leader) ++gpairs;
-                    stage.push(leader && acc, edge_key(u, pvv[uu], a.sink.nb), a.sink, lane);
-                }
+                for (int o = SPAN / 2; o > 0; o >>= 1) ps[0] += __shfl_xor_sync(kFull, ps[0], o);
+                const uint32_t pj = j0 + lane / SPAN;
+                const bool okm = (lane % SPAN) == 0 && pj < nlive;
+                const uint32_t pm = list[okm ? pj : j0];
+                const bool acc = decide_lane(ps[0], okm, a.tp, u, pm, st);
+                gpairs += okm ? 1u : 0u;
+                stage.push(acc, edge_key(u, pm, a.sink.nb), a.sink, lane);
+            }
             }
             __syncwarp();
         }
