@@ -1,6 +1,10 @@
 """Build libsngb.so (the C-ABI library) in-tree for sm_100a.
 
     python -m paper_2006_06743_b200.build [--verbose]
+    python -m paper_2006_06743_b200.build --variant NAME -DMACRO=1 ...   (A/B builds)
+
+A variant compiles with the extra nvcc flags into build/NAME/ and links
+tools/ab/libsngb_NAME.so (select it at run time with SNGB_LIBRARY=...).
 
 Objects are compiled in parallel with nvcc and linked into
 paper_2006_06743_b200/lib/libsngb.so, which travels to the GPU box with the
@@ -39,12 +43,12 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+def _compile(src: str, verbose: bool, obj_dir: str = OBJ, extra: tuple = ()) -> str:
+    obj = os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + \
         [os.path.join(ROOT, "include", "sngb.h")]
     if _stale(obj, deps):
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
@@ -52,17 +56,31 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+def build(verbose: bool = False, variant: str | None = None, extra: tuple = ()) -> str:
+    obj_dir = os.path.join(OBJ, variant) if variant else OBJ
+    lib = os.path.join(ROOT, "tools", "ab", f"libsngb_{variant}.so") if variant else LIB
+    os.makedirs(obj_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    if variant:  # always rebuild: the flags are not part of the staleness check
+        for src in SOURCES:
+            o = os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
+            if os.path.exists(o):
+                os.remove(o)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    if _stale(LIB, objs):
-        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
+        objs = list(ex.map(lambda s: _compile(s, verbose, obj_dir, tuple(extra)), SOURCES))
+    if variant or _stale(lib, objs):
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs,
                "-lcudart"]
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv))
+    argv = sys.argv[1:]
+    name = None
+    if "--variant" in argv:
+        i = argv.index("--variant")
+        name = argv[i + 1]
+        argv = argv[:i] + argv[i + 2:]
+    print(build(verbose="--verbose" in argv, variant=name,
+                extra=tuple(a for a in argv if a != "--verbose")))

@@ -86,7 +86,7 @@ struct DevCtx {
     cudaEvent_t fork = nullptr, join = nullptr;
     // host-buffer calls: the points are uploaded in row chunks on `copy`,
     // chunk k's arrival is up_ev[k]; compute starts on the first chunk
-    static constexpr int kMaxChunks = 8;
+    static constexpr int kMaxChunks = 16;
     cudaStream_t copy = nullptr;
     cudaEvent_t up_start = nullptr;
     cudaEvent_t up_ev[kMaxChunks] = {};
@@ -262,8 +262,11 @@ uint32_t gather_phases(const DevCtx& c, uint64_t n, uint32_t stride, uint64_t dr
     const uint64_t table = n * stride * 4ull;
     const uint64_t slice = env_u64("SNGB_L2_PHASE_BYTES", (uint64_t)(0.5 * c.l2_bytes));
     if (slice == 0 || table <= slice || stride < 64 || draws == 0) return 1;
+    // a phase re-generates every draw: ~1.2e-12 s per pair against ~2.3e-13*d s
+    // of gather, so wider rows afford more phases (d = 1000: 0.5 % each)
     const uint64_t p = (table + slice - 1) / slice;
-    return p <= 4 ? (uint32_t)p : 1u;
+    const uint64_t cap = std::min<uint64_t>(16, std::max<uint64_t>(2, stride / 32));
+    return p <= cap ? (uint32_t)p : 1u;
 }
 
 struct GraphResult {

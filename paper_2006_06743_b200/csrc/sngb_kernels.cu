@@ -57,8 +57,21 @@ struct Unroll {
 // run the gather as L2-blocked phases (one slice of the rows per launch) when
 // the row table is a small multiple of L2; a single phase covers [0, n).
 // ---------------------------------------------------------------------------
+// Resident blocks per SM that ptxas must leave room for.  Wide rows (G = 32)
+// get up to 128 registers for two rows in flight per warp (measured:
+// 126 registers and 8.8 ms on cfg2 vs 112 and 9.3 ms under the default
+// heuristic); narrow rows keep the occupancy their latency-bound gathers need.
+#ifndef SNGB_WIDE_MINB
+#define SNGB_WIDE_MINB 1
+#endif
+template <int G, int V>
+struct MinBlocks {
+    static constexpr int value =
+        G == 32 ? (V == 8 ? 2 : SNGB_WIDE_MINB) : (G == 16 ? 2 : (G == 8 ? 3 : 4));
+};
+
 template <int G, int V, int R, bool F2, bool EXH>
-__global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
+__global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const GatherArgs a) {
     using Vec = typename std::conditional<F2, float2, float4>::type;
     constexpr int NG = 32 / G;
     constexpr int U = Unroll<G, V, R>::value;
@@ -203,7 +216,7 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
 #pragma unroll
                     for (int vv = 0; vv < V; ++vv) {
                         if (vv < V - 1 || lane + 32 * vv < W) rows[uu][vv] = ldg_row2(row + 32 * vv);
-                        else rows[uu][vv] = q2[vv];  // outside the row: contributes 0
+                        else rows[uu][vv] = F4x2{0ull, 0ull};  // outside the row (query is 0 too)
                     }
                 }
                 // scheduling fence: keeps all U*V loads in flight together
