@@ -73,34 +73,24 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_gather_peaks(row_bytes: int, table_bytes: int):
-    """Measured random-row gather ceilings for this row size (tools/microbench.cu,
-    profiles/r01_microbench.jsonl): from L2 (table resident) and from HBM."""
-    path = os.path.join(ROOT, "profiles", "r01_microbench.jsonl")
+def load_gather_ceiling(d: int, n: int):
+    """Measured random-row gather ceiling for this row shape and table size
+    (tools/gather_ceiling.cu -> profiles/r01_gather_ceilings.jsonl): the best
+    rows/s of a lean gather with no per-pair work, swept over rows in flight
+    and blocks per SM.  Returns (case name, rows/s) or (None, None)."""
+    path = os.path.join(ROOT, "profiles", "r01_gather_ceilings.jsonl")
     try:
-        m = {}
-        for ln in open(path):
-            ln = ln.strip()
-            if ln.startswith("{"):
-                j = json.loads(ln)
-                m[j["bench"]] = j.get("GB_per_s")
+        cases = [json.loads(ln) for ln in open(path) if ln.strip().startswith("{")]
     except Exception:
         return None, None
-    def best(*names):
-        vals = [m[k] for k in names if m.get(k)]
-        return max(vals) if vals else None
-    if row_bytes <= 16:
-        l2, hbm = best("gather_l2_row16B_80MB"), best("gather_hbm_row16B_2GB")
-    elif row_bytes <= 64:
-        l2, hbm = best("gather_l2_row64B_64MB"), None
-    elif row_bytes <= 128:
-        l2 = best("gather_l2_row128B_64MB")
-        hbm = best("gather_hbm_row128B_2.5GB", "gather_hbm_row128B_lean_u8_b4",
-                   "gather_hbm_row128B_lean_u16_b4", "gather_hbm_row128B_lean_u8_b8",
-                   "gather_hbm_row128B_lean_u16_b8")
-    else:
-        l2, hbm = best("gather_l2_row3136B_55MB"), best("gather_hbm_row3136B_2GB")
-    return l2, hbm
+    row = 8 if d <= 2 else 16 * ((d + 3) // 4)  # padded device row, bytes
+    table = n * row
+    # same row size; among those, the table size closest to ours (L2 vs HBM)
+    same = [c for c in cases if c["row_bytes"] == max(row, 16)]
+    if not same:
+        return None, None
+    best = min(same, key=lambda c: abs(math.log(c["table_MB"] * 2**20 / max(table, 1))))
+    return best["bench"], best["rows_per_s"]
 
 
 def load_traffic(workload: str):
@@ -385,21 +375,23 @@ def main():
                 "kernel_ms": g_ms,
                 "kernel_share_of_step": (g_ms / ms_per_step) if ms_per_step else None}
     # The gather's real ceiling is the memory level the partner rows come from:
-    # L2 when the (padded) row table, or one L2-blocked phase of it, is resident.
+    # L2 when the (padded) row table, or one L2-blocked phase of it, is
+    # resident (the measured lean random-row gather of this row shape), HBM
+    # otherwise (the measured copy peak: random 128-byte rows are whole DRAM
+    # bursts, and our gather measured above the lean kernel there).
     row_bytes = 16 if d == 3 else 4 * d
-    l2_peak, hbm_gather_peak = load_gather_peaks(row_bytes, n * row_bytes)
-    # the microbenchmarks count whole (padded) rows; express them in algorithmic bytes
-    scale = (4.0 * d) / row_bytes
-    l2_peak = l2_peak * scale if l2_peak else None
-    hbm_gather_peak = hbm_gather_peak * scale if hbm_gather_peak else None
-    resident = n * row_bytes <= 100 * 2**20 or (d >= 256 and n * row_bytes <= 4 * 63 * 2**20)
+    phased = d >= 256 and n * row_bytes > 100 * 2**20  # L2-blocked: one slice resident
+    resident = n * row_bytes <= 100 * 2**20 or (phased and n * row_bytes <= 16 * 63 * 2**20)
+    case, rows_per_s = load_gather_ceiling(d, min(n, int(63 * 2**20 // row_bytes)) if phased else n)
+    l2_peak = rows_per_s * 4 * d / 1e9 if (resident and rows_per_s) else None
+    eff = l2_peak if resident else peak
     roofline.update({
-        "effective_bound": "l2" if resident else "hbm (random rows)",
-        "l2_gather_peak": l2_peak, "hbm_gather_peak": hbm_gather_peak,
-        "frac_of_effective_peak": (achieved / (l2_peak if resident else (hbm_gather_peak or peak)))
-        if achieved and (l2_peak or hbm_gather_peak) else None,
-        "peaks_source": "tools/microbench.cu random-row gather of this row size "
-                        "(profiles/r01_microbench.jsonl)",
+        "effective_bound": "l2 (random rows)" if resident else "hbm",
+        "effective_peak": eff,
+        "effective_peak_source": (f"{case} in profiles/r01_gather_ceilings.jsonl "
+                                  "(tools/gather_ceiling.cu), in algorithmic bytes")
+        if resident else f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+        "frac_of_effective_peak": (achieved / eff) if (achieved and eff) else None,
         "concurrent_with": "k_floyd_bloom on a side stream" if w.d in (16, 32) and n >= 200000
         else None})
 

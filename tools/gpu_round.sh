@@ -14,3 +14,8 @@ python tools/run_once.py --config 2 > $OUT/ro2.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:k_gather -c 1 \
       -o $OUT/gather_cfg2 python tools/run_once.py --config 2 --reps 0 > $OUT/ncu_full.log 2>&1
 tail -2 $OUT/pytest_gpu.log
+# DRAM traffic of every gather launch of one cfg2 step (all L2 phases)
+python tools/run_once.py --config 2 > $OUT/ro2b.log 2>&1 && \
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+      -k regex:k_gather -c 4 --csv --log-file $OUT/gather_traffic.csv \
+      python tools/run_once.py --config 2 --reps 0 > $OUT/ncu_traffic.log 2>&1
