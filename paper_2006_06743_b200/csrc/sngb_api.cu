@@ -83,6 +83,8 @@ struct DevCtx {
     uint64_t l2_bytes = 126ull << 20;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;          // sampler runs here, concurrently with the gather
+    cudaStream_t hi = nullptr;            // high-priority stream for the gather (SNGB_PRIO)
+    cudaEvent_t hi_fork = nullptr, hi_join = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     // host-buffer calls: the points are uploaded in row chunks on `copy`,
     // chunk k's arrival is up_ev[k]; compute starts on the first chunk
@@ -92,14 +94,14 @@ struct DevCtx {
     cudaEvent_t up_ev[kMaxChunks] = {};
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
-        flags, rank, temp, labels, roles;
+        flags, rank, temp, labels, roles, work;
     unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
     cudaEvent_t ev[12] = {};
     uint64_t edge_hint = 0;  // last needed edge capacity for this context
 
     void release() {
         for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
-                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles})
+                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work})
             b->release();
     }
 };
@@ -140,7 +142,12 @@ DevCtx& get_ctx(int dev) {
         CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
         c->l2_bytes = (uint64_t)l2;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        int prio_lo = 0, prio_hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
+        CK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, prio_hi));
+        CK(cudaEventCreateWithFlags(&c->hi_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->hi_join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
@@ -301,10 +308,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     const bool pad = stride != d || (reinterpret_cast<uintptr_t>(d_pts) % align) != 0;
     if (pad) c.pts.ensure(n * stride * sizeof(float));
     const float* pts = pad ? c.pts.as<float>() : d_pts;
+    cudaStream_t gs = s;  // the gather's stream (c.hi under SNGB_PRIO)
     auto prepare_rows = [&](uint64_t lo, uint64_t hi) {
         if (hi > lo)
             CK(launch_prepare_points(d_pts + lo * d, pad ? c.pts.as<float>() + lo * stride : nullptr,
-                                     hi - lo, d, stride, dc, s));
+                                     hi - lo, d, stride, dc, gs));
     };
 
     // ---- sampling geometry (graph.cpp:138-140) ----
@@ -368,14 +376,14 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         if (attempt > 0)
             CK(cudaMemsetAsync(dc, 0, C_UNIQUE * sizeof(unsigned long long), s));
         tm.mark(E_PREPARED);
-        // Run the sampler concurrently with the gather when both are large and
-        // use different resources (narrow rows: the gather is L2/HBM-latency
-        // bound, the sampler shared-memory/ALU bound).  Measured: cfg5 2.80 ->
-        // 2.44 s, cfg3 14.8 -> 13.4 ms; cfg4 (16-byte rows) neutral, small or
-        // wide-row problems lose.
-        const uint64_t ov = env_u64("SNGB_OVERLAP", 2);  // 0 off, 1 on, 2 auto
+        // Overlap: the sampler on the side stream concurrently with a
+        // non-persistent gather (SNGB_OVERLAP 0 off, 1 on, 2 auto).  Auto for
+        // large narrow-row problems, where it measured 2-3 % better than the
+        // sequential order with dynamic row claiming (cfg3, cfg4; cfg5 equal);
+        // small and wide-row problems lose.
+        const uint64_t ov = env_u64("SNGB_OVERLAP", 2);
         const bool overlap =
-            !exhaustive && (ov == 1 || (ov == 2 && stride >= 8 && stride <= 64 && (re - rb) >= 200000));
+            !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 200000));
         // host upload: the sampler reads no points, so it also runs while they arrive
         const bool side = !exhaustive && (overlap || (h_src && attempt == 0));
         if (!exhaustive) {
@@ -397,7 +405,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 // the Floyd bookkeeping needs no point data: run it on the side
                 // stream while the gather runs here; non-persistent grids let the
                 // block scheduler interleave the two kernels on every SM
-                sa.rows_per_block = overlap ? 32 : 0;
+                sa.rows_per_block = (uint32_t)env_u64("SNGB_SAMPLER_RPB", overlap ? 32 : 0);
                 CK(cudaEventRecord(c.fork, s));
                 CK(cudaStreamWaitEvent(c.side, c.fork, 0));
                 tm.mark_on(E_SIDE0, c.side);
@@ -422,7 +430,23 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         ga.base = (uint32_t)base;
         ga.seed_mixed = seed_mixed;
         ga.force_mod = test_force_mod();
-        ga.rows_per_block = overlap ? 8 * 16 : 0;
+        ga.rows_per_block = (uint32_t)env_u64("SNGB_GATHER_RPB", overlap ? 8 * 16 : 0);
+        // dynamic row claiming (persistent grid): one zeroed counter per launch
+        constexpr uint32_t kWorkSlots = 256;
+        const bool dyn = ga.rows_per_block == 0 && env_u64("SNGB_GATHER_DYN", 1) == 1;
+        uint32_t work_slot = 0;
+        if (dyn) {
+            c.work.ensure(kWorkSlots * 8);
+            CK(cudaMemsetAsync(c.work.p, 0, kWorkSlots * 8, s));
+        }
+        // SNGB_PRIO=1: gather on a high-priority stream, so the block scheduler
+        // prefers its blocks and the (low-priority) sampler fills the gaps
+        const bool prio = side && env_u64("SNGB_PRIO", 0) == 1;
+        if (prio) {
+            CK(cudaEventRecord(c.hi_fork, s));
+            CK(cudaStreamWaitEvent(c.hi, c.hi_fork, 0));
+            gs = c.hi;
+        }
         // L2-blocked phases: each launch tests only partners in one slice of
         // the rows, small enough to stay L2-resident while every vertex's
         // draws are regenerated (cheap) and its query row streamed.
@@ -432,14 +456,23 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             ga.row_end = std::min(re, qhi);
             ga.part_lo = plo;
             ga.part_hi = phi;
-            if (ga.row_end > ga.row_begin) CK(launch_gather(ga, exhaustive, s, c.num_sms));
+            if (ga.row_end <= ga.row_begin) return;
+            ga.work = nullptr;
+            if (dyn && work_slot < kWorkSlots) {
+                ga.work = c.work.as<unsigned long long>() + work_slot++;
+                // ~16 claims per resident warp, at most 32 rows per claim
+                const uint64_t warps = (uint64_t)c.num_sms * 64;
+                ga.grab = (uint32_t)std::max<uint64_t>(
+                    1, std::min<uint64_t>(32, (ga.row_end - ga.row_begin) / (warps * 16)));
+            }
+            CK(launch_gather(ga, exhaustive, gs, c.num_sms));
         };
         if (h_src && attempt == 0 && chunks == phases && phases > 1) {
             // triangular schedule over (query chunk, partner slice) blocks:
             // once chunk k is in, every block it completes can run -- queries
             // <= k against slice k, then chunk k against the earlier slices
             for (uint32_t k = 0; k < phases; ++k) {
-                CK(cudaStreamWaitEvent(s, c.up_ev[k], 0));
+                CK(cudaStreamWaitEvent(gs, c.up_ev[k], 0));
                 prepare_rows(chunk_lo(k), chunk_lo(k + 1));
                 gather(0, part(k + 1), part(k), part(k + 1));
                 for (uint32_t j = 0; j < k; ++j) gather(part(k), part(k + 1), part(j), part(j + 1));
@@ -447,10 +480,15 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         } else {
             if (h_src && attempt == 0)
                 for (uint32_t k = 0; k < chunks; ++k) {
-                    CK(cudaStreamWaitEvent(s, c.up_ev[k], 0));
+                    CK(cudaStreamWaitEvent(gs, c.up_ev[k], 0));
                     prepare_rows(chunk_lo(k), chunk_lo(k + 1));
                 }
             for (uint32_t ph = 0; ph < phases; ++ph) gather(rb, re, part(ph), part(ph + 1));
+        }
+        if (prio) {
+            CK(cudaEventRecord(c.hi_join, c.hi));
+            CK(cudaStreamWaitEvent(s, c.hi_join, 0));
+            gs = s;
         }
         tm.mark(E_GATHERED);  // gather kernel(s) done (concurrent with the sampler)
         if (side) CK(cudaStreamWaitEvent(s, c.join, 0));  // extras need the sampler

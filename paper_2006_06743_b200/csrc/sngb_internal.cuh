@@ -63,6 +63,8 @@ struct GatherArgs {
     uint32_t force_mod;   // test hook (0 = off), see test_fire()
     uint32_t part_lo, part_hi;  // partner rows tested by this launch (L2-blocked phases)
     uint32_t rows_per_block;    // 0: persistent grid; else one block per this many rows
+    unsigned long long* work;   // non-null: warps claim `grab` rows at a time from *work (zeroed)
+    uint32_t grab;
 };
 
 // Test hook (env SNGB_TEST_FORCE_IRREGULAR=m): pretend the Lemire reject
