@@ -18,9 +18,10 @@
 //       are then resolved in index order against the collided bitmap.  Every
 //       collided draw emits its replacement j_i as an extra.
 //
-// Filters and lists are double-buffered by vertex parity and each thread
-// clears the filter words its previous-vertex draws touched, so there are two
-// barriers per vertex and no table clears.  A list overflow or a Lemire reject
+// Filters and lists are double-buffered by vertex parity: while a vertex runs
+// on parity p, the workers clear parity p^1's filters with 16-byte stores (the
+// barriers of vertex u separate that clear from its reuse by vertex u+1), so
+// there are two barriers per vertex.  A list overflow or a Lemire reject
 // pre-condition replays the vertex exactly and sequentially.
 #pragma once
 
@@ -223,46 +224,42 @@ __global__ void __launch_bounds__(kBloomBlock) k_floyd_bloom(const SamplerArgs a
         }
     } else {
         // ---- workers: P1 filter bits + chain candidates, P2 group list ----
-        uint32_t prevw[MAXR];  // filter words touched by the previous vertex (parity 1-p)
-#pragma unroll
-        for (int r = 0; r < MAXR; ++r) prevw[r] = 0xffffffffu;
         uint32_t par = 0, vcount = 0;
+        const uint64_t dz = (uint64_t)kT * kGamma;  // counter step between a thread's draws
         for (uint64_t u = a.row_begin + blockIdx.x; u < a.row_end; u += gridDim.x) {
             par ^= 1u;
             if (++vcount > 2) bar_sync(kBarFree + par, kBloomBlock);  // parity par reusable
             uint32_t* f = filt + par * WB;
             uint32_t* sb = shared_bits + par * WB;
-            uint32_t* fo = filt + (par ^ 1u) * WB;
-            uint32_t* sbo = shared_bits + (par ^ 1u) * WB;
             unsigned long long* gl = glist + par * kGroupCap;
             uint32_t* cl = clist + par * kChainCap;
             uint32_t* cnt = s_cnt[par];
+            {  // clear the other parity's filters (last used by vertex u - 1)
+                uint4* fo = reinterpret_cast<uint4*>(filt + (par ^ 1u) * WB);
+                uint4* so = reinterpret_cast<uint4*>(shared_bits + (par ^ 1u) * WB);
+                const uint4 z4 = make_uint4(0, 0, 0, 0);
+                for (uint32_t w = tid; w < WB / 4; w += kT) {
+                    fo[w] = z4;
+                    so[w] = z4;
+                }
+            }
             const uint64_t key = vertex_key(a.seed_mixed, u);
+            uint64_t z = key + (uint64_t)(tid + 1) * kGamma;  // stream_at(key, i + 1), i = tid
 
             uint32_t tr[MAXR];
             bool fired = false;
 #pragma unroll
-            for (int r = 0; r < MAXR; ++r) {
+            for (int r = 0; r < MAXR; ++r, z += dz) {
                 const uint32_t i = tid + kT * r;
-                bool fi = false;
-                tr[r] = (i < D) ? lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fi) : 0u;
-                fired |= (i < D) && (fi || test_fire(a.force_mod, u, i, D));
-            }
-#pragma unroll
-            for (int r = 0; r < MAXR; ++r) {
-                if (prevw[r] != 0xffffffffu) {
-                    fo[prevw[r]] = 0;
-                    sbo[prevw[r]] = 0;
-                }
-                const uint32_t i = tid + kT * r;
-                prevw[r] = 0xffffffffu;
                 if (i < D) {
-                    const uint32_t t = tr[r];
+                    bool fi;
+                    const uint32_t t = lemire32(mix(z), base + i + 1, fi);
+                    fired |= fi | test_fire(a.force_mod, u, i, D);
+                    tr[r] = t;
                     const uint32_t h = (t * 0x9E3779B1u) >> shift;
                     const uint32_t w = h >> 5, bit = 1u << (h & 31);
-                    prevw[r] = w;
                     if (atomicOr(&f[w], bit) & bit) atomicOr(&sb[w], bit);
-                    if (t >= base && t - base < i) {
+                    if (t - base < i && t >= base) {
                         const uint32_t p = atomicAdd(&cnt[1], 1u);
                         if (p < kChainCap) cl[p] = i;
                     }
@@ -280,8 +277,6 @@ __global__ void __launch_bounds__(kBloomBlock) k_floyd_bloom(const SamplerArgs a
                 }
                 bar_sync(kBarWorkers, kT);
                 for (uint32_t s = tid; s < 4 * WB; s += kT) filt[s] = 0;
-#pragma unroll
-                for (int r = 0; r < MAXR; ++r) prevw[r] = 0xffffffffu;
                 bar_sync(kBarWorkers, kT);
                 bar_arrive(kBarReady + par, kBloomBlock);
             };
