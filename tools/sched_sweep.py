@@ -16,6 +16,7 @@ from paper_2006_06743_b200 import synthetic  # noqa: E402
 
 SETTINGS = {
     "default": {},
+    "sequential": {"SNGB_OVERLAP": "0"},
     "static_persistent": {"SNGB_GATHER_DYN": "0"},
     "nonpersistent_rpb128": {"SNGB_GATHER_RPB": "128"},
     "overlap_rpb128": {"SNGB_OVERLAP": "1"},
