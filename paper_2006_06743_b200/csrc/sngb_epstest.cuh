@@ -74,6 +74,32 @@ __device__ __forceinline__ F4x2 to_x2(float4 v) {
     asm("mov.b64 %0, {%1, %2};" : "=l"(r.hi) : "f"(v.z), "f"(v.w));
     return r;
 }
+// 8-byte rows (d <= 2): one f32x2 register per row.
+__device__ __forceinline__ unsigned long long ldg_b64(const float2* p) {
+    unsigned long long r;
+    asm("ld.global.nc.b64 %0, [%1];" : "=l"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ unsigned long long ldg_b64(const float4*) { return 0; }  // unused
+__device__ __forceinline__ F4x2 ldg_row2(const float2*) { return F4x2{0, 0}; }      // unused
+__device__ __forceinline__ unsigned long long to_x1(float2 v) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+    return r;
+}
+__device__ __forceinline__ unsigned long long to_x1(float4) { return 0; }  // unused
+__device__ __forceinline__ F4x2 to_x2(float2) { return F4x2{0, 0}; }       // unused
+__device__ __forceinline__ void diff1x2(unsigned long long a, unsigned long long b,
+                                        unsigned long long& acc) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc) : "l"(d));
+}
+__device__ __forceinline__ float acc1_sum(unsigned long long acc) {
+    float x, y;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(acc));
+    return x + y;
+}
 struct Acc2 {
     unsigned long long xy = 0, zw = 0;  // two f32x2 accumulators (+0.0f each)
 };

@@ -111,13 +111,26 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
 #pragma unroll
         for (int vv = 0; vv < V; ++vv) {
             const uint32_t c = q + G * vv;
-            qv[vv] = (c < W) ? (G == 32 ? ldg_stream(P + u * W + c) : ldg_row(P + u * W + c))
-                             : vzero<Vec>();
+            if constexpr (G == 32)
+                qv[vv] = (c < W) ? ldg_stream(P + u * W + c) : vzero<Vec>();
+            else  // narrow: past the row end, the last column (partners read it too)
+                qv[vv] = ldg_row(P + u * W + (c < W ? c : W - 1));
+        }
+        using QRow = typename std::conditional<F2, unsigned long long, F4x2>::type;
+        QRow q2[G < 32 ? V : 1];
+        if constexpr (G < 32) {
+#pragma unroll
+            for (int vv = 0; vv < V; ++vv) {
+                if constexpr (F2) q2[vv] = to_x1(qv[vv]);
+                else q2[vv] = to_x2(qv[vv]);
+            }
         }
         uint32_t limit = EXH ? (uint32_t)(a.n - 1 - u) : a.draws;
-        const uint64_t key = EXH ? 0ull : vertex_key(a.seed_mixed, u);
+        // stream_at(key, i + 1) for i = i0 + 32k + lane, carried incrementally
+        // (nothing for ptxas to rematerialise from the vertex key per chunk)
+        uint64_t z = EXH ? 0ull : vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
 
-        for (uint32_t i0 = 0; i0 < limit; i0 += 32 * R) {
+        for (uint32_t i0 = 0; i0 < limit; i0 += 32 * R, z += (uint64_t)(32 * R) * kGamma) {
             uint32_t pv[R];
             if (!EXH) {
                 uint32_t first_fire = 0xffffffffu;
@@ -128,7 +141,7 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
                     bool fire = false;
                     uint32_t t = 0;
                     if (valid) {
-                        t = lemire32(stream_at(key, (uint64_t)i + 1), a.base + i + 1, fire);
+                        t = lemire32(mix(z + (uint64_t)(32 * k) * kGamma), a.base + i + 1, fire);
                         fire |= test_fire(a.force_mod, u, i, a.draws);
                     }
                     pv[k] = t + (t >= (uint32_t)u ? 1u : 0u);
@@ -137,32 +150,47 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
                 }
                 if (first_fire != 0xffffffffu) limit = first_fire;  // irregular: cut here
             }
-            if (G < 32) {
-                // narrow rows: every lane's draw is one pair; group g takes the
-                // pairs of lanes g + NG*m straight from registers (no staging)
+            if constexpr (G < 32) {
+                // Narrow rows: every lane's draw is one pair; group g takes the
+                // pairs of lanes g + NG*m straight from registers (no staging).
+                // All R*G rows of the chunk are loaded before any is used (a
+                // warp-sync fence keeps ptxas from sinking them), so R*G*V
+                // 16-byte loads per lane are in flight together.  A masked pair
+                // (tail, other partner slice) reads the query row itself, and a
+                // lane past the row end reads the row's last column for both
+                // query and partner, so neither needs a zero-fill and both add 0.
+                constexpr int UG = G;
+                uint32_t pvk[R];
+                unsigned vmk[R], any = 0;
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const uint32_t i = i0 + 32 * k + lane;
-                    const uint32_t p = EXH ? (uint32_t)u + 1 + i : pv[k];
-                    const unsigned vm = __ballot_sync(kFull, i < limit && p >= plo && p < phi);
-                    if (vm == 0) continue;
-                    constexpr int UG = G < 32 ? G : 1;
-                    Vec rows[UG][V];
-                    uint32_t pvv[UG];
-                    bool ok[UG];
+                    pvk[k] = EXH ? (uint32_t)u + 1 + i : pv[k];
+                    vmk[k] = __ballot_sync(kFull, i < limit && pvk[k] >= plo && pvk[k] < phi);
+                    any |= vmk[k];
+                }
+                if (any == 0) continue;
+                using Row = typename std::conditional<F2, unsigned long long, F4x2>::type;
+                Row rows[R][UG][V];
+#pragma unroll
+                for (int k = 0; k < R; ++k)
 #pragma unroll
                     for (int uu = 0; uu < UG; ++uu) {
                         const int src = (G == 1) ? lane : (g + NG * uu);
-                        pvv[uu] = (G == 1) ? p : __shfl_sync(kFull, p, src);
-                        ok[uu] = (vm >> src) & 1u;
+                        const uint32_t pp = (G == 1) ? pvk[k] : __shfl_sync(kFull, pvk[k], src);
+                        const bool ok = (vmk[k] >> src) & 1u;
 #pragma unroll
                         for (int vv = 0; vv < V; ++vv) {
                             const uint32_t c = q + G * vv;
-                            rows[uu][vv] = (ok[uu] && c < W)
-                                               ? ldg_row(P + (uint64_t)pvv[uu] * W + c)
-                                               : vzero<Vec>();
+                            const uint64_t row = (ok && c < W) ? pp : u;
+                            const Vec* ptr = P + row * W + (c < W ? c : W - 1);
+                            if constexpr (F2) rows[k][uu][vv] = ldg_b64(ptr);
+                            else rows[k][uu][vv] = ldg_row2(ptr);
                         }
                     }
+                __syncwarp();  // scheduling fence (see the wide-row path)
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
                     // partial sums of the G pairs of this group, then a
                     // transposed reduce-scatter (G-1 shuffles for G pairs instead
                     // of log2(G) per pair): lane q ends with the total of pair q,
@@ -170,10 +198,17 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
                     float ps[UG];
 #pragma unroll
                     for (int uu = 0; uu < UG; ++uu) {
-                        float s = 0.f;
+                        if constexpr (F2) {
+                            unsigned long long acc = 0;
 #pragma unroll
-                        for (int vv = 0; vv < V; ++vv) s = diff2(qv[vv], rows[uu][vv], s);
-                        ps[uu] = s;
+                            for (int vv = 0; vv < V; ++vv) diff1x2(q2[vv], rows[k][uu][vv], acc);
+                            ps[uu] = acc1_sum(acc);
+                        } else {
+                            Acc2 acc;
+#pragma unroll
+                            for (int vv = 0; vv < V; ++vv) diff2x2(q2[vv], rows[k][uu][vv], acc);
+                            ps[uu] = acc2_sum(acc);
+                        }
                     }
 #pragma unroll
                     for (int o = UG / 2; o > 0; o >>= 1) {
@@ -186,8 +221,8 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
                         }
                     }
                     const int src = (G == 1) ? lane : (g + NG * q);  // my pair's draw lane
-                    const uint32_t pm = (G == 1) ? p : __shfl_sync(kFull, p, src);
-                    const bool okm = (vm >> src) & 1u;
+                    const uint32_t pm = (G == 1) ? pvk[k] : __shfl_sync(kFull, pvk[k], src);
+                    const bool okm = (vmk[k] >> src) & 1u;
                     const bool acc = decide_lane(ps[0], okm, a.tp, u, pm, st);
                     gpairs += okm ? 1u : 0u;
                     stage.push(acc, edge_key(u, pm, a.sink.nb), a.sink, lane);
@@ -215,9 +250,9 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
             // k*32/U, which alone decides and emits it.
             if constexpr (G == 32 && !F2) {
             constexpr int SPAN = 32 / U;  // lanes per pair after the scatter
-            F4x2 q2[V];
+            F4x2 qw[V];
 #pragma unroll
-            for (int vv = 0; vv < V; ++vv) q2[vv] = to_x2(qv[vv]);
+            for (int vv = 0; vv < V; ++vv) qw[vv] = to_x2(qv[vv]);
 #pragma unroll 1
             for (uint32_t j0 = 0; j0 < nlive; j0 += U) {
                 F4x2 rows[U][V];
@@ -240,7 +275,7 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
                 for (int uu = 0; uu < U; ++uu) {
                     Acc2 acc;
 #pragma unroll
-                    for (int vv = 0; vv < V; ++vv) diff2x2(q2[vv], rows[uu][vv], acc);
+                    for (int vv = 0; vv < V; ++vv) diff2x2(qw[vv], rows[uu][vv], acc);
                     ps[uu] = acc2_sum(acc);
                 }
 #pragma unroll
@@ -384,7 +419,9 @@ template <bool EXH>
 cudaError_t gather_dispatch(const GatherArgs& a, cudaStream_t s, int num_sms) {
     if (a.tp.stride == 2) return gather_one<1, 1, 4, true, EXH>(a, s, num_sms);
     const uint32_t W = a.tp.stride / 4;
-    if (W == 1) return gather_one<1, 1, 4, false, EXH>(a, s, num_sms);
+    // 16-byte rows: 2 chunks of 32 draws per step (R = 4 spilled at 64 registers
+    // and measured 37 % slower on cfg4)
+    if (W == 1) return gather_one<1, 1, 2, false, EXH>(a, s, num_sms);
     if (W <= 2) return gather_one<2, 1, 2, false, EXH>(a, s, num_sms);
     if (W <= 4) return gather_one<4, 1, 1, false, EXH>(a, s, num_sms);
     if (W <= 8) return gather_one<8, 1, 1, false, EXH>(a, s, num_sms);
