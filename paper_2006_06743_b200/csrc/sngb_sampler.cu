@@ -289,8 +289,11 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
         a.key_bits = bg.bits_log2;
         a.col_words = bg.col_words;
         const size_t smem = bloom_smem_bytes(bg);
-        auto k = D <= 1024   ? k_floyd_bloom<4>
+        // draws per worker thread = ceil(D / 256), every slot computed
+        auto k = D <= 768    ? k_floyd_bloom<3>
+                 : D <= 1024 ? k_floyd_bloom<4>
                  : D <= 2048 ? k_floyd_bloom<8>
+                 : D <= 2560 ? k_floyd_bloom<10>
                  : D <= 3072 ? k_floyd_bloom<12>
                              : k_floyd_bloom<16>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
