@@ -38,15 +38,30 @@ __device__ __forceinline__ void decode(unsigned long long k, uint32_t nb, uint32
 
 // Edge-centric kernels read the edge count from the device (m_ptr: the
 // DeviceSelect output, no host round trip) or, when m_ptr is null, take m_host.
+// Sorted keys come in runs of equal smaller endpoint a (~E/n long), so the
+// edge kernels give each thread kRun consecutive keys: one atomic per run of a
+// for the degree, and union-find keeps a's root across the run.
+constexpr int kRun = 8;
+
 __global__ void k_degrees(const unsigned long long* __restrict__ keys, const unsigned long long* m_ptr,
                           uint64_t m_host, uint32_t nb, uint32_t* deg) {
     const uint64_t m = m_ptr ? *m_ptr : m_host;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t a, b;
-        decode(keys[e], nb, a, b);
-        atomicAdd(&deg[a], 1u);
-        atomicAdd(&deg[b], 1u);
+    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c * kRun < m;
+         c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t e1 = (c + 1) * kRun < m ? (c + 1) * kRun : m;
+        uint32_t run_a = 0xffffffffu, run = 0;
+        for (uint64_t e = c * kRun; e < e1; ++e) {
+            uint32_t a, b;
+            decode(keys[e], nb, a, b);
+            if (a != run_a) {
+                if (run) atomicAdd(&deg[run_a], run);
+                run_a = a;
+                run = 0;
+            }
+            ++run;
+            atomicAdd(&deg[b], 1u);
+        }
+        if (run) atomicAdd(&deg[run_a], run);
     }
 }
 
@@ -80,20 +95,29 @@ __global__ void k_union(const unsigned long long* __restrict__ keys, const unsig
                         uint64_t m_host, uint32_t nb, const uint8_t* __restrict__ core,
                         uint32_t* parent) {
     const uint64_t m = m_ptr ? *m_ptr : m_host;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t a, b;
-        decode(keys[e], nb, a, b);
-        if (!core[a] || !core[b]) continue;
-        for (;;) {
-            uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
-            if (ra == rb) break;
-            if (ra > rb) {
-                const uint32_t t = ra;
-                ra = rb;
-                rb = t;
+    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c * kRun < m;
+         c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t e1 = (c + 1) * kRun < m ? (c + 1) * kRun : m;
+        uint32_t run_a = 0xffffffffu, ra = 0;
+        for (uint64_t e = c * kRun; e < e1; ++e) {
+            uint32_t a, b;
+            decode(keys[e], nb, a, b);
+            if (!core[a] || !core[b]) continue;
+            if (a != run_a) {
+                run_a = a;
+                ra = uf_find(parent, a);
             }
-            if (atomicCAS(&parent[rb], rb, ra) == rb) break;
+            for (;;) {
+                // ra is in a's tree; walk up if another thread hooked it meanwhile
+                for (uint32_t p = parent[ra]; p != ra; p = parent[ra]) ra = p;
+                const uint32_t rb = uf_find(parent, b);
+                if (ra == rb) break;
+                const uint32_t lo = ra < rb ? ra : rb, hi = ra < rb ? rb : ra;
+                if (atomicCAS(&parent[hi], hi, lo) == hi) {
+                    ra = lo;  // the merged root (a's side may just have been hooked)
+                    break;
+                }
+            }
         }
     }
 }

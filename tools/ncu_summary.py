@@ -1,0 +1,87 @@
+"""Summarise an ncu --set full capture as markdown (key throughput, traffic,
+occupancy and stall metrics, plus the opcode mix).  Not part of the product.
+
+    python tools/ncu_summary.py REPORT.ncu-rep "title" [units_of_work] [unit_name]
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("launch__registers_per_thread", "registers / thread"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active (% of peak)"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active (%)"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput (% of peak)"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1 throughput (% of peak)"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate (%)"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+]
+
+
+def ncu_csv(rep, *args):
+    out = subprocess.run(["ncu", "-i", rep, *args, "--csv"], capture_output=True, text=True,
+                         check=True).stdout
+    return list(csv.reader(io.StringIO(out)))
+
+
+def main():
+    rep, title = sys.argv[1], sys.argv[2]
+    units = float(sys.argv[3]) if len(sys.argv) > 3 else None
+    uname = sys.argv[4] if len(sys.argv) > 4 else "unit"
+    raw = ncu_csv(rep, "--page", "raw")
+    hdr, unit_row, vals = raw[0], raw[1], raw[2]
+    kname = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
+    print(f"# {title}\n")
+    print(f"Kernel: `{kname}`  \nReport: `{rep}` (`ncu --set full --clock-control none`)\n")
+    print("| metric | value |\n|---|---|")
+    inst = None
+    for m, label in METRICS:
+        if m in hdr:
+            v, u = vals[hdr.index(m)], unit_row[hdr.index(m)]
+            print(f"| {label} (`{m}`) | {v} {u} |")
+            if m == "smsp__inst_executed.sum":
+                inst = float(v.replace(",", ""))
+    if units and inst:
+        print(f"| warp instructions per {uname} | {inst / units:.2f} |")
+    stalls = []
+    for i, h in enumerate(hdr):
+        if "issue_stalled" in h and h.endswith("per_issue_active.ratio"):
+            try:
+                stalls.append((float(vals[i]), h))
+            except ValueError:
+                pass
+    print("\nTop stall reasons (warps stalled per issued instruction):\n")
+    for v, h in sorted(stalls, reverse=True)[:6]:
+        name = h.replace("smsp__average_warps_issue_stalled_", "").replace(
+            "_per_issue_active.ratio", "")
+        print(f"- {name}: {v:.2f}")
+    src = ncu_csv(rep, "--page", "source", "--print-source", "sass")
+    shdr = src[1]
+    si, ei = shdr.index("Source"), shdr.index("Instructions Executed")
+    ops = collections.Counter()
+    tot = 0
+    for r in src[2:]:
+        try:
+            e = int(r[ei])
+        except (ValueError, IndexError):
+            continue
+        t = r[si].strip().split()
+        if not t:
+            continue
+        op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
+        ops[op] += e
+        tot += e
+    print("\nOpcode mix (share of executed warp instructions):\n")
+    print(", ".join(f"{o} {100 * e / tot:.1f} %" for o, e in ops.most_common(12)))
+
+
+if __name__ == "__main__":
+    main()
