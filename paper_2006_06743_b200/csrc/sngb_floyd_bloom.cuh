@@ -180,16 +180,11 @@ __global__ void __launch_bounds__(kBloomBlock) k_floyd_bloom(const SamplerArgs a
             uint32_t* cnt = s_cnt[par];
             const uint32_t ng = cnt[0], nc = cnt[1];
             if (ng || nc) {
-                // first occurrence per value: (t, min index) in a small hash of
-                // 2^hl >= 2 * ng slots (load <= 1/2); only that prefix is used,
-                // so only that prefix is reset afterwards
-                uint32_t hl = 5;
-                while ((1u << hl) < 2 * ng && hl < kHashLog2) ++hl;
-                const uint32_t hmask = (1u << hl) - 1;
+                // first occurrence per value: (t, min index) in a small hash
                 for (uint32_t p = lane; p < ng; p += 32) {
                     const unsigned long long e = gl[p];
                     const uint32_t t = (uint32_t)(e >> 32);
-                    uint32_t h = (t * 0x85EBCA6Bu) >> (32 - hl);
+                    uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
                     for (;;) {
                         const unsigned long long old = atomicCAS(&htab[h], ~0ull, e);
                         if (old == ~0ull) break;
@@ -197,23 +192,23 @@ __global__ void __launch_bounds__(kBloomBlock) k_floyd_bloom(const SamplerArgs a
                             atomicMin(&htab[h], e);
                             break;
                         }
-                        h = (h + 1) & hmask;
+                        h = (h + 1) & (kHashSlots - 1);
                     }
                 }
                 __syncwarp();
                 for (uint32_t p = lane; p < ng; p += 32) {
                     const unsigned long long e = gl[p];
                     const uint32_t t = (uint32_t)(e >> 32), i = (uint32_t)e;
-                    uint32_t h = (t * 0x85EBCA6Bu) >> (32 - hl);
-                    while ((uint32_t)(htab[h] >> 32) != t) h = (h + 1) & hmask;
+                    uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
+                    while ((uint32_t)(htab[h] >> 32) != t) h = (h + 1) & (kHashSlots - 1);
                     if ((uint32_t)htab[h] != i) {  // an earlier draw has the same value
                         atomicOr(&colbits[i >> 5], 1u << (i & 31));
                         emit(u, base + i);
                         ++ncol;
                     }
                 }
-                __syncwarp();  // all lookups done: reset the used prefix of the hash
-                for (uint32_t s2 = lane; s2 <= hmask; s2 += 32) htab[s2] = ~0ull;
+                __syncwarp();  // all lookups done: reset the whole (8 KB) hash
+                for (uint32_t s2 = lane; s2 < kHashSlots; s2 += 32) htab[s2] = ~0ull;
                 __syncwarp();
                 if (lane == 0 && nc) {
                     const uint64_t key = vertex_key(a.seed_mixed, u);
