@@ -73,7 +73,7 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_gather_ceiling(d: int, n: int):
+def load_gather_ceiling(d: int, n: int, row: int | None = None):
     """Measured random-row gather ceiling for this row shape and table size
     (tools/gather_ceiling.cu -> profiles/r01_gather_ceilings.jsonl): the best
     rows/s of a lean gather with no per-pair work, swept over rows in flight
@@ -83,7 +83,8 @@ def load_gather_ceiling(d: int, n: int):
         cases = [json.loads(ln) for ln in open(path) if ln.strip().startswith("{")]
     except Exception:
         return None, None
-    row = 8 if d <= 2 else 16 * ((d + 3) // 4)  # padded device row, bytes
+    if row is None:
+        row = 8 if d <= 2 else 16 * ((d + 3) // 4)  # padded device row, bytes
     table = n * row
     # same row size; among those, the table size closest to ours (L2 vs HBM)
     same = [c for c in cases if c["row_bytes"] == max(row, 16)]
@@ -274,6 +275,7 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     gather_ms, gather_bytes, gather_pairs, launches, lib_launches = [], 0, 0, 0, 0
+    filter_bits = 32
     stage = {}
     info = None
     if world > 1:
@@ -286,6 +288,7 @@ def main():
         ev[k][1].record(stream)
         gather_ms.append(info.ms_gather)
         gather_bytes = info.gather_bytes
+        filter_bits = getattr(info, "filter_bits", 32) or 32
         gather_pairs = info.gather_pairs
         launches += info.kernel_launches
         lib_launches += info.library_launches
@@ -366,24 +369,31 @@ def main():
     peak, peak_kind = load_peaks()
     g_ms = statistics.mean(gather_ms) if gather_ms else 0.0
     achieved = gather_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else None
-    roofline = {"bound": "hbm", "kernel": "k_gather", "achieved": achieved, "peak": peak,
+    q8 = filter_bits == 8
+    bpp = gather_bytes / gather_pairs if gather_pairs else 4 * d  # algorithmic bytes per pair
+    roofline = {"bound": "hbm", "kernel": "k_gather_q8" if q8 else "k_gather",
+                "achieved": achieved, "peak": peak,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": load_traffic(w.name),
+                "traffic": load_traffic(w.name) if not q8 else None,
                 "algorithmic_bytes_per_launch": gather_bytes,
-                "bytes_per_pair": 4 * d, "pairs_per_launch": gather_pairs,
+                "bytes_per_pair": bpp, "pairs_per_launch": gather_pairs,
+                "filter": ("8-bit exact filter: u8 rows + norm, DP4A integer distances, "
+                           "integer accept/reject thresholds, fp64 recheck in the band")
+                if q8 else "fp32 rows, fp32 guard band, fp64 recheck in the band",
                 "kernel_ms": g_ms,
                 "kernel_share_of_step": (g_ms / ms_per_step) if ms_per_step else None}
     # The gather's real ceiling is the memory level the partner rows come from:
-    # L2 when the (padded) row table, or one L2-blocked phase of it, is
-    # resident (the measured lean random-row gather of this row shape), HBM
-    # otherwise (the measured copy peak: random 128-byte rows are whole DRAM
-    # bursts, and our gather measured above the lean kernel there).
-    row_bytes = 16 if d == 3 else 4 * d
+    # L2 when the row table (fp32 padded, or the 8-bit rows), or one L2-blocked
+    # phase of it, is resident (the measured lean random-row gather of this row
+    # shape), HBM otherwise (the measured copy peak: random 128-byte rows are
+    # whole DRAM bursts, and our gather measured above the lean kernel there).
+    row_bytes = (16 * ((d + 15) // 16 + 1)) if q8 else (16 if d == 3 else 4 * d)
     phased = d >= 256 and n * row_bytes > 100 * 2**20  # L2-blocked: one slice resident
     resident = n * row_bytes <= 100 * 2**20 or (phased and n * row_bytes <= 16 * 63 * 2**20)
-    case, rows_per_s = load_gather_ceiling(d, min(n, int(63 * 2**20 // row_bytes)) if phased else n)
-    l2_peak = rows_per_s * 4 * d / 1e9 if (resident and rows_per_s) else None
+    case, rows_per_s = load_gather_ceiling(
+        d, min(n, int(63 * 2**20 // row_bytes)) if phased else n, row_bytes if q8 else None)
+    l2_peak = rows_per_s * bpp / 1e9 if (resident and rows_per_s) else None
     eff = l2_peak if resident else peak
     roofline.update({
         "effective_bound": "l2 (random rows)" if resident else "hbm",
@@ -407,7 +417,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8" if q8 else "f32",
             "data": "synthetic (seeded generator, BASELINE.json shape)",
             "config": {"workload": w.name, "n": n, "d": d, "eps": w.eps, "rate": w.rate,
                        "min_pts": w.min_pts, "seed": w.seed, "draws": w.draws, "pairs": pairs,

@@ -17,9 +17,10 @@
  *
  * Semantics are the reference's, bit for bit: the same per-vertex Floyd
  * partner sets from the same (seed, vertex) counter streams (rng.hpp), the
- * same fp64 eps decision (distance.hpp:75-83; fp32 is used only where the
- * decision is provably identical, every other pair is re-evaluated in the
- * reference's exact fp64 order), the same core mask, components, border ties
+ * same fp64 eps decision (distance.hpp:75-83; an fp32 or, for wide rows, an
+ * 8-bit filter decides a pair only where its error bound proves the decision
+ * identical, every other pair is re-evaluated in the reference's exact fp64
+ * order), the same core mask, components, border ties
  * and relabelling (clusterer.cpp:7-52).  Points are fp32 row-major n x d
  * (the reference widens to fp64; fp32 -> fp64 widening is exact).
  *
@@ -35,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SNGB_ABI_VERSION 1
+#define SNGB_ABI_VERSION 2
 
 /* Status codes.  1..6 carry the reference's std::invalid_argument messages. */
 enum {
@@ -78,16 +79,21 @@ typedef struct sngb_info {
     uint64_t irregular_vertices; /* vertices whose stream hit the Lemire reject test */
     /* eps-test exactness accounting (north star: traceability of fp32 decisions) */
     uint64_t pairs_evaluated;  /* pairs the GPU actually tested (incl. duplicate t draws) */
-    uint64_t band_rechecks;    /* fp32 sum inside the guard band -> exact fp64 recheck */
+    uint64_t band_rechecks;    /* filter value inside the guard band -> exact fp64 recheck */
     uint64_t band_1e6;         /* of those, |s32 - eps^2| <= 1e-6 * eps^2 */
     uint64_t fp32_flips;       /* pairs where a bare fp32 test would have decided wrongly */
     uint64_t directed_accepts; /* accepted (u,v) emissions before symmetrise/dedup */
     /* stage times in ms (only with SNGB_FLAG_TIMING; CUDA events on the run stream) */
     float ms_total, ms_upload, ms_sample, ms_gather, ms_extras, ms_sort, ms_cluster, ms_download;
     uint64_t gather_pairs; /* pairs evaluated by the dominant gather kernel */
-    uint64_t gather_bytes; /* its algorithmic bytes: gather_pairs * 4 * d */
+    uint64_t gather_bytes; /* its algorithmic bytes (see filter_bits) */
     uint64_t kernel_launches; /* hand-written kernels launched by this call (CUB not counted) */
     uint64_t library_launches; /* CUB radix-sort / select / scan kernels launched by this call */
+    /* ABI 2: the filter the gather ran with -- 32: fp32 rows (gather_bytes = pairs * 4d);
+     * 8: the exact 8-bit filter for wide rows (gather_bytes = pairs * (d + 4): the
+     * row's bytes and its norm; band_rechecks counts its exact fp64 re-evaluations) */
+    uint32_t filter_bits;
+    uint32_t reserved;
 } sngb_info;
 
 /* sng::sng_dbscan (clusterer.hpp:42) on HOST buffers: pts[n*d] fp32 row-major,

@@ -94,14 +94,15 @@ struct DevCtx {
     cudaEvent_t up_ev[kMaxChunks] = {};
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
-        flags, rank, temp, labels, roles, work;
+        flags, rank, temp, labels, roles, work, q8;
+    cudaEvent_t qev = nullptr;  // min/max of the points copied to the host (8-bit filter)
     unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
     cudaEvent_t ev[12] = {};
     uint64_t edge_hint = 0;  // last needed edge capacity for this context
 
     void release() {
         for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
-                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work})
+                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8})
             b->release();
     }
 };
@@ -151,6 +152,7 @@ DevCtx& get_ctx(int dev) {
         CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->qev, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->up_start, cudaEventDisableTiming));
         for (auto& e : c->up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaMallocHost(&c->h_counters, C_COUNT * sizeof(unsigned long long)));
@@ -283,6 +285,7 @@ struct GraphResult {
     uint64_t draws = 0;
     bool exhaustive = false;
     uint64_t raw = 0;
+    bool q8 = false;  // the gather ran the 8-bit filter
 };
 
 // Prepare points and run the graph build for rows [rb, re).  Leaves sorted
@@ -309,15 +312,26 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     if (pad) c.pts.ensure(n * stride * sizeof(float));
     const float* pts = pad ? c.pts.as<float>() : d_pts;
     cudaStream_t gs = s;  // the gather's stream (c.hi under SNGB_PRIO)
+    bool q8_try = false;  // wide rows: min/max for the 8-bit filter (sngb_quant.cu)
     auto prepare_rows = [&](uint64_t lo, uint64_t hi) {
         if (hi > lo)
             CK(launch_prepare_points(d_pts + lo * d, pad ? c.pts.as<float>() + lo * stride : nullptr,
-                                     hi - lo, d, stride, dc, gs));
+                                     hi - lo, d, stride, dc, q8_try, gs));
+    };
+    // after the last prepare: the min/max to the host, waited for only when the
+    // 8-bit plan is made (the sampler is already running by then)
+    auto minmax_to_host = [&]() {
+        CK(cudaMemcpyAsync(&c.h_counters[C_QMIN], &dc[C_QMIN], 2 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, gs));
+        CK(cudaEventRecord(c.qev, gs));
     };
 
     // ---- sampling geometry (graph.cpp:138-140) ----
     const uint64_t draws = draws_for(n, rate);
     const bool exhaustive = draws >= n - 1;
+    // SNGB_Q8: 0 off, 1 auto (use when the band is narrow), 2 force (tests)
+    const uint64_t q8_mode = env_u64("SNGB_Q8", 1);
+    q8_try = !exhaustive && d >= 128 && d <= 1024 && q8_mode != 0;
     const uint64_t rows = re - rb;
     const uint32_t nb = bits_for(n - 1);
     const uint64_t base = (n - 1) - draws;
@@ -367,8 +381,14 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         }
         tm.mark_on(E_UPLOADED, c.copy);
     };
-    if (!h_src) prepare_rows(0, n);
+    if (!h_src) {
+        prepare_rows(0, n);
+        if (q8_try) minmax_to_host();
+    }
     tm.mark(E_PREPARED);
+    bool q8_on = false;
+    Q8Plan q8p{};
+    uint32_t gphases = phases;  // partner slices of the gather (8-bit rows: their own count)
 
     for (int attempt = 0; attempt < 4; ++attempt) {
         c.keys.ensure(edge_cap * 8);
@@ -418,6 +438,29 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             }
         }
         if (h_src && attempt == 0) start_upload();
+        if (q8_try && attempt == 0) {
+            if (h_src) {  // the scale needs every value: wait for the whole upload
+                for (uint32_t k = 0; k < chunks; ++k) {
+                    CK(cudaStreamWaitEvent(gs, c.up_ev[k], 0));
+                    prepare_rows(chunk_lo(k), chunk_lo(k + 1));
+                }
+                minmax_to_host();
+            }
+            CK(cudaEventSynchronize(c.qev));
+            const float lo = ordered_value(~(uint32_t)c.h_counters[C_QMIN]);
+            const float hi = ordered_value((uint32_t)c.h_counters[C_QMAX]);
+            const bool useful = q8_plan(lo, hi, d, tp.eps2, q8p);
+            q8_on = !c.h_counters[C_NONFINITE] && (useful || (q8_mode == 2 && q8p.s > 0));
+            gr.q8 = q8_on;
+            if (q8_on) {
+                const uint32_t nd = (d + 15) / 16;
+                c.q8.ensure(n * (nd + 1) * 16ull);
+                q8p.args.rows = c.q8.as<uint4>();
+                q8p.args.nd = nd;
+                CK(launch_quantize(pts, stride, n, d, q8p, c.q8.as<uint4>(), gs, c.num_sms));
+                gphases = gather_phases(c, n, 4 * (nd + 1), draws);
+            }
+        }
         tm.mark(E_SAMPLED);
         GatherArgs ga{};
         ga.tp = tp;
@@ -450,7 +493,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         // L2-blocked phases: each launch tests only partners in one slice of
         // the rows, small enough to stay L2-resident while every vertex's
         // draws are regenerated (cheap) and its query row streamed.
-        auto part = [&](uint32_t ph) { return (uint32_t)(n * ph / phases); };
+        auto part = [&](uint32_t ph) { return (uint32_t)(n * ph / gphases); };
         auto gather = [&](uint64_t qlo, uint64_t qhi, uint32_t plo, uint32_t phi) {
             ga.row_begin = std::max(rb, qlo);
             ga.row_end = std::min(re, qhi);
@@ -465,9 +508,10 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 ga.grab = (uint32_t)std::max<uint64_t>(
                     1, std::min<uint64_t>(32, (ga.row_end - ga.row_begin) / (warps * 16)));
             }
-            CK(launch_gather(ga, exhaustive, gs, c.num_sms));
+            if (q8_on) CK(launch_gather_q8(ga, q8p.args, gs, c.num_sms));
+            else CK(launch_gather(ga, exhaustive, gs, c.num_sms));
         };
-        if (h_src && attempt == 0 && chunks == phases && phases > 1) {
+        if (h_src && attempt == 0 && !q8_try && chunks == phases && phases > 1) {
             // triangular schedule over (query chunk, partner slice) blocks:
             // once chunk k is in, every block it completes can run -- queries
             // <= k against slice k, then chunk k against the earlier slices
@@ -478,12 +522,12 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 for (uint32_t j = 0; j < k; ++j) gather(part(k), part(k + 1), part(j), part(j + 1));
             }
         } else {
-            if (h_src && attempt == 0)
+            if (h_src && attempt == 0 && !q8_try)
                 for (uint32_t k = 0; k < chunks; ++k) {
                     CK(cudaStreamWaitEvent(gs, c.up_ev[k], 0));
                     prepare_rows(chunk_lo(k), chunk_lo(k + 1));
                 }
-            for (uint32_t ph = 0; ph < phases; ++ph) gather(rb, re, part(ph), part(ph + 1));
+            for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
         }
         if (prio) {
             CK(cudaEventRecord(c.hi_join, c.hi));
@@ -573,7 +617,8 @@ void fill_info(sngb_info* info, const unsigned long long* hc, uint64_t n, uint32
     info->fp32_flips = hc[C_FLIPS];
     info->directed_accepts = hc[C_EDGE_CURSOR];
     info->gather_pairs = hc[C_GATHER_PAIRS];
-    info->gather_bytes = hc[C_GATHER_PAIRS] * 4ull * d;
+    info->filter_bits = gr.q8 ? 8 : 32;
+    info->gather_bytes = hc[C_GATHER_PAIRS] * (gr.q8 ? (uint64_t)d + 4 : 4ull * d);
     if (clustered) {
         info->cluster_count = (int32_t)hc[C_CLUSTERS];
         info->core_count = (uint32_t)hc[C_CORE];

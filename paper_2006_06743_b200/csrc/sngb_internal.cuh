@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 
 namespace sngb {
 
@@ -28,6 +29,8 @@ enum Counter : int {
     C_CLUSTERS,
     C_BADKEY,            // self loop / out-of-range endpoint in caller keys
     C_CHANGED,           // merge step: vertices whose component root moved
+    C_QMIN,              // max of ~ordered(value): the dataset minimum (8-bit filter scale)
+    C_QMAX,              // max of ordered(value): the dataset maximum
     C_COUNT
 };
 
@@ -108,12 +111,49 @@ void note_launch(int hand_written, int library = 0);
 
 // ---- launchers (sngb_kernels.cu) ----
 cudaError_t launch_prepare_points(const float* src, float* dst, uint64_t n, uint32_t d,
-                                  uint32_t stride, unsigned long long* counters, cudaStream_t s);
+                                  uint32_t stride, unsigned long long* counters, bool minmax,
+                                  cudaStream_t s);
+// float <-> unsigned key with the same order (min/max by integer atomics)
+__host__ __device__ __forceinline__ uint32_t ordered_key(float f) {
+    uint32_t u;
+#ifdef __CUDA_ARCH__
+    u = __float_as_uint(f);
+#else
+    std::memcpy(&u, &f, 4);
+#endif
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float ordered_value(uint32_t k) {
+    const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    float f;
+#ifdef __CUDA_ARCH__
+    f = __uint_as_float(u);
+#else
+    std::memcpy(&f, &u, 4);
+#endif
+    return f;
+}
 // sngb_sampler.cu
 void floyd_geometry(uint32_t draws, uint32_t& slots, uint32_t& col_words);
 size_t floyd_scratch_bytes(uint32_t draws, int num_sms);
 cudaError_t launch_sampler(const SamplerArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_gather(const GatherArgs& a, bool exhaustive, cudaStream_t s, int num_sms);
+// sngb_quant.cu: the 8-bit filter for wide rows (exact via integer thresholds
+// on Q2 = sum (qa - qb)^2 plus the fp64 recheck in the band)
+struct Q8Args {
+    const uint4* rows;   // n rows of nd + 1 16-byte chunks: bytes, zero pad, norm chunk
+    uint32_t nd;         // data chunks per row = ceil(d / 16)
+    int32_t accept_max;  // Q2 <= accept_max: the reference accepts
+    int32_t reject_min;  // Q2 >  reject_min: the reference rejects (else exact recheck)
+};
+struct Q8Plan {
+    double s, lo;  // scale (a power of two) and offset (a multiple of s)
+    Q8Args args;
+};
+bool q8_plan(float lo, float hi, uint32_t d, double eps2, Q8Plan& p);
+cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint32_t d,
+                            const Q8Plan& p, uint4* out, cudaStream_t s, int num_sms);
+cudaError_t launch_gather_q8(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms);
 cudaError_t launch_extras(const ExtrasArgs& a, cudaStream_t s, int num_sms);
 
 // ---- cluster stage (sngb_cluster.cu) ----

@@ -353,38 +353,56 @@ __global__ void __launch_bounds__(256) k_extras(const ExtrasArgs a) {
 // kernel only checks.
 // ---------------------------------------------------------------------------
 __global__ void k_prepare(const float* __restrict__ src, float* __restrict__ dst, uint64_t n,
-                          uint32_t d, uint32_t stride, unsigned long long* counters) {
+                          uint32_t d, uint32_t stride, unsigned long long* counters, bool minmax) {
     const uint64_t total = dst ? n * stride : n * d;
     unsigned bad = 0;
+    uint32_t kmin = 0, kmax = 0;  // kmin = max of ~key (0 = nothing seen)
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (uint64_t)gridDim.x * blockDim.x) {
+        float v;
+        bool real = true;
         if (dst) {
             const uint64_t r = idx / stride;
             const uint32_t c = (uint32_t)(idx - r * stride);
-            float v = 0.f;
-            if (c < d) {
-                v = src[r * d + c];
-                bad += !isfinite(v);
-            }
+            v = 0.f;
+            real = c < d;
+            if (real) v = src[r * d + c];
             dst[idx] = v;
         } else {
-            bad += !isfinite(src[idx]);
+            v = src[idx];
+        }
+        if (real) {
+            bad += !isfinite(v);
+            if (minmax) {
+                const uint32_t k = ordered_key(v);
+                kmin = max(kmin, ~k);
+                kmax = max(kmax, k);
+            }
         }
     }
     bad = __reduce_add_sync(kFull, bad);
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&counters[C_NONFINITE], (unsigned long long)bad);
+    if (minmax) {
+        kmin = __reduce_max_sync(kFull, kmin);
+        kmax = __reduce_max_sync(kFull, kmax);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(&counters[C_QMIN], (unsigned long long)kmin);
+            atomicMax(&counters[C_QMAX], (unsigned long long)kmax);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_prepare_points(const float* src, float* dst, uint64_t n, uint32_t d,
-                                  uint32_t stride, unsigned long long* counters, cudaStream_t s) {
+                                  uint32_t stride, unsigned long long* counters, bool minmax,
+                                  cudaStream_t s) {
     const uint64_t total = dst ? n * stride : n * d;
     uint64_t blocks = (total + 255) / 256;
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     if (blocks == 0) blocks = 1;
-    k_prepare<<<(unsigned)blocks, 256, 0, s>>>(src, dst, n, d, stride, counters);
+    k_prepare<<<(unsigned)blocks, 256, 0, s>>>(src, dst, n, d, stride, counters, minmax);
     note_launch(1);
     return cudaGetLastError();
 }

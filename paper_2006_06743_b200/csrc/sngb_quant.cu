@@ -1,0 +1,257 @@
+// sngb_quant.cu -- the 8-bit filter for wide rows: the gather reads an 8-bit
+// copy of the points (4x fewer bytes than fp32) and still decides every pair
+// exactly as the reference does.
+//
+// Quantisation.  s is a power of two >= (max - min)/254 and lo' = floor(min/s)*s,
+// so q = rint((a - lo')/s) in [0, 255] is computed exactly in fp64 (up to a
+// relative 2^-45 in a - lo' for tiny |a|) and a = lo' + s*q + e with
+// |e| <= s/2 * (1 + 2^-30).  Each row stores its bytes, zero padded to 16-byte
+// chunks, then one chunk holding its norm N = sum q^2.
+//
+// Filter.  For a pair, Q2 = sum (qa - qb)^2 = Na + Nb - 2 sum qa*qb is an exact
+// integer (DP4A).  With Dk = s*dqk, |Ek| <= s' = s(1 + 2^-30), Q1 = sum |dqk| <=
+// sqrt(d Q2) (Cauchy-Schwarz), the true squared distance S satisfies
+//   S <= sum (s|dqk| + s')^2          <= (s*sqrt(Q2) + s'*sqrt(d))^2
+//   S >= sum (dk^2 - 2|dk|s')         >= s^2 Q2 - 2 s s' sqrt(d Q2)
+// and the reference's fp64 sum is within (d+1) 2^-53 S of S.  Hence
+//   Q2 <= A  = ((sqrt(eps2 (1 - 2^-40)) - s' sqrt(d)) / s)^2      => accept
+//   Q2 >  B  = ((s' sqrt(d) + sqrt(s'^2 d + eps2 (1 + 2^-40))) / s)^2 => reject
+// (A rounded down, B up, with a relative 2^-30 margin for the fp64 evaluation),
+// and a pair with A < Q2 <= B is re-evaluated with the reference's exact fp64
+// operation order on the fp32 rows -- the same recheck the fp32 filter uses.
+// The host enables the path only when that band is narrow relative to eps
+// (a data set with a huge value range relative to eps keeps the fp32 filter).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "sngb_device.cuh"
+#include "sngb_epstest.cuh"
+#include "sngb_internal.cuh"
+#include "sngb_rng.cuh"
+
+namespace sngb {
+
+bool q8_plan(float lo_f, float hi_f, uint32_t d, double eps2, Q8Plan& p) {
+    const double lo = lo_f, hi = hi_f;
+    const double need = (hi - lo) / 254.0 * (1.0 + 1e-12);
+    if (!(need > 0.0) || !std::isfinite(need)) return false;
+    int e = 0;
+    std::frexp(need, &e);  // need = m * 2^e, m in [0.5, 1)
+    const double s = std::ldexp(1.0, e);
+    p.s = s;
+    p.lo = std::floor(lo / s) * s;
+    const double sp = s * (1.0 + std::ldexp(1.0, -30));
+    const double sd = std::sqrt((double)d);
+    const double e_lo = eps2 * (1.0 - std::ldexp(1.0, -40));
+    const double e_hi = eps2 * (1.0 + std::ldexp(1.0, -40));
+    const double qmax = (double)d * 255.0 * 255.0;  // largest possible Q2
+    const double ta = (std::sqrt(e_lo) - sp * sd) / s;
+    const double a = ta > 0.0 ? std::floor(ta * ta * (1.0 - std::ldexp(1.0, -30))) : -1.0;
+    const double tb = (sp * sd + std::sqrt(sp * sp * d + e_hi)) / s;
+    const double b = std::ceil(tb * tb * (1.0 + std::ldexp(1.0, -30)));
+    p.args.accept_max = (int32_t)std::min(a, qmax + 1.0);
+    p.args.reject_min = (int32_t)std::min(b, qmax + 1.0);
+    // worthwhile if the band is narrow in distance units (<= 25 % of eps wide)
+    const double band = (std::sqrt(std::max(b, 0.0)) - std::sqrt(std::max(a, 0.0))) * s;
+    return a >= 0.0 && band <= 0.25 * std::sqrt(eps2);
+}
+
+namespace {
+
+// warp per row: bytes q of the row's d values, zero padded, then the norm chunk
+__global__ void k_quantize(const float* __restrict__ pts, uint32_t stride, uint64_t n, uint32_t d,
+                           double lo, double inv_s, uint32_t nd, uint4* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = gw; r < n; r += nw) {
+        const float* row = pts + r * stride;
+        uint4* orow = out + r * (nd + 1);
+        uint32_t norm = 0;
+        for (uint32_t c = lane; c < nd; c += 32) {
+            uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t k = 16 * c + j;
+                uint32_t q = 0;
+                if (k < d) {
+                    const double x = rint(((double)row[k] - lo) * inv_s);
+                    q = x <= 0.0 ? 0u : (x >= 255.0 ? 255u : (uint32_t)x);
+                }
+                w[j >> 2] |= q << (8 * (j & 3));
+                norm += q * q;
+            }
+            orow[c] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        norm = __reduce_add_sync(kFull, norm);
+        if (lane == 0) orow[nd] = make_uint4(norm, 0, 0, 0);
+    }
+}
+
+__device__ __forceinline__ uint32_t dot16(uint4 a, uint4 b, uint32_t acc) {
+    acc = __dp4a(a.x, b.x, acc);
+    acc = __dp4a(a.y, b.y, acc);
+    acc = __dp4a(a.z, b.z, acc);
+    return __dp4a(a.w, b.w, acc);
+}
+
+// Wide-row gather over the 8-bit rows: the k_gather G = 32 structure (dynamic
+// row claiming, draws regenerated from their counters, live pairs compacted
+// per 32-draw chunk, U rows per step behind a warp-sync fence, transposed
+// reduce-scatter leaving pair k's sum in lane 32k/U) with integer arithmetic.
+template <int V8, int U>
+__global__ void __launch_bounds__(256, 2) k_gather_q8(const GatherArgs a, const Q8Args q8) {
+    __shared__ unsigned long long s_stage[kWarpsPerBlock][kStage];
+    __shared__ uint32_t s_list[kWarpsPerBlock][32];
+    constexpr int SPAN = 32 / U;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
+    const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerBlock;
+    const uint4* __restrict__ Q = q8.rows;
+    const uint32_t RW = q8.nd + 1, nd = q8.nd;
+    const uint32_t plo = a.part_lo, phi = a.part_hi;
+    uint32_t* list = s_list[wib];
+    WarpStage<kStage> stage{s_stage[wib], 0};
+    TestStats st;
+    unsigned long long gpairs = 0;
+
+    uint64_t u = a.row_begin + gw, chunk_end = a.row_end;
+    auto grab = [&]() {
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(a.work, (unsigned long long)a.grab);
+        b0 = __shfl_sync(kFull, b0, 0);
+        u = a.row_begin + b0;
+        chunk_end = u + a.grab < a.row_end ? u + a.grab : a.row_end;
+    };
+    if (a.work) grab();
+    for (; u < chunk_end; (a.work && u + 1 >= chunk_end) ? grab() : (void)(u += a.work ? 1 : nw)) {
+        uint4 qq[V8];
+        uint32_t nu = 0;
+#pragma unroll
+        for (int vv = 0; vv < V8; ++vv) {
+            const uint32_t c = lane + 32 * vv;
+            qq[vv] = c < RW ? __ldg(Q + u * RW + c) : make_uint4(0, 0, 0, 0);
+            if (c == nd) {
+                nu = qq[vv].x;
+                qq[vv] = make_uint4(0, 0, 0, 0);
+            }
+        }
+        nu = __reduce_add_sync(kFull, nu);  // one lane holds the query's norm
+        uint32_t limit = a.draws;
+        uint64_t z = vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
+        for (uint32_t i0 = 0; i0 < limit; i0 += 32, z += 32ull * kGamma) {
+            const uint32_t i = i0 + lane;
+            const bool valid = i < limit;
+            bool fire = false;
+            uint32_t t = 0;
+            if (valid) {
+                t = lemire32(mix(z), a.base + i + 1, fire);
+                fire |= test_fire(a.force_mod, u, i, a.draws);
+            }
+            const uint32_t p = t + (t >= (uint32_t)u ? 1u : 0u);
+            const unsigned fm = __ballot_sync(kFull, valid && fire);
+            if (fm) limit = i0 + __ffs(fm) - 1;  // irregular vertex: cut here
+            const bool live = i < limit && p >= plo && p < phi;
+            const unsigned m = __ballot_sync(kFull, live);
+            if (live) list[__popc(m & lanemask_lt())] = p;
+            const uint32_t nlive = __popc(m);
+            __syncwarp();
+#pragma unroll 1
+            for (uint32_t j0 = 0; j0 < nlive; j0 += U) {
+                uint4 rows[U][V8];
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    const uint32_t j = j0 + uu;
+                    const uint32_t pv = list[j < nlive ? j : j0];
+#pragma unroll
+                    for (int vv = 0; vv < V8; ++vv) {
+                        const uint32_t c = lane + 32 * vv;
+                        rows[uu][vv] = c < RW ? __ldg(Q + (uint64_t)pv * RW + c)
+                                              : make_uint4(0, 0, 0, 0);
+                    }
+                }
+                __syncwarp();  // scheduling fence: all U*V8 loads in flight together
+                int ps[U];
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    uint32_t dot = 0, nv = 0;
+#pragma unroll
+                    for (int vv = 0; vv < V8; ++vv) {
+                        const uint32_t c = lane + 32 * vv;
+                        dot = dot16(qq[vv], rows[uu][vv], dot);  // query norm chunk is zeroed
+                        if (c == nd) nv = rows[uu][vv].x;
+                    }
+                    ps[uu] = (int)nv - 2 * (int)dot;  // partial of Nb - 2 sum qa qb
+                }
+#pragma unroll
+                for (int o = 16, mm = U; mm > 1; o >>= 1, mm >>= 1) {
+                    const bool hi = (lane & o) != 0;
+#pragma unroll
+                    for (int k = 0; k < mm / 2; ++k) {
+                        const int mine = hi ? ps[k + mm / 2] : ps[k];
+                        const int other = hi ? ps[k] : ps[k + mm / 2];
+                        ps[k] = mine + __shfl_xor_sync(kFull, other, o);
+                    }
+                }
+#pragma unroll
+                for (int o = SPAN / 2; o > 0; o >>= 1) ps[0] += __shfl_xor_sync(kFull, ps[0], o);
+                const uint32_t pj = j0 + lane / SPAN;
+                const bool okm = (lane % SPAN) == 0 && pj < nlive;
+                const uint32_t pm = list[okm ? pj : j0];
+                const int q2 = (int)nu + ps[0];
+                bool acc = okm && q2 <= q8.accept_max;
+                if (okm && q2 > q8.accept_max && q2 <= q8.reject_min) {  // band: exact recheck
+                    acc = exact_within(a.tp, u, pm);
+                    st.band++;
+                }
+                gpairs += okm ? 1u : 0u;
+                stage.push(acc, edge_key(u, pm, a.sink.nb), a.sink, lane);
+            }
+            __syncwarp();
+        }
+    }
+    stage.flush(a.sink, lane);
+    st.pairs = gpairs;
+    flush_stats(st, gpairs, a.counters, lane);
+}
+
+template <int V8>
+cudaError_t q8_one(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
+    auto k = k_gather_q8<V8, 4>;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t rows = a.row_end - a.row_begin;
+    const uint64_t want = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const uint64_t cap = (uint64_t)num_sms * per_sm;
+    k<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(a, q);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint32_t d,
+                            const Q8Plan& p, uint4* out, cudaStream_t s, int num_sms) {
+    const uint32_t nd = (d + 15) / 16;
+    uint64_t blocks = (n + 7) / 8;
+    if (blocks > (uint64_t)num_sms * 16) blocks = (uint64_t)num_sms * 16;
+    k_quantize<<<(unsigned)(blocks ? blocks : 1), 256, 0, s>>>(pts, stride, n, d, p.lo, 1.0 / p.s,
+                                                                nd, out);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_q8(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
+    if (a.row_end <= a.row_begin) return cudaSuccess;
+    switch ((q.nd + 1 + 31) / 32) {
+        case 1: return q8_one<1>(a, q, s, num_sms);
+        case 2: return q8_one<2>(a, q, s, num_sms);
+        case 3: return q8_one<3>(a, q, s, num_sms);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace sngb

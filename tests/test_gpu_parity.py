@@ -205,3 +205,70 @@ def test_nonfinite_rejected_after_deferred_check():
     pts[1234, 1] = 0.5
     labels, _, _ = sng.sng_dbscan_device(torch.from_numpy(pts).cuda(), 0.03, 10, 0.1, 1)
     assert labels.numel() == 2000
+
+
+# ---- the 8-bit filter for wide rows (sngb_quant.cu) ------------------------
+def _q8_case(n, d, seed, spread=1.0):
+    rng = np.random.default_rng(seed)
+    centers = rng.random((8, d), dtype=np.float32)
+    pts = centers[rng.integers(0, 8, n)] + rng.normal(0, 0.1 * spread, (n, d)).astype(np.float32)
+    return np.ascontiguousarray(pts, np.float32)
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("n,d,rate,seed", [(3000, 128, 0.05, 3), (2500, 784, 0.04, 5),
+                                           (2000, 1000, 0.05, 9)])
+def test_q8_filter_matches_oracle(oracle, monkeypatch, mode, n, d, rate, seed):
+    """SNGB_Q8=0 (fp32 filter), 1 (auto), 2 (forced): identical to the oracle."""
+    monkeypatch.setenv("SNGB_Q8", mode)
+    pts = _q8_case(n, d, seed)
+    # eps at a within-cluster distance quantile: plenty of pairs near eps
+    i = np.arange(0, n - 1, 7)
+    dist = np.sqrt(((pts[i] - pts[i + 1]) ** 2).sum(1))
+    eps = float(np.quantile(dist, 0.1))
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=eps, min_pts=3, rate=rate, seed=seed),
+                       info)
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, 3, rate, seed)
+    _assert_same(c, info, labels, roles, oinfo)
+
+
+def test_q8_band_stress_exact(oracle, monkeypatch):
+    """Every pair distance within a few percent of eps: the band holds most
+    pairs, which all take the exact fp64 recheck -- still bit-exact."""
+    monkeypatch.setenv("SNGB_Q8", "2")
+    rng = np.random.default_rng(11)
+    n, d = 2000, 256
+    base = rng.random(d, dtype=np.float32)
+    pts = (base + rng.normal(0, 0.05, (n, d))).astype(np.float32)
+    i = np.arange(0, n - 1, 3)
+    eps = float(np.median(np.sqrt(((pts[i] - pts[i + 1]) ** 2).sum(1))))
+    st = sng.BuildStats()
+    g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.1, seed=2, stats=st)
+    keys, evals = oracle.sampled_edges(pts, eps, 0.1, 2)
+    np.testing.assert_array_equal(g.keys, keys)
+    assert st.distance_evals == evals
+
+
+def test_q8_huge_range_forced(oracle, monkeypatch):
+    """A value range far wider than eps: auto keeps the fp32 filter, forcing the
+    8-bit one puts nearly every pair in the band -- results unchanged."""
+    pts = _q8_case(1500, 160, 4)
+    pts[17, 3] = 1e6  # one far outlier stretches the 8-bit scale
+    eps = 1.5
+    keys, _ = oracle.sampled_edges(pts, eps, 0.05, 4)
+    for mode in ("1", "2"):
+        monkeypatch.setenv("SNGB_Q8", mode)
+        g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.05, seed=4)
+        np.testing.assert_array_equal(g.keys, keys)
+
+
+def test_q8_forced_irregular_exact(oracle, monkeypatch):
+    """Lemire-reject replays (test hook) through the 8-bit gather kernel."""
+    pts = _q8_case(3000, 200, 8)
+    eps = 1.2
+    keys, _ = oracle.sampled_edges(pts, eps, 0.04, 8)
+    monkeypatch.setenv("SNGB_Q8", "2")
+    monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", "5")
+    g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.04, seed=8)
+    np.testing.assert_array_equal(g.keys, keys)

@@ -136,11 +136,13 @@ int main() {
     const Case c5{"cfg5_row128B_2560MB", 2560ull << 20, 128};
     const Case c2l2{"cfg2_row3136B_55MB_slice", 55ull << 20, 3136};
     const Case c2hbm{"cfg2_row3136B_220MB_full", 220ull << 20, 3136};
+    const Case c2q8{"cfg2_q8_row800B_56MB", 56ull << 20, 800};
     sweep<1, 1>(c1, tab, sink, sms);
     sweep<1, 1>(c4, tab, sink, sms);
     sweep<4, 1>(c3, tab, sink, sms);
     sweep<8, 1>(c5, tab, sink, sms);
     sweep<32, 7>(c2l2, tab, sink, sms);
     sweep<32, 7>(c2hbm, tab, sink, sms);
+    sweep<32, 2>(c2q8, tab, sink, sms);
     return 0;
 }
