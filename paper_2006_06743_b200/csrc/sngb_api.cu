@@ -544,7 +544,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             ea.extras = c.extras.as<unsigned long long>();
             ea.count_ptr = &dc[C_EXTRA_CURSOR];
             ea.capacity = extras_cap;
-            CK(launch_extras(ea, s, c.num_sms));
+            if (q8_on) CK(launch_extras_q8(ea, q8p.args, s, c.num_sms));
+            else CK(launch_extras(ea, s, c.num_sms));
         }
         tm.mark(E_EXTRAS);
         CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * sizeof(unsigned long long),

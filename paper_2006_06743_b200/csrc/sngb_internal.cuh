@@ -154,6 +154,7 @@ bool q8_plan(float lo, float hi, uint32_t d, double eps2, Q8Plan& p);
 cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint32_t d,
                             const Q8Plan& p, uint4* out, cudaStream_t s, int num_sms);
 cudaError_t launch_gather_q8(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms);
+cudaError_t launch_extras_q8(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, int num_sms);
 cudaError_t launch_extras(const ExtrasArgs& a, cudaStream_t s, int num_sms);
 
 // ---- cluster stage (sngb_cluster.cu) ----

@@ -357,7 +357,30 @@ __global__ void k_prepare(const float* __restrict__ src, float* __restrict__ dst
     const uint64_t total = dst ? n * stride : n * d;
     unsigned bad = 0;
     uint32_t kmin = 0, kmax = 0;  // kmin = max of ~key (0 = nothing seen)
-    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+    auto see = [&](float v) {
+        bad += !isfinite(v);
+        if (minmax) {
+            const uint32_t k = ordered_key(v);
+            kmin = max(kmin, ~k);
+            kmax = max(kmax, k);
+        }
+    };
+    uint64_t first = 0;
+    if (!dst && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        // check-only pass over an aligned table: 16-byte loads, scalar tail
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        const uint64_t n4 = total / 4;
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+             i += (uint64_t)gridDim.x * blockDim.x) {
+            const float4 v = __ldg(s4 + i);
+            see(v.x);
+            see(v.y);
+            see(v.z);
+            see(v.w);
+        }
+        first = n4 * 4;
+    }
+    for (uint64_t idx = first + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (uint64_t)gridDim.x * blockDim.x) {
         float v;
         bool real = true;
@@ -371,14 +394,7 @@ __global__ void k_prepare(const float* __restrict__ src, float* __restrict__ dst
         } else {
             v = src[idx];
         }
-        if (real) {
-            bad += !isfinite(v);
-            if (minmax) {
-                const uint32_t k = ordered_key(v);
-                kmin = max(kmin, ~k);
-                kmax = max(kmax, k);
-            }
-        }
+        if (real) see(v);
     }
     bad = __reduce_add_sync(kFull, bad);
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&counters[C_NONFINITE], (unsigned long long)bad);

@@ -73,15 +73,19 @@ __global__ void k_quantize(const float* __restrict__ pts, uint32_t stride, uint6
         for (uint32_t c = lane; c < nd; c += 32) {
             uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint32_t k = 16 * c + j;
-                uint32_t q = 0;
-                if (k < d) {
-                    const double x = rint(((double)row[k] - lo) * inv_s);
-                    q = x <= 0.0 ? 0u : (x >= 255.0 ? 255u : (uint32_t)x);
+            for (int j4 = 0; j4 < 4; ++j4) {
+                const uint32_t k0 = 16 * c + 4 * j4;
+                if (k0 >= d) break;  // rows are 16-byte aligned with a stride of ceil4(d)
+                const float4 v = __ldg(reinterpret_cast<const float4*>(row + k0));
+                const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double x = rint(((double)vs[j] - lo) * inv_s);
+                    const uint32_t q = k0 + j >= d ? 0u  // padding past d quantises to 0
+                                       : x <= 0.0 ? 0u : (x >= 255.0 ? 255u : (uint32_t)x);
+                    w[j4] |= q << (8 * j);
+                    norm += q * q;
                 }
-                w[j >> 2] |= q << (8 * (j & 3));
-                norm += q * q;
             }
             orow[c] = make_uint4(w[0], w[1], w[2], w[3]);
         }
@@ -217,6 +221,63 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8(const GatherArgs a, const 
     flush_stats(st, gpairs, a.counters, lane);
 }
 
+// Floyd replacement pairs through the 8-bit filter: one pair per warp step
+template <int V8>
+__global__ void __launch_bounds__(256) k_extras_q8(const ExtrasArgs a, const Q8Args q8) {
+    __shared__ unsigned long long s_stage[kWarpsPerBlock][kStage];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
+    const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerBlock;
+    const uint4* __restrict__ Q = q8.rows;
+    const uint32_t RW = q8.nd + 1, nd = q8.nd;
+    WarpStage<kStage> stage{s_stage[wib], 0};
+    TestStats st;
+    uint64_t count = *a.count_ptr;
+    if (count > a.capacity) count = a.capacity;
+    for (uint64_t p = gw; p < count; p += nw) {
+        const unsigned long long rec = a.extras[p];
+        const uint64_t u = rec >> 32, v = rec & 0xffffffffull;
+        int part = 0;
+        uint32_t dot = 0;
+#pragma unroll
+        for (int vv = 0; vv < V8; ++vv) {
+            const uint32_t c = lane + 32 * vv;
+            if (c < nd) {
+                dot = dot16(__ldg(Q + u * RW + c), __ldg(Q + v * RW + c), dot);
+            } else if (c == nd) {
+                part = (int)(__ldg(Q + u * RW + c).x + __ldg(Q + v * RW + c).x);
+            }
+        }
+        part -= 2 * (int)dot;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+        bool acc = part <= q8.accept_max;
+        if (lane == 0 && !acc && part <= q8.reject_min) {  // band: exact recheck
+            acc = exact_within(a.tp, u, v);
+            st.band++;
+        }
+        acc = __shfl_sync(kFull, acc, 0);
+        if (lane == 0) st.pairs++;
+        stage.push(lane == 0 && acc, edge_key(u, v, a.sink.nb), a.sink, lane);
+    }
+    stage.flush(a.sink, lane);
+    flush_stats(st, 0, a.counters, lane);
+}
+
+template <int V8>
+cudaError_t extras_q8_one(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
+    auto k = k_extras_q8<V8>;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t want = (a.capacity + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const uint64_t cap = (uint64_t)num_sms * per_sm;
+    const uint64_t g = want < cap ? want : cap;
+    k<<<(unsigned)(g ? g : 1), 256, 0, s>>>(a, q);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
 template <int V8>
 cudaError_t q8_one(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
     auto k = k_gather_q8<V8, 4>;
@@ -242,6 +303,16 @@ cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint3
                                                                 nd, out);
     note_launch(1);
     return cudaGetLastError();
+}
+
+cudaError_t launch_extras_q8(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
+    if (a.capacity == 0) return cudaSuccess;
+    switch ((q.nd + 1 + 31) / 32) {
+        case 1: return extras_q8_one<1>(a, q, s, num_sms);
+        case 2: return extras_q8_one<2>(a, q, s, num_sms);
+        case 3: return extras_q8_one<3>(a, q, s, num_sms);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t launch_gather_q8(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {

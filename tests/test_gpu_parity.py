@@ -217,7 +217,8 @@ def _q8_case(n, d, seed, spread=1.0):
 
 @pytest.mark.parametrize("mode", ["0", "1", "2"])
 @pytest.mark.parametrize("n,d,rate,seed", [(3000, 128, 0.05, 3), (2500, 784, 0.04, 5),
-                                           (2000, 1000, 0.05, 9)])
+                                           (2000, 1000, 0.05, 9), (2200, 131, 0.05, 6),
+                                           (1800, 250, 0.06, 12)])
 def test_q8_filter_matches_oracle(oracle, monkeypatch, mode, n, d, rate, seed):
     """SNGB_Q8=0 (fp32 filter), 1 (auto), 2 (forced): identical to the oracle."""
     monkeypatch.setenv("SNGB_Q8", mode)
