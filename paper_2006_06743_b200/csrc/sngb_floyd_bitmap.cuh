@@ -7,7 +7,12 @@
 // dup/chain lists of k_floyd_fast.  Here one warp walks a vertex's draws in
 // reference order, 32 at a time, with an exact membership bitmap:
 //   in_prev : bit t set by an earlier chunk;
-//   dup     : an earlier lane of this chunk drew the same t (match.any);
+//   dup     : an earlier lane of this chunk drew the same t.  Every lane ORs
+//             its own t first; a lane that did not see t before but gets its
+//             bit back set shares t with another lane of the chunk, and only
+//             then (a ballot, ~32^2/2n of the chunks) is the chunk resolved
+//             exactly by match.any (0.5 lane-ops per SM-cycle: too slow to
+//             run on every chunk);
 //   chain   : t equals the replacement j_l of an earlier collided lane of
 //             this chunk -- resolved by an in-order lane scan, only when the
 //             (rare) precondition base + c0 <= t < j holds for some lane.
@@ -56,8 +61,15 @@ __global__ void __launch_bounds__(256) k_floyd_bitmap(const SamplerArgs a) {
                 break;
             }
             const bool in_prev = valid && ((bm[t >> 5] >> (t & 31)) & 1u);
-            const unsigned mm = __match_any_sync(kFull, valid ? t : (0xffffffffu - lane));
-            bool col = valid && (in_prev || (mm & lanemask_lt()) != 0);
+            // set t now: a collided draw's t is in the set anyway, so the final
+            // bitmap is unchanged (the replacements j are added below)
+            const uint32_t old = valid ? atomicOr(&bm[t >> 5], 1u << (t & 31)) : 0u;
+            const bool clash = valid && !in_prev && ((old >> (t & 31)) & 1u);
+            bool col = in_prev;
+            if (__ballot_sync(kFull, clash)) {
+                const unsigned mm = __match_any_sync(kFull, valid ? t : (0xffffffffu - lane));
+                col = valid && (in_prev || (mm & lanemask_lt()) != 0);
+            }
             const uint32_t j = base + i;  // Floyd's replacement value for draw i
             if (__ballot_sync(kFull, valid && !col && t >= base + c0 && t < j)) {
                 for (int l = 0; l < 31; ++l) {
@@ -65,10 +77,7 @@ __global__ void __launch_bounds__(256) k_floyd_bitmap(const SamplerArgs a) {
                     if (cl && lane > l && valid && !col && t == base + c0 + l) col = true;
                 }
             }
-            if (valid) {
-                const uint32_t e = col ? j : t;
-                atomicOr(&bm[e >> 5], 1u << (e & 31));
-            }
+            if (valid && col) atomicOr(&bm[j >> 5], 1u << (j & 31));
             __syncwarp();
             const unsigned cm = __ballot_sync(kFull, col);
             if (lane == 0) ncol += __popc(cm);

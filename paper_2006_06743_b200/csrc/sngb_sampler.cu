@@ -266,8 +266,9 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
     SamplerArgs a = in;
     const uint32_t D = a.draws;
     // small n: exact per-warp bitmap of the chosen values, draws in reference order
+    // (up to 9 KB per warp: n <= 73 k, 2 blocks of 8 warps per SM)
     const uint64_t bm_words = (((a.n - 1) + 31) / 32 + 3) & ~3ull;
-    if (bm_words * 4 <= 4096 && !std::getenv("SNGB_FLOYD_NO_BITMAP")) {
+    if (bm_words * 4 <= 9216 && !std::getenv("SNGB_FLOYD_NO_BITMAP")) {
         a.col_words = (uint32_t)bm_words;
         const int wpb = 8;
         const size_t smem = (size_t)wpb * (bm_words * 4 + kBitmapStage * 8);
