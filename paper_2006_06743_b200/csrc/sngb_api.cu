@@ -389,6 +389,12 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     bool q8_on = false;
     Q8Plan q8p{};
     uint32_t gphases = phases;  // partner slices of the gather (8-bit rows: their own count)
+    // host upload state: leading chunks prepared / quantised on gs.  With the
+    // 8-bit filter the plan is made from chunk 0 (q8_pipe) so the gather can
+    // start while the rest uploads; the final sync checks that every value
+    // fits the plan's range, else the build is redone with a global plan.
+    uint32_t prepared = h_src ? 0 : chunks, quantized = 0;
+    bool q8_pipe = false, q8_replan = false;
 
     for (int attempt = 0; attempt < 4; ++attempt) {
         c.keys.ensure(edge_cap * 8);
@@ -438,27 +444,46 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             }
         }
         if (h_src && attempt == 0) start_upload();
-        if (q8_try && attempt == 0) {
-            if (h_src) {  // the scale needs every value: wait for the whole upload
-                for (uint32_t k = 0; k < chunks; ++k) {
+        auto quantize_rows = [&](uint64_t r0, uint64_t r1) {
+            if (r1 > r0)
+                CK(launch_quantize(pts + r0 * stride, stride, r1 - r0, d, q8p,
+                                   c.q8.as<uint4>() + r0 * (q8p.args.nd + 1), gs, c.num_sms));
+        };
+        if (q8_try && (attempt == 0 || q8_replan)) {
+            const bool pipe = h_src && attempt == 0 && chunks > 1;
+            if (h_src && attempt == 0) {
+                const uint32_t upto = pipe ? 1 : chunks;
+                for (uint32_t k = prepared; k < upto; ++k) {
                     CK(cudaStreamWaitEvent(gs, c.up_ev[k], 0));
                     prepare_rows(chunk_lo(k), chunk_lo(k + 1));
                 }
+                prepared = upto;
                 minmax_to_host();
             }
-            CK(cudaEventSynchronize(c.qev));
+            // a re-plan reads the global min/max kept in h_counters by the last sync
+            if (!q8_replan) CK(cudaEventSynchronize(c.qev));
             const float lo = ordered_value(~(uint32_t)c.h_counters[C_QMIN]);
             const float hi = ordered_value((uint32_t)c.h_counters[C_QMAX]);
             const bool useful = q8_plan(lo, hi, d, tp.eps2, q8p);
             q8_on = !c.h_counters[C_NONFINITE] && (useful || (q8_mode == 2 && q8p.s > 0));
             gr.q8 = q8_on;
+            q8_pipe = q8_on && pipe;
+            q8_replan = false;
+            gphases = phases;
             if (q8_on) {
                 const uint32_t nd = (d + 15) / 16;
                 c.q8.ensure(n * (nd + 1) * 16ull);
                 q8p.args.rows = c.q8.as<uint4>();
                 q8p.args.nd = nd;
-                CK(launch_quantize(pts, stride, n, d, q8p, c.q8.as<uint4>(), gs, c.num_sms));
-                gphases = gather_phases(c, n, 4 * (nd + 1), draws);
+                if (q8_pipe) {  // chunk 0 now, the others as they arrive
+                    quantize_rows(0, chunk_lo(1));
+                    quantized = 1;
+                    gphases = chunks;
+                } else {
+                    quantize_rows(0, n);
+                    quantized = chunks;
+                    gphases = gather_phases(c, n, 4 * (nd + 1), draws);
+                }
             }
         }
         tm.mark(E_SAMPLED);
@@ -511,22 +536,27 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             if (q8_on) CK(launch_gather_q8(ga, q8p.args, gs, c.num_sms));
             else CK(launch_gather(ga, exhaustive, gs, c.num_sms));
         };
-        if (h_src && attempt == 0 && !q8_try && chunks == phases && phases > 1) {
+        auto land_chunk = [&](uint32_t k) {  // chunk k uploaded, prepared, quantised
+            if (k >= prepared) {
+                CK(cudaStreamWaitEvent(gs, c.up_ev[k], 0));
+                prepare_rows(chunk_lo(k), chunk_lo(k + 1));
+            }
+            if (q8_on && k >= quantized) quantize_rows(chunk_lo(k), chunk_lo(k + 1));
+        };
+        if (h_src && attempt == 0 && prepared < chunks && chunks == gphases && gphases > 1) {
             // triangular schedule over (query chunk, partner slice) blocks:
             // once chunk k is in, every block it completes can run -- queries
             // <= k against slice k, then chunk k against the earlier slices
-            for (uint32_t k = 0; k < phases; ++k) {
-                CK(cudaStreamWaitEvent(gs, c.up_ev[k], 0));
-                prepare_rows(chunk_lo(k), chunk_lo(k + 1));
+            for (uint32_t k = 0; k < gphases; ++k) {
+                land_chunk(k);
                 gather(0, part(k + 1), part(k), part(k + 1));
                 for (uint32_t j = 0; j < k; ++j) gather(part(k), part(k + 1), part(j), part(j + 1));
             }
+            prepared = quantized = chunks;
         } else {
-            if (h_src && attempt == 0 && !q8_try)
-                for (uint32_t k = 0; k < chunks; ++k) {
-                    CK(cudaStreamWaitEvent(gs, c.up_ev[k], 0));
-                    prepare_rows(chunk_lo(k), chunk_lo(k + 1));
-                }
+            if (h_src && attempt == 0)
+                for (uint32_t k = 0; k < chunks; ++k) land_chunk(k);
+            prepared = quantized = chunks;
             for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
         }
         if (prio) {
@@ -552,6 +582,19 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (c.h_counters[C_NONFINITE]) return SNGB_ERR_NONFINITE;
+        if (q8_pipe) {  // the plan came from chunk 0: does it cover every value?
+            const double glo = ordered_value(~(uint32_t)c.h_counters[C_QMIN]);
+            const double ghi = ordered_value((uint32_t)c.h_counters[C_QMAX]);
+            q8_pipe = false;
+            if (glo < q8p.lo || ghi > q8p.lo + 255.0 * q8p.s) {
+                if (attempt == 3) {
+                    g_detail = "8-bit plan retries exhausted";
+                    throw CudaFail{cudaErrorUnknown};
+                }
+                q8_replan = true;  // redo with the global range (the data is resident)
+                continue;
+            }
+        }
         const uint64_t need_e = c.h_counters[C_EDGE_CURSOR];
         const uint64_t need_x = c.h_counters[C_EXTRA_CURSOR];
         const bool ok = need_e <= edge_cap && (exhaustive || need_x <= extras_cap);

@@ -273,3 +273,22 @@ def test_q8_forced_irregular_exact(oracle, monkeypatch):
     monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", "5")
     g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.04, seed=8)
     np.testing.assert_array_equal(g.keys, keys)
+
+
+@pytest.mark.parametrize("stretch,bits", [(1.0, 8), (2.5, 8), (5.0, 32)])
+def test_q8_pipelined_host_upload(oracle, stretch, bits):
+    """Host-buffer call, 2 upload chunks: the 8-bit plan is made from chunk 0 and
+    the gather starts before the rest arrives.  With stretch > 2 the last rows
+    leave chunk 0's range, the end-of-build check fails and the build is redone
+    from the global range: still 8-bit at 2.5, the fp32 filter at 5 (the band
+    of the global scale is too wide) -- all bit-identical to the oracle."""
+    n, d = 25000, 784
+    pts = synthetic.generate(2, n=n)
+    pts[n - 3000:] *= stretch
+    rate, seed, eps = 100 / n, 2, 4.5
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=eps, min_pts=5, rate=rate, seed=seed),
+                       info)
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, 5, rate, seed)
+    _assert_same(c, info, labels, roles, oinfo)
+    assert info.gpu["filter_bits"] == bits
