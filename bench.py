@@ -375,7 +375,7 @@ def main():
                 "achieved": achieved, "peak": peak,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": load_traffic(w.name) if not q8 else None,
+                "traffic": load_traffic(w.name + ("_q8" if q8 else "")),
                 "algorithmic_bytes_per_launch": gather_bytes,
                 "bytes_per_pair": bpp, "pairs_per_launch": gather_pairs,
                 "filter": ("8-bit exact filter: u8 rows + norm, DP4A integer distances, "

@@ -107,6 +107,7 @@ __global__ void k_union(const unsigned long long* __restrict__ keys, const unsig
                 run_a = a;
                 ra = uf_find(parent, a);
             }
+            if (parent[b] == ra) continue;  // b already hangs off a's root
             for (;;) {
                 // ra is in a's tree; walk up if another thread hooked it meanwhile
                 for (uint32_t p = parent[ra]; p != ra; p = parent[ra]) ra = p;
@@ -118,6 +119,29 @@ __global__ void k_union(const unsigned long long* __restrict__ keys, const unsig
                     break;
                 }
             }
+        }
+    }
+}
+
+// Afforest-style first round: union each vertex with the first neighbour of its
+// run of keys only (one edge per vertex), so that after a compression most
+// core vertices already point at their component's root and the full pass can
+// dismiss an edge with two loads (parent[a] == parent[b]) instead of two finds.
+__global__ void k_union_first(const unsigned long long* __restrict__ keys,
+                              const unsigned long long* m_ptr, uint64_t m_host, uint32_t nb,
+                              const uint8_t* __restrict__ core, uint32_t* parent) {
+    const uint64_t m = m_ptr ? *m_ptr : m_host;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t a, b;
+        decode(keys[e], nb, a, b);
+        if (e > 0 && (uint32_t)(keys[e - 1] >> nb) == a) continue;  // not a run's first key
+        if (!core[a] || !core[b]) continue;
+        for (;;) {
+            const uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
+            if (ra == rb) break;
+            const uint32_t lo = ra < rb ? ra : rb, hi = ra < rb ? rb : ra;
+            if (atomicCAS(&parent[hi], hi, lo) == hi) break;
         }
     }
 }
@@ -351,7 +375,11 @@ cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned
     const unsigned ge = grid_for(m, num_sms), gn = grid_for(n + 1, num_sms);
     if (m) k_degrees<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.deg);
     k_init<<<gn, 256, 0, s>>>(b.deg, n, (uint32_t)min_pts, b.core, b.parent, b.broot, b.first);
-    if (m) k_union<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.core, b.parent);
+    if (m) {
+        k_union_first<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.core, b.parent);
+        k_compress<<<gn, 256, 0, s>>>(n, b.core, b.parent);
+        k_union<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.core, b.parent);
+    }
     k_compress<<<gn, 256, 0, s>>>(n, b.core, b.parent);
     if (m) k_border<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.core, b.parent, b.broot);
     k_first<<<gn, 256, 0, s>>>(n, b.core, b.parent, b.broot, b.first);
@@ -362,7 +390,7 @@ cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned
     k_labels<<<gn, 256, 0, s>>>(n, b.core, b.parent, b.broot, b.first, b.rank, labels, roles,
                                 counters);
     k_store_clusters<<<1, 1, 0, s>>>(b.rank, n, counters);
-    note_launch(m ? 9 : 6, 2);  // + CUB scan (init + sweep)
+    note_launch(m ? 11 : 6, 2);  // + CUB scan (init + sweep)
     return cudaGetLastError();
 }
 
