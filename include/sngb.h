@@ -126,6 +126,23 @@ int sngb_sampled_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps,
                            uint64_t seed, const sngb_opts* opts, uint64_t* keys_out,
                            uint64_t capacity, uint64_t* count_out, sngb_info* info_out);
 
+/* fp64 input -- the reference's own Dataset type (dataset.hpp:69-71).  Values
+ * that are not exactly fp32 are kept in fp64 on the device: the filter works on
+ * them rounded to fp32 (or quantised to 8 bits from the fp64 values) with its
+ * accept / reject thresholds widened by the rounding bound
+ * sqrt(d) (2^-23 max|x| + 2^-149), and every pair in the band is re-evaluated
+ * with the reference's fp64 operation order on the fp64 values.  Same results
+ * as the reference, bit for bit. */
+int sngb_dbscan_f64(const double* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                    double rate, uint64_t seed, const sngb_opts* opts, int32_t* labels_out,
+                    uint8_t* roles_out, sngb_info* info_out);
+int sngb_dbscan_f64_device(const double* d_pts, uint64_t n, uint32_t d, double eps,
+                           int32_t min_pts, double rate, uint64_t seed, const sngb_opts* opts,
+                           int32_t* d_labels, uint8_t* d_roles, sngb_info* info_out);
+int sngb_sampled_edges_f64(const double* pts, uint64_t n, uint32_t d, double eps, double rate,
+                           uint64_t seed, const sngb_opts* opts, uint64_t* keys_out,
+                           uint64_t capacity, uint64_t* count_out, sngb_info* info_out);
+
 /* sng::cluster_graph (clusterer.hpp:38) over canonical edge keys on the device
  * (any order, duplicates allowed -- they are sorted and deduplicated first,
  * graph.cpp:34-40).  This is the merge step of the multi-GPU path: every rank

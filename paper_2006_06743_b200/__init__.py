@@ -87,9 +87,11 @@ class Distance:
 class Dataset:
     """Row-major n x dim matrix of finite reals (dataset.hpp:16-71).
 
-    Stored as fp32 on the way to the device.  fp64 input must be exactly
-    representable in fp32 (widening back is then exact and the results are
-    the reference's); other fp64 input is rejected rather than rounded.
+    fp32 input, and fp64 input whose values are all exactly fp32, are stored as
+    fp32 (widening back is exact).  Other fp64 input is kept in fp64
+    (``values64``) and runs the fp64 entry points, which filter on rounded
+    values with a widened guard band and recheck in fp64 -- the reference's
+    results either way.
     """
 
     def __init__(self, values, dim: int | None = None):
@@ -107,16 +109,18 @@ class Dataset:
             raise InvalidArgument("dataset dimension must be >= 1")
         if a.shape[0] == 0:
             raise InvalidArgument("dataset values do not form n x dim rows")
+        self.values64 = None
         if a.dtype == np.float32:
             f = np.ascontiguousarray(a)
         else:
-            a64 = np.asarray(a, np.float64)
-            f = np.ascontiguousarray(a64.astype(np.float32))
-            if not np.array_equal(f.astype(np.float64), a64, equal_nan=True):
-                raise NotImplementedError(
-                    "fp64 data that is not exactly representable in fp32 is not supported "
-                    "by the fp32 GPU path")
-        if not np.isfinite(f).all():
+            a64 = np.ascontiguousarray(a, np.float64)
+            if not np.isfinite(a64).all():
+                raise InvalidArgument("dataset contains a non-finite value")
+            with np.errstate(over="ignore"):
+                f = np.ascontiguousarray(a64.astype(np.float32))
+            if not np.array_equal(f.astype(np.float64), a64):
+                self.values64 = a64  # not exactly fp32: the fp64 path
+        if not np.isfinite(f).all() and self.values64 is None:
             raise InvalidArgument("dataset contains a non-finite value")
         self.values = f
         self.truth = None
@@ -231,11 +235,14 @@ def sng_dbscan(data: Dataset, params: SngParams, info: ClusterRunInfo | None = N
     roles = np.empty(n, np.uint8)
     gi = SngbInfo()
     o = _opts(params.device, timing)
-    rc = _lib.lib().sngb_dbscan_f32(
-        pts.ctypes.data_as(C.POINTER(C.c_float)), n, d, float(params.eps), int(params.min_pts),
-        float(params.rate), int(params.seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o),
-        labels.ctypes.data_as(C.POINTER(C.c_int32)), roles.ctypes.data_as(C.POINTER(C.c_uint8)),
-        C.byref(gi))
+    if data.values64 is not None:
+        fn, arg = _lib.lib().sngb_dbscan_f64, data.values64.ctypes.data_as(C.POINTER(C.c_double))
+    else:
+        fn, arg = _lib.lib().sngb_dbscan_f32, pts.ctypes.data_as(C.POINTER(C.c_float))
+    rc = fn(arg, n, d, float(params.eps), int(params.min_pts), float(params.rate),
+            int(params.seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o),
+            labels.ctypes.data_as(C.POINTER(C.c_int32)),
+            roles.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(gi))
     _check(rc)
     if info is not None:
         info.distance_evals = gi.distance_evals
@@ -259,14 +266,15 @@ def build_sampled_graph(data: Dataset, eps: float, rate: float, dist: Distance |
     gi = SngbInfo()
     o = _opts(device)
     cnt = C.c_uint64(0)
-    f32p = pts.ctypes.data_as(C.POINTER(C.c_float))
+    if data.values64 is not None:
+        fn, arg = L.sngb_sampled_edges_f64, data.values64.ctypes.data_as(C.POINTER(C.c_double))
+    else:
+        fn, arg = L.sngb_sampled_edges_f32, pts.ctypes.data_as(C.POINTER(C.c_float))
     cap = 1 << 20
     while True:
         keys = np.empty(cap, np.uint64)
-        rc = L.sngb_sampled_edges_f32(f32p, n, d, float(eps), float(rate),
-                                      int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o),
-                                      keys.ctypes.data_as(C.POINTER(C.c_uint64)), cap,
-                                      C.byref(cnt), C.byref(gi))
+        rc = fn(arg, n, d, float(eps), float(rate), int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(o),
+                keys.ctypes.data_as(C.POINTER(C.c_uint64)), cap, C.byref(cnt), C.byref(gi))
         if rc == _lib.SNGB_ERR_CAPACITY:
             cap = int(cnt.value)
             continue

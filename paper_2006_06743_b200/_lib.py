@@ -35,6 +35,7 @@ EXPORTS = [
     "sngb_last_error_detail", "sngb_abi_version", "sngb_device_count", "sngb_release_pools",
     "sngb_unique_keys_device", "sngb_degrees_device", "sngb_components_device",
     "sngb_border_device", "sngb_relabel_device",
+    "sngb_dbscan_f64", "sngb_dbscan_f64_device", "sngb_sampled_edges_f64",
 ]
 
 
@@ -107,6 +108,17 @@ def lib() -> C.CDLL:
         L.sngb_border_device.argtypes = [vp, C.c_uint64, C.c_uint64, vp, C.c_int32, vp, optp, vp]
         L.sngb_relabel_device.restype = C.c_int
         L.sngb_relabel_device.argtypes = [C.c_uint64, vp, C.c_int32, vp, vp, optp, vp, vp, infop]
+        f64p = C.POINTER(C.c_double)
+        L.sngb_dbscan_f64.restype = C.c_int
+        L.sngb_dbscan_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                      C.c_double, C.c_uint64, optp, i32p, u8p, infop]
+        L.sngb_dbscan_f64_device.restype = C.c_int
+        L.sngb_dbscan_f64_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                             C.c_double, C.c_uint64, optp, vp, vp, infop]
+        L.sngb_sampled_edges_f64.restype = C.c_int
+        L.sngb_sampled_edges_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double,
+                                             C.c_double, C.c_uint64, optp, u64p, C.c_uint64, u64p,
+                                             infop]
         L.sngb_strerror.restype = C.c_char_p
         L.sngb_strerror.argtypes = [C.c_int]
         L.sngb_last_error_detail.restype = C.c_char_p

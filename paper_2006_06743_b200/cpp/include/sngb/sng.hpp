@@ -2,8 +2,8 @@
 // point, implemented over the C ABI (include/sngb.h, libsngb.so).
 //
 // Same names, argument meaning and error behaviour as the reference:
-//   sng::Dataset         proj/include/sng/dataset.hpp:16-71   (fp64 rows; here
-//                        converted to fp32, rejected if not exactly representable)
+//   sng::Dataset         proj/include/sng/dataset.hpp:16-71   (fp64 rows: kept
+//                        as fp32 when exact, else as fp64 for the fp64 entry points)
 //   sng::SngParams       proj/include/sng/clusterer.hpp:11-24
 //   sng::ClusterRunInfo  proj/include/sng/clusterer.hpp:27-31
 //   sng::Clustering      proj/include/sng/dataset.hpp:78-91
@@ -37,14 +37,14 @@ public:
         if (values.empty() || values.size() % dim_ != 0)
             throw std::invalid_argument("dataset values do not form n x dim rows");
         values_.resize(values.size());
+        bool exact = true;
         for (std::size_t i = 0; i < values.size(); ++i) {
             if (!std::isfinite(values[i]))
                 throw std::invalid_argument("dataset contains a non-finite value");
             values_[i] = static_cast<float>(values[i]);
-            if (static_cast<double>(values_[i]) != values[i])
-                throw std::invalid_argument(
-                    "value not exactly representable in fp32 (the GPU path is fp32-exact only)");
+            exact = exact && static_cast<double>(values_[i]) == values[i];
         }
+        if (!exact) values64_ = std::move(values);  // fp32 cannot hold them: the fp64 path
     }
     Dataset(std::vector<float> values, std::size_t dim) : values_(std::move(values)), dim_(dim) {
         if (dim_ == 0) throw std::invalid_argument("dataset dimension must be >= 1");
@@ -57,9 +57,16 @@ public:
     std::size_t dim() const { return dim_; }
     bool empty() const { return values_.empty(); }
     const std::vector<float>& values_f32() const { return values_; }
+    bool is_fp64() const { return !values64_.empty(); }
+    const std::vector<double>& values_f64() const { return values64_; }
+    // the reference's accessor (dataset.hpp:69-71): the rows as fp64
+    std::vector<double> values() const {
+        return is_fp64() ? values64_ : std::vector<double>(values_.begin(), values_.end());
+    }
 
 private:
     std::vector<float> values_;
+    std::vector<double> values64_;
     std::size_t dim_ = 0;
 };
 
@@ -116,9 +123,14 @@ inline Clustering sng_dbscan(const Dataset& data, const SngParams& params,
     std::vector<std::uint8_t> roles(n);
     sngb_opts o{params.device, 0u, nullptr, 0, 0};
     sngb_info gi{};
-    detail::check(sngb_dbscan_f32(data.values_f32().data(), n, static_cast<std::uint32_t>(data.dim()),
-                                  params.eps, params.min_pts, params.rate, params.seed, &o,
-                                  labels.data(), roles.data(), &gi));
+    const auto d = static_cast<std::uint32_t>(data.dim());
+    detail::check(data.is_fp64()
+                      ? sngb_dbscan_f64(data.values_f64().data(), n, d, params.eps, params.min_pts,
+                                        params.rate, params.seed, &o, labels.data(), roles.data(),
+                                        &gi)
+                      : sngb_dbscan_f32(data.values_f32().data(), n, d, params.eps, params.min_pts,
+                                        params.rate, params.seed, &o, labels.data(), roles.data(),
+                                        &gi));
     Clustering c;
     c.assignment = std::move(labels);
     c.role.resize(n);

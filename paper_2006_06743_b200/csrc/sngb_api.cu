@@ -94,7 +94,7 @@ struct DevCtx {
     cudaEvent_t up_ev[kMaxChunks] = {};
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
-        flags, rank, temp, labels, roles, work, q8;
+        flags, rank, temp, labels, roles, work, q8, upload64;
     cudaEvent_t qev = nullptr;  // min/max of the points copied to the host (8-bit filter)
     unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
     cudaEvent_t ev[12] = {};
@@ -102,7 +102,7 @@ struct DevCtx {
 
     void release() {
         for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
-                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8})
+                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64})
             b->release();
     }
 };
@@ -207,7 +207,12 @@ float f32_up(double x) {
 // satisfies |s32 - S| <= ((1+u)^(2d+12) - 1) S + (2d+16) 2^-149 for the exact
 // S; the reference's fp64 sum is within (d+1) 2^-53 S of S.  rel below
 // over-covers both, so s32 < lo => ref accepts, s32 > hi => ref rejects.
-TestParams make_test(const float* pts, uint32_t stride, uint32_t d, double eps) {
+// fp64 input (round_dist > 0): the fp32 rows are the caller's values rounded to
+// nearest, |x32 - x| <= 2^-24 |x| + 2^-150, so the Euclidean distance of the
+// rounded rows is within round_dist = sqrt(d) (2^-23 max|x| + 2^-149) of the
+// true one; the accept / reject thresholds move by that much in distance.
+TestParams make_test(const float* pts, uint32_t stride, uint32_t d, double eps,
+                     double round_dist = 0.0) {
     TestParams tp{};
     tp.pts = pts;
     tp.stride = stride;
@@ -215,8 +220,11 @@ TestParams make_test(const float* pts, uint32_t stride, uint32_t d, double eps) 
     tp.eps2 = eps * eps;
     const double rel = (2.0 * d + 16.0) * std::ldexp(1.0, -24) * 1.25 + 1e-12;
     const double abs_ = (2.0 * d + 16.0) * std::ldexp(1.0, -148);
-    const double lo = tp.eps2 * (1.0 - rel) - abs_;
-    const double hi = tp.eps2 * (1.0 + rel) + abs_;
+    const double ea = std::sqrt(tp.eps2) * (1.0 - 1e-12) - round_dist;  // accept below (distance)
+    const double eb = std::sqrt(tp.eps2) * (1.0 + 1e-12) + round_dist;  // reject above
+    const double lo = round_dist > 0.0 ? (ea > 0.0 ? ea * ea * (1.0 - rel) - abs_ : -1.0)
+                                       : tp.eps2 * (1.0 - rel) - abs_;
+    const double hi = round_dist > 0.0 ? eb * eb * (1.0 + rel) + abs_ : tp.eps2 * (1.0 + rel) + abs_;
     tp.lo_thr = lo > 0 ? f32_down(lo) : 0.0f;
     tp.hi_thr = hi < (double)FLT_MAX / 4 ? f32_up(hi) : INFINITY;
     tp.eps2f = (float)tp.eps2;
@@ -296,7 +304,7 @@ struct GraphResult {
 // the sampler and (L2-blocked case) with the gather of the chunks already in.
 int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64_t n, uint32_t d,
                 double eps, double rate, uint64_t seed, uint64_t rb, uint64_t re,
-                GraphResult& gr, const float* h_src = nullptr) {
+                GraphResult& gr, const float* h_src = nullptr, const double* d_pts64 = nullptr) {
     unsigned long long* dc = nullptr;
     c.counters.ensure(C_COUNT * sizeof(unsigned long long));
     dc = c.counters.as<unsigned long long>();
@@ -308,13 +316,18 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     // every eps-test).
     const uint32_t stride = d <= 2 ? 2u : ((d + 3u) & ~3u);
     const size_t align = stride == 2 ? 8 : 16;
-    const bool pad = stride != d || (reinterpret_cast<uintptr_t>(d_pts) % align) != 0;
+    const bool f64 = d_pts64 != nullptr;  // fp64 input: rounded into the padded fp32 table
+    const bool pad = f64 || stride != d || (reinterpret_cast<uintptr_t>(d_pts) % align) != 0;
     if (pad) c.pts.ensure(n * stride * sizeof(float));
     const float* pts = pad ? c.pts.as<float>() : d_pts;
     cudaStream_t gs = s;  // the gather's stream (c.hi under SNGB_PRIO)
     bool q8_try = false;  // wide rows: min/max for the 8-bit filter (sngb_quant.cu)
     auto prepare_rows = [&](uint64_t lo, uint64_t hi) {
-        if (hi > lo)
+        if (hi <= lo) return;
+        if (f64)
+            CK(launch_prepare_points_f64(d_pts64 + lo * d, c.pts.as<float>() + lo * stride,
+                                         hi - lo, d, stride, dc, gs));
+        else
             CK(launch_prepare_points(d_pts + lo * d, pad ? c.pts.as<float>() + lo * stride : nullptr,
                                      hi - lo, d, stride, dc, q8_try, gs));
     };
@@ -361,7 +374,20 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     uint32_t slots = 64, col_words = 4;
     if (!exhaustive) floyd_geometry((uint32_t)draws, slots, col_words);
 
-    const TestParams tp = make_test(pts, stride, d, eps);
+    // fp64 input: the fp32 thresholds need max|x| before any test runs
+    double round_dist = 0.0;
+    if (f64) {
+        prepare_rows(0, n);
+        minmax_to_host();
+        CK(cudaEventSynchronize(c.qev));
+        const double lo = ordered_value64(~c.h_counters[C_QMIN]);
+        const double hi = ordered_value64(c.h_counters[C_QMAX]);
+        const double m = std::max(std::fabs(lo), std::fabs(hi));
+        round_dist = std::sqrt((double)d) * (std::ldexp(m, -23) + std::ldexp(1.0, -149)) *
+                     (1.0 + 1e-9);
+    }
+    TestParams tp = make_test(pts, stride, d, eps, round_dist);
+    tp.pts64 = d_pts64;
     const uint64_t seed_mixed = seed_part(seed);
     const uint32_t phases = gather_phases(c, n, stride, draws);
 
@@ -381,7 +407,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         }
         tm.mark_on(E_UPLOADED, c.copy);
     };
-    if (!h_src) {
+    if (!h_src && !f64) {
         prepare_rows(0, n);
         if (q8_try) minmax_to_host();
     }
@@ -447,7 +473,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         auto quantize_rows = [&](uint64_t r0, uint64_t r1) {
             if (r1 > r0)
                 CK(launch_quantize(pts + r0 * stride, stride, r1 - r0, d, q8p,
-                                   c.q8.as<uint4>() + r0 * (q8p.args.nd + 1), gs, c.num_sms));
+                                   c.q8.as<uint4>() + r0 * (q8p.args.nd + 1), gs, c.num_sms,
+                                   f64 ? d_pts64 + r0 * d : nullptr));
         };
         if (q8_try && (attempt == 0 || q8_replan)) {
             const bool pipe = h_src && attempt == 0 && chunks > 1;
@@ -462,8 +489,10 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             }
             // a re-plan reads the global min/max kept in h_counters by the last sync
             if (!q8_replan) CK(cudaEventSynchronize(c.qev));
-            const float lo = ordered_value(~(uint32_t)c.h_counters[C_QMIN]);
-            const float hi = ordered_value((uint32_t)c.h_counters[C_QMAX]);
+            const double lo = f64 ? ordered_value64(~c.h_counters[C_QMIN])
+                                  : (double)ordered_value(~(uint32_t)c.h_counters[C_QMIN]);
+            const double hi = f64 ? ordered_value64(c.h_counters[C_QMAX])
+                                  : (double)ordered_value((uint32_t)c.h_counters[C_QMAX]);
             const bool useful = q8_plan(lo, hi, d, tp.eps2, q8p);
             q8_on = !c.h_counters[C_NONFINITE] && (useful || (q8_mode == 2 && q8p.s > 0));
             gr.q8 = q8_on;
@@ -699,8 +728,9 @@ int guarded(F&& f) {
 // Full pipeline on device buffers; labels/roles device pointers.
 int dbscan_device(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64_t n, uint32_t d,
                   double eps, int32_t min_pts, double rate, uint64_t seed, int32_t* d_labels,
-                  uint8_t* d_roles, GraphResult& gr, const float* h_src = nullptr) {
-    int rc = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, 0, n, gr, h_src);
+                  uint8_t* d_roles, GraphResult& gr, const float* h_src = nullptr,
+                  const double* d_pts64 = nullptr) {
+    int rc = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, 0, n, gr, h_src, d_pts64);
     if (rc) return rc;
     ClusterBuffers b{};
     ensure_cluster_bufs(c, n, b);
@@ -982,6 +1012,121 @@ int sngb_cluster_edges_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n
         CK(cudaStreamSynchronize(s));
         if (c.h_counters[C_BADKEY]) return SNGB_ERR_ARG;
         fill_info(info, c.h_counters, n, 0, gr, 0, tm, true, false);
+        return SNGB_OK;
+    });
+}
+
+// ---- fp64 input (the reference's Dataset is fp64, dataset.hpp:69-71) -------
+int sngb_dbscan_f64_device(const double* d_pts, uint64_t n, uint32_t d, double eps,
+                           int32_t min_pts, double rate, uint64_t seed, const sngb_opts* opts,
+                           int32_t* d_labels, uint8_t* d_roles, sngb_info* info) {
+    int rc = validate(n, d, eps, min_pts, rate, true);
+    if (rc) return rc;
+    if (!d_pts || !d_labels || !d_roles) return SNGB_ERR_ARG;
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    return guarded([&]() -> int {
+        const int dev = resolve_device(opts);
+        DeviceGuard dg(dev);
+        DevCtx& c = get_ctx(dev);
+        std::lock_guard<std::mutex> lk(c.mu);
+        cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
+        Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
+        tm.mark(E_START);
+        tm.mark(E_UPLOADED);
+        GraphResult gr;
+        int r = dbscan_device(c, s, tm, nullptr, n, d, eps, min_pts, rate, seed, d_labels, d_roles,
+                              gr, nullptr, d_pts);
+        if (r) return r;
+        tm.mark(E_DOWNLOADED);
+        tm.mark(E_END);
+        CK(cudaMemcpyAsync(c.h_counters, c.counters.p, C_COUNT * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fill_info(info, c.h_counters, n, d, gr, n, tm, true, false);
+        return SNGB_OK;
+    });
+}
+
+int sngb_dbscan_f64(const double* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                    double rate, uint64_t seed, const sngb_opts* opts, int32_t* labels_out,
+                    uint8_t* roles_out, sngb_info* info) {
+    int rc = validate(n, d, eps, min_pts, rate, true);
+    if (rc) return rc;
+    if (!pts || !labels_out || !roles_out) return SNGB_ERR_ARG;
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    return guarded([&]() -> int {
+        const int dev = resolve_device(opts);
+        DeviceGuard dg(dev);
+        DevCtx& c = get_ctx(dev);
+        std::lock_guard<std::mutex> lk(c.mu);
+        cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
+        Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
+        tm.mark(E_START);
+        c.upload64.ensure(n * d * sizeof(double));
+        CK(cudaMemcpyAsync(c.upload64.p, pts, n * d * sizeof(double), cudaMemcpyHostToDevice, s));
+        tm.mark(E_UPLOADED);
+        c.labels.ensure(n * 4);
+        c.roles.ensure(n);
+        GraphResult gr;
+        int r = dbscan_device(c, s, tm, nullptr, n, d, eps, min_pts, rate, seed,
+                              c.labels.as<int32_t>(), c.roles.as<uint8_t>(), gr, nullptr,
+                              c.upload64.as<double>());
+        if (r) return r;
+        CK(cudaMemcpyAsync(labels_out, c.labels.p, n * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(roles_out, c.roles.p, n, cudaMemcpyDeviceToHost, s));
+        tm.mark(E_DOWNLOADED);
+        tm.mark(E_END);
+        CK(cudaMemcpyAsync(c.h_counters, c.counters.p, C_COUNT * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fill_info(info, c.h_counters, n, d, gr, n, tm, true, true);
+        return SNGB_OK;
+    });
+}
+
+int sngb_sampled_edges_f64(const double* pts, uint64_t n, uint32_t d, double eps, double rate,
+                           uint64_t seed, const sngb_opts* opts, uint64_t* keys_out,
+                           uint64_t capacity, uint64_t* count_out, sngb_info* info) {
+    int rc = validate(n, d, eps, 1, rate, false);
+    if (rc) return rc;
+    if (!pts || !count_out) return SNGB_ERR_ARG;
+    const uint64_t rb = opts ? opts->row_begin : 0;
+    const uint64_t re = (opts && opts->row_end) ? opts->row_end : n;
+    if (rb > re || re > n) return SNGB_ERR_ARG;
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    return guarded([&]() -> int {
+        const int dev = resolve_device(opts);
+        DeviceGuard dg(dev);
+        DevCtx& c = get_ctx(dev);
+        std::lock_guard<std::mutex> lk(c.mu);
+        cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
+        Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
+        tm.mark(E_START);
+        c.upload64.ensure(n * d * sizeof(double));
+        CK(cudaMemcpyAsync(c.upload64.p, pts, n * d * sizeof(double), cudaMemcpyHostToDevice, s));
+        tm.mark(E_UPLOADED);
+        GraphResult gr;
+        int r = build_graph(c, s, tm, nullptr, n, d, eps, rate, seed, rb, re, gr, nullptr,
+                            c.upload64.as<double>());
+        if (r) return r;
+        tm.mark(E_CLUSTERED);
+        unsigned long long* dc = c.counters.as<unsigned long long>();
+        CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t m = c.h_counters[C_UNIQUE];
+        *count_out = m;
+        if (m > capacity) {
+            fill_info(info, c.h_counters, n, d, gr, re - rb, tm, false, true);
+            return SNGB_ERR_CAPACITY;
+        }
+        if (m && !keys_out) return SNGB_ERR_ARG;
+        unsigned long long* conv = (gr.ukeys == c.keys.as<unsigned long long>())
+                                       ? c.keys_alt.as<unsigned long long>()
+                                       : c.keys.as<unsigned long long>();
+        CK(launch_convert_keys(gr.ukeys, conv, m, gr.nb, false, n, dc, s, c.num_sms));
+        if (m) CK(cudaMemcpyAsync(keys_out, conv, m * 8, cudaMemcpyDeviceToHost, s));
+        tm.mark(E_DOWNLOADED);
+        tm.mark(E_END);
+        CK(cudaStreamSynchronize(s));
+        fill_info(info, c.h_counters, n, d, gr, re - rb, tm, false, true);
         return SNGB_OK;
     });
 }

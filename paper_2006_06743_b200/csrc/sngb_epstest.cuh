@@ -125,13 +125,23 @@ __device__ __forceinline__ unsigned long long edge_key(uint64_t u, uint64_t v, u
 
 // distance.hpp:75-83 verbatim in fp64: s += (a_k - b_k)^2 sequentially in k,
 // no contraction (explicit _rn intrinsics), then s <= eps*eps.
+// fp64 input: on the caller's fp64 rows, exactly as the reference does.
 static __device__ __noinline__ bool exact_within(const TestParams tp, uint64_t u, uint64_t v) {
-    const float* a = tp.pts + u * tp.stride;
-    const float* b = tp.pts + v * tp.stride;
     double s = 0.0;
-    for (uint32_t k = 0; k < tp.d; ++k) {
-        const double t = __dsub_rn((double)a[k], (double)b[k]);
-        s = __dadd_rn(s, __dmul_rn(t, t));
+    if (tp.pts64) {
+        const double* a = tp.pts64 + u * tp.d;
+        const double* b = tp.pts64 + v * tp.d;
+        for (uint32_t k = 0; k < tp.d; ++k) {
+            const double t = __dsub_rn(a[k], b[k]);
+            s = __dadd_rn(s, __dmul_rn(t, t));
+        }
+    } else {
+        const float* a = tp.pts + u * tp.stride;
+        const float* b = tp.pts + v * tp.stride;
+        for (uint32_t k = 0; k < tp.d; ++k) {
+            const double t = __dsub_rn((double)a[k], (double)b[k]);
+            s = __dadd_rn(s, __dmul_rn(t, t));
+        }
     }
     return s <= tp.eps2;
 }

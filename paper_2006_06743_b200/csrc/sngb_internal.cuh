@@ -44,6 +44,8 @@ struct TestParams {
     float hi_thr;      // s32 >  hi_thr  => exact s64 >  eps2 (reject)
     float eps2f;       // (float)eps2, for the bare-fp32 comparison statistics
     double eps2;       // eps * eps in fp64, as distance.hpp:82 computes it
+    const double* pts64;  // fp64 input: the caller's rows (d per row) for the exact
+                          // recheck; pts then holds them rounded to fp32.  null: fp32 input
 };
 
 // Canonical undirected edge keys: (min << nb) | max with nb = bits(n-1).
@@ -113,6 +115,11 @@ void note_launch(int hand_written, int library = 0);
 cudaError_t launch_prepare_points(const float* src, float* dst, uint64_t n, uint32_t d,
                                   uint32_t stride, unsigned long long* counters, bool minmax,
                                   cudaStream_t s);
+// fp64 input: round into the padded fp32 table, count non-finite values, and
+// the exact fp64 min / max as ordered 64-bit keys in C_QMIN / C_QMAX
+cudaError_t launch_prepare_points_f64(const double* src, float* dst, uint64_t n, uint32_t d,
+                                      uint32_t stride, unsigned long long* counters,
+                                      cudaStream_t s);
 // float <-> unsigned key with the same order (min/max by integer atomics)
 __host__ __device__ __forceinline__ uint32_t ordered_key(float f) {
     uint32_t u;
@@ -122,6 +129,25 @@ __host__ __device__ __forceinline__ uint32_t ordered_key(float f) {
     std::memcpy(&u, &f, 4);
 #endif
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ __forceinline__ uint64_t ordered_key64(double f) {
+    uint64_t u;
+#ifdef __CUDA_ARCH__
+    u = (uint64_t)__double_as_longlong(f);
+#else
+    std::memcpy(&u, &f, 8);
+#endif
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double ordered_value64(uint64_t k) {
+    const uint64_t u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    double f;
+#ifdef __CUDA_ARCH__
+    f = __longlong_as_double((long long)u);
+#else
+    std::memcpy(&f, &u, 8);
+#endif
+    return f;
 }
 __host__ __device__ __forceinline__ float ordered_value(uint32_t k) {
     const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
@@ -150,9 +176,10 @@ struct Q8Plan {
     double s, lo;  // scale (a power of two) and offset (a multiple of s)
     Q8Args args;
 };
-bool q8_plan(float lo, float hi, uint32_t d, double eps2, Q8Plan& p);
+bool q8_plan(double lo, double hi, uint32_t d, double eps2, Q8Plan& p);
 cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint32_t d,
-                            const Q8Plan& p, uint4* out, cudaStream_t s, int num_sms);
+                            const Q8Plan& p, uint4* out, cudaStream_t s, int num_sms,
+                            const double* pts64 = nullptr);
 cudaError_t launch_gather_q8(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms);
 cudaError_t launch_extras_q8(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, int num_sms);
 cudaError_t launch_extras(const ExtrasArgs& a, cudaStream_t s, int num_sms);

@@ -408,9 +408,55 @@ __global__ void k_prepare(const float* __restrict__ src, float* __restrict__ dst
     }
 }
 
+// fp64 input: round each value to fp32 (to nearest) into the padded table,
+// count non-finite values, reduce the exact fp64 min / max.
+__global__ void k_prepare_f64(const double* __restrict__ src, float* __restrict__ dst, uint64_t n,
+                              uint32_t d, uint32_t stride, unsigned long long* counters) {
+    const uint64_t total = n * stride;
+    unsigned bad = 0;
+    unsigned long long kmin = 0, kmax = 0;
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = idx / stride;
+        const uint32_t c = (uint32_t)(idx - r * stride);
+        float v = 0.f;
+        if (c < d) {
+            const double x = src[r * d + c];
+            bad += !isfinite(x);
+            const unsigned long long k = ordered_key64(x);
+            kmin = max(kmin, ~k);
+            kmax = max(kmax, k);
+            v = __double2float_rn(x);
+        }
+        dst[idx] = v;
+    }
+    bad = __reduce_add_sync(kFull, bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&counters[C_NONFINITE], (unsigned long long)bad);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = max(kmin, __shfl_xor_sync(kFull, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&counters[C_QMIN], kmin);
+        atomicMax(&counters[C_QMAX], kmax);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+cudaError_t launch_prepare_points_f64(const double* src, float* dst, uint64_t n, uint32_t d,
+                                      uint32_t stride, unsigned long long* counters,
+                                      cudaStream_t s) {
+    uint64_t blocks = (n * stride + 255) / 256;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    if (blocks == 0) blocks = 1;
+    k_prepare_f64<<<(unsigned)blocks, 256, 0, s>>>(src, dst, n, d, stride, counters);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_prepare_points(const float* src, float* dst, uint64_t n, uint32_t d,
                                   uint32_t stride, unsigned long long* counters, bool minmax,
                                   cudaStream_t s) {

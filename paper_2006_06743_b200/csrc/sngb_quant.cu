@@ -33,8 +33,7 @@
 
 namespace sngb {
 
-bool q8_plan(float lo_f, float hi_f, uint32_t d, double eps2, Q8Plan& p) {
-    const double lo = lo_f, hi = hi_f;
+bool q8_plan(double lo, double hi, uint32_t d, double eps2, Q8Plan& p) {
     const double need = (hi - lo) / 254.0 * (1.0 + 1e-12);
     if (!(need > 0.0) || !std::isfinite(need)) return false;
     int e = 0;
@@ -62,7 +61,8 @@ namespace {
 
 // warp per row: bytes q of the row's d values, zero padded, then the norm chunk
 __global__ void k_quantize(const float* __restrict__ pts, uint32_t stride, uint64_t n, uint32_t d,
-                           double lo, double inv_s, uint32_t nd, uint4* __restrict__ out) {
+                           double lo, double inv_s, uint32_t nd, uint4* __restrict__ out,
+                           const double* __restrict__ pts64) {
     const int lane = threadIdx.x & 31;
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -76,11 +76,17 @@ __global__ void k_quantize(const float* __restrict__ pts, uint32_t stride, uint6
             for (int j4 = 0; j4 < 4; ++j4) {
                 const uint32_t k0 = 16 * c + 4 * j4;
                 if (k0 >= d) break;  // rows are 16-byte aligned with a stride of ceil4(d)
-                const float4 v = __ldg(reinterpret_cast<const float4*>(row + k0));
-                const float vs[4] = {v.x, v.y, v.z, v.w};
+                double vs[4];
+                if (pts64) {  // fp64 input: quantise the caller's values themselves
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) vs[j] = k0 + j < d ? pts64[r * d + k0 + j] : 0.0;
+                } else {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(row + k0));
+                    vs[0] = v.x, vs[1] = v.y, vs[2] = v.z, vs[3] = v.w;
+                }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const double x = rint(((double)vs[j] - lo) * inv_s);
+                    const double x = rint((vs[j] - lo) * inv_s);
                     const uint32_t q = k0 + j >= d ? 0u  // padding past d quantises to 0
                                        : x <= 0.0 ? 0u : (x >= 255.0 ? 255u : (uint32_t)x);
                     w[j4] |= q << (8 * j);
@@ -295,12 +301,13 @@ cudaError_t q8_one(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num
 }  // namespace
 
 cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint32_t d,
-                            const Q8Plan& p, uint4* out, cudaStream_t s, int num_sms) {
+                            const Q8Plan& p, uint4* out, cudaStream_t s, int num_sms,
+                            const double* pts64) {
     const uint32_t nd = (d + 15) / 16;
     uint64_t blocks = (n + 7) / 8;
     if (blocks > (uint64_t)num_sms * 16) blocks = (uint64_t)num_sms * 16;
     k_quantize<<<(unsigned)(blocks ? blocks : 1), 256, 0, s>>>(pts, stride, n, d, p.lo, 1.0 / p.s,
-                                                                nd, out);
+                                                                nd, out, pts64);
     note_launch(1);
     return cudaGetLastError();
 }

@@ -2,10 +2,12 @@
 // would against sng/clusterer.hpp.  Exit codes: 0 ok, 2 wrong result,
 // 3 no GPU (std::runtime_error), 4 unexpected exception text.
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "sngb/io.hpp"
 #include "sngb/sng.hpp"
 
 int main() {
@@ -31,7 +33,21 @@ int main() {
                         info.edges == 2 && info.distance_evals == 12;
         std::printf("clusters=%d edges=%zu evals=%llu\n", c.cluster_count, info.edges,
                     (unsigned long long)info.distance_evals);
-        return ok ? 0 : 2;
+        if (!ok) return 2;
+        // the same example as fp64 values fp32 cannot hold, through an SNGD file
+        // and a label file: the fp64 entry point, same clustering
+        const char* dir = std::getenv("DEMO_DIR");
+        const std::string base = dir ? dir : ".";
+        sng::save_binary(sng::Dataset(std::vector<double>{0.1, 0.6, 10.1, 10.6}, 1),
+                         base + "/demo.sngd");
+        sng::Dataset d64 = sng::load_binary(base + "/demo.sngd");
+        if (!d64.is_fp64()) return 2;
+        sng::Clustering c64 = sng::sng_dbscan(d64, p, &info);
+        sng::save_clustering(c64, base + "/demo.labels");
+        const bool ok64 = sng::load_labels(base + "/demo.labels") == c.assignment &&
+                          info.gpu.filter_bits == 32;
+        std::printf("fp64 via SNGD: clusters=%d ok=%d\n", c64.cluster_count, (int)ok64);
+        return ok64 ? 0 : 2;
     } catch (const std::runtime_error& e) {
         std::printf("runtime_error: %s\n", e.what());
         return 3;

@@ -35,5 +35,7 @@ def test_cpp_mirror_builds_and_fails_loudly_without_gpu(tmp_path):
 @pytest.mark.gpu
 def test_cpp_mirror_on_gpu(tmp_path):
     exe = _build(tmp_path)
-    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True,
+                       env={**os.environ, "DEMO_DIR": str(tmp_path)})
     assert r.returncode == 0, r.stdout + r.stderr
+    assert "fp64 via SNGD: clusters=2 ok=1" in r.stdout

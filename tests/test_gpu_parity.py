@@ -292,3 +292,60 @@ def test_q8_pipelined_host_upload(oracle, stretch, bits):
     labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, 5, rate, seed)
     _assert_same(c, info, labels, roles, oinfo)
     assert info.gpu["filter_bits"] == bits
+
+
+# ---- fp64 input (the reference's Dataset type) -----------------------------
+def _ref_or_skip():
+    import os
+    from oracle import REF_SO, Reference
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref/libsngref.so not built")
+    return Reference()
+
+
+@pytest.mark.parametrize("q8", ["0", "1"])
+@pytest.mark.parametrize("n,d,eps,rate,seed,scale", [
+    (3000, 2, 0.03, 0.1, 1, 1.0), (4000, 16, 0.5, 0.05, 3, 1.0), (2500, 200, 1.4, 0.05, 7, 1.0),
+    (2000, 784, 4.5, 0.05, 2, 1.0), (3000, 3, 0.1, 0.2, 4, 1e4)])
+def test_fp64_input_matches_reference(monkeypatch, q8, n, d, eps, rate, seed, scale):
+    """fp64 data that fp32 cannot hold: the f64 entry points (fp32 / 8-bit filter
+    on rounded or requantised values, widened band, fp64 recheck on the fp64
+    rows) against the reference compiled from its own sources."""
+    ref = _ref_or_skip()
+    monkeypatch.setenv("SNGB_Q8", q8)
+    rng = np.random.default_rng(seed)
+    cfg = {2: 1, 16: 3, 3: 4}.get(d, 2)
+    base = synthetic.generate(cfg, n=n).astype(np.float64) if d in (2, 16, 3, 784) else \
+        rng.random((n, d)) * 2.0
+    pts = base * scale + rng.normal(0, 1e-7, base.shape) * scale  # break fp32 exactness
+    ds = sng.Dataset(pts)
+    assert ds.values64 is not None
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(ds, sng.SngParams(eps=eps * scale, min_pts=4, rate=rate, seed=seed), info)
+    rds = ref.dataset(pts)
+    labels, roles, rinfo = ref.sng_dbscan(rds, eps * scale, 4, rate, seed)
+    np.testing.assert_array_equal(c.assignment, labels)
+    np.testing.assert_array_equal(c.role, roles)
+    assert info.edges == rinfo["edges"] and info.distance_evals == rinfo["distance_evals"]
+    keys, evals, _ = ref.sampled_edges(rds, eps * scale, rate, seed)
+    g = sng.build_sampled_graph(ds, eps * scale, rate, seed=seed)
+    np.testing.assert_array_equal(g.keys, keys)
+
+
+def test_fp64_band_edges_exact():
+    """fp64 pairs placed within a few ulps of eps: the fp32 rounding cannot
+    decide them, the fp64 recheck must, exactly as the reference."""
+    ref = _ref_or_skip()
+    n, d = 2000, 8
+    rng = np.random.default_rng(21)
+    centers = rng.random((n // 2, d))
+    direction = rng.normal(size=(n // 2, d))
+    direction /= np.linalg.norm(direction, axis=1, keepdims=True)
+    eps = 0.3
+    jitter = rng.choice([-3, -1, 0, 1, 3], size=(n // 2, 1)) * 1e-15
+    pts = np.concatenate([centers, centers + direction * (eps + jitter)])
+    ds = sng.Dataset(pts)
+    assert ds.values64 is not None
+    g = sng.build_sampled_graph(ds, eps, 1.0, seed=3)
+    keys, _, _ = ref.sampled_edges(ref.dataset(pts), eps, 1.0, 3)
+    np.testing.assert_array_equal(g.keys, keys)

@@ -35,8 +35,9 @@ def test_dataset_rules():  # dataset.hpp:21-27
         sng.Dataset(np.array([[np.nan, 0.0]], np.float32))
     ds = sng.Dataset(np.arange(6, dtype=np.float64), dim=3)
     assert ds.size() == 2 and ds.dim() == 3 and ds.values.dtype == np.float32
-    with pytest.raises(NotImplementedError):
-        sng.Dataset(np.array([[0.1, 0.2]]))  # fp64 values that fp32 cannot hold exactly
+    ds64 = sng.Dataset(np.array([[0.1, 0.2]]))  # fp64 values that fp32 cannot hold exactly
+    assert ds64.values64 is not None and ds64.values64.dtype == np.float64
+    assert ds.values64 is None  # fp32-exact fp64 input takes the fp32 path
 
 
 def test_distance_parse():  # distance.hpp:37-43
