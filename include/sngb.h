@@ -51,11 +51,17 @@ enum {
     SNGB_ERR_ARG = 8,        /* null pointer / bad row range */
     SNGB_ERR_NO_DEVICE = 9,  /* no usable CUDA device (there is no CPU fallback) */
     SNGB_ERR_CUDA = 10,      /* CUDA runtime error; see sngb_last_error_detail() */
-    SNGB_ERR_CAPACITY = 11   /* caller-provided output buffer too small; *count_out = needed */
+    SNGB_ERR_CAPACITY = 11,  /* caller-provided output buffer too small; *count_out = needed */
+    SNGB_ERR_ZERO_VECTOR = 12 /* "cosine distance is undefined for zero vectors" distance.hpp:97 */
 };
 
 /* opts.flags */
 #define SNGB_FLAG_TIMING 0x1u /* record per-stage CUDA-event times into sngb_info */
+/* The metric of Distance::within (distance.hpp:75-84); default Euclidean.
+ * Manhattan: sum |a_k - b_k| <= eps; cosine: 1 - clamp(dot / (|a| |b|)) <= eps,
+ * SNGB_ERR_ZERO_VECTOR when a row has a zero fp64 norm (n >= 2). */
+#define SNGB_FLAG_MANHATTAN 0x2u
+#define SNGB_FLAG_COSINE 0x4u
 
 typedef struct sngb_opts {
     int32_t device;     /* CUDA ordinal; -1 = current device */

@@ -191,7 +191,12 @@ class Reference:
         L.sngref_reference_dbscan.argtypes = [C.c_void_p, C.c_double, C.c_int32,
                                               C.POINTER(C.c_int32), C.POINTER(C.c_uint8)]
         L.sngref_free.argtypes = [C.c_void_p]
+        L.sngref_set_metric.argtypes = [C.c_int]
         self.L = L
+
+    def set_metric(self, name: str) -> None:
+        """Distance for the next calls on this thread: euclidean / manhattan / cosine."""
+        self.L.sngref_set_metric({"euclidean": 0, "manhattan": 1, "cosine": 2}[name])
 
     def hw_threads(self) -> int:
         return int(self.L.sngref_hw_threads())

@@ -78,6 +78,14 @@ void sngref_dataset_free(void* ds) { delete static_cast<sng::Dataset*>(ds); }
 
 // info[0]=distance_evals info[1]=edges info[2]=graph_bytes info[3]=cluster_count
 // *ms = wall time of the sng_dbscan call alone.
+// metric for the calls below (test infrastructure): 0 Euclidean, 1 Manhattan, 2 cosine
+static thread_local int g_metric = 0;
+void sngref_set_metric(int m) { g_metric = m; }
+static sng::Distance metric_dist() {
+    return g_metric == 1 ? sng::Distance::manhattan()
+                         : (g_metric == 2 ? sng::Distance::cosine() : sng::Distance::euclidean());
+}
+
 int sngref_dbscan(void* ds, double eps, int32_t min_pts, double rate, uint64_t seed, int threads,
                   int32_t* labels, uint8_t* roles, uint64_t* info, double* ms) {
     try {
@@ -88,6 +96,7 @@ int sngref_dbscan(void* ds, double eps, int32_t min_pts, double rate, uint64_t s
         p.rate = rate;
         p.seed = seed;
         p.threads = threads;
+        p.dist = metric_dist();
         sng::ClusterRunInfo ri;
         auto t0 = std::chrono::steady_clock::now();
         sng::Clustering c = sng::sng_dbscan(data, p, &ri);
@@ -116,8 +125,8 @@ int sngref_sampled_edges(void* ds, double eps, double rate, uint64_t seed, int t
         const auto& data = *static_cast<sng::Dataset*>(ds);
         sng::BuildStats st;
         auto t0 = std::chrono::steady_clock::now();
-        sng::SampledGraph g = sng::build_sampled_graph(data, eps, rate, sng::Distance::euclidean(),
-                                                       seed, threads, &st);
+        sng::SampledGraph g = sng::build_sampled_graph(data, eps, rate, metric_dist(), seed,
+                                                       threads, &st);
         auto t1 = std::chrono::steady_clock::now();
         if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         auto e = g.edges();

@@ -52,7 +52,7 @@ def _check(rc: int) -> None:
     msg = _lib.strerror(rc)
     if rc in (_lib.SNGB_ERR_EPS, _lib.SNGB_ERR_MINPTS, _lib.SNGB_ERR_RATE, _lib.SNGB_ERR_EMPTY,
               _lib.SNGB_ERR_DIM, _lib.SNGB_ERR_NONFINITE, _lib.SNGB_ERR_TOO_LARGE,
-              _lib.SNGB_ERR_ARG):
+              _lib.SNGB_ERR_ARG, _lib.SNGB_ERR_ZERO_VECTOR):
         raise InvalidArgument(msg)
     if rc == _lib.SNGB_ERR_CUDA:
         msg = f"{msg}: {_lib.last_error_detail()}"
@@ -64,17 +64,36 @@ def device_count() -> int:
 
 
 class Distance:
-    """distance.hpp: only the Euclidean metric runs on the GPU path."""
+    """distance.hpp: Euclidean, Manhattan and cosine run on the GPU path (the
+    fp32 filter plus the reference's fp64 recheck); a Python callback (the
+    reference's Metric::Custom) cannot, and raises NotImplementedError."""
+
+    _FLAGS = {"euclidean": 0, "manhattan": 0x2, "cosine": 0x4}
 
     def __init__(self, kind: str = "euclidean"):
-        if kind != "euclidean":
-            raise NotImplementedError(
-                f"distance '{kind}' is not on the B200 hot path (Euclidean only)")
+        if kind not in self._FLAGS:
+            raise NotImplementedError(f"distance '{kind}' is not on the B200 hot path")
         self.kind = kind
+
+    @property
+    def flags(self) -> int:
+        return self._FLAGS[self.kind]
 
     @staticmethod
     def euclidean() -> "Distance":
         return Distance("euclidean")
+
+    @staticmethod
+    def manhattan() -> "Distance":
+        return Distance("manhattan")
+
+    @staticmethod
+    def cosine() -> "Distance":
+        return Distance("cosine")
+
+    @staticmethod
+    def custom(fn, expected_dim=None) -> "Distance":
+        raise NotImplementedError("a Python distance callback cannot run on the GPU path")
 
     @staticmethod
     def parse(name: str) -> "Distance":  # distance.hpp:37-43
@@ -216,9 +235,9 @@ class SampledGraph:
 
 
 def _opts(device: int = -1, timing: bool = False, stream: int = 0, row_begin: int = 0,
-          row_end: int = 0) -> SngbOpts:
-    return SngbOpts(device, SNGB_FLAG_TIMING if timing else 0, C.c_void_p(stream or None),
-                    row_begin, row_end)
+          row_end: int = 0, dist: "Distance | None" = None) -> SngbOpts:
+    flags = (SNGB_FLAG_TIMING if timing else 0) | (dist.flags if dist is not None else 0)
+    return SngbOpts(device, flags, C.c_void_p(stream or None), row_begin, row_end)
 
 
 def sng_dbscan(data: Dataset, params: SngParams, info: ClusterRunInfo | None = None,
@@ -227,14 +246,14 @@ def sng_dbscan(data: Dataset, params: SngParams, info: ClusterRunInfo | None = N
     if not isinstance(data, Dataset):
         data = Dataset(data)
     params.validate()
-    if not isinstance(params.dist, Distance) or params.dist.kind != "euclidean":
-        raise NotImplementedError("only the Euclidean metric is on the GPU path")
+    if not isinstance(params.dist, Distance):
+        raise NotImplementedError("a Python distance callback cannot run on the GPU path")
     pts = data.values
     n, d = pts.shape
     labels = np.empty(n, np.int32)
     roles = np.empty(n, np.uint8)
     gi = SngbInfo()
-    o = _opts(params.device, timing)
+    o = _opts(params.device, timing, dist=params.dist)
     if data.values64 is not None:
         fn, arg = _lib.lib().sngb_dbscan_f64, data.values64.ctypes.data_as(C.POINTER(C.c_double))
     else:
@@ -258,13 +277,13 @@ def build_sampled_graph(data: Dataset, eps: float, rate: float, dist: Distance |
     """sng::build_sampled_graph (graph.hpp:65-66, graph.cpp:133-189) on the GPU."""
     if not isinstance(data, Dataset):
         data = Dataset(data)
-    if dist is not None and dist.kind != "euclidean":
-        raise NotImplementedError("only the Euclidean metric is on the GPU path")
+    if dist is not None and not isinstance(dist, Distance):
+        raise NotImplementedError("a Python distance callback cannot run on the GPU path")
     pts = data.values
     n, d = pts.shape
     L = _lib.lib()
     gi = SngbInfo()
-    o = _opts(device)
+    o = _opts(device, dist=dist)
     cnt = C.c_uint64(0)
     if data.values64 is not None:
         fn, arg = L.sngb_sampled_edges_f64, data.values64.ctypes.data_as(C.POINTER(C.c_double))

@@ -26,7 +26,10 @@ SNGB_ERR_ARG = 8
 SNGB_ERR_NO_DEVICE = 9
 SNGB_ERR_CUDA = 10
 SNGB_ERR_CAPACITY = 11
+SNGB_ERR_ZERO_VECTOR = 12
 SNGB_FLAG_TIMING = 0x1
+SNGB_FLAG_MANHATTAN = 0x2
+SNGB_FLAG_COSINE = 0x4
 
 # Every symbol include/sngb.h declares (checked by tests/test_abi.py).
 EXPORTS = [

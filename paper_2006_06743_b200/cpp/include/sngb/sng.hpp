@@ -4,6 +4,8 @@
 // Same names, argument meaning and error behaviour as the reference:
 //   sng::Dataset         proj/include/sng/dataset.hpp:16-71   (fp64 rows: kept
 //                        as fp32 when exact, else as fp64 for the fp64 entry points)
+//   sng::Distance        proj/include/sng/distance.hpp:13-43 (euclidean, manhattan,
+//                        cosine; no custom callbacks on the GPU path)
 //   sng::SngParams       proj/include/sng/clusterer.hpp:11-24
 //   sng::ClusterRunInfo  proj/include/sng/clusterer.hpp:27-31
 //   sng::Clustering      proj/include/sng/dataset.hpp:78-91
@@ -70,11 +72,37 @@ private:
     std::size_t dim_ = 0;
 };
 
+enum class Metric { Euclidean, Manhattan, Cosine, Custom };
+
+class Distance {
+public:
+    static Distance euclidean() { return Distance(Metric::Euclidean); }
+    static Distance manhattan() { return Distance(Metric::Manhattan); }
+    static Distance cosine() { return Distance(Metric::Cosine); }
+    static Distance parse(const std::string& name) {
+        if (name == "euclidean") return euclidean();
+        if (name == "manhattan") return manhattan();
+        if (name == "cosine") return cosine();
+        throw std::invalid_argument("unknown distance '" + name +
+                                    "' (expected euclidean, manhattan, or cosine)");
+    }
+    Metric kind() const { return kind_; }
+    std::uint32_t flags() const {
+        return kind_ == Metric::Manhattan ? SNGB_FLAG_MANHATTAN
+                                          : (kind_ == Metric::Cosine ? SNGB_FLAG_COSINE : 0u);
+    }
+
+private:
+    explicit Distance(Metric k) : kind_(k) {}
+    Metric kind_;
+};
+
 struct SngParams {
     double eps = 0.0;
     int min_pts = 1;
     double rate = 1.0;
     std::uint64_t seed = 0;
+    Distance dist = Distance::euclidean();
     int threads = 0;  // CPU workers in the reference; unused by the GPU path
     int device = -1;  // CUDA ordinal (-1 = current)
 
@@ -121,7 +149,7 @@ inline Clustering sng_dbscan(const Dataset& data, const SngParams& params,
     const std::size_t n = data.size();
     std::vector<std::int32_t> labels(n);
     std::vector<std::uint8_t> roles(n);
-    sngb_opts o{params.device, 0u, nullptr, 0, 0};
+    sngb_opts o{params.device, params.dist.flags(), nullptr, 0, 0};
     sngb_info gi{};
     const auto d = static_cast<std::uint32_t>(data.dim());
     detail::check(data.is_fp64()

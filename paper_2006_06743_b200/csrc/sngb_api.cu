@@ -94,15 +94,16 @@ struct DevCtx {
     cudaEvent_t up_ev[kMaxChunks] = {};
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
-        flags, rank, temp, labels, roles, work, q8, upload64;
+        flags, rank, temp, labels, roles, work, q8, upload64, rnorm, band;
     cudaEvent_t qev = nullptr;  // min/max of the points copied to the host (8-bit filter)
     unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
     cudaEvent_t ev[12] = {};
     uint64_t edge_hint = 0;  // last needed edge capacity for this context
+    uint64_t band_hint = 0;  // last needed band-list capacity
 
     void release() {
         for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
-                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64})
+                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band})
             b->release();
     }
 };
@@ -212,12 +213,43 @@ float f32_up(double x) {
 // rounded rows is within round_dist = sqrt(d) (2^-23 max|x| + 2^-149) of the
 // true one; the accept / reject thresholds move by that much in distance.
 TestParams make_test(const float* pts, uint32_t stride, uint32_t d, double eps,
-                     double round_dist = 0.0) {
+                     double round_dist = 0.0, int32_t metric = kMetricEuclid,
+                     double round_max = 0.0) {
     TestParams tp{};
     tp.pts = pts;
     tp.stride = stride;
     tp.d = d;
     tp.eps2 = eps * eps;
+    tp.eps = eps;
+    tp.metric = metric;
+    const double u = std::ldexp(1.0, -24);
+    if (metric == kMetricManhattan) {
+        // |s32 - S| <= ((1+u)^(d+2) - 1) S + (d+2) 2^-149 for S = sum |a - b|, any
+        // order; fp64 input moves each |a_k - b_k| by <= 2 (2^-24 max|x| + 2^-150)
+        const double rel = 1.25 * (d + 2.0) * u + 1e-12;
+        const double abs_ = (d + 2.0) * std::ldexp(1.0, -148);
+        const double rl1 = round_max > 0.0
+                               ? d * 2.0 * (std::ldexp(round_max, -24) + std::ldexp(1.0, -150)) *
+                                     (1.0 + 1e-9)
+                               : 0.0;
+        const double ea = eps * (1.0 - 1e-12) - rl1, eb = eps * (1.0 + 1e-12) + rl1;
+        tp.lo_thr = ea > 0.0 ? f32_down(ea * (1.0 - rel) - abs_) : -1.0f;
+        tp.hi_thr = f32_up(eb * (1.0 + rel) + abs_);
+        tp.eps2f = (float)eps;
+        return tp;
+    }
+    if (metric == kMetricCosine) {
+        // the filter value is x = -c32, c32 = dot32 / (|a|32 |b|32): |c32 - C| <=
+        // 2 gamma_d + 6u (Cauchy-Schwarz bounds the dot's error by gamma_d |a||b|);
+        // fp64 input: rounding each row moves C by <= 4u more (+ margin)
+        const double gd = d * u / (1.0 - d * u);
+        const double dc = 1.25 * (2.0 * gd + 6.0 * u) + (round_max > 0.0 ? 1.25 * 8.0 * u : 0.0);
+        const double edge = eps - 1.0;  // x <= eps - 1  <=>  1 - c <= eps
+        tp.lo_thr = f32_down(edge - 1e-12 - dc);
+        tp.hi_thr = f32_up(edge + 1e-12 + dc);
+        tp.eps2f = (float)edge;
+        return tp;
+    }
     const double rel = (2.0 * d + 16.0) * std::ldexp(1.0, -24) * 1.25 + 1e-12;
     const double abs_ = (2.0 * d + 16.0) * std::ldexp(1.0, -148);
     const double ea = std::sqrt(tp.eps2) * (1.0 - 1e-12) - round_dist;  // accept below (distance)
@@ -229,6 +261,18 @@ TestParams make_test(const float* pts, uint32_t stride, uint32_t d, double eps,
     tp.hi_thr = hi < (double)FLT_MAX / 4 ? f32_up(hi) : INFINITY;
     tp.eps2f = (float)tp.eps2;
     return tp;
+}
+
+// Distance::within metric from opts->flags (SNGB_FLAG_MANHATTAN / _COSINE)
+int32_t metric_of(const sngb_opts* o) {
+    const uint32_t f = o ? o->flags : 0u;
+    if (f & SNGB_FLAG_MANHATTAN) return kMetricManhattan;
+    if (f & SNGB_FLAG_COSINE) return kMetricCosine;
+    return kMetricEuclid;
+}
+bool metric_flags_ok(const sngb_opts* o) {
+    const uint32_t f = o ? o->flags : 0u;
+    return !((f & SNGB_FLAG_MANHATTAN) && (f & SNGB_FLAG_COSINE));
 }
 
 int validate(uint64_t n, uint32_t d, double eps, int32_t min_pts, double rate, bool need_minpts) {
@@ -304,7 +348,8 @@ struct GraphResult {
 // the sampler and (L2-blocked case) with the gather of the chunks already in.
 int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64_t n, uint32_t d,
                 double eps, double rate, uint64_t seed, uint64_t rb, uint64_t re,
-                GraphResult& gr, const float* h_src = nullptr, const double* d_pts64 = nullptr) {
+                GraphResult& gr, const float* h_src = nullptr, const double* d_pts64 = nullptr,
+                int32_t metric = kMetricEuclid) {
     unsigned long long* dc = nullptr;
     c.counters.ensure(C_COUNT * sizeof(unsigned long long));
     dc = c.counters.as<unsigned long long>();
@@ -344,7 +389,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     const bool exhaustive = draws >= n - 1;
     // SNGB_Q8: 0 off, 1 auto (use when the band is narrow), 2 force (tests)
     const uint64_t q8_mode = env_u64("SNGB_Q8", 1);
-    q8_try = !exhaustive && d >= 128 && d <= 1024 && q8_mode != 0;
+    q8_try = metric == kMetricEuclid && !exhaustive && d >= 128 && d <= 1024 && q8_mode != 0;
     const uint64_t rows = re - rb;
     const uint32_t nb = bits_for(n - 1);
     const uint64_t base = (n - 1) - draws;
@@ -375,7 +420,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     if (!exhaustive) floyd_geometry((uint32_t)draws, slots, col_words);
 
     // fp64 input: the fp32 thresholds need max|x| before any test runs
-    double round_dist = 0.0;
+    double round_dist = 0.0, max_abs = 0.0;
     if (f64) {
         prepare_rows(0, n);
         minmax_to_host();
@@ -383,16 +428,29 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         const double lo = ordered_value64(~c.h_counters[C_QMIN]);
         const double hi = ordered_value64(c.h_counters[C_QMAX]);
         const double m = std::max(std::fabs(lo), std::fabs(hi));
+        max_abs = m;
         round_dist = std::sqrt((double)d) * (std::ldexp(m, -23) + std::ldexp(1.0, -149)) *
                      (1.0 + 1e-9);
     }
-    TestParams tp = make_test(pts, stride, d, eps, round_dist);
+    TestParams tp = make_test(pts, stride, d, eps, round_dist, metric, max_abs);
     tp.pts64 = d_pts64;
+    if (metric == kMetricCosine) {
+        c.rnorm.ensure(n * sizeof(float));
+        tp.rnorm = c.rnorm.as<float>();
+    }
+    bool norms_done = metric != kMetricCosine;
+    auto ensure_norms = [&]() {  // after the last prepare, before any cosine test
+        if (norms_done) return;
+        CK(launch_row_norms(tp, n, c.rnorm.as<float>(), dc, gs, c.num_sms));
+        norms_done = true;
+    };
     const uint64_t seed_mixed = seed_part(seed);
     const uint32_t phases = gather_phases(c, n, stride, draws);
 
     // ---- host upload in row chunks (chunk k = L2 phase k when phased) ----
-    const uint32_t chunks = h_src ? std::min<uint32_t>(phases, DevCtx::kMaxChunks) : 1;
+    // (other metrics: one chunk -- the cosine row norms need every row first)
+    const uint32_t chunks =
+        h_src && metric == kMetricEuclid ? std::min<uint32_t>(phases, DevCtx::kMaxChunks) : 1;
     auto chunk_lo = [&](uint32_t k) { return n * k / chunks; };
     // issued after the sampler launch: a pageable source blocks the host while
     // it is staged, and the sampler should already be running by then
@@ -422,11 +480,21 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     uint32_t prepared = h_src ? 0 : chunks, quantized = 0;
     bool q8_pipe = false, q8_replan = false;
 
+    // band list (pairs the filter cannot decide, resolved exactly by k_band)
+    uint64_t band_cap = std::max<uint64_t>(1ull << 16, std::min<uint64_t>(pairs / 4096, 1ull << 24));
+    band_cap = std::max<uint64_t>(band_cap, c.band_hint);
     for (int attempt = 0; attempt < 4; ++attempt) {
         c.keys.ensure(edge_cap * 8);
+        c.band.ensure(band_cap * 16);
+        tp.band = c.band.as<uint4>();
+        tp.band_cursor = &dc[C_BAND_CURSOR];
+        tp.band_cap = band_cap;
         c.extras.ensure(std::max<uint64_t>(extras_cap, 1) * 8);
         if (attempt > 0)
+        {
             CK(cudaMemsetAsync(dc, 0, C_UNIQUE * sizeof(unsigned long long), s));
+            CK(cudaMemsetAsync(&dc[C_BAND_CURSOR], 0, sizeof(unsigned long long), s));
+        }
         tm.mark(E_PREPARED);
         // Overlap: the sampler on the side stream concurrently with a
         // non-persistent gather (SNGB_OVERLAP 0 off, 1 on, 2 auto).  Auto for
@@ -562,7 +630,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 ga.grab = (uint32_t)std::max<uint64_t>(
                     1, std::min<uint64_t>(32, (ga.row_end - ga.row_begin) / (warps * 16)));
             }
-            if (q8_on) CK(launch_gather_q8(ga, q8p.args, gs, c.num_sms));
+            if (metric != kMetricEuclid) CK(launch_gather_metric(ga, exhaustive, gs, c.num_sms));
+            else if (q8_on) CK(launch_gather_q8(ga, q8p.args, gs, c.num_sms));
             else CK(launch_gather(ga, exhaustive, gs, c.num_sms));
         };
         auto land_chunk = [&](uint32_t k) {  // chunk k uploaded, prepared, quantised
@@ -586,6 +655,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             if (h_src && attempt == 0)
                 for (uint32_t k = 0; k < chunks; ++k) land_chunk(k);
             prepared = quantized = chunks;
+            ensure_norms();
             for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
         }
         if (prio) {
@@ -603,14 +673,18 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             ea.extras = c.extras.as<unsigned long long>();
             ea.count_ptr = &dc[C_EXTRA_CURSOR];
             ea.capacity = extras_cap;
-            if (q8_on) CK(launch_extras_q8(ea, q8p.args, s, c.num_sms));
+            if (metric != kMetricEuclid) CK(launch_extras_metric(ea, s, c.num_sms));
+            else if (q8_on) CK(launch_extras_q8(ea, q8p.args, s, c.num_sms));
             else CK(launch_extras(ea, s, c.num_sms));
         }
+        CK(launch_band(tp, ga.sink, dc, s, c.num_sms));  // the band pairs, decided exactly
         tm.mark(E_EXTRAS);
         CK(cudaMemcpyAsync(c.h_counters, dc, C_COUNT * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (c.h_counters[C_NONFINITE]) return SNGB_ERR_NONFINITE;
+        if (metric == kMetricCosine && n >= 2 && c.h_counters[C_ZERO_ROWS])
+            return SNGB_ERR_ZERO_VECTOR;  // distance.hpp:96-97 (any zero row meets a pair)
         if (q8_pipe) {  // the plan came from chunk 0: does it cover every value?
             const double glo = ordered_value(~(uint32_t)c.h_counters[C_QMIN]);
             const double ghi = ordered_value((uint32_t)c.h_counters[C_QMAX]);
@@ -626,7 +700,9 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         }
         const uint64_t need_e = c.h_counters[C_EDGE_CURSOR];
         const uint64_t need_x = c.h_counters[C_EXTRA_CURSOR];
-        const bool ok = need_e <= edge_cap && (exhaustive || need_x <= extras_cap);
+        const uint64_t need_b = c.h_counters[C_BAND_CURSOR];
+        const bool ok = need_e <= edge_cap && (exhaustive || need_x <= extras_cap) &&
+                        need_b <= band_cap;
         if (ok) {
             gr.raw = need_e;
             c.edge_hint = std::max<uint64_t>(c.edge_hint, need_e);
@@ -636,6 +712,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             g_detail = "edge buffer overflow after retries";
             throw CudaFail{cudaErrorMemoryAllocation};
         }
+        if (need_b > band_cap) band_cap = need_b + need_b / 8 + 1024;
+        c.band_hint = std::max<uint64_t>(c.band_hint, band_cap);
         if (need_e > edge_cap) edge_cap = need_e + need_e / 8 + 1024;
         if (need_x > extras_cap) extras_cap = need_x + need_x / 8 + 1024;
         c.edge_hint = std::max<uint64_t>(c.edge_hint, edge_cap);
@@ -729,8 +807,8 @@ int guarded(F&& f) {
 int dbscan_device(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64_t n, uint32_t d,
                   double eps, int32_t min_pts, double rate, uint64_t seed, int32_t* d_labels,
                   uint8_t* d_roles, GraphResult& gr, const float* h_src = nullptr,
-                  const double* d_pts64 = nullptr) {
-    int rc = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, 0, n, gr, h_src, d_pts64);
+                  const double* d_pts64 = nullptr, int32_t metric = kMetricEuclid) {
+    int rc = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, 0, n, gr, h_src, d_pts64, metric);
     if (rc) return rc;
     ClusterBuffers b{};
     ensure_cluster_bufs(c, n, b);
@@ -748,6 +826,7 @@ template <class F>
 int merge_step(const sngb_opts* opts, uint64_t n, F&& f) {
     if (n == 0) return SNGB_ERR_EMPTY;
     if (n > 0x7fffffffull) return SNGB_ERR_TOO_LARGE;  // int32 vertex arrays
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
@@ -796,6 +875,7 @@ const char* sngb_strerror(int code) {
         case SNGB_ERR_NO_DEVICE: return "no CUDA device available (the GPU path has no CPU fallback)";
         case SNGB_ERR_CUDA: return "CUDA error";
         case SNGB_ERR_CAPACITY: return "output buffer too small";
+        case SNGB_ERR_ZERO_VECTOR: return "cosine distance is undefined for zero vectors";
         default: return "unknown error";
     }
 }
@@ -819,6 +899,7 @@ int sngb_dbscan_f32_device(const float* d_pts, uint64_t n, uint32_t d, double ep
     int rc = validate(n, d, eps, min_pts, rate, true);
     if (rc) return rc;
     if (!d_pts || !d_labels || !d_roles) return SNGB_ERR_ARG;
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
@@ -830,7 +911,8 @@ int sngb_dbscan_f32_device(const float* d_pts, uint64_t n, uint32_t d, double ep
         tm.mark(E_START);
         tm.mark(E_UPLOADED);
         GraphResult gr;
-        int r = dbscan_device(c, s, tm, d_pts, n, d, eps, min_pts, rate, seed, d_labels, d_roles, gr);
+        int r = dbscan_device(c, s, tm, d_pts, n, d, eps, min_pts, rate, seed, d_labels, d_roles, gr,
+                              nullptr, nullptr, metric_of(opts));
         if (r) return r;
         tm.mark(E_DOWNLOADED);
         tm.mark(E_END);
@@ -847,6 +929,7 @@ int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_
     int rc = validate(n, d, eps, min_pts, rate, true);
     if (rc) return rc;
     if (!pts || !labels_out || !roles_out) return SNGB_ERR_ARG;
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
@@ -862,7 +945,8 @@ int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_
         GraphResult gr;
         // the upload is chunked and overlapped inside build_graph
         int r = dbscan_device(c, s, tm, c.upload.as<float>(), n, d, eps, min_pts, rate, seed,
-                              c.labels.as<int32_t>(), c.roles.as<uint8_t>(), gr, pts);
+                              c.labels.as<int32_t>(), c.roles.as<uint8_t>(), gr, pts, nullptr,
+                              metric_of(opts));
         if (r) return r;
         CK(cudaMemcpyAsync(labels_out, c.labels.p, n * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(roles_out, c.roles.p, n, cudaMemcpyDeviceToHost, s));
@@ -885,6 +969,7 @@ int sngb_sampled_edges_f32_device(const float* d_pts, uint64_t n, uint32_t d, do
     const uint64_t rb = opts ? opts->row_begin : 0;
     const uint64_t re = (opts && opts->row_end) ? opts->row_end : n;
     if (rb > re || re > n) return SNGB_ERR_ARG;
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
@@ -896,7 +981,8 @@ int sngb_sampled_edges_f32_device(const float* d_pts, uint64_t n, uint32_t d, do
         tm.mark(E_START);
         tm.mark(E_UPLOADED);
         GraphResult gr;
-        int r = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, rb, re, gr);
+        int r = build_graph(c, s, tm, d_pts, n, d, eps, rate, seed, rb, re, gr, nullptr, nullptr,
+                            metric_of(opts));
         if (r) return r;
         tm.mark(E_CLUSTERED);
         tm.mark(E_DOWNLOADED);
@@ -925,6 +1011,7 @@ int sngb_sampled_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps,
     const uint64_t rb = opts ? opts->row_begin : 0;
     const uint64_t re = (opts && opts->row_end) ? opts->row_end : n;
     if (rb > re || re > n) return SNGB_ERR_ARG;
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
@@ -937,7 +1024,7 @@ int sngb_sampled_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps,
         c.upload.ensure(n * d * sizeof(float));
         GraphResult gr;
         int r = build_graph(c, s, tm, c.upload.as<float>(), n, d, eps, rate, seed, rb, re, gr,
-                            pts);
+                            pts, nullptr, metric_of(opts));
         if (r) return r;
         tm.mark(E_CLUSTERED);
         unsigned long long* dc = c.counters.as<unsigned long long>();
@@ -970,6 +1057,7 @@ int sngb_cluster_edges_device(const uint64_t* d_keys, uint64_t nkeys, uint64_t n
     if (n == 0) return SNGB_ERR_EMPTY;
     if (n >= 0xffffff00ull) return SNGB_ERR_TOO_LARGE;
     if ((nkeys && !d_keys) || !d_labels || !d_roles) return SNGB_ERR_ARG;
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
@@ -1023,6 +1111,7 @@ int sngb_dbscan_f64_device(const double* d_pts, uint64_t n, uint32_t d, double e
     int rc = validate(n, d, eps, min_pts, rate, true);
     if (rc) return rc;
     if (!d_pts || !d_labels || !d_roles) return SNGB_ERR_ARG;
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
@@ -1035,7 +1124,7 @@ int sngb_dbscan_f64_device(const double* d_pts, uint64_t n, uint32_t d, double e
         tm.mark(E_UPLOADED);
         GraphResult gr;
         int r = dbscan_device(c, s, tm, nullptr, n, d, eps, min_pts, rate, seed, d_labels, d_roles,
-                              gr, nullptr, d_pts);
+                              gr, nullptr, d_pts, metric_of(opts));
         if (r) return r;
         tm.mark(E_DOWNLOADED);
         tm.mark(E_END);
@@ -1052,6 +1141,7 @@ int sngb_dbscan_f64(const double* pts, uint64_t n, uint32_t d, double eps, int32
     int rc = validate(n, d, eps, min_pts, rate, true);
     if (rc) return rc;
     if (!pts || !labels_out || !roles_out) return SNGB_ERR_ARG;
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
@@ -1069,7 +1159,7 @@ int sngb_dbscan_f64(const double* pts, uint64_t n, uint32_t d, double eps, int32
         GraphResult gr;
         int r = dbscan_device(c, s, tm, nullptr, n, d, eps, min_pts, rate, seed,
                               c.labels.as<int32_t>(), c.roles.as<uint8_t>(), gr, nullptr,
-                              c.upload64.as<double>());
+                              c.upload64.as<double>(), metric_of(opts));
         if (r) return r;
         CK(cudaMemcpyAsync(labels_out, c.labels.p, n * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(roles_out, c.roles.p, n, cudaMemcpyDeviceToHost, s));
@@ -1091,6 +1181,7 @@ int sngb_sampled_edges_f64(const double* pts, uint64_t n, uint32_t d, double eps
     const uint64_t rb = opts ? opts->row_begin : 0;
     const uint64_t re = (opts && opts->row_end) ? opts->row_end : n;
     if (rb > re || re > n) return SNGB_ERR_ARG;
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
@@ -1105,7 +1196,7 @@ int sngb_sampled_edges_f64(const double* pts, uint64_t n, uint32_t d, double eps
         tm.mark(E_UPLOADED);
         GraphResult gr;
         int r = build_graph(c, s, tm, nullptr, n, d, eps, rate, seed, rb, re, gr, nullptr,
-                            c.upload64.as<double>());
+                            c.upload64.as<double>(), metric_of(opts));
         if (r) return r;
         tm.mark(E_CLUSTERED);
         unsigned long long* dc = c.counters.as<unsigned long long>();

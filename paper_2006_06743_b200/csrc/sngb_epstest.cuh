@@ -125,65 +125,98 @@ __device__ __forceinline__ unsigned long long edge_key(uint64_t u, uint64_t v, u
 
 // distance.hpp:75-83 verbatim in fp64: s += (a_k - b_k)^2 sequentially in k,
 // no contraction (explicit _rn intrinsics), then s <= eps*eps.
+// Distance::within for Manhattan / cosine (distance.hpp:55-68, 91-103), fp64 in
+// the reference's order.  Zero-norm rows never get here (SNGB_ERR_ZERO_VECTOR).
+template <class Row>
+__device__ __forceinline__ bool exact_within_metric(int metric, uint32_t d, double eps,
+                                                    const Row* a, const Row* b) {
+    if (metric == kMetricManhattan) {
+        double s = 0.0;
+        for (uint32_t k = 0; k < d; ++k) s = __dadd_rn(s, fabs(__dsub_rn(a[k], b[k])));
+        return s <= eps;
+    }
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    for (uint32_t k = 0; k < d; ++k) {
+        const double x = a[k], y = b[k];
+        dot = __dadd_rn(dot, __dmul_rn(x, y));
+        na = __dadd_rn(na, __dmul_rn(x, x));
+        nb = __dadd_rn(nb, __dmul_rn(y, y));
+    }
+    double c = __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb)));
+    if (c > 1.0) c = 1.0;
+    if (c < -1.0) c = -1.0;
+    return __dsub_rn(1.0, c) <= eps;
+}
+
+// The exact decision (rarely taken): scalar arguments, so a caller holding the
+// test parameters in its kernel-parameter block does not marshal the struct.
 // fp64 input: on the caller's fp64 rows, exactly as the reference does.
-static __device__ __noinline__ bool exact_within(const TestParams tp, uint64_t u, uint64_t v) {
+static __device__ __noinline__ bool exact_core(const float* pts, uint32_t stride, uint32_t d,
+                                               double eps2, double eps, const double* pts64,
+                                               int metric, uint64_t u, uint64_t v) {
+    if (metric != kMetricEuclid) {
+        if (pts64) return exact_within_metric(metric, d, eps, pts64 + u * d, pts64 + v * d);
+        return exact_within_metric(metric, d, eps, pts + u * stride, pts + v * stride);
+    }
     double s = 0.0;
-    if (tp.pts64) {
-        const double* a = tp.pts64 + u * tp.d;
-        const double* b = tp.pts64 + v * tp.d;
-        for (uint32_t k = 0; k < tp.d; ++k) {
+    if (pts64) {
+        const double* a = pts64 + u * d;
+        const double* b = pts64 + v * d;
+        for (uint32_t k = 0; k < d; ++k) {
             const double t = __dsub_rn(a[k], b[k]);
             s = __dadd_rn(s, __dmul_rn(t, t));
         }
     } else {
-        const float* a = tp.pts + u * tp.stride;
-        const float* b = tp.pts + v * tp.stride;
-        for (uint32_t k = 0; k < tp.d; ++k) {
+        const float* a = pts + u * stride;
+        const float* b = pts + v * stride;
+        for (uint32_t k = 0; k < d; ++k) {
             const double t = __dsub_rn((double)a[k], (double)b[k]);
             s = __dadd_rn(s, __dmul_rn(t, t));
         }
     }
-    return s <= tp.eps2;
+    return s <= eps2;
+}
+
+__device__ __forceinline__ bool exact_within(const TestParams& tp, uint64_t u, uint64_t v) {
+    return exact_core(tp.pts, tp.stride, tp.d, tp.eps2, tp.eps, tp.pts64, tp.metric, u, v);
 }
 
 struct TestStats {
     unsigned long long pairs = 0, band = 0, band6 = 0, flips = 0;
 };
 
-// Decide one pair per G-lane group.  `s` is group-uniform.  Returns the exact
-// reference decision to every lane.  Must be called by all 32 lanes.
+// A pair the filter cannot decide: appended to the band list (k_band decides it
+// exactly later and emits the edge if the reference accepts it).
+__device__ __forceinline__ void band_push(const TestParams& tp, uint64_t u, uint64_t v, float s) {
+    const unsigned long long slot = atomicAdd(tp.band_cursor, 1ull);
+    if (slot < tp.band_cap)
+        tp.band[slot] = make_uint4((uint32_t)u, (uint32_t)v, __float_as_uint(s), 0u);
+}
+
+// Filter decision of one pair per G-lane group (`s` group-uniform): true iff
+// the pair is accepted outright; a band pair is handed to k_band and reads as
+// not accepted here.
 __device__ __forceinline__ bool decide(float s, bool ok, bool leader, int leader_lane,
                                        const TestParams& tp, uint64_t u, uint64_t v,
                                        TestStats& st) {
+    (void)leader_lane;
     const bool need = ok && !(s < tp.lo_thr) && !(s > tp.hi_thr);
-    bool acc = ok && (s < tp.lo_thr);
-    const unsigned nm = __ballot_sync(kFull, need);
-    if (nm) {
-        bool ex = false;
-        if (need && leader) {
-            ex = exact_within(tp, u, v);
-            st.band++;
-            if (fabsf(s - tp.eps2f) <= 1e-6f * tp.eps2f) st.band6++;
-            if ((s <= tp.eps2f) != ex) st.flips++;
-        }
-        ex = __shfl_sync(kFull, ex, leader_lane);
-        if (need) acc = ex;
+    if (need && leader) {
+        band_push(tp, u, v, s);
+        st.band++;
     }
-    return acc;
+    return ok && (s < tp.lo_thr);
 }
 
-// Same decision when every lane owns one pair (no group broadcast needed).
+// Same when every lane owns one pair.
 __device__ __forceinline__ bool decide_lane(float s, bool ok, const TestParams& tp, uint64_t u,
                                             uint64_t v, TestStats& st) {
     const bool need = ok && !(s < tp.lo_thr) && !(s > tp.hi_thr);
-    bool acc = ok && (s < tp.lo_thr);
     if (need) {
-        acc = exact_within(tp, u, v);
+        band_push(tp, u, v, s);
         st.band++;
-        if (fabsf(s - tp.eps2f) <= 1e-6f * tp.eps2f) st.band6++;
-        if ((s <= tp.eps2f) != acc) st.flips++;
     }
-    return acc;
+    return ok && (s < tp.lo_thr);
 }
 
 __device__ __forceinline__ void flush_stats(const TestStats& st, unsigned long long gpairs,

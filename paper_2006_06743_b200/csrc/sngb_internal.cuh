@@ -29,6 +29,8 @@ enum Counter : int {
     C_CLUSTERS,
     C_BADKEY,            // self loop / out-of-range endpoint in caller keys
     C_CHANGED,           // merge step: vertices whose component root moved
+    C_ZERO_ROWS,         // cosine: rows whose fp64 norm is 0 (distance.hpp:97)
+    C_BAND_CURSOR,       // band pairs appended (see TestParams::band)
     C_QMIN,              // max of ~ordered(value): the dataset minimum (8-bit filter scale)
     C_QMAX,              // max of ordered(value): the dataset maximum
     C_COUNT
@@ -46,7 +48,17 @@ struct TestParams {
     double eps2;       // eps * eps in fp64, as distance.hpp:82 computes it
     const double* pts64;  // fp64 input: the caller's rows (d per row) for the exact
                           // recheck; pts then holds them rounded to fp32.  null: fp32 input
+    int32_t metric;       // kMetricEuclid / kMetricManhattan / kMetricCosine
+    double eps;           // the metric's eps (Manhattan, cosine compare against it)
+    const float* rnorm;   // cosine: fp32 |row| per row (sqrt of the fp32 sum of squares)
+    // pairs whose filter value lands in the band: appended here by the filter
+    // kernels, decided exactly (fp64, the reference's order) by k_band afterwards,
+    // so the rare exact path costs the hot kernels no registers
+    uint4* band;                      // {u, v, filter value bits, 0}
+    unsigned long long* band_cursor;  // may exceed band_cap (the host retries)
+    unsigned long long band_cap;
 };
+constexpr int32_t kMetricEuclid = 0, kMetricManhattan = 1, kMetricCosine = 2;
 
 // Canonical undirected edge keys: (min << nb) | max with nb = bits(n-1).
 struct EdgeSink {
@@ -164,6 +176,15 @@ void floyd_geometry(uint32_t draws, uint32_t& slots, uint32_t& col_words);
 size_t floyd_scratch_bytes(uint32_t draws, int num_sms);
 cudaError_t launch_sampler(const SamplerArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_gather(const GatherArgs& a, bool exhaustive, cudaStream_t s, int num_sms);
+// exact fp64 decision of the band pairs; accepted ones go to `sink`
+cudaError_t launch_band(const TestParams& tp, const EdgeSink& sink, unsigned long long* counters,
+                        cudaStream_t s, int num_sms);
+// sngb_metric.cu: Manhattan / cosine (fp32 filter + the reference's fp64 recheck)
+cudaError_t launch_row_norms(const TestParams& tp, uint64_t n, float* rnorm,
+                             unsigned long long* counters, cudaStream_t s, int num_sms);
+cudaError_t launch_gather_metric(const GatherArgs& a, bool exhaustive, cudaStream_t s,
+                                 int num_sms);
+cudaError_t launch_extras_metric(const ExtrasArgs& a, cudaStream_t s, int num_sms);
 // sngb_quant.cu: the 8-bit filter for wide rows (exact via integer thresholds
 // on Q2 = sum (qa - qb)^2 plus the fp64 recheck in the band)
 struct Q8Args {

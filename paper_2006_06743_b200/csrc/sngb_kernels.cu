@@ -443,9 +443,43 @@ __global__ void k_prepare_f64(const double* __restrict__ src, float* __restrict_
     }
 }
 
+// k_band: the exact decision (distance.hpp, fp64, the reference's order) of
+// every pair a filter kernel left in its band; the accepted ones are emitted.
+// Also the band statistics: pairs within 1e-6 of eps^2 by the filter value and
+// pairs a bare fp32 test would have decided wrongly (fp32 filters only).
+__global__ void k_band(const TestParams tp, const EdgeSink sink, unsigned long long* counters) {
+    uint64_t count = *tp.band_cursor;
+    if (count > tp.band_cap) count = tp.band_cap;
+    unsigned b6 = 0, flips = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 r = tp.band[i];
+        const bool acc = exact_within(tp, r.x, r.y);
+        const float s = __uint_as_float(r.z);
+        b6 += fabsf(s - tp.eps2f) <= 1e-6f * fabsf(tp.eps2f) ? 1u : 0u;
+        flips += (s == s && (s <= tp.eps2f) != acc) ? 1u : 0u;
+        if (acc) {
+            const unsigned long long slot = atomicAdd(sink.cursor, 1ull);
+            if (slot < sink.capacity) sink.keys[slot] = edge_key(r.x, r.y, sink.nb);
+        }
+    }
+    b6 = __reduce_add_sync(kFull, b6);
+    flips = __reduce_add_sync(kFull, flips);
+    if ((threadIdx.x & 31) == 0) {
+        if (b6) atomicAdd(&counters[C_BAND6], (unsigned long long)b6);
+        if (flips) atomicAdd(&counters[C_FLIPS], (unsigned long long)flips);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+cudaError_t launch_band(const TestParams& tp, const EdgeSink& sink, unsigned long long* counters,
+                        cudaStream_t s, int num_sms) {
+    k_band<<<(unsigned)(num_sms * 4), 256, 0, s>>>(tp, sink, counters);
+    note_launch(1);
+    return cudaGetLastError();
+}
 cudaError_t launch_prepare_points_f64(const double* src, float* dst, uint64_t n, uint32_t d,
                                       uint32_t stride, unsigned long long* counters,
                                       cudaStream_t s) {

@@ -211,9 +211,9 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8(const GatherArgs a, const 
                 const bool okm = (lane % SPAN) == 0 && pj < nlive;
                 const uint32_t pm = list[okm ? pj : j0];
                 const int q2 = (int)nu + ps[0];
-                bool acc = okm && q2 <= q8.accept_max;
-                if (okm && q2 > q8.accept_max && q2 <= q8.reject_min) {  // band: exact recheck
-                    acc = exact_within(a.tp, u, pm);
+                const bool acc = okm && q2 <= q8.accept_max;
+                if (okm && q2 > q8.accept_max && q2 <= q8.reject_min) {  // band: k_band decides
+                    band_push(a.tp, u, pm, __int_as_float(0x7fc00000));
                     st.band++;
                 }
                 gpairs += okm ? 1u : 0u;
@@ -257,12 +257,11 @@ __global__ void __launch_bounds__(256) k_extras_q8(const ExtrasArgs a, const Q8A
         part -= 2 * (int)dot;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-        bool acc = part <= q8.accept_max;
-        if (lane == 0 && !acc && part <= q8.reject_min) {  // band: exact recheck
-            acc = exact_within(a.tp, u, v);
+        const bool acc = part <= q8.accept_max;
+        if (lane == 0 && !acc && part <= q8.reject_min) {  // band: k_band decides
+            band_push(a.tp, u, v, __int_as_float(0x7fc00000));
             st.band++;
         }
-        acc = __shfl_sync(kFull, acc, 0);
         if (lane == 0) st.pairs++;
         stage.push(lane == 0 && acc, edge_key(u, v, a.sink.nb), a.sink, lane);
     }

@@ -47,7 +47,12 @@ int main() {
         const bool ok64 = sng::load_labels(base + "/demo.labels") == c.assignment &&
                           info.gpu.filter_bits == 32;
         std::printf("fp64 via SNGD: clusters=%d ok=%d\n", c64.cluster_count, (int)ok64);
-        return ok64 ? 0 : 2;
+        if (!ok64) return 2;
+        // Manhattan on the same example: |0 - 0.5| = 0.5 <= 1, clusters unchanged
+        p.dist = sng::Distance::parse("manhattan");
+        sng::Clustering cm = sng::sng_dbscan(ds, p, &info);
+        std::printf("manhattan: clusters=%d\n", cm.cluster_count);
+        return cm.assignment == c.assignment ? 0 : 2;
     } catch (const std::runtime_error& e) {
         std::printf("runtime_error: %s\n", e.what());
         return 3;

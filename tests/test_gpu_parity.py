@@ -349,3 +349,54 @@ def test_fp64_band_edges_exact():
     g = sng.build_sampled_graph(ds, eps, 1.0, seed=3)
     keys, _, _ = ref.sampled_edges(ref.dataset(pts), eps, 1.0, 3)
     np.testing.assert_array_equal(g.keys, keys)
+
+
+# ---- Manhattan and cosine (distance.hpp:55-68, 91-103) ----------------------
+@pytest.mark.parametrize("metric", ["manhattan", "cosine"])
+@pytest.mark.parametrize("n,d,rate,seed,f64", [
+    (3000, 2, 0.1, 1, False), (4000, 16, 0.05, 3, False), (2500, 200, 0.05, 7, False),
+    (2000, 784, 0.05, 2, False), (3000, 16, 0.05, 5, True), (600, 8, 1.0, 9, False)])
+def test_metric_matches_reference(metric, n, d, rate, seed, f64):
+    ref = _ref_or_skip()
+    ref.set_metric(metric)
+    try:
+        rng = np.random.default_rng(seed)
+        cfg = {2: 1, 16: 3, 784: 2}.get(d)
+        pts = synthetic.generate(cfg, n=n).astype(np.float64) if cfg else rng.random((n, d))
+        if metric == "cosine":
+            pts = pts + 0.5  # keep rows away from the origin
+        if f64:
+            pts = pts + rng.normal(0, 1e-7, pts.shape)
+        else:
+            pts = pts.astype(np.float32)
+        # eps at a low quantile of the pair distances: plenty of accepted pairs
+        i = np.arange(0, n - 1, 5)
+        a, b = pts[i].astype(np.float64), pts[i + 1].astype(np.float64)
+        dist = np.abs(a - b).sum(1) if metric == "manhattan" else \
+            1 - (a * b).sum(1) / np.linalg.norm(a, axis=1) / np.linalg.norm(b, axis=1)
+        eps = float(np.quantile(dist, 0.1))
+        ds = sng.Dataset(pts)
+        dm = sng.Distance.parse(metric)
+        info = sng.ClusterRunInfo()
+        c = sng.sng_dbscan(ds, sng.SngParams(eps=eps, min_pts=3, rate=rate, seed=seed, dist=dm),
+                           info)
+        rds = ref.dataset(pts)
+        labels, roles, rinfo = ref.sng_dbscan(rds, eps, 3, rate, seed)
+        np.testing.assert_array_equal(c.assignment, labels)
+        np.testing.assert_array_equal(c.role, roles)
+        assert info.edges == rinfo["edges"] and info.distance_evals == rinfo["distance_evals"]
+        keys, _, _ = ref.sampled_edges(rds, eps, rate, seed)
+        g = sng.build_sampled_graph(ds, eps, rate, dist=dm, seed=seed)
+        np.testing.assert_array_equal(g.keys, keys)
+    finally:
+        ref.set_metric("euclidean")
+
+
+def test_cosine_zero_vector_is_an_error():
+    pts = np.random.default_rng(0).random((500, 8), dtype=np.float32)
+    pts[77] = 0.0
+    p = sng.SngParams(eps=0.1, min_pts=3, rate=0.1, seed=1, dist=sng.Distance.cosine())
+    with pytest.raises(sng.InvalidArgument, match="cosine distance is undefined for zero vectors"):
+        sng.sng_dbscan(sng.Dataset(pts), p)
+    pts[77] = 1e-30  # tiny but non-zero in fp64: not an error
+    sng.sng_dbscan(sng.Dataset(pts), p)

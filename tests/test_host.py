@@ -44,8 +44,10 @@ def test_distance_parse():  # distance.hpp:37-43
     assert sng.Distance.parse("euclidean").kind == "euclidean"
     with pytest.raises(sng.InvalidArgument, match="unknown distance 'l7'"):
         sng.Distance.parse("l7")
+    assert sng.Distance.parse("cosine").flags == 0x4
+    assert sng.Distance.parse("manhattan").flags == 0x2
     with pytest.raises(NotImplementedError):
-        sng.Distance.parse("cosine")
+        sng.Distance.custom(lambda a, b: 0.0)
 
 
 def test_point_roles_and_noise_label():  # dataset.hpp:13,74
