@@ -132,6 +132,29 @@ int sngb_sampled_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps,
                            uint64_t seed, const sngb_opts* opts, uint64_t* keys_out,
                            uint64_t capacity, uint64_t* count_out, sngb_info* info_out);
 
+/* Many small problems at once (the theory lab calls
+ * sng_dbscan for many n <= 1e5 datasets, theory.cpp:239-256).  Each problem is
+ * what one sngb_dbscan_f32 call would take (flags: SNGB_FLAG_MANHATTAN /
+ * _COSINE); the problems run concurrently on up to SNGB_BATCH_SLOTS (default
+ * 8) host workers with their own device contexts and streams, so their kernel
+ * launches and host syncs overlap.  Per-problem status in `status`; returns
+ * SNGB_OK or the first failing problem's status. */
+typedef struct sngb_problem {
+    const float* pts;
+    uint64_t n;
+    uint32_t d;
+    uint32_t flags;
+    double eps;
+    double rate;
+    uint64_t seed;
+    int32_t min_pts;
+    int32_t status; /* out */
+    int32_t* labels_out;
+    uint8_t* roles_out;
+    sngb_info* info_out; /* optional */
+} sngb_problem;
+int sngb_dbscan_batch_f32(sngb_problem* problems, uint64_t count, const sngb_opts* opts);
+
 /* fp64 input -- the reference's own Dataset type (dataset.hpp:69-71).  Values
  * that are not exactly fp32 are kept in fp64 on the device: the filter works on
  * them rounded to fp32 (or quantised to 8 bits from the fp64 values) with its

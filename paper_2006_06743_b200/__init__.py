@@ -457,3 +457,38 @@ def relabel_device(n: int, degree, min_pts: int, parent, border):
                                           border.data_ptr(), C.byref(o), labels.data_ptr(),
                                           roles.data_ptr(), C.byref(gi)))
     return labels, roles, gi
+
+
+def sng_dbscan_batch(problems, device: int = -1):
+    """Many small sng_dbscan calls at once (sngb_dbscan_batch_f32): `problems`
+    is a sequence of (Dataset or array, SngParams); returns one Clustering per
+    problem, identical to separate calls.  fp64 data that fp32 cannot hold is
+    run one problem at a time through the fp64 entry point."""
+    items = [(d if isinstance(d, Dataset) else Dataset(d), p) for d, p in problems]
+    out = [None] * len(items)
+    batch = []
+    for i, (ds, p) in enumerate(items):
+        p.validate()
+        if ds.values64 is not None or not isinstance(p.dist, Distance):
+            out[i] = sng_dbscan(ds, p)
+        else:
+            batch.append(i)
+    arr = (_lib.SngbProblem * max(len(batch), 1))()
+    keep = []
+    for k, i in enumerate(batch):
+        ds, p = items[i]
+        n, d = ds.values.shape
+        labels, roles, info = np.empty(n, np.int32), np.empty(n, np.uint8), SngbInfo()
+        keep.append((labels, roles, info))
+        arr[k] = _lib.SngbProblem(ds.values.ctypes.data, n, d, p.dist.flags, float(p.eps),
+                                  float(p.rate), int(p.seed) & 0xFFFFFFFFFFFFFFFF,
+                                  int(p.min_pts), 0, labels.ctypes.data, roles.ctypes.data,
+                                  C.addressof(info))
+    if batch:
+        o = _opts(device)
+        _lib.lib().sngb_dbscan_batch_f32(arr, len(batch), C.byref(o))
+        for k, i in enumerate(batch):
+            _check(arr[k].status)
+            labels, roles, info = keep[k]
+            out[i] = Clustering(labels, roles, int(info.cluster_count))
+    return out

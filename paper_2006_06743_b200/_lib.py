@@ -39,6 +39,7 @@ EXPORTS = [
     "sngb_unique_keys_device", "sngb_degrees_device", "sngb_components_device",
     "sngb_border_device", "sngb_relabel_device",
     "sngb_dbscan_f64", "sngb_dbscan_f64_device", "sngb_sampled_edges_f64",
+    "sngb_dbscan_batch_f32",
 ]
 
 
@@ -65,6 +66,13 @@ class SngbInfo(C.Structure):
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class SngbProblem(C.Structure):
+    _fields_ = [("pts", C.c_void_p), ("n", C.c_uint64), ("d", C.c_uint32), ("flags", C.c_uint32),
+                ("eps", C.c_double), ("rate", C.c_double), ("seed", C.c_uint64),
+                ("min_pts", C.c_int32), ("status", C.c_int32), ("labels_out", C.c_void_p),
+                ("roles_out", C.c_void_p), ("info_out", C.c_void_p)]
 
 
 _lib = None
@@ -122,6 +130,8 @@ def lib() -> C.CDLL:
         L.sngb_sampled_edges_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double,
                                              C.c_double, C.c_uint64, optp, u64p, C.c_uint64, u64p,
                                              infop]
+        L.sngb_dbscan_batch_f32.restype = C.c_int
+        L.sngb_dbscan_batch_f32.argtypes = [C.POINTER(SngbProblem), C.c_uint64, optp]
         L.sngb_strerror.restype = C.c_char_p
         L.sngb_strerror.argtypes = [C.c_int]
         L.sngb_last_error_detail.restype = C.c_char_p

@@ -71,7 +71,7 @@ def build(verbose: bool = False, variant: str | None = None, extra: tuple = ()) 
         objs = list(ex.map(lambda s: _compile(s, verbose, obj_dir, tuple(extra)), SOURCES))
     if variant or _stale(lib, objs):
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs,
-               "-lcudart"]
+               "-lcudart", "-lpthread"]
         subprocess.run(cmd, check=True)
     return lib
 

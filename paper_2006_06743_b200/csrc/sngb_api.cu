@@ -18,6 +18,8 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -133,10 +135,14 @@ int device_count() {
     return n;
 }
 
-DevCtx& get_ctx(int dev) {
+// One context per (device, slot): slot 0 serves the single-problem calls,
+// slots 1.. the concurrent workers of sngb_dbscan_batch_f32.
+constexpr int kMaxSlots = 16;
+DevCtx& get_ctx(int dev, int slot = 0) {
     std::lock_guard<std::mutex> lk(g_ctx_mu);
-    if ((int)g_ctx.size() <= dev) g_ctx.resize(dev + 1);
-    if (!g_ctx[dev]) {
+    const size_t idx = (size_t)dev * kMaxSlots + (size_t)slot;
+    if (g_ctx.size() <= idx) g_ctx.resize(idx + 1);
+    if (!g_ctx[idx]) {
         auto c = std::make_unique<DevCtx>();
         c->dev = dev;
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -158,9 +164,9 @@ DevCtx& get_ctx(int dev) {
         for (auto& e : c->up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaMallocHost(&c->h_counters, C_COUNT * sizeof(unsigned long long)));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
-        g_ctx[dev] = std::move(c);
+        g_ctx[idx] = std::move(c);
     }
-    return *g_ctx[dev];
+    return *g_ctx[idx];
 }
 
 int resolve_device(const sngb_opts* o) {
@@ -923,9 +929,9 @@ int sngb_dbscan_f32_device(const float* d_pts, uint64_t n, uint32_t d, double ep
     });
 }
 
-int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
-                    double rate, uint64_t seed, const sngb_opts* opts, int32_t* labels_out,
-                    uint8_t* roles_out, sngb_info* info) {
+static int dbscan_f32_host(int slot, const float* pts, uint64_t n, uint32_t d, double eps,
+                           int32_t min_pts, double rate, uint64_t seed, const sngb_opts* opts,
+                           int32_t* labels_out, uint8_t* roles_out, sngb_info* info) {
     int rc = validate(n, d, eps, min_pts, rate, true);
     if (rc) return rc;
     if (!pts || !labels_out || !roles_out) return SNGB_ERR_ARG;
@@ -934,7 +940,7 @@ int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
         DeviceGuard dg(dev);
-        DevCtx& c = get_ctx(dev);
+        DevCtx& c = get_ctx(dev, slot);
         std::lock_guard<std::mutex> lk(c.mu);
         cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : c.stream;
         Timer tm{c, s, opts && (opts->flags & SNGB_FLAG_TIMING)};
@@ -957,6 +963,44 @@ int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_
         fill_info(info, c.h_counters, n, d, gr, n, tm, true, true);
         return SNGB_OK;
     });
+}
+
+int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                    double rate, uint64_t seed, const sngb_opts* opts, int32_t* labels_out,
+                    uint8_t* roles_out, sngb_info* info) {
+    return dbscan_f32_host(0, pts, n, d, eps, min_pts, rate, seed, opts, labels_out, roles_out,
+                           info);
+}
+
+// Many small problems (the theory lab's pattern, theory.cpp:239-256): up to
+// SNGB_BATCH_SLOTS (default 8) host workers, each with its own device context
+// and streams, run the problems concurrently so their launch latencies and
+// host syncs overlap on the GPU.  Results as if each were a separate call.
+int sngb_dbscan_batch_f32(sngb_problem* probs, uint64_t count, const sngb_opts* opts) {
+    if (count && !probs) return SNGB_ERR_ARG;
+    if (count == 0) return SNGB_OK;
+    const uint64_t want = env_u64("SNGB_BATCH_SLOTS", 8);
+    const int slots = (int)std::max<uint64_t>(1, std::min<uint64_t>({count, want, (uint64_t)kMaxSlots}));
+    std::atomic<uint64_t> next{0};
+    auto worker = [&](int slot) {
+        for (;;) {
+            const uint64_t i = next.fetch_add(1);
+            if (i >= count) break;
+            sngb_problem& p = probs[i];
+            sngb_opts o = opts ? *opts : sngb_opts{-1, 0u, nullptr, 0, 0};
+            o.stream = nullptr;  // each worker runs on its own context's stream
+            o.flags = (o.flags & SNGB_FLAG_TIMING) | p.flags;
+            p.status = dbscan_f32_host(slot, p.pts, p.n, p.d, p.eps, p.min_pts, p.rate, p.seed, &o,
+                                       p.labels_out, p.roles_out, p.info_out);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int sl = 1; sl < slots; ++sl) pool.emplace_back(worker, sl);
+    worker(0);
+    for (auto& t : pool) t.join();
+    for (uint64_t i = 0; i < count; ++i)
+        if (probs[i].status != SNGB_OK) return probs[i].status;
+    return SNGB_OK;
 }
 
 int sngb_sampled_edges_f32_device(const float* d_pts, uint64_t n, uint32_t d, double eps,

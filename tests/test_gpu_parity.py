@@ -400,3 +400,28 @@ def test_cosine_zero_vector_is_an_error():
         sng.sng_dbscan(sng.Dataset(pts), p)
     pts[77] = 1e-30  # tiny but non-zero in fp64: not an error
     sng.sng_dbscan(sng.Dataset(pts), p)
+
+
+def test_batch_equals_separate_calls(oracle):
+    """sngb_dbscan_batch_f32: 40 small problems of mixed shape and metric run
+    concurrently; every result equals its separate call (and the oracle)."""
+    rng = np.random.default_rng(5)
+    problems = []
+    for i in range(40):
+        n = int(rng.integers(300, 6000))
+        cfg = [1, 3, 4][i % 3]
+        w = synthetic.CONFIGS[cfg]
+        pts = synthetic.generate(cfg, n=n)
+        dist = sng.Distance.euclidean() if i % 5 else sng.Distance.manhattan()
+        rate = min(1.0, float(rng.uniform(0.02, 0.3)))
+        problems.append((pts, sng.SngParams(eps=w.eps * (1.5 if i % 5 == 0 else 1.0),
+                                             min_pts=w.min_pts, rate=rate, seed=i, dist=dist)))
+    got = sng.sng_dbscan_batch(problems)
+    for (pts, p), c in zip(problems, got):
+        single = sng.sng_dbscan(sng.Dataset(pts), p)
+        np.testing.assert_array_equal(c.assignment, single.assignment)
+        np.testing.assert_array_equal(c.role, single.role)
+        assert c.cluster_count == single.cluster_count
+        if p.dist.kind == "euclidean":
+            labels, roles, _, _ = oracle.sng_dbscan(pts, p.eps, p.min_pts, p.rate, p.seed)
+            np.testing.assert_array_equal(c.assignment, labels)
