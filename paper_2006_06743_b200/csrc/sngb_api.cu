@@ -636,7 +636,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 ga.grab = (uint32_t)std::max<uint64_t>(
                     1, std::min<uint64_t>(32, (ga.row_end - ga.row_begin) / (warps * 16)));
             }
-            if (metric != kMetricEuclid) CK(launch_gather_metric(ga, exhaustive, gs, c.num_sms));
+            if (metric != kMetricEuclid || d > 1024)
+                CK(launch_gather_metric(ga, exhaustive, gs, c.num_sms));
             else if (q8_on) CK(launch_gather_q8(ga, q8p.args, gs, c.num_sms));
             else CK(launch_gather(ga, exhaustive, gs, c.num_sms));
         };
@@ -679,7 +680,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             ea.extras = c.extras.as<unsigned long long>();
             ea.count_ptr = &dc[C_EXTRA_CURSOR];
             ea.capacity = extras_cap;
-            if (metric != kMetricEuclid) CK(launch_extras_metric(ea, s, c.num_sms));
+            if (metric != kMetricEuclid || d > 1024) CK(launch_extras_metric(ea, s, c.num_sms));
             else if (q8_on) CK(launch_extras_q8(ea, q8p.args, s, c.num_sms));
             else CK(launch_extras(ea, s, c.num_sms));
         }

@@ -549,7 +549,7 @@ cudaError_t gather_dispatch(const GatherArgs& a, cudaStream_t s, int num_sms) {
         case 6: return gather_one<32, 6, 1, false, EXH>(a, s, num_sms);
         case 7: return gather_one<32, 7, 1, false, EXH>(a, s, num_sms);
         case 8: return gather_one<32, 8, 1, false, EXH>(a, s, num_sms);
-        default: return cudaErrorInvalidValue;  // d > 1024: not supported yet
+        default: return cudaErrorInvalidValue;  // d > 1024 runs the generic kernel (sngb_metric.cu)
     }
 }
 

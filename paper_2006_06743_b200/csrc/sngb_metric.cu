@@ -1,4 +1,5 @@
-// sngb_metric.cu -- the Manhattan and cosine metrics of Distance::within
+// sngb_metric.cu -- the Manhattan and cosine metrics of Distance::within, and
+// the Euclidean one for rows wider than the specialised gathers (d > 1024)
 // (proj/include/sng/distance.hpp:55-68, 75-84, 91-103) on the sampled-graph
 // path.  Same structure as k_gather (draws regenerated from their counters,
 // live pairs compacted per 32-draw chunk, dynamic row claiming), one G-lane
@@ -57,11 +58,16 @@ __device__ __forceinline__ float pair_value(const TestParams& tp, uint64_t u, ui
     float acc = 0.f;
     for (uint32_t k = q; k < tp.d; k += G) {
         const float x = __ldg(a + k), y = __ldg(b + k);
-        acc = METRIC == kMetricManhattan ? acc + fabsf(x - y) : fmaf(x, y, acc);
+        if (METRIC == kMetricEuclid) {
+            const float t = x - y;
+            acc = fmaf(t, t, acc);
+        } else {
+            acc = METRIC == kMetricManhattan ? acc + fabsf(x - y) : fmaf(x, y, acc);
+        }
     }
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-    if (METRIC == kMetricManhattan) return acc;
+    if (METRIC != kMetricCosine) return acc;
     return -(acc / (__ldg(tp.rnorm + u) * __ldg(tp.rnorm + v)));  // NaN for a zero fp32 norm
 }
 
@@ -195,6 +201,8 @@ cudaError_t launch_gather_metric(const GatherArgs& a, bool exhaustive, cudaStrea
                                  int num_sms) {
     if (a.row_end <= a.row_begin) return cudaSuccess;
     const bool wide = a.tp.d > 64;
+    if (a.tp.metric == kMetricEuclid)  // d > 1024 (the specialised gathers stop there)
+        return gather_metric_one<kMetricEuclid, 32>(a, exhaustive, s, num_sms);
     if (a.tp.metric == kMetricManhattan)
         return wide ? gather_metric_one<kMetricManhattan, 32>(a, exhaustive, s, num_sms)
                     : gather_metric_one<kMetricManhattan, 8>(a, exhaustive, s, num_sms);
@@ -205,6 +213,7 @@ cudaError_t launch_gather_metric(const GatherArgs& a, bool exhaustive, cudaStrea
 cudaError_t launch_extras_metric(const ExtrasArgs& a, cudaStream_t s, int num_sms) {
     if (a.capacity == 0) return cudaSuccess;
     const bool wide = a.tp.d > 64;
+    if (a.tp.metric == kMetricEuclid) return extras_metric_one<kMetricEuclid, 32>(a, s, num_sms);
     if (a.tp.metric == kMetricManhattan)
         return wide ? extras_metric_one<kMetricManhattan, 32>(a, s, num_sms)
                     : extras_metric_one<kMetricManhattan, 8>(a, s, num_sms);

@@ -425,3 +425,21 @@ def test_batch_equals_separate_calls(oracle):
         if p.dist.kind == "euclidean":
             labels, roles, _, _ = oracle.sng_dbscan(pts, p.eps, p.min_pts, p.rate, p.seed)
             np.testing.assert_array_equal(c.assignment, labels)
+
+
+# ---- edge shapes ----------------------------------------------------------
+@pytest.mark.parametrize("n,d,rate", [(1, 3, 0.5), (2, 1, 1.0), (2, 5, 0.3), (3, 2000, 0.7),
+                                      (1200, 1500, 0.05), (800, 3000, 1.0)])
+def test_edge_shapes_match_oracle(oracle, n, d, rate):
+    """n = 1 and 2 (no or one draw), and rows wider than the specialised
+    gathers (d > 1024: the generic kernel), incl. the s = 1 branch."""
+    rng = np.random.default_rng(n + d)
+    pts = rng.random((n, d), dtype=np.float32)
+    i = np.arange(0, max(n - 1, 1), 3)
+    eps = float(np.quantile(np.sqrt(((pts[i] - pts[np.minimum(i + 1, n - 1)]) ** 2).sum(1)), 0.2)
+                if n > 1 else 1.0) + 1e-3
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=eps, min_pts=2, rate=rate, seed=3),
+                       info)
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, 2, rate, 3)
+    _assert_same(c, info, labels, roles, oinfo)
