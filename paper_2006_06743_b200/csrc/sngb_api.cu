@@ -655,7 +655,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             for (uint32_t k = 0; k < gphases; ++k) {
                 land_chunk(k);
                 gather(0, part(k + 1), part(k), part(k + 1));
-                for (uint32_t j = 0; j < k; ++j) gather(part(k), part(k + 1), part(j), part(j + 1));
+                if (q8_on) {  // the 8-bit table is L2-resident whole: one launch for the rest
+                    if (k > 0) gather(part(k), part(k + 1), 0, part(k));
+                } else {      // fp32: one L2 slice of partners per launch
+                    for (uint32_t j = 0; j < k; ++j) gather(part(k), part(k + 1), part(j), part(j + 1));
+                }
             }
             prepared = quantized = chunks;
         } else {
