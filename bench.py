@@ -73,7 +73,10 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_gather_ceiling(d: int, n: int, row: int | None = None):
+Q8_SPLIT_MIN_RW, Q8_HEAD_BYTES, Q8_HEAD_VALS = 40, 256, 240  # sngb_internal.cuh kSplitMinRW, kHead
+
+
+def load_gather_ceiling(d: int, n: int, row: int | None = None, read: int | None = None):
     """Measured random-row gather ceiling for this row shape and table size
     (tools/gather_ceiling.cu -> profiles/r01_gather_ceilings.jsonl): the best
     rows/s of a lean gather with no per-pair work, swept over rows in flight
@@ -87,7 +90,8 @@ def load_gather_ceiling(d: int, n: int, row: int | None = None):
         row = 8 if d <= 2 else 16 * ((d + 3) // 4)  # padded device row, bytes
     table = n * row
     # same row size; among those, the table size closest to ours (L2 vs HBM)
-    same = [c for c in cases if c["row_bytes"] == max(row, 16)]
+    same = [c for c in cases if c["row_bytes"] == max(row, 16)
+            and c.get("read_bytes", c["row_bytes"]) == (read or c["row_bytes"])]
     if not same:
         return None, None
     best = min(same, key=lambda c: abs(math.log(c["table_MB"] * 2**20 / max(table, 1))))
@@ -370,8 +374,10 @@ def main():
     g_ms = statistics.mean(gather_ms) if gather_ms else 0.0
     achieved = gather_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else None
     q8 = filter_bits == 8
+    q8_split = q8 and (d + 15) // 16 + 1 >= Q8_SPLIT_MIN_RW  # head/tail gather (k_gather_q8s)
     bpp = gather_bytes / gather_pairs if gather_pairs else 4 * d  # algorithmic bytes per pair
-    roofline = {"bound": "hbm", "kernel": "k_gather_q8" if q8 else "k_gather",
+    kname = ("k_gather_q8s" if q8_split else "k_gather_q8") if q8 else "k_gather"
+    roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
@@ -379,7 +385,9 @@ def main():
                 "algorithmic_bytes_per_launch": gather_bytes,
                 "bytes_per_pair": bpp, "pairs_per_launch": gather_pairs,
                 "filter": ("8-bit exact filter: u8 rows + norm, DP4A integer distances, "
-                           "integer accept/reject thresholds, fp64 recheck in the band")
+                           "integer accept/reject thresholds, fp64 recheck in the band"
+                           + ("; exact early reject on the 240-value head, survivors read "
+                              "the tail" if q8_split else ""))
                 if q8 else "fp32 rows, fp32 guard band, fp64 recheck in the band",
                 "kernel_ms": g_ms,
                 "kernel_share_of_step": (g_ms / ms_per_step) if ms_per_step else None}
@@ -394,6 +402,18 @@ def main():
     case, rows_per_s = load_gather_ceiling(
         d, min(n, int(63 * 2**20 // row_bytes)) if phased else n, row_bytes if q8 else None)
     l2_peak = rows_per_s * bpp / 1e9 if (resident and rows_per_s) else None
+    if q8_split and resident and rows_per_s and gather_pairs:
+        # every pair reads its 256-B head, a fraction f of them the rest of the
+        # row: the ceiling is the time-weighted mix of the two measured gathers
+        hcase, heads_per_s = load_gather_ceiling(d, n, row_bytes, Q8_HEAD_BYTES)
+        head_alg = Q8_HEAD_VALS + 4
+        f = max(0.0, (bpp - head_alg) / (d - Q8_HEAD_VALS + 4))
+        roofline["tail_fraction"] = f
+        if heads_per_s:
+            l2_peak = bpp / (1.0 / heads_per_s + f / rows_per_s) / 1e9
+            case = f"{hcase} + {case}"
+        else:
+            l2_peak = None
     eff = l2_peak if resident else peak
     roofline.update({
         "effective_bound": "l2 (random rows)" if resident else "hbm",

@@ -395,7 +395,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     const bool exhaustive = draws >= n - 1;
     // SNGB_Q8: 0 off, 1 auto (use when the band is narrow), 2 force (tests)
     const uint64_t q8_mode = env_u64("SNGB_Q8", 1);
-    q8_try = metric == kMetricEuclid && !exhaustive && d >= 128 && d <= 1024 && q8_mode != 0;
+    // the 8-bit gathers hold a row in <= 3 chunks per lane: d <= 16 * (3 * 32 - 1)
+    q8_try = metric == kMetricEuclid && !exhaustive && d >= 128 && d <= 1520 && q8_mode != 0;
     const uint64_t rows = re - rb;
     const uint32_t nb = bits_for(n - 1);
     const uint64_t base = (n - 1) - draws;
@@ -636,9 +637,9 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 ga.grab = (uint32_t)std::max<uint64_t>(
                     1, std::min<uint64_t>(32, (ga.row_end - ga.row_begin) / (warps * 16)));
             }
-            if (metric != kMetricEuclid || d > 1024)
+            if (q8_on) CK(launch_gather_q8(ga, q8p.args, gs, c.num_sms));
+            else if (metric != kMetricEuclid || d > 1024)
                 CK(launch_gather_metric(ga, exhaustive, gs, c.num_sms));
-            else if (q8_on) CK(launch_gather_q8(ga, q8p.args, gs, c.num_sms));
             else CK(launch_gather(ga, exhaustive, gs, c.num_sms));
         };
         auto land_chunk = [&](uint32_t k) {  // chunk k uploaded, prepared, quantised
@@ -684,8 +685,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             ea.extras = c.extras.as<unsigned long long>();
             ea.count_ptr = &dc[C_EXTRA_CURSOR];
             ea.capacity = extras_cap;
-            if (metric != kMetricEuclid || d > 1024) CK(launch_extras_metric(ea, s, c.num_sms));
-            else if (q8_on) CK(launch_extras_q8(ea, q8p.args, s, c.num_sms));
+            if (q8_on) CK(launch_extras_q8(ea, q8p.args, s, c.num_sms));
+            else if (metric != kMetricEuclid || d > 1024) CK(launch_extras_metric(ea, s, c.num_sms));
             else CK(launch_extras(ea, s, c.num_sms));
         }
         CK(launch_band(tp, ga.sink, dc, s, c.num_sms));  // the band pairs, decided exactly
@@ -780,7 +781,11 @@ void fill_info(sngb_info* info, const unsigned long long* hc, uint64_t n, uint32
     info->directed_accepts = hc[C_EDGE_CURSOR];
     info->gather_pairs = hc[C_GATHER_PAIRS];
     info->filter_bits = gr.q8 ? 8 : 32;
-    info->gather_bytes = hc[C_GATHER_PAIRS] * (gr.q8 ? (uint64_t)d + 4 : 4ull * d);
+    if (gr.q8 && q8_split((d + 15) / 16))  // every pair reads its head, survivors the rest
+        info->gather_bytes = hc[C_GATHER_PAIRS] * (kHeadVals + 4ull) +
+                             hc[C_TAIL_PAIRS] * ((uint64_t)d - kHeadVals + 4);
+    else
+        info->gather_bytes = hc[C_GATHER_PAIRS] * (gr.q8 ? (uint64_t)d + 4 : 4ull * d);
     if (clustered) {
         info->cluster_count = (int32_t)hc[C_CLUSTERS];
         info->core_count = (uint32_t)hc[C_CORE];

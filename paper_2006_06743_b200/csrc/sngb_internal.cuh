@@ -33,6 +33,7 @@ enum Counter : int {
     C_BAND_CURSOR,       // band pairs appended (see TestParams::band)
     C_QMIN,              // max of ~ordered(value): the dataset minimum (8-bit filter scale)
     C_QMAX,              // max of ordered(value): the dataset maximum
+    C_TAIL_PAIRS,        // 8-bit filter: pairs the head did not reject (read their tail)
     C_COUNT
 };
 
@@ -187,8 +188,13 @@ cudaError_t launch_gather_metric(const GatherArgs& a, bool exhaustive, cudaStrea
 cudaError_t launch_extras_metric(const ExtrasArgs& a, cudaStream_t s, int num_sms);
 // sngb_quant.cu: the 8-bit filter for wide rows (exact via integer thresholds
 // on Q2 = sum (qa - qb)^2 plus the fp64 recheck in the band)
+// 8-bit row layout: chunk 0 = (N over the first kHeadVals values, N over the
+// row, 0, 0), chunks 1..nd the bytes; the head is chunks [0, kHead)
+constexpr uint32_t kHead = 16;  // half a warp per head in k_gather_q8s
+constexpr uint32_t kHeadVals = 16 * (kHead - 1);
+constexpr uint32_t kSplitMinRW = 40;  // rows this wide take the early-reject gather
 struct Q8Args {
-    const uint4* rows;   // n rows of nd + 1 16-byte chunks: bytes, zero pad, norm chunk
+    const uint4* rows;   // n rows of nd + 1 16-byte chunks: norm chunk, bytes, zero pad
     uint32_t nd;         // data chunks per row = ceil(d / 16)
     int32_t accept_max;  // Q2 <= accept_max: the reference accepts
     int32_t reject_min;  // Q2 >  reject_min: the reference rejects (else exact recheck)
@@ -198,6 +204,7 @@ struct Q8Plan {
     Q8Args args;
 };
 bool q8_plan(double lo, double hi, uint32_t d, double eps2, Q8Plan& p);
+bool q8_split(uint32_t nd);  // rows of nd data chunks take the early-reject gather
 cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint32_t d,
                             const Q8Plan& p, uint4* out, cudaStream_t s, int num_sms,
                             const double* pts64 = nullptr);

@@ -5,8 +5,9 @@
 // Quantisation.  s is a power of two >= (max - min)/254 and lo' = floor(min/s)*s,
 // so q = rint((a - lo')/s) in [0, 255] is computed exactly in fp64 (up to a
 // relative 2^-45 in a - lo' for tiny |a|) and a = lo' + s*q + e with
-// |e| <= s/2 * (1 + 2^-30).  Each row stores its bytes, zero padded to 16-byte
-// chunks, then one chunk holding its norm N = sum q^2.
+// |e| <= s/2 * (1 + 2^-30).  Each row stores one chunk with its norms (the head
+// norm, over the first kHeadVals values, and N = sum q^2), then its bytes, zero
+// padded to 16-byte chunks.
 //
 // Filter.  For a pair, Q2 = sum (qa - qb)^2 = Na + Nb - 2 sum qa*qb is an exact
 // integer (DP4A).  With Dk = s*dqk, |Ek| <= s' = s(1 + 2^-30), Q1 = sum |dqk| <=
@@ -21,10 +22,17 @@
 // operation order on the fp32 rows -- the same recheck the fp32 filter uses.
 // The host enables the path only when that band is narrow relative to eps
 // (a data set with a huge value range relative to eps keeps the fp32 filter).
+//
+// Early rejection (k_gather_q8s, rows of >= kSplitMinRW chunks).  The partial
+// sum over the row's head, Q2h = Nha + Nhb - 2 sum_head qa*qb, satisfies
+// Q2h <= Q2, so Q2h > B rejects exactly; only the survivors read their tail.
+// A sampled pair is far more often a non-neighbour than a neighbour (eps is
+// small against the typical distance), so most pairs cost the head's bytes.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sngb_device.cuh"
 #include "sngb_epstest.cuh"
@@ -32,6 +40,12 @@
 #include "sngb_rng.cuh"
 
 namespace sngb {
+
+bool q8_split(uint32_t nd) {
+    const char* e = std::getenv("SNGB_Q8_SPLIT");  // 0 off, 1 on (default: by width)
+    const int mode = e ? std::atoi(e) : -1;
+    return mode == 0 ? false : (mode == 1 ? nd + 1 >= kHead + 1 : nd + 1 >= kSplitMinRW);
+}
 
 bool q8_plan(double lo, double hi, uint32_t d, double eps2, Q8Plan& p) {
     const double need = (hi - lo) / 254.0 * (1.0 + 1e-12);
@@ -59,7 +73,8 @@ bool q8_plan(double lo, double hi, uint32_t d, double eps2, Q8Plan& p) {
 
 namespace {
 
-// warp per row: bytes q of the row's d values, zero padded, then the norm chunk
+// warp per row: the norm chunk (N over the head's values, N over the row), then
+// bytes q of the row's d values, zero padded
 __global__ void k_quantize(const float* __restrict__ pts, uint32_t stride, uint64_t n, uint32_t d,
                            double lo, double inv_s, uint32_t nd, uint4* __restrict__ out,
                            const double* __restrict__ pts64) {
@@ -69,7 +84,7 @@ __global__ void k_quantize(const float* __restrict__ pts, uint32_t stride, uint6
     for (uint64_t r = gw; r < n; r += nw) {
         const float* row = pts + r * stride;
         uint4* orow = out + r * (nd + 1);
-        uint32_t norm = 0;
+        uint32_t norm = 0, norm_head = 0;
         for (uint32_t c = lane; c < nd; c += 32) {
             uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -91,12 +106,14 @@ __global__ void k_quantize(const float* __restrict__ pts, uint32_t stride, uint6
                                        : x <= 0.0 ? 0u : (x >= 255.0 ? 255u : (uint32_t)x);
                     w[j4] |= q << (8 * j);
                     norm += q * q;
+                    norm_head += c < kHead - 1 ? q * q : 0u;
                 }
             }
-            orow[c] = make_uint4(w[0], w[1], w[2], w[3]);
+            orow[1 + c] = make_uint4(w[0], w[1], w[2], w[3]);
         }
         norm = __reduce_add_sync(kFull, norm);
-        if (lane == 0) orow[nd] = make_uint4(norm, 0, 0, 0);
+        norm_head = __reduce_add_sync(kFull, norm_head);
+        if (lane == 0) orow[0] = make_uint4(norm_head, norm, 0, 0);
     }
 }
 
@@ -120,7 +137,7 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8(const GatherArgs a, const 
     const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
     const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerBlock;
     const uint4* __restrict__ Q = q8.rows;
-    const uint32_t RW = q8.nd + 1, nd = q8.nd;
+    const uint32_t RW = q8.nd + 1;
     const uint32_t plo = a.part_lo, phi = a.part_hi;
     uint32_t* list = s_list[wib];
     WarpStage<kStage> stage{s_stage[wib], 0};
@@ -143,8 +160,8 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8(const GatherArgs a, const 
         for (int vv = 0; vv < V8; ++vv) {
             const uint32_t c = lane + 32 * vv;
             qq[vv] = c < RW ? __ldg(Q + u * RW + c) : make_uint4(0, 0, 0, 0);
-            if (c == nd) {
-                nu = qq[vv].x;
+            if (c == 0) {
+                nu = qq[vv].y;
                 qq[vv] = make_uint4(0, 0, 0, 0);
             }
         }
@@ -191,7 +208,7 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8(const GatherArgs a, const 
                     for (int vv = 0; vv < V8; ++vv) {
                         const uint32_t c = lane + 32 * vv;
                         dot = dot16(qq[vv], rows[uu][vv], dot);  // query norm chunk is zeroed
-                        if (c == nd) nv = rows[uu][vv].x;
+                        if (c == 0) nv = rows[uu][vv].y;
                     }
                     ps[uu] = (int)nv - 2 * (int)dot;  // partial of Nb - 2 sum qa qb
                 }
@@ -227,6 +244,193 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8(const GatherArgs a, const 
     flush_stats(st, gpairs, a.counters, lane);
 }
 
+// Early-reject gather for wide rows.  Phase A: half a warp per pair reads the
+// pair's head (kHead chunks, the norm chunk first), UA pairs per half-warp step;
+// pairs whose head sum already exceeds reject_min are rejected, the others are
+// queued with Q2h + Nta.  Phase B: the full warp finishes UB queued pairs per
+// step over the tail chunks plus the norm chunk (for Ntb = N - Nhead).  The
+// queue holds one query row's survivors; it drains in whole steps after every
+// 32-draw chunk and completely at the end of the row.
+template <int VT, int UA, int UB>
+__global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const Q8Args q8) {
+    __shared__ unsigned long long s_stage[kWarpsPerBlock][kStage];
+    __shared__ uint32_t s_list[kWarpsPerBlock][32];
+    __shared__ uint32_t s_qp[kWarpsPerBlock][64];
+    __shared__ int s_qh[kWarpsPerBlock][64];
+    constexpr int SPANA = 16 / UA, SPANB = 32 / UB;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int hc = lane & 15;  // head chunk of this lane
+    const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
+    const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerBlock;
+    const uint4* __restrict__ Q = q8.rows;
+    const uint32_t RW = q8.nd + 1, T = RW - kHead;  // tail chunks; slot T = norm chunk
+    const uint32_t plo = a.part_lo, phi = a.part_hi;
+    uint32_t* list = s_list[wib];
+    uint32_t* qp = s_qp[wib];
+    int* qh2 = s_qh[wib];
+    WarpStage<kStage> stage{s_stage[wib], 0};
+    TestStats st;
+    unsigned long long gpairs = 0, tails = 0;
+
+    uint64_t u = a.row_begin + gw, chunk_end = a.row_end;
+    auto grab = [&]() {
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(a.work, (unsigned long long)a.grab);
+        b0 = __shfl_sync(kFull, b0, 0);
+        u = a.row_begin + b0;
+        chunk_end = u + a.grab < a.row_end ? u + a.grab : a.row_end;
+    };
+    if (a.work) grab();
+    for (; u < chunk_end; (a.work && u + 1 >= chunk_end) ? grab() : (void)(u += a.work ? 1 : nw)) {
+        uint4 qh = __ldg(Q + u * RW + hc);
+        const uint32_t nha = __shfl_sync(kFull, qh.x, 0), nfa = __shfl_sync(kFull, qh.y, 0);
+        if (hc == 0) qh = make_uint4(0, 0, 0, 0);
+        uint4 qt[VT];
+#pragma unroll
+        for (int v = 0; v < VT; ++v) {
+            const uint32_t sl = lane + 32 * v;
+            qt[v] = sl < T ? __ldg(Q + u * RW + kHead + sl) : make_uint4(0, 0, 0, 0);
+        }
+        const int nta = (int)(nfa - nha);
+        uint32_t qn = 0;  // queued survivors (warp-uniform)
+
+        // phase B over queue entries [e0, e0 + UB) of which those < qend are real
+        auto tail_step = [&](uint32_t e0, uint32_t qend) {
+            uint4 rows[UB][VT];
+#pragma unroll
+            for (int uu = 0; uu < UB; ++uu) {
+                const uint32_t e = e0 + uu;
+                const uint32_t pv = qp[e < qend ? e : e0];
+#pragma unroll
+                for (int v = 0; v < VT; ++v) {
+                    const uint32_t sl = lane + 32 * v;
+                    rows[uu][v] = sl <= T ? __ldg(Q + (uint64_t)pv * RW + (sl < T ? kHead + sl : 0))
+                                          : make_uint4(0, 0, 0, 0);
+                }
+            }
+            __syncwarp();  // scheduling fence: all UB*VT loads in flight together
+            int ps[UB];
+#pragma unroll
+            for (int uu = 0; uu < UB; ++uu) {
+                uint32_t dot = 0;
+                int nt = 0;
+#pragma unroll
+                for (int v = 0; v < VT; ++v) {
+                    dot = dot16(qt[v], rows[uu][v], dot);  // the query's slot T is zero
+                    if (lane + 32 * v == T) nt = (int)(rows[uu][v].y - rows[uu][v].x);
+                }
+                ps[uu] = nt - 2 * (int)dot;
+            }
+#pragma unroll
+            for (int o = 16, mm = UB; mm > 1; o >>= 1, mm >>= 1) {
+                const bool hi = (lane & o) != 0;
+#pragma unroll
+                for (int k = 0; k < mm / 2; ++k) {
+                    const int mine = hi ? ps[k + mm / 2] : ps[k];
+                    const int other = hi ? ps[k] : ps[k + mm / 2];
+                    ps[k] = mine + __shfl_xor_sync(kFull, other, o);
+                }
+            }
+#pragma unroll
+            for (int o = SPANB / 2; o > 0; o >>= 1) ps[0] += __shfl_xor_sync(kFull, ps[0], o);
+            const uint32_t e = e0 + lane / SPANB;
+            const bool okm = (lane % SPANB) == 0 && e < qend;
+            const uint32_t pm = qp[okm ? e : e0];
+            const int q2 = qh2[okm ? e : e0] + ps[0];
+            const bool acc = okm && q2 <= q8.accept_max;
+            if (okm && q2 > q8.accept_max && q2 <= q8.reject_min) {  // band: k_band decides
+                band_push(a.tp, u, pm, __int_as_float(0x7fc00000));
+                st.band++;
+            }
+            tails += okm ? 1u : 0u;
+            stage.push(acc, edge_key(u, pm, a.sink.nb), a.sink, lane);
+        };
+
+        uint32_t limit = a.draws;
+        uint64_t z = vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
+        for (uint32_t i0 = 0; i0 < limit; i0 += 32, z += 32ull * kGamma) {
+            const uint32_t i = i0 + lane;
+            const bool valid = i < limit;
+            bool fire = false;
+            uint32_t t = 0;
+            if (valid) {
+                t = lemire32(mix(z), a.base + i + 1, fire);
+                fire |= test_fire(a.force_mod, u, i, a.draws);
+            }
+            const uint32_t p = t + (t >= (uint32_t)u ? 1u : 0u);
+            const unsigned fm = __ballot_sync(kFull, valid && fire);
+            if (fm) limit = i0 + __ffs(fm) - 1;  // irregular vertex: cut here
+            const bool live = i < limit && p >= plo && p < phi;
+            const unsigned m = __ballot_sync(kFull, live);
+            if (live) list[__popc(m & lanemask_lt())] = p;
+            const uint32_t nlive = __popc(m);
+            __syncwarp();
+            // phase A: heads, 2*UA pairs per step
+#pragma unroll 1
+            for (uint32_t j0 = 0; j0 < nlive; j0 += 2 * UA) {
+                uint4 rows[UA];
+#pragma unroll
+                for (int k = 0; k < UA; ++k) {
+                    const uint32_t j = j0 + (lane >> 4) * UA + k;
+                    const uint32_t pv = list[j < nlive ? j : j0];
+                    rows[k] = __ldg(Q + (uint64_t)pv * RW + hc);
+                }
+                __syncwarp();
+                int ps[UA];
+#pragma unroll
+                for (int k = 0; k < UA; ++k)
+                    ps[k] = (hc == 0 ? (int)rows[k].x : 0) - 2 * (int)dot16(qh, rows[k], 0u);
+#pragma unroll
+                for (int o = 8, mm = UA; mm > 1; o >>= 1, mm >>= 1) {
+                    const bool hi = (lane & o) != 0;
+#pragma unroll
+                    for (int k = 0; k < mm / 2; ++k) {
+                        const int mine = hi ? ps[k + mm / 2] : ps[k];
+                        const int other = hi ? ps[k] : ps[k + mm / 2];
+                        ps[k] = mine + __shfl_xor_sync(kFull, other, o);
+                    }
+                }
+#pragma unroll
+                for (int o = SPANA / 2; o > 0; o >>= 1) ps[0] += __shfl_xor_sync(kFull, ps[0], o);
+                const uint32_t pj = j0 + lane / SPANA;
+                const bool okm = (lane % SPANA) == 0 && pj < nlive;
+                const int q2h = (int)nha + ps[0];
+                const bool keep = okm && q2h <= q8.reject_min;  // else Q2 >= Q2h > B: reject
+                gpairs += okm ? 1u : 0u;
+                const unsigned km = __ballot_sync(kFull, keep);
+                if (keep) {
+                    const uint32_t slot = qn + __popc(km & lanemask_lt());
+                    qp[slot] = list[pj];
+                    qh2[slot] = q2h + nta;
+                }
+                qn += __popc(km);
+            }
+            __syncwarp();
+            // phase B: whole steps now, the remainder waits for more survivors
+            if (qn >= (uint32_t)UB) {
+                uint32_t e0 = 0;
+#pragma unroll 1
+                for (; e0 + UB <= qn; e0 += UB) tail_step(e0, qn);
+                const uint32_t rem = qn - e0;
+                uint32_t mp = 0;
+                int mh = 0;
+                if ((uint32_t)lane < rem) mp = qp[e0 + lane], mh = qh2[e0 + lane];
+                __syncwarp();
+                if ((uint32_t)lane < rem) qp[lane] = mp, qh2[lane] = mh;
+                qn = rem;
+            }
+            __syncwarp();
+        }
+        if (qn) tail_step(0, qn);
+        __syncwarp();
+    }
+    stage.flush(a.sink, lane);
+    st.pairs = gpairs;
+    flush_stats(st, gpairs, a.counters, lane);
+    const unsigned long long tw = warp_sum(tails);
+    if (lane == 0 && tw) atomicAdd(&a.counters[C_TAIL_PAIRS], tw);
+}
+
 // Floyd replacement pairs through the 8-bit filter: one pair per warp step
 template <int V8>
 __global__ void __launch_bounds__(256) k_extras_q8(const ExtrasArgs a, const Q8Args q8) {
@@ -235,7 +439,7 @@ __global__ void __launch_bounds__(256) k_extras_q8(const ExtrasArgs a, const Q8A
     const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
     const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerBlock;
     const uint4* __restrict__ Q = q8.rows;
-    const uint32_t RW = q8.nd + 1, nd = q8.nd;
+    const uint32_t RW = q8.nd + 1;
     WarpStage<kStage> stage{s_stage[wib], 0};
     TestStats st;
     uint64_t count = *a.count_ptr;
@@ -248,10 +452,10 @@ __global__ void __launch_bounds__(256) k_extras_q8(const ExtrasArgs a, const Q8A
 #pragma unroll
         for (int vv = 0; vv < V8; ++vv) {
             const uint32_t c = lane + 32 * vv;
-            if (c < nd) {
+            if (c == 0) {
+                part = (int)(__ldg(Q + u * RW).y + __ldg(Q + v * RW).y);
+            } else if (c < RW) {
                 dot = dot16(__ldg(Q + u * RW + c), __ldg(Q + v * RW + c), dot);
-            } else if (c == nd) {
-                part = (int)(__ldg(Q + u * RW + c).x + __ldg(Q + v * RW + c).x);
             }
         }
         part -= 2 * (int)dot;
@@ -283,10 +487,8 @@ cudaError_t extras_q8_one(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, 
     return cudaGetLastError();
 }
 
-template <int V8>
-cudaError_t q8_one(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
-    // 8 rows per step (measured: U = 2 3.48 ms, 4 2.77 ms, 8 2.62 ms on cfg2)
-    auto k = k_gather_q8<V8, 8>;
+template <typename K>
+cudaError_t q8_launch(K k, const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
     if (per_sm < 1) per_sm = 1;
@@ -324,10 +526,22 @@ cudaError_t launch_extras_q8(const ExtrasArgs& a, const Q8Args& q, cudaStream_t 
 
 cudaError_t launch_gather_q8(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
     if (a.row_end <= a.row_begin) return cudaSuccess;
-    switch ((q.nd + 1 + 31) / 32) {
-        case 1: return q8_one<1>(a, q, s, num_sms);
-        case 2: return q8_one<2>(a, q, s, num_sms);
-        case 3: return q8_one<3>(a, q, s, num_sms);
+    const uint32_t rw = q.nd + 1;
+    if (q8_split(q.nd)) {
+        switch ((rw - kHead + 1 + 31) / 32) {  // tail chunks + the norm chunk
+            // UA 16, UB 8 (measured on cfg2: gather 1.21 ms; UA 8 1.40, UA 4 1.73, UB 4
+            // 1.32; 3 blocks/SM 1.31-1.76); UB 4 where 8 would spill
+            case 1: return q8_launch(k_gather_q8s<1, 16, 8>, a, q, s, num_sms);
+            case 2: return q8_launch(k_gather_q8s<2, 16, 8>, a, q, s, num_sms);
+            case 3: return q8_launch(k_gather_q8s<3, 16, 4>, a, q, s, num_sms);
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    // 8 rows per step (measured: U = 2 3.48 ms, 4 2.77 ms, 8 2.62 ms on cfg2)
+    switch ((rw + 31) / 32) {
+        case 1: return q8_launch(k_gather_q8<1, 8>, a, q, s, num_sms);
+        case 2: return q8_launch(k_gather_q8<2, 8>, a, q, s, num_sms);
+        case 3: return q8_launch(k_gather_q8<3, 8>, a, q, s, num_sms);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -294,6 +294,52 @@ def test_q8_pipelined_host_upload(oracle, stretch, bits):
     assert info.gpu["filter_bits"] == bits
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("n,d,rate,seed,q", [(1500, 256, 0.08, 21, 0.1), (2000, 640, 0.05, 22, 0.1),
+                                             (1600, 1300, 0.05, 23, 0.1), (2500, 784, 0.04, 24, 0.5),
+                                             (1800, 1000, 0.05, 25, 0.9)])
+def test_q8_early_reject_matches_oracle(oracle, monkeypatch, split, n, d, rate, seed, q):
+    """The head/tail gather (SNGB_Q8_SPLIT=1; tail slots 1, 2 and 3 warp widths)
+    and the one-pass gather (=0) on the same wide rows: identical to the oracle,
+    with eps at low and high within-cluster quantiles (few / many survivors)."""
+    monkeypatch.setenv("SNGB_Q8", "2")
+    monkeypatch.setenv("SNGB_Q8_SPLIT", split)
+    pts = _q8_case(n, d, seed)
+    i = np.arange(0, n - 1, 7)
+    eps = float(np.quantile(np.sqrt(((pts[i] - pts[i + 1]) ** 2).sum(1)), q))
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=eps, min_pts=3, rate=rate, seed=seed),
+                       info)
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, 3, rate, seed)
+    _assert_same(c, info, labels, roles, oinfo)
+    assert info.gpu["filter_bits"] == 8
+
+
+def test_q8_early_reject_irregular_exact(oracle, monkeypatch):
+    """Lemire-reject replays through the head/tail gather."""
+    pts = _q8_case(2500, 784, 8)
+    eps = 3.0
+    keys, _ = oracle.sampled_edges(pts, eps, 0.04, 8)
+    monkeypatch.setenv("SNGB_Q8", "2")
+    monkeypatch.setenv("SNGB_Q8_SPLIT", "1")
+    monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", "5")
+    g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.04, seed=8)
+    np.testing.assert_array_equal(g.keys, keys)
+
+
+def test_q8_early_reject_reads_fewer_bytes():
+    """On the cfg2 data most sampled pairs are rejected by their head: the
+    algorithmic bytes (head for every pair, tail for survivors) fall well below
+    a full row per pair."""
+    n, d = 20000, 784
+    pts = synthetic.generate(2, n=n)
+    info = sng.ClusterRunInfo()
+    sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=4.5, min_pts=10, rate=0.01, seed=2), info)
+    g = info.gpu
+    assert g["filter_bits"] == 8
+    assert g["gather_bytes"] < 0.6 * g["gather_pairs"] * (d + 4)
+
+
 # ---- fp64 input (the reference's Dataset type) -----------------------------
 def _ref_or_skip():
     import os

@@ -9,7 +9,8 @@
 // takes columns q, q+G, ...; V = ceil(W/G)), UN independent rows in flight per
 // group per iteration.  Row indices are a hash of (group, iteration, k) -- no
 // dependency chain -- and the loaded values feed one running sum so nothing is
-// dead code.  Every case is swept over UN and resident blocks per SM and the
+// dead code.  A case may read only the first R chunks of each row (the
+// 8-bit gather's head: k_gather_q8s reads 256 B of every 800-B row).  Every case is swept over UN and resident blocks per SM and the
 // best rate is reported: an upper bound for a kernel that also has to do
 // per-pair work, not an estimate of one.
 #include <cuda_runtime.h>
@@ -38,7 +39,7 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 
 template <int G, int V, int UN>
 __global__ void __launch_bounds__(256) k_lean(const float4* __restrict__ tab, uint64_t rows,
-                                              uint32_t W, uint32_t iters, float* sink) {
+                                              uint32_t W, uint32_t R, uint32_t iters, float* sink) {
     const int lane = threadIdx.x & 31, q = lane % G;
     const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) / G;
     float acc = 0.f;
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(256) k_lean(const float4* __restrict__ tab, ui
             const float4* row = tab + r * W + q;
 #pragma unroll
             for (int c = 0; c < V; ++c)
-                v[k][c] = (q + G * c < (int)W) ? __ldg(row + G * c) : make_float4(0, 0, 0, 0);
+                v[k][c] = (q + G * c < (int)R) ? __ldg(row + G * c) : make_float4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int k = 0; k < UN; ++k)
@@ -85,20 +86,23 @@ struct Case {
     const char* name;
     size_t table_bytes;
     uint32_t row_bytes;  // stride in the padded device layout
+    uint32_t read_bytes = 0;  // bytes read from the start of each row (0: all)
 };
 
 template <int G, int V, int UN>
 double run(const Case& c, const float4* tab, float* sink, int sms, int bpsm) {
     const uint32_t W = c.row_bytes / 16;
+    const uint32_t rb = c.read_bytes ? c.read_bytes : c.row_bytes, R = rb / 16;
     const uint64_t rows = c.table_bytes / c.row_bytes;
     const int blocks = sms * bpsm;
     const double groups = (double)blocks * 256 / G;
     // ~2 GB of rows per launch, at least 4 iterations
-    uint32_t iters = (uint32_t)(2e9 / (groups * UN * c.row_bytes));
+    uint32_t iters = (uint32_t)(2e9 / (groups * UN * rb));
     if (iters < 4) iters = 4;
-    const float ms = time_ms([&] { k_lean<G, V, UN><<<blocks, 256>>>(tab, rows, W, iters, sink); });
+    const float ms =
+        time_ms([&] { k_lean<G, V, UN><<<blocks, 256>>>(tab, rows, W, R, iters, sink); });
     const double nrows = groups * iters * UN;
-    return nrows * c.row_bytes / (ms * 1e-3) / 1e9;  // GB/s of whole rows
+    return nrows * rb / (ms * 1e-3) / 1e9;  // GB/s of the bytes read
 }
 
 template <int G, int V>
@@ -113,13 +117,16 @@ void sweep(const Case& c, const float4* tab, float* sink, int sms) {
         if (r2 > best) best = r2, bu = 4, bb = bpsm;
         if (r3 > best) best = r3, bu = 8, bb = bpsm;
     }
-    printf("{\"bench\": \"ceiling_%s\", \"row_bytes\": %u, \"table_MB\": %.1f, \"GB_per_s\": %.1f, "
-           "\"rows_per_s\": %.4g, \"best_rows_in_flight_per_group\": %d, \"best_blocks_per_sm\": %d}\n",
-           c.name, c.row_bytes, c.table_bytes / 1048576.0, best, best * 1e9 / c.row_bytes, bu, bb);
+    const uint32_t rb = c.read_bytes ? c.read_bytes : c.row_bytes;
+    printf("{\"bench\": \"ceiling_%s\", \"row_bytes\": %u, \"read_bytes\": %u, \"table_MB\": %.1f, "
+           "\"GB_per_s\": %.1f, \"rows_per_s\": %.4g, \"best_rows_in_flight_per_group\": %d, "
+           "\"best_blocks_per_sm\": %d}\n",
+           c.name, c.row_bytes, rb, c.table_bytes / 1048576.0, best, best * 1e9 / rb, bu, bb);
     fflush(stdout);
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const bool only_new = argc > 1;  // any argument: just the head-segment case
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const size_t max_bytes = 2560ull << 20;
@@ -137,12 +144,16 @@ int main() {
     const Case c2l2{"cfg2_row3136B_55MB_slice", 55ull << 20, 3136};
     const Case c2hbm{"cfg2_row3136B_220MB_full", 220ull << 20, 3136};
     const Case c2q8{"cfg2_q8_row800B_56MB", 56ull << 20, 800};
-    sweep<1, 1>(c1, tab, sink, sms);
-    sweep<1, 1>(c4, tab, sink, sms);
-    sweep<4, 1>(c3, tab, sink, sms);
-    sweep<8, 1>(c5, tab, sink, sms);
-    sweep<32, 7>(c2l2, tab, sink, sms);
-    sweep<32, 7>(c2hbm, tab, sink, sms);
-    sweep<32, 2>(c2q8, tab, sink, sms);
+    if (!only_new) {
+        sweep<1, 1>(c1, tab, sink, sms);
+        sweep<1, 1>(c4, tab, sink, sms);
+        sweep<4, 1>(c3, tab, sink, sms);
+        sweep<8, 1>(c5, tab, sink, sms);
+        sweep<32, 7>(c2l2, tab, sink, sms);
+        sweep<32, 7>(c2hbm, tab, sink, sms);
+        sweep<32, 2>(c2q8, tab, sink, sms);
+    }
+    const Case c2q8h{"cfg2_q8_head256B_of_row800B_56MB", 56ull << 20, 800, 256};
+    sweep<16, 1>(c2q8h, tab, sink, sms);
     return 0;
 }
