@@ -456,8 +456,14 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
 
     // ---- host upload in row chunks (chunk k = L2 phase k when phased) ----
     // (other metrics: one chunk -- the cosine row norms need every row first)
-    const uint32_t chunks =
+    // With the 8-bit filter (its table is L2-resident whole) the chunk count only
+    // sets the triangle's granularity: finer chunks start the gather sooner and
+    // leave less of it behind the last chunk (SNGB_Q8_CHUNKS, default 8).
+    uint32_t chunks =
         h_src && metric == kMetricEuclid ? std::min<uint32_t>(phases, DevCtx::kMaxChunks) : 1;
+    if (h_src && q8_try && n * d * 4ull >= (8ull << 20))
+        chunks = (uint32_t)std::min<uint64_t>(
+            std::max<uint64_t>(env_u64("SNGB_Q8_CHUNKS", 8), 1), DevCtx::kMaxChunks);
     auto chunk_lo = [&](uint32_t k) { return n * k / chunks; };
     // issued after the sampler launch: a pageable source blocks the host while
     // it is staged, and the sampler should already be running by then

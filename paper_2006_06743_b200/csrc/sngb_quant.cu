@@ -248,13 +248,14 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8(const GatherArgs a, const 
 // pair's head (kHead chunks, the norm chunk first), UA pairs per half-warp step;
 // pairs whose head sum already exceeds reject_min are rejected, the others are
 // queued with Q2h + Nta.  Phase B: the full warp finishes UB queued pairs per
-// step over the tail chunks plus the norm chunk (for Ntb = N - Nhead).  The
-// queue holds one query row's survivors; it drains in whole steps after every
-// 32-draw chunk and completely at the end of the row.
+// step over the tail chunks plus the norm chunk (for Ntb = N - Nhead).  Both
+// lists hold one query row's pairs and run in whole steps as they fill (live
+// partners accumulate across 32-draw chunks: a launch restricted to a partner
+// slice finds few per chunk), the remainders at the end of the row.
 template <int VT, int UA, int UB>
 __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const Q8Args q8) {
     __shared__ unsigned long long s_stage[kWarpsPerBlock][kStage];
-    __shared__ uint32_t s_list[kWarpsPerBlock][32];
+    __shared__ uint32_t s_list[kWarpsPerBlock][64];
     __shared__ uint32_t s_qp[kWarpsPerBlock][64];
     __shared__ int s_qh[kWarpsPerBlock][64];
     constexpr int SPANA = 16 / UA, SPANB = 32 / UB;
@@ -304,8 +305,9 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
 #pragma unroll
                 for (int v = 0; v < VT; ++v) {
                     const uint32_t sl = lane + 32 * v;
-                    rows[uu][v] = sl <= T ? __ldg(Q + (uint64_t)pv * RW + (sl < T ? kHead + sl : 0))
-                                          : make_uint4(0, 0, 0, 0);
+                    rows[uu][v] = sl <= T && e < qend
+                                      ? __ldg(Q + (uint64_t)pv * RW + (sl < T ? kHead + sl : 0))
+                                      : make_uint4(0, 0, 0, 0);
                 }
             }
             __syncwarp();  // scheduling fence: all UB*VT loads in flight together
@@ -346,6 +348,62 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
             stage.push(acc, edge_key(u, pm, a.sink.nb), a.sink, lane);
         };
 
+        // phase A over list[0, nA), nA <= 2*UA: heads, survivors appended to the queue
+        auto head_step = [&](uint32_t nA) {
+            uint4 rows[UA];
+#pragma unroll
+            for (int k = 0; k < UA; ++k) {
+                const uint32_t j = (lane >> 4) * UA + k;
+                rows[k] = j < nA ? __ldg(Q + (uint64_t)list[j] * RW + hc) : make_uint4(0, 0, 0, 0);
+            }
+            __syncwarp();
+            int ps[UA];
+#pragma unroll
+            for (int k = 0; k < UA; ++k)
+                ps[k] = (hc == 0 ? (int)rows[k].x : 0) - 2 * (int)dot16(qh, rows[k], 0u);
+#pragma unroll
+            for (int o = 8, mm = UA; mm > 1; o >>= 1, mm >>= 1) {
+                const bool hi = (lane & o) != 0;
+#pragma unroll
+                for (int k = 0; k < mm / 2; ++k) {
+                    const int mine = hi ? ps[k + mm / 2] : ps[k];
+                    const int other = hi ? ps[k] : ps[k + mm / 2];
+                    ps[k] = mine + __shfl_xor_sync(kFull, other, o);
+                }
+            }
+#pragma unroll
+            for (int o = SPANA / 2; o > 0; o >>= 1) ps[0] += __shfl_xor_sync(kFull, ps[0], o);
+            const uint32_t pj = lane / SPANA;
+            const bool okm = (lane % SPANA) == 0 && pj < nA;
+            const int q2h = (int)nha + ps[0];
+            const bool keep = okm && q2h <= q8.reject_min;  // else Q2 >= Q2h > B: reject
+            gpairs += okm ? 1u : 0u;
+            const unsigned km = __ballot_sync(kFull, keep);
+            if (keep) {
+                const uint32_t slot = qn + __popc(km & lanemask_lt());
+                qp[slot] = list[pj];
+                qh2[slot] = q2h + nta;
+            }
+            qn += __popc(km);
+            __syncwarp();
+        };
+        // phase B in whole steps; the remainder (< UB) moves to the front
+        auto drain = [&]() {
+            if (qn < (uint32_t)UB) return;
+            uint32_t e0 = 0;
+#pragma unroll 1
+            for (; e0 + UB <= qn; e0 += UB) tail_step(e0, qn);
+            const uint32_t rem = qn - e0;
+            uint32_t mp = 0;
+            int mh = 0;
+            if ((uint32_t)lane < rem) mp = qp[e0 + lane], mh = qh2[e0 + lane];
+            __syncwarp();
+            if ((uint32_t)lane < rem) qp[lane] = mp, qh2[lane] = mh;
+            qn = rem;
+            __syncwarp();
+        };
+
+        uint32_t nl = 0;  // live partners waiting for phase A (warp-uniform)
         uint32_t limit = a.draws;
         uint64_t z = vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
         for (uint32_t i0 = 0; i0 < limit; i0 += 32, z += 32ull * kGamma) {
@@ -362,65 +420,22 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
             if (fm) limit = i0 + __ffs(fm) - 1;  // irregular vertex: cut here
             const bool live = i < limit && p >= plo && p < phi;
             const unsigned m = __ballot_sync(kFull, live);
-            if (live) list[__popc(m & lanemask_lt())] = p;
-            const uint32_t nlive = __popc(m);
+            if (live) list[nl + __popc(m & lanemask_lt())] = p;
+            nl += __popc(m);
             __syncwarp();
-            // phase A: heads, 2*UA pairs per step
-#pragma unroll 1
-            for (uint32_t j0 = 0; j0 < nlive; j0 += 2 * UA) {
-                uint4 rows[UA];
-#pragma unroll
-                for (int k = 0; k < UA; ++k) {
-                    const uint32_t j = j0 + (lane >> 4) * UA + k;
-                    const uint32_t pv = list[j < nlive ? j : j0];
-                    rows[k] = __ldg(Q + (uint64_t)pv * RW + hc);
-                }
+            if (nl >= 2 * UA) {
+                head_step(2 * UA);
+                const uint32_t rem = nl - 2 * UA;  // < 32: move them to the front
+                const uint32_t mp = (uint32_t)lane < rem ? list[2 * UA + lane] : 0u;
                 __syncwarp();
-                int ps[UA];
-#pragma unroll
-                for (int k = 0; k < UA; ++k)
-                    ps[k] = (hc == 0 ? (int)rows[k].x : 0) - 2 * (int)dot16(qh, rows[k], 0u);
-#pragma unroll
-                for (int o = 8, mm = UA; mm > 1; o >>= 1, mm >>= 1) {
-                    const bool hi = (lane & o) != 0;
-#pragma unroll
-                    for (int k = 0; k < mm / 2; ++k) {
-                        const int mine = hi ? ps[k + mm / 2] : ps[k];
-                        const int other = hi ? ps[k] : ps[k + mm / 2];
-                        ps[k] = mine + __shfl_xor_sync(kFull, other, o);
-                    }
-                }
-#pragma unroll
-                for (int o = SPANA / 2; o > 0; o >>= 1) ps[0] += __shfl_xor_sync(kFull, ps[0], o);
-                const uint32_t pj = j0 + lane / SPANA;
-                const bool okm = (lane % SPANA) == 0 && pj < nlive;
-                const int q2h = (int)nha + ps[0];
-                const bool keep = okm && q2h <= q8.reject_min;  // else Q2 >= Q2h > B: reject
-                gpairs += okm ? 1u : 0u;
-                const unsigned km = __ballot_sync(kFull, keep);
-                if (keep) {
-                    const uint32_t slot = qn + __popc(km & lanemask_lt());
-                    qp[slot] = list[pj];
-                    qh2[slot] = q2h + nta;
-                }
-                qn += __popc(km);
-            }
-            __syncwarp();
-            // phase B: whole steps now, the remainder waits for more survivors
-            if (qn >= (uint32_t)UB) {
-                uint32_t e0 = 0;
-#pragma unroll 1
-                for (; e0 + UB <= qn; e0 += UB) tail_step(e0, qn);
-                const uint32_t rem = qn - e0;
-                uint32_t mp = 0;
-                int mh = 0;
-                if ((uint32_t)lane < rem) mp = qp[e0 + lane], mh = qh2[e0 + lane];
+                if ((uint32_t)lane < rem) list[lane] = mp;
+                nl = rem;
                 __syncwarp();
-                if ((uint32_t)lane < rem) qp[lane] = mp, qh2[lane] = mh;
-                qn = rem;
             }
-            __syncwarp();
+            drain();
         }
+        if (nl) head_step(nl);
+        drain();
         if (qn) tail_step(0, qn);
         __syncwarp();
     }
