@@ -258,7 +258,8 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
     __shared__ uint32_t s_list[kWarpsPerBlock][64];
     __shared__ uint32_t s_qp[kWarpsPerBlock][64];
     __shared__ int s_qh[kWarpsPerBlock][64];
-    constexpr int SPANA = 16 / UA, SPANB = 32 / UB;
+    static_assert(UA == 16, "phase A leaves one pair per lane");
+    constexpr int SPANB = 32 / UB;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int hc = lane & 15;  // head chunk of this lane
     const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
@@ -305,9 +306,8 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
 #pragma unroll
                 for (int v = 0; v < VT; ++v) {
                     const uint32_t sl = lane + 32 * v;
-                    rows[uu][v] = sl <= T && e < qend
-                                      ? __ldg(Q + (uint64_t)pv * RW + (sl < T ? kHead + sl : 0))
-                                      : make_uint4(0, 0, 0, 0);
+                    // slots past T re-read the norm chunk: the query is zero there
+                    rows[uu][v] = __ldg(Q + (uint64_t)pv * RW + (sl < T ? kHead + sl : 0));
                 }
             }
             __syncwarp();  // scheduling fence: all UB*VT loads in flight together
@@ -352,9 +352,9 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
         auto head_step = [&](uint32_t nA) {
             uint4 rows[UA];
 #pragma unroll
-            for (int k = 0; k < UA; ++k) {
+            for (int k = 0; k < UA; ++k) {  // pairs past nA re-read pair 0's head (masked below)
                 const uint32_t j = (lane >> 4) * UA + k;
-                rows[k] = j < nA ? __ldg(Q + (uint64_t)list[j] * RW + hc) : make_uint4(0, 0, 0, 0);
+                rows[k] = __ldg(Q + (uint64_t)list[j < nA ? j : 0] * RW + hc);
             }
             __syncwarp();
             int ps[UA];
@@ -371,10 +371,8 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
                     ps[k] = mine + __shfl_xor_sync(kFull, other, o);
                 }
             }
-#pragma unroll
-            for (int o = SPANA / 2; o > 0; o >>= 1) ps[0] += __shfl_xor_sync(kFull, ps[0], o);
-            const uint32_t pj = lane / SPANA;
-            const bool okm = (lane % SPANA) == 0 && pj < nA;
+            const uint32_t pj = lane;  // pair of this lane
+            const bool okm = pj < nA;
             const int q2h = (int)nha + ps[0];
             const bool keep = okm && q2h <= q8.reject_min;  // else Q2 >= Q2h > B: reject
             gpairs += okm ? 1u : 0u;
