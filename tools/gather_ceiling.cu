@@ -126,7 +126,9 @@ void sweep(const Case& c, const float4* tab, float* sink, int sms) {
 }
 
 int main(int argc, char** argv) {
-    const bool only_new = argc > 1;  // any argument: just the head-segment case
+    // any argument: just the newest cases ("q5": the cfg5 reduced-precision tables)
+    const bool only_new = argc > 1;
+    const bool q5 = argc > 1 && argv[1][0] == 'q';
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const size_t max_bytes = 2560ull << 20;
@@ -152,6 +154,17 @@ int main(int argc, char** argv) {
         sweep<32, 7>(c2l2, tab, sink, sms);
         sweep<32, 7>(c2hbm, tab, sink, sms);
         sweep<32, 2>(c2q8, tab, sink, sms);
+    }
+    if (q5) {
+        // cfg5 (20 M rows, d = 32) as 8-bit (32-B rows, 640 MB), 16-bit (64 B, 1280 MB)
+        // and 4-bit (16 B, 320 MB) tables: random rows from HBM at sector granularity
+        const Case c5q8{"cfg5_q8_row32B_640MB", 640ull << 20, 32};
+        const Case c5q16{"cfg5_q16_row64B_1280MB", 1280ull << 20, 64};
+        const Case c5q4{"cfg5_q4_row16B_320MB", 320ull << 20, 16};
+        sweep<1, 1>(c5q4, tab, sink, sms);
+        sweep<2, 1>(c5q8, tab, sink, sms);
+        sweep<4, 1>(c5q16, tab, sink, sms);
+        return 0;
     }
     const Case c2q8h{"cfg2_q8_head256B_of_row800B_56MB", 56ull << 20, 800, 256};
     sweep<16, 1>(c2q8h, tab, sink, sms);
