@@ -98,6 +98,21 @@ def load_gather_ceiling(d: int, n: int, row: int | None = None, read: int | None
     return best["bench"], best["rows_per_s"]
 
 
+def load_head_ceiling(n: int):
+    """Measured random 4-byte-row gather (the head table, n x 4 bytes) closest in
+    table size: (case name, rows/s) or (None, None)."""
+    path = os.path.join(ROOT, "profiles", "r01_gather_ceilings.jsonl")
+    try:
+        cases = [json.loads(ln) for ln in open(path) if ln.strip().startswith("{")]
+    except Exception:
+        return None, None
+    same = [c for c in cases if c["bench"].startswith("ceiling_head4B")]
+    if not same:
+        return None, None
+    best = min(same, key=lambda c: abs(math.log(c["table_MB"] * 2**20 / max(4 * n, 1))))
+    return best["bench"], best["rows_per_s"]
+
+
 def load_traffic(workload: str):
     """dram bytes per gather launch from the committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -374,21 +389,25 @@ def main():
     g_ms = statistics.mean(gather_ms) if gather_ms else 0.0
     achieved = gather_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else None
     q8 = filter_bits == 8
+    head = filter_bits == 16  # sngb_head.cu: 4-byte head for every pair, fp32 row for survivors
     q8_split = q8 and (d + 15) // 16 + 1 >= Q8_SPLIT_MIN_RW  # head/tail gather (k_gather_q8s)
     bpp = gather_bytes / gather_pairs if gather_pairs else 4 * d  # algorithmic bytes per pair
-    kname = ("k_gather_q8s" if q8_split else "k_gather_q8") if q8 else "k_gather"
+    kname = ("k_gather_q8s" if q8_split else "k_gather_q8") if q8 else (
+        "k_gather_head" if head else "k_gather")
     roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": load_traffic(w.name + ("_q8" if q8 else "")),
+                "traffic": load_traffic(w.name + ("_q8" if q8 else ("_head" if head else ""))),
                 "algorithmic_bytes_per_launch": gather_bytes,
                 "bytes_per_pair": bpp, "pairs_per_launch": gather_pairs,
                 "filter": ("8-bit exact filter: u8 rows + norm, DP4A integer distances, "
                            "integer accept/reject thresholds, fp64 recheck in the band"
                            + ("; exact early reject on the 240-value head, survivors read "
                               "the tail" if q8_split else ""))
-                if q8 else "fp32 rows, fp32 guard band, fp64 recheck in the band",
+                if q8 else ("exact reject on a 4-byte head (two 16-bit coordinates, L2-resident); "
+                            "survivors: fp32 rows, fp32 guard band, fp64 recheck in the band"
+                            if head else "fp32 rows, fp32 guard band, fp64 recheck in the band"),
                 "kernel_ms": g_ms,
                 "kernel_share_of_step": (g_ms / ms_per_step) if ms_per_step else None}
     # The gather's real ceiling is the memory level the partner rows come from:
@@ -414,9 +433,23 @@ def main():
             case = f"{hcase} + {case}"
         else:
             l2_peak = None
+    if head and gather_pairs:
+        # every pair reads its 4-byte head (L2), a fraction f its fp32 row (L2 or
+        # HBM by table size): the ceiling is the time-weighted mix of the two
+        # measured gathers; for an HBM-resident fp32 table the survivors' rows
+        # come at the measured random-row rate of that table, not the copy peak
+        hcase, heads_per_s = load_head_ceiling(n)
+        rcase, frows_per_s = load_gather_ceiling(d, n)
+        f = max(0.0, (bpp - 4) / (4 * d))
+        roofline["tail_fraction"] = f
+        if heads_per_s and frows_per_s:
+            l2_peak = bpp / (1.0 / heads_per_s + f / frows_per_s) / 1e9
+            case = f"{hcase} + {rcase}"
+            resident = True
     eff = l2_peak if resident else peak
     roofline.update({
-        "effective_bound": "l2 (random rows)" if resident else "hbm",
+        "effective_bound": ("l2 heads + survivor rows" if head else "l2 (random rows)")
+        if resident else "hbm",
         "effective_peak": eff,
         "effective_peak_source": (f"{case} in profiles/r01_gather_ceilings.jsonl "
                                   "(tools/gather_ceiling.cu), in algorithmic bytes")
@@ -437,7 +470,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8" if q8 else "f32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8" if q8 else ("u16+f32" if head else "f32"),
             "data": "synthetic (seeded generator, BASELINE.json shape)",
             "config": {"workload": w.name, "n": n, "d": d, "eps": w.eps, "rate": w.rate,
                        "min_pts": w.min_pts, "seed": w.seed, "draws": w.draws, "pairs": pairs,

@@ -23,7 +23,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libsngb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["sngb_api.cu", "sngb_kernels.cu", "sngb_quant.cu", "sngb_metric.cu", "sngb_sampler.cu",
+SOURCES = ["sngb_api.cu", "sngb_kernels.cu", "sngb_quant.cu", "sngb_metric.cu", "sngb_head.cu", "sngb_sampler.cu",
            "sngb_cluster.cu"]
 HEADERS = ["sngb_internal.cuh", "sngb_rng.cuh", "sngb_device.cuh", "sngb_epstest.cuh",
            "sngb_floyd_bitmap.cuh", "sngb_floyd_bloom.cuh"]

@@ -344,6 +344,7 @@ struct GraphResult {
     bool exhaustive = false;
     uint64_t raw = 0;
     bool q8 = false;  // the gather ran the 8-bit filter
+    bool head = false;  // the gather ran the 16-bit head filter (sngb_head.cu)
 };
 
 // Prepare points and run the graph build for rows [rb, re).  Leaves sorted
@@ -373,6 +374,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     const float* pts = pad ? c.pts.as<float>() : d_pts;
     cudaStream_t gs = s;  // the gather's stream (c.hi under SNGB_PRIO)
     bool q8_try = false;  // wide rows: min/max for the 8-bit filter (sngb_quant.cu)
+    bool head_try = false;  // narrow rows beyond L2: the head filter (sngb_head.cu)
     auto prepare_rows = [&](uint64_t lo, uint64_t hi) {
         if (hi <= lo) return;
         if (f64)
@@ -380,7 +382,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                                          hi - lo, d, stride, dc, gs));
         else
             CK(launch_prepare_points(d_pts + lo * d, pad ? c.pts.as<float>() + lo * stride : nullptr,
-                                     hi - lo, d, stride, dc, q8_try, gs));
+                                     hi - lo, d, stride, dc, q8_try || head_try, gs));
     };
     // after the last prepare: the min/max to the host, waited for only when the
     // 8-bit plan is made (the sampler is already running by then)
@@ -397,6 +399,17 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     const uint64_t q8_mode = env_u64("SNGB_Q8", 1);
     // the 8-bit gathers hold a row in <= 3 chunks per lane: d <= 16 * (3 * 32 - 1)
     q8_try = metric == kMetricEuclid && !exhaustive && d >= 128 && d <= 1520 && q8_mode != 0;
+    // SNGB_HEAD: 0 off, 1 auto, 2 force (tests).  Auto when the fp32 table does
+    // not fit half the L2 and the 4-byte head table fits 3/4 of it (cfg5); fp32
+    // input only (fp64 rows would need the rounding bound in the head too).
+    const uint64_t head_mode = env_u64("SNGB_HEAD", 1);
+    {
+        const uint64_t tab = n * (uint64_t)((d + 3) & ~3u) * 4ull;
+        const bool fit = n * 4ull <= c.l2_bytes * 3 / 4;
+        head_try = metric == kMetricEuclid && !exhaustive && !q8_try && d_pts64 == nullptr &&
+                   d >= 3 && d <= 1024 && n >= 2 &&
+                   (head_mode == 2 || (head_mode == 1 && d >= 8 && fit && 2 * tab > c.l2_bytes));
+    }
     const uint64_t rows = re - rb;
     const uint32_t nb = bits_for(n - 1);
     const uint64_t base = (n - 1) - draws;
@@ -480,11 +493,12 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     };
     if (!h_src && !f64) {
         prepare_rows(0, n);
-        if (q8_try) minmax_to_host();
+        if (q8_try || head_try) minmax_to_host();
     }
     tm.mark(E_PREPARED);
-    bool q8_on = false;
+    bool q8_on = false, head_on = false;
     Q8Plan q8p{};
+    HeadPlan hp{};
     uint32_t gphases = phases;  // partner slices of the gather (8-bit rows: their own count)
     // host upload state: leading chunks prepared / quantised on gs.  With the
     // 8-bit filter the plan is made from chunk 0 (q8_pipe) so the gather can
@@ -557,8 +571,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                                    c.q8.as<uint4>() + r0 * (q8p.args.nd + 1), gs, c.num_sms,
                                    f64 ? d_pts64 + r0 * d : nullptr));
         };
-        if (q8_try && (attempt == 0 || q8_replan)) {
-            const bool pipe = h_src && attempt == 0 && chunks > 1;
+        if ((q8_try || head_try) && (attempt == 0 || q8_replan)) {
+            const bool pipe = q8_try && h_src && attempt == 0 && chunks > 1;
             if (h_src && attempt == 0) {
                 const uint32_t upto = pipe ? 1 : chunks;
                 for (uint32_t k = prepared; k < upto; ++k) {
@@ -574,12 +588,23 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                                   : (double)ordered_value(~(uint32_t)c.h_counters[C_QMIN]);
             const double hi = f64 ? ordered_value64(c.h_counters[C_QMAX])
                                   : (double)ordered_value((uint32_t)c.h_counters[C_QMAX]);
-            const bool useful = q8_plan(lo, hi, d, tp.eps2, q8p);
-            q8_on = !c.h_counters[C_NONFINITE] && (useful || (q8_mode == 2 && q8p.s > 0));
+            if (head_try) {
+                const bool useful = head_plan(lo, hi, d, tp.eps2, hp);
+                head_on = !c.h_counters[C_NONFINITE] && (useful || (head_mode == 2 && hp.s > 0));
+                gr.head = head_on;
+                if (head_on) {
+                    c.q8.ensure(n * 4ull);  // the head table (exclusive with the 8-bit rows)
+                    hp.args.head = c.q8.as<uint32_t>();
+                    CK(launch_head_quantize(pts, stride, n, hp, c.q8.as<uint32_t>(), gs, c.num_sms));
+                    gphases = 1;  // the fp32 rows are read by survivors only
+                }
+            }
+            const bool useful = q8_try && q8_plan(lo, hi, d, tp.eps2, q8p);
+            q8_on = q8_try && !c.h_counters[C_NONFINITE] && (useful || (q8_mode == 2 && q8p.s > 0));
             gr.q8 = q8_on;
             q8_pipe = q8_on && pipe;
             q8_replan = false;
-            gphases = phases;
+            if (!head_on) gphases = phases;
             if (q8_on) {
                 const uint32_t nd = (d + 15) / 16;
                 c.q8.ensure(n * (nd + 1) * 16ull);
@@ -644,6 +669,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                     1, std::min<uint64_t>(32, (ga.row_end - ga.row_begin) / (warps * 16)));
             }
             if (q8_on) CK(launch_gather_q8(ga, q8p.args, gs, c.num_sms));
+            else if (head_on) CK(launch_gather_head(ga, hp.args, gs, c.num_sms));
             else if (metric != kMetricEuclid || d > 1024)
                 CK(launch_gather_metric(ga, exhaustive, gs, c.num_sms));
             else CK(launch_gather(ga, exhaustive, gs, c.num_sms));
@@ -786,8 +812,10 @@ void fill_info(sngb_info* info, const unsigned long long* hc, uint64_t n, uint32
     info->fp32_flips = hc[C_FLIPS];
     info->directed_accepts = hc[C_EDGE_CURSOR];
     info->gather_pairs = hc[C_GATHER_PAIRS];
-    info->filter_bits = gr.q8 ? 8 : 32;
-    if (gr.q8 && q8_split((d + 15) / 16))  // every pair reads its head, survivors the rest
+    info->filter_bits = gr.q8 ? 8 : (gr.head ? 16 : 32);
+    if (gr.head)  // every pair reads its 4-byte head, survivors their fp32 row
+        info->gather_bytes = hc[C_GATHER_PAIRS] * 4ull + hc[C_TAIL_PAIRS] * 4ull * d;
+    else if (gr.q8 && q8_split((d + 15) / 16))  // every pair reads its head, survivors the rest
         info->gather_bytes = hc[C_GATHER_PAIRS] * (kHeadVals + 4ull) +
                              hc[C_TAIL_PAIRS] * ((uint64_t)d - kHeadVals + 4);
     else

@@ -95,3 +95,19 @@ def test_full_size_properties(oracle, cfg):
     np.testing.assert_array_equal(keys2, keys)
     np.testing.assert_array_equal(labels2, labels)
 
+
+
+def test_cfg5_head_filter_equals_fp32_filter(monkeypatch):
+    """cfg5 at full size: the auto path (head filter, 16) and the plain fp32
+    gather (SNGB_HEAD=0) give the same edge list, bit for bit."""
+    import torch
+    w = synthetic.CONFIGS[5]
+    x = torch.from_numpy(synthetic.generate(5)).cuda()
+    k_auto, gi = sng.sampled_edges_device(x, w.eps, w.rate, w.seed)
+    torch.cuda.synchronize()
+    assert gi.filter_bits == 16
+    monkeypatch.setenv("SNGB_HEAD", "0")
+    k_fp32, gi0 = sng.sampled_edges_device(x, w.eps, w.rate, w.seed)
+    torch.cuda.synchronize()
+    assert gi0.filter_bits == 32
+    assert torch.equal(k_auto, k_fp32)

@@ -340,6 +340,105 @@ def test_q8_early_reject_reads_fewer_bytes():
     assert g["gather_bytes"] < 0.6 * g["gather_pairs"] * (d + 4)
 
 
+# ---- the head filter for narrow rows beyond L2 (sngb_head.cu) --------------
+def _head_case(n, d, seed, k=12, spread=0.05, box=20.0):
+    rng = np.random.default_rng(seed)
+    centers = (rng.random((k, d)) * box).astype(np.float32)
+    pts = centers[rng.integers(0, k, n)] + rng.normal(0, spread, (n, d)).astype(np.float32)
+    return np.ascontiguousarray(pts, np.float32)
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+@pytest.mark.parametrize("n,d,rate,seed,q", [(3000, 3, 0.05, 31, 0.3), (2500, 5, 0.06, 32, 0.5),
+                                             (3000, 8, 0.05, 33, 0.2), (2800, 16, 0.05, 34, 0.6),
+                                             (3000, 32, 0.04, 35, 0.3), (2000, 33, 0.06, 36, 0.9),
+                                             (2200, 64, 0.05, 37, 0.4), (1800, 100, 0.06, 38, 0.5),
+                                             (1500, 200, 0.08, 39, 0.3)])
+def test_head_filter_matches_oracle(oracle, monkeypatch, mode, n, d, rate, seed, q):
+    """SNGB_HEAD=2 forces the head filter (exact reject on two 16-bit
+    coordinates, fp32 test for survivors) on every row width it serves; =0 is
+    the plain fp32 gather.  eps at low and high within-cluster quantiles (few /
+    many survivors): both identical to the oracle."""
+    monkeypatch.setenv("SNGB_HEAD", mode)
+    monkeypatch.setenv("SNGB_Q8", "0")
+    pts = _head_case(n, d, seed)
+    i = np.arange(0, n - 1, 5)
+    dist = np.sqrt(((pts[i] - pts[i + 1]) ** 2).sum(1))
+    dist = dist[dist < 1.0]  # within-cluster pairs
+    eps = float(np.quantile(dist, q))
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=eps, min_pts=3, rate=rate, seed=seed),
+                       info)
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, 3, rate, seed)
+    _assert_same(c, info, labels, roles, oinfo)
+    assert info.gpu["filter_bits"] == (16 if mode == "2" else 32)
+    if mode == "2":  # survivors read their row: the gather moves fewer bytes than fp32
+        g = info.gpu
+        assert g["gather_bytes"] < g["gather_pairs"] * 4 * d
+
+
+def test_head_filter_band_stress_exact(oracle, monkeypatch):
+    """One tight blob and eps at the median pair distance: the head rejects
+    almost nothing, most pairs take the fp32 test and many its band -- exact."""
+    monkeypatch.setenv("SNGB_HEAD", "2")
+    rng = np.random.default_rng(41)
+    n, d = 3000, 24
+    pts = (rng.random(d, dtype=np.float32) + rng.normal(0, 0.05, (n, d))).astype(np.float32)
+    i = np.arange(0, n - 1, 3)
+    eps = float(np.median(np.sqrt(((pts[i] - pts[i + 1]) ** 2).sum(1))))
+    st = sng.BuildStats()
+    g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.1, seed=3, stats=st)
+    keys, evals = oracle.sampled_edges(pts, eps, 0.1, 3)
+    np.testing.assert_array_equal(g.keys, keys)
+    assert st.distance_evals == evals
+
+
+def test_head_filter_outlier_and_irregular_exact(oracle, monkeypatch):
+    """A far outlier stretches the 16-bit scale (coarse head); Lemire-reject
+    replays (test hook) through the head gather -- the edge set is unchanged."""
+    pts = _head_case(4000, 32, 42)
+    pts[77, 0] = 3e5
+    eps = 0.4
+    keys, _ = oracle.sampled_edges(pts, eps, 0.04, 42)
+    monkeypatch.setenv("SNGB_HEAD", "2")
+    g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.04, seed=42)
+    np.testing.assert_array_equal(g.keys, keys)
+    monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", "5")
+    g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.04, seed=42)
+    np.testing.assert_array_equal(g.keys, keys)
+
+
+def test_head_filter_device_api_and_row_range(oracle, monkeypatch):
+    """Device-resident call and a query-row range (the multi-GPU shard step)."""
+    import torch
+    monkeypatch.setenv("SNGB_HEAD", "2")
+    pts = _head_case(6000, 32, 43)
+    eps, rate, seed = 0.3, 0.03, 43
+    labels, roles, gi = sng.sng_dbscan_device(torch.from_numpy(pts).cuda(), eps, 4, rate, seed)
+    torch.cuda.synchronize()
+    ol, orl, oinfo, _ = oracle.sng_dbscan(pts, eps, 4, rate, seed)
+    np.testing.assert_array_equal(labels.cpu().numpy(), ol)
+    np.testing.assert_array_equal(roles.cpu().numpy(), orl)
+    rb, re = 1000, 4321
+    okeys, _ = oracle.sampled_edges_rows(pts, eps, rate, seed, rb, re)
+    np.testing.assert_array_equal(_host_edges_rows(pts, eps, rate, seed, rb, re), okeys)
+
+
+def test_head_filter_auto_on_cfg5_shape(oracle):
+    """cfg5's row shape (d = 32) with the fp32 table beyond half the L2: auto
+    selects the head filter; labels identical to the oracle."""
+    n = 600_000
+    pts = synthetic.generate(5, n=n)
+    w = synthetic.CONFIGS[5]
+    rate = 60 / n
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=w.eps, min_pts=w.min_pts, rate=rate,
+                                                       seed=w.seed), info)
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, w.eps, w.min_pts, rate, w.seed)
+    _assert_same(c, info, labels, roles, oinfo)
+    assert info.gpu["filter_bits"] == 16
+
+
 # ---- fp64 input (the reference's Dataset type) -----------------------------
 def _ref_or_skip():
     import os

@@ -27,4 +27,5 @@ for _ in range(1 + a.reps):
     labels, roles, gi = sng.sng_dbscan_device(x, w.eps, w.min_pts, rate, w.seed, timing=True)
 torch.cuda.synchronize()
 print({k: v for k, v in gi.as_dict().items() if k.startswith("ms_") or k in
-       ("edges", "cluster_count", "collisions", "kernel_launches", "gather_bytes")})
+       ("edges", "cluster_count", "collisions", "kernel_launches", "gather_bytes",
+                                                    "gather_pairs", "filter_bits", "band_rechecks")})
