@@ -440,7 +440,9 @@ def main():
         # come at the measured random-row rate of that table, not the copy peak
         hcase, heads_per_s = load_head_ceiling(n)
         rcase, frows_per_s = load_gather_ceiling(d, n)
-        f = max(0.0, (bpp - 4) / (4 * d))
+        hb = getattr(info, "head_bytes", 4) or 4
+        roofline["head_bytes"] = hb
+        f = max(0.0, (bpp - hb) / (4 * d))
         roofline["tail_fraction"] = f
         if heads_per_s and frows_per_s:
             l2_peak = bpp / (1.0 / heads_per_s + f / frows_per_s) / 1e9

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SNGB_ABI_VERSION 2
+#define SNGB_ABI_VERSION 3
 
 /* Status codes.  1..6 carry the reference's std::invalid_argument messages. */
 enum {
@@ -97,9 +97,12 @@ typedef struct sngb_info {
     uint64_t library_launches; /* CUB radix-sort / select / scan kernels launched by this call */
     /* ABI 2: the filter the gather ran with -- 32: fp32 rows (gather_bytes = pairs * 4d);
      * 8: the exact 8-bit filter for wide rows (gather_bytes = pairs * (d + 4): the
-     * row's bytes and its norm; band_rechecks counts its exact fp64 re-evaluations) */
+     * row's bytes and its norm; band_rechecks counts its exact fp64 re-evaluations);
+     * ABI 3 -- 16: the head filter for narrow rows (an exact reject on a head of a
+     * few 8/16-bit coordinates per row, head_bytes each; gather_bytes = pairs *
+     * head_bytes + survivors * 4d, survivors taking the fp32 test) */
     uint32_t filter_bits;
-    uint32_t reserved;
+    uint32_t head_bytes;
 } sngb_info;
 
 /* sng::sng_dbscan (clusterer.hpp:42) on HOST buffers: pts[n*d] fp32 row-major,

@@ -61,7 +61,7 @@ class SngbInfo(C.Structure):
         ("ms_cluster", C.c_float), ("ms_download", C.c_float),
         ("gather_pairs", C.c_uint64), ("gather_bytes", C.c_uint64),
         ("kernel_launches", C.c_uint64), ("library_launches", C.c_uint64),
-        ("filter_bits", C.c_uint32), ("reserved", C.c_uint32),
+        ("filter_bits", C.c_uint32), ("head_bytes", C.c_uint32),
     ]
 
     def as_dict(self) -> dict:

@@ -344,7 +344,7 @@ struct GraphResult {
     bool exhaustive = false;
     uint64_t raw = 0;
     bool q8 = false;  // the gather ran the 8-bit filter
-    bool head = false;  // the gather ran the 16-bit head filter (sngb_head.cu)
+    uint32_t head = 0;  // the gather ran the head filter (sngb_head.cu): its bytes per row
 };
 
 // Prepare points and run the graph build for rows [rb, re).  Leaves sorted
@@ -399,16 +399,22 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     const uint64_t q8_mode = env_u64("SNGB_Q8", 1);
     // the 8-bit gathers hold a row in <= 3 chunks per lane: d <= 16 * (3 * 32 - 1)
     q8_try = metric == kMetricEuclid && !exhaustive && d >= 128 && d <= 1520 && q8_mode != 0;
-    // SNGB_HEAD: 0 off, 1 auto, 2 force (tests).  Auto when the fp32 table does
-    // not fit half the L2 and the 4-byte head table fits 3/4 of it (cfg5); fp32
-    // input only (fp64 rows would need the rounding bound in the head too).
+    // SNGB_HEAD: 0 off, 1 auto, 2 force (tests); SNGB_HEAD_KIND picks the format.
+    // Auto for large problems whose head table stays L2-resident (a table read
+    // by every SM keeps about half the L2): 4-byte heads up to 0.4 L2, 2-byte
+    // heads (cfg5) up to twice that many rows.  fp32 input only (fp64 rows would
+    // need their rounding bound in the head too).
     const uint64_t head_mode = env_u64("SNGB_HEAD", 1);
+    int head_kind = -1;
     {
-        const uint64_t tab = n * (uint64_t)((d + 3) & ~3u) * 4ull;
-        const bool fit = n * 4ull <= c.l2_bytes * 3 / 4;
+        const uint64_t budget = c.l2_bytes * 2 / 5;
+        head_kind = n * 4ull <= budget ? kHeadDefault4 : (n * 2ull <= budget ? kHeadU8x2 : -1);
+        const uint64_t forced = env_u64("SNGB_HEAD_KIND", 99);
+        if (forced <= 2) head_kind = (int)forced;
+        if (head_mode == 2 && head_kind < 0) head_kind = kHeadU8x2;
         head_try = metric == kMetricEuclid && !exhaustive && !q8_try && d_pts64 == nullptr &&
-                   d >= 3 && d <= 1024 && n >= 2 &&
-                   (head_mode == 2 || (head_mode == 1 && d >= 8 && fit && 2 * tab > c.l2_bytes));
+                   d >= 3 && d <= 1024 && n >= 2 && head_kind >= 0 &&
+                   (head_mode == 2 || (head_mode == 1 && n >= 65536));
     }
     const uint64_t rows = re - rb;
     const uint32_t nb = bits_for(n - 1);
@@ -589,13 +595,14 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             const double hi = f64 ? ordered_value64(c.h_counters[C_QMAX])
                                   : (double)ordered_value((uint32_t)c.h_counters[C_QMAX]);
             if (head_try) {
-                const bool useful = head_plan(lo, hi, d, tp.eps2, hp);
+                const bool useful = head_plan(lo, hi, d, tp.eps2, head_kind, hp);
                 head_on = !c.h_counters[C_NONFINITE] && (useful || (head_mode == 2 && hp.s > 0));
-                gr.head = head_on;
+                gr.head = head_on ? (head_kind == kHeadU8x2 ? 2u : 4u) : 0u;
                 if (head_on) {
-                    c.q8.ensure(n * 4ull);  // the head table (exclusive with the 8-bit rows)
-                    hp.args.head = c.q8.as<uint32_t>();
-                    CK(launch_head_quantize(pts, stride, n, hp, c.q8.as<uint32_t>(), gs, c.num_sms));
+                    // the head table (exclusive with the 8-bit rows)
+                    c.q8.ensure(n * (head_kind == kHeadU8x2 ? 2ull : 4ull));
+                    hp.args.head = c.q8.p;
+                    CK(launch_head_quantize(pts, stride, n, hp, c.q8.p, gs, c.num_sms));
                     gphases = 1;  // the fp32 rows are read by survivors only
                 }
             }
@@ -813,8 +820,9 @@ void fill_info(sngb_info* info, const unsigned long long* hc, uint64_t n, uint32
     info->directed_accepts = hc[C_EDGE_CURSOR];
     info->gather_pairs = hc[C_GATHER_PAIRS];
     info->filter_bits = gr.q8 ? 8 : (gr.head ? 16 : 32);
-    if (gr.head)  // every pair reads its 4-byte head, survivors their fp32 row
-        info->gather_bytes = hc[C_GATHER_PAIRS] * 4ull + hc[C_TAIL_PAIRS] * 4ull * d;
+    info->head_bytes = gr.head;
+    if (gr.head)  // every pair reads its head, survivors their fp32 row
+        info->gather_bytes = hc[C_GATHER_PAIRS] * gr.head + hc[C_TAIL_PAIRS] * 4ull * d;
     else if (gr.q8 && q8_split((d + 15) / 16))  // every pair reads its head, survivors the rest
         info->gather_bytes = hc[C_GATHER_PAIRS] * (kHeadVals + 4ull) +
                              hc[C_TAIL_PAIRS] * ((uint64_t)d - kHeadVals + 4);

@@ -1,31 +1,39 @@
-// sngb_head.cu -- the head filter for narrow rows that do not stay in L2: an
-// exact early reject on a compact, L2-resident copy of each row's first two
-// coordinates, so most sampled pairs never touch the fp32 table in HBM.
+// sngb_head.cu -- the head filter for narrow rows: an exact early reject on a
+// compact, L2-resident copy of a few coordinates of each row, so most sampled
+// pairs never read their fp32 row.
 //
 // Why.  A random row from HBM costs one DRAM access whether it is 16, 32, 64
 // or 128 bytes wide (measured on B200, tools/gather_ceiling.cu: 6.3e10, 4.9e10,
 // 4.2e10 and 4.2e10 random rows/s), so on a table like cfg5's (20 M x 128 B =
-// 2.56 GB) fewer bytes per row buy nothing -- only a table that fits the 126 MB
-// L2 does.  Two 16-bit coordinates per row is 4 bytes (cfg5: 80 MB).
+// 2.56 GB) fewer bytes per row buy nothing -- only a table that stays in L2
+// does.  L2 keeps a line near the SMs that read it on both dies, so a table
+// read uniformly by all SMs stays resident only up to about half the 126 MB
+// (an 80 MB head table measured a 43 % hit rate).  Three head formats, picked
+// by the host so the table fits: four 8-bit coordinates (4 B), two 16-bit
+// coordinates (4 B), two 8-bit coordinates (2 B; cfg5: 40 MB).  On L2-resident
+// tables the head also saves instructions: one 2-4 byte load and a few integer
+// ops instead of a G-lane row gather and reduction per pair.
 //
-// Quantisation (host plan, head_plan).  s is a power of two >= (max - min)/65534
-// over all values and lo' = floor(min/s)*s, so q = rint((a - lo')/s) fits 16 bits
+// Quantisation (host plan, head_plan).  s is a power of two >= (max - min)/(2^b - 2)
+// over all values and lo' = floor(min/s)*s, so q = rint((a - lo')/s) fits b bits
 // and |a - (lo' + s q)| <= s/2 (1 + 2^-30) (the fp64 evaluation, as in
 // sngb_quant.cu).  For a pair and s' = s(1 + 2^-30), per coordinate
-// |(a_j - b_j) - s(qa_j - qb_j)| <= s', hence over the two head coordinates
-// (triangle inequality)  |a_h - b_h| >= s*sqrt(Q) - s'*sqrt(2),  Q = sum_h dq^2,
+// |(a_j - b_j) - s(qa_j - qb_j)| <= s', hence over the k head coordinates
+// (triangle inequality)  |a_h - b_h| >= s*sqrt(Q) - s'*sqrt(k),  Q = sum_h dq^2,
 // and the full squared distance S >= |a_h - b_h|^2.  So
-//     Q > B = ((sqrt(eps2 (1 + 2^-40)) + s' sqrt(2)) / s)^2   =>   S > eps2 (1 + 2^-40)
+//     Q > B = ((sqrt(eps2 (1 + 2^-40)) + s' sqrt(k)) / s)^2   =>   S > eps2 (1 + 2^-40)
 // and the reference's fp64 sum (within (d+1) 2^-53 S of S, distance.hpp:75-83)
-// exceeds eps2: it rejects.  The kernel evaluates Q in fp32 (dq exact, two
-// roundings), so it compares against B (1 + 2^-20) rounded up.  Pairs the head
-// does not reject take the unchanged fp32 test (guard band, exact fp64 recheck in
-// the band: sngb_epstest.cuh) on their fp32 rows.  Decisions are the reference's
-// whatever the data; only the speed depends on how many pairs the head rejects
-// (cfg5: ~95 %, the pairs from different clusters).
+// exceeds eps2: it rejects.  Q is exact for 8-bit heads (DP4A of |dq|) and fp32
+// with two roundings for 16-bit ones (dq exact), so the kernel compares against
+// B (1 + 2^-20) rounded up.  Pairs the head does not reject take the unchanged
+// fp32 test (guard band, exact fp64 recheck in the band: sngb_epstest.cuh) on
+// their fp32 rows.  Decisions are the reference's whatever the data; only the
+// speed depends on how many pairs the head rejects (cfg5: ~95 %, the pairs from
+// different clusters).
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdint>
 
 #include "sngb_device.cuh"
@@ -35,43 +43,74 @@
 
 namespace sngb {
 
-bool head_plan(double lo, double hi, uint32_t d, double eps2, HeadPlan& p) {
-    if (d < 2) return false;
-    const double need = (hi - lo) / 65534.0 * (1.0 + 1e-12);
+bool head_plan(double lo, double hi, uint32_t d, double eps2, int kind, HeadPlan& p) {
+    const int bits = kind == kHeadU16x2 ? 16 : 8;
+    const uint32_t k = std::min<uint32_t>(d, kind == kHeadU8x4 ? 4u : 2u);
+    if (k < 2) return false;
+    const double need = (hi - lo) / (std::ldexp(1.0, bits) - 2.0) * (1.0 + 1e-12);
     if (!(need > 0.0) || !std::isfinite(need)) return false;
     int e = 0;
     std::frexp(need, &e);  // need = m * 2^e, m in [0.5, 1)
     const double s = std::ldexp(1.0, e);
     p.s = s;
     p.lo = std::floor(lo / s) * s;
+    p.args.kind = kind;
+    p.args.coords = k;
     const double sp = s * (1.0 + std::ldexp(1.0, -30));
     const double e_hi = eps2 * (1.0 + std::ldexp(1.0, -40));
-    const double tb = (std::sqrt(e_hi) + sp * std::sqrt(2.0)) / s;
+    const double tb = (std::sqrt(e_hi) + sp * std::sqrt((double)k)) / s;
     const double b = tb * tb * (1.0 + std::ldexp(1.0, -20));
     p.args.reject = std::nextafter((float)b, INFINITY);
     // useless if the rejection radius covers the data's whole range
-    return std::sqrt(b) * s < 0.5 * (hi - lo) * std::sqrt(2.0);
+    return std::sqrt(b) * s < 0.5 * (hi - lo) * std::sqrt((double)k);
 }
 
 namespace {
 
-// thread per row: the first two values of the padded fp32 row -> two u16
+// thread per row: the first k values of the padded fp32 row -> the head word
+template <int KIND>
 __global__ void k_head_quantize(const float* __restrict__ pts, uint32_t stride, uint64_t n,
-                                double lo, double inv_s, uint32_t* __restrict__ out) {
+                                uint32_t k, double lo, double inv_s, void* __restrict__ out) {
+    constexpr double qmax = KIND == kHeadU16x2 ? 65535.0 : 255.0;
     for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
          r += (uint64_t)gridDim.x * blockDim.x) {
-        const float2 v = __ldg(reinterpret_cast<const float2*>(pts + r * stride));
-        const double x0 = rint(((double)v.x - lo) * inv_s), x1 = rint(((double)v.y - lo) * inv_s);
-        const uint32_t q0 = x0 <= 0.0 ? 0u : (x0 >= 65535.0 ? 65535u : (uint32_t)x0);
-        const uint32_t q1 = x1 <= 0.0 ? 0u : (x1 >= 65535.0 ? 65535u : (uint32_t)x1);
-        out[r] = q0 | (q1 << 16);
+        // stride >= 4 (d >= 3): the first 16 bytes of the row are in the table
+        const float4 v = __ldg(reinterpret_cast<const float4*>(pts + r * stride));
+        const float vs[4] = {v.x, v.y, v.z, v.w};
+        uint32_t w = 0;
+#pragma unroll
+        for (int j = 0; j < (KIND == kHeadU8x4 ? 4 : 2); ++j) {
+            const double x = rint(((double)vs[j] - lo) * inv_s);
+            const uint32_t q = (uint32_t)j >= k ? 0u : (x <= 0.0 ? 0u : (x >= qmax ? (uint32_t)qmax : (uint32_t)x));
+            w |= q << (j * (KIND == kHeadU16x2 ? 16 : 8));
+        }
+        if (KIND == kHeadU8x2) static_cast<uint16_t*>(out)[r] = (uint16_t)w;
+        else static_cast<uint32_t*>(out)[r] = w;
     }
 }
 
+__device__ __forceinline__ F4x2 ldg_row2_ef(const float4* p, uint64_t pol) {
+    F4x2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.b64 {%0, %1}, [%2], %3;" : "=l"(r.lo), "=l"(r.hi) : "l"(p), "l"(pol));
+    return r;
+}
+
+// the head's Q = sum dq^2: exact (integer) for 8-bit heads, fp32 for 16-bit ones
+template <int KIND>
 __device__ __forceinline__ float head_q(uint32_t a, uint32_t b) {
-    const float dx = (float)((int)(a & 0xffffu) - (int)(b & 0xffffu));
-    const float dy = (float)((int)(a >> 16) - (int)(b >> 16));
-    return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+    if constexpr (KIND == kHeadU16x2) {
+        const float dx = (float)((int)(a & 0xffffu) - (int)(b & 0xffffu));
+        const float dy = (float)((int)(a >> 16) - (int)(b >> 16));
+        return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+    } else {
+        const uint32_t ad = __vabsdiffu4(a, b);
+        return (float)__dp4a(ad, ad, 0u);
+    }
+}
+template <int KIND>
+__device__ __forceinline__ uint32_t head_load(const void* h, uint32_t r) {
+    if constexpr (KIND == kHeadU8x2) return __ldg(static_cast<const unsigned short*>(h) + r);
+    else return __ldg(static_cast<const uint32_t*>(h) + r);
 }
 
 // k_gather_head: one warp per query row (dynamic row claiming, as k_gather).
@@ -80,7 +119,7 @@ __device__ __forceinline__ float head_q(uint32_t a, uint32_t b) {
 // head; survivors are queued per warp and, UF per G-lane group at a time, take
 // the fp32 test on their full rows (G lanes x V float4 per row, as the narrow
 // k_gather path: masked pairs and columns past the row end read the query row).
-template <int G, int V, int R>
+template <int KIND, int G, int V, int R>
 __global__ void __launch_bounds__(256, V >= 4 ? 2 : 4) k_gather_head(const GatherArgs a, const HeadArgs h) {
     constexpr int NG = 32 / G;
     constexpr int UF = 2;               // fp32 rows per group per step
@@ -95,11 +134,12 @@ __global__ void __launch_bounds__(256, V >= 4 ? 2 : 4) k_gather_head(const Gathe
     const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
     const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerBlock;
     const float4* __restrict__ P = reinterpret_cast<const float4*>(a.tp.pts);
-    const uint32_t* __restrict__ H = h.head;
+    const void* __restrict__ H = h.head;
     const uint32_t W = a.tp.stride / 4;
     const uint32_t plo = a.part_lo, phi = a.part_hi;
     const float reject = h.reject;
     uint32_t* queue = s_queue[wib];
+    const uint64_t pol = evict_first_policy();  // survivor rows must not evict the heads
 
     WarpStage<kStage> stage{s_stage[wib], 0};
     TestStats st;
@@ -121,7 +161,9 @@ __global__ void __launch_bounds__(256, V >= 4 ? 2 : 4) k_gather_head(const Gathe
             const uint32_t c = q + G * vv;
             qv[vv] = to_x2(ldg_row(P + u * W + (c < W ? c : W - 1)));
         }
-        const uint32_t hq = __ldg(H + u);
+        const uint32_t hq = head_load<KIND>(H, (uint32_t)u);
+        // test hook (test_fire) resolved once per vertex: the draw index it fires at
+        const uint32_t hook = (a.force_mod != 0 && (u % a.force_mod) == 0) ? a.draws / 2 : 0xffffffffu;
         uint32_t qn = 0;  // queued survivors (warp-uniform)
 
         // fp32 test of queue entries [e0, e0 + STEP) of which those < qend are real
@@ -138,7 +180,7 @@ __global__ void __launch_bounds__(256, V >= 4 ? 2 : 4) k_gather_head(const Gathe
                 for (int vv = 0; vv < V; ++vv) {
                     const uint32_t c = q + G * vv;
                     const uint64_t row = (oke[uu] && c < W) ? pe[uu] : u;
-                    rows[uu][vv] = ldg_row2(P + row * W + (c < W ? c : W - 1));
+                    rows[uu][vv] = ldg_row2_ef(P + row * W + (c < W ? c : W - 1), pol);
                 }
             }
             __syncwarp();  // scheduling fence: all UF*V loads in flight together
@@ -159,32 +201,39 @@ __global__ void __launch_bounds__(256, V >= 4 ? 2 : 4) k_gather_head(const Gathe
         uint32_t limit = a.draws;
         uint64_t z = vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
         for (uint32_t i0 = 0; i0 < limit; i0 += 32 * R, z += (uint64_t)(32 * R) * kGamma) {
+            // draws of this step, branch-free (the test hook resolved per vertex;
+            // lanes past the limit compute a throw-away draw and read row u)
             uint32_t pv[R];
-            uint32_t first_fire = 0xffffffffu;
+            unsigned fires = 0;
 #pragma unroll
             for (int k = 0; k < R; ++k) {
                 const uint32_t i = i0 + 32 * k + lane;
+                bool fire;
+                const uint32_t t = lemire32(mix(z + (uint64_t)(32 * k) * kGamma), a.base + i + 1, fire);
                 const bool valid = i < limit;
-                bool fire = false;
-                uint32_t t = 0;
-                if (valid) {
-                    t = lemire32(mix(z + (uint64_t)(32 * k) * kGamma), a.base + i + 1, fire);
-                    fire |= test_fire(a.force_mod, u, i, a.draws);
-                }
-                pv[k] = t + (t >= (uint32_t)u ? 1u : 0u);
-                const unsigned fm = __ballot_sync(kFull, valid && fire);
-                if (fm && first_fire == 0xffffffffu) first_fire = i0 + 32 * k + __ffs(fm) - 1;
+                fires |= ((fire || i == hook) && valid) ? (1u << k) : 0u;
+                const uint32_t p = t + (t >= (uint32_t)u ? 1u : 0u);
+                pv[k] = valid ? p : (uint32_t)u;
             }
-            if (first_fire != 0xffffffffu) limit = first_fire;  // irregular: cut here
+            if (__any_sync(kFull, fires != 0)) {  // rare: irregular vertex, cut at the first fire
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    const unsigned fm = __ballot_sync(kFull, (fires >> k) & 1u);
+                    if (fm) {
+                        limit = i0 + 32 * k + __ffs(fm) - 1;
+                        break;
+                    }
+                }
+            }
             uint32_t hb[R];
 #pragma unroll
-            for (int k = 0; k < R; ++k) hb[k] = __ldg(H + pv[k]);  // pv < n always
+            for (int k = 0; k < R; ++k) hb[k] = head_load<KIND>(H, pv[k]);  // pv < n always
 #pragma unroll
             for (int k = 0; k < R; ++k) {
                 const uint32_t i = i0 + 32 * k + lane;
                 const bool live = i < limit && pv[k] >= plo && pv[k] < phi;
                 gpairs += live ? 1u : 0u;
-                const bool keep = live && !(head_q(hq, hb[k]) > reject);
+                const bool keep = live && !(head_q<KIND>(hq, hb[k]) > reject);
                 const unsigned km = __ballot_sync(kFull, keep);
                 if (keep) queue[qn + __popc(km & lanemask_lt())] = pv[k];
                 qn += __popc(km);
@@ -212,9 +261,9 @@ __global__ void __launch_bounds__(256, V >= 4 ? 2 : 4) k_gather_head(const Gathe
     if (lane == 0 && tw) atomicAdd(&a.counters[C_TAIL_PAIRS], tw);
 }
 
-template <int G, int V, int R>
+template <int KIND, int G, int V, int R>
 cudaError_t head_one(const GatherArgs& a, const HeadArgs& h, cudaStream_t s, int num_sms) {
-    auto k = k_gather_head<G, V, R>;
+    auto k = k_gather_head<KIND, G, V, R>;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
     if (per_sm < 1) per_sm = 1;
@@ -229,27 +278,43 @@ cudaError_t head_one(const GatherArgs& a, const HeadArgs& h, cudaStream_t s, int
 }  // namespace
 
 cudaError_t launch_head_quantize(const float* pts, uint32_t stride, uint64_t n, const HeadPlan& p,
-                                 uint32_t* out, cudaStream_t s, int num_sms) {
+                                 void* out, cudaStream_t s, int num_sms) {
     uint64_t blocks = (n + 255) / 256;
     if (blocks > (uint64_t)num_sms * 16) blocks = (uint64_t)num_sms * 16;
-    k_head_quantize<<<(unsigned)(blocks ? blocks : 1), 256, 0, s>>>(pts, stride, n, p.lo,
-                                                                     1.0 / p.s, out);
+    const unsigned g = (unsigned)(blocks ? blocks : 1);
+    const uint32_t k = p.args.coords;
+    switch (p.args.kind) {
+        case kHeadU16x2: k_head_quantize<kHeadU16x2><<<g, 256, 0, s>>>(pts, stride, n, k, p.lo, 1.0 / p.s, out); break;
+        case kHeadU8x4: k_head_quantize<kHeadU8x4><<<g, 256, 0, s>>>(pts, stride, n, k, p.lo, 1.0 / p.s, out); break;
+        default: k_head_quantize<kHeadU8x2><<<g, 256, 0, s>>>(pts, stride, n, k, p.lo, 1.0 / p.s, out); break;
+    }
     note_launch(1);
     return cudaGetLastError();
 }
 
+namespace {
+template <int KIND>
+cudaError_t head_dispatch(const GatherArgs& a, const HeadArgs& h, cudaStream_t s, int num_sms) {
+    const uint32_t W = a.tp.stride / 4;  // stride is a multiple of 4 for d >= 3
+    if (W <= 2) return head_one<KIND, 2, 1, 4>(a, h, s, num_sms);
+    if (W <= 4) return head_one<KIND, 4, 1, 4>(a, h, s, num_sms);
+    if (W <= 8) return head_one<KIND, 8, 1, 4>(a, h, s, num_sms);
+    if (W <= 16) return head_one<KIND, 16, 1, 4>(a, h, s, num_sms);
+    if (W <= 32) return head_one<KIND, 32, 1, 4>(a, h, s, num_sms);
+    if (W <= 64) return head_one<KIND, 32, 2, 4>(a, h, s, num_sms);
+    if (W <= 128) return head_one<KIND, 32, 4, 2>(a, h, s, num_sms);
+    if (W <= 256) return head_one<KIND, 32, 8, 2>(a, h, s, num_sms);
+    return cudaErrorInvalidValue;
+}
+}  // namespace
+
 cudaError_t launch_gather_head(const GatherArgs& a, const HeadArgs& h, cudaStream_t s, int num_sms) {
     if (a.row_end <= a.row_begin) return cudaSuccess;
-    const uint32_t W = a.tp.stride / 4;  // stride is a multiple of 4 for d >= 3
-    if (W <= 2) return head_one<2, 1, 4>(a, h, s, num_sms);
-    if (W <= 4) return head_one<4, 1, 4>(a, h, s, num_sms);
-    if (W <= 8) return head_one<8, 1, 4>(a, h, s, num_sms);
-    if (W <= 16) return head_one<16, 1, 4>(a, h, s, num_sms);
-    if (W <= 32) return head_one<32, 1, 4>(a, h, s, num_sms);
-    if (W <= 64) return head_one<32, 2, 4>(a, h, s, num_sms);
-    if (W <= 128) return head_one<32, 4, 2>(a, h, s, num_sms);
-    if (W <= 256) return head_one<32, 8, 2>(a, h, s, num_sms);
-    return cudaErrorInvalidValue;
+    switch (h.kind) {
+        case kHeadU16x2: return head_dispatch<kHeadU16x2>(a, h, s, num_sms);
+        case kHeadU8x4: return head_dispatch<kHeadU8x4>(a, h, s, num_sms);
+        default: return head_dispatch<kHeadU8x2>(a, h, s, num_sms);
+    }
 }
 
 }  // namespace sngb

@@ -211,19 +211,26 @@ cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint3
 cudaError_t launch_gather_q8(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms);
 cudaError_t launch_extras_q8(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, int num_sms);
 cudaError_t launch_extras(const ExtrasArgs& a, cudaStream_t s, int num_sms);
-// Head filter for narrow rows beyond L2 (sngb_head.cu): two 16-bit coordinates
-// per row, exact early reject, survivors take the fp32 test.
+// Head filter for narrow rows (sngb_head.cu): a few coordinates per row in a
+// compact L2-resident table, exact early reject, survivors take the fp32 test.
+constexpr int kHeadU16x2 = 0, kHeadU8x4 = 1, kHeadU8x2 = 2;  // head formats (4, 4, 2 bytes)
+#ifndef SNGB_HEAD_DEFAULT4
+#define SNGB_HEAD_DEFAULT4 0
+#endif
+constexpr int kHeadDefault4 = SNGB_HEAD_DEFAULT4;  // the 4-byte format auto picks
 struct HeadArgs {
-    const uint32_t* head;  // n rows: q0 | q1 << 16 (the first two coordinates)
-    float reject;          // fp32 head distance (in q units^2) > reject: the reference rejects
+    const void* head;  // n head words: coordinate j in bits [j*b, (j+1)*b), b = 16 or 8
+    float reject;      // head Q (q units^2) > reject: the reference rejects
+    int32_t kind;      // kHead*
+    uint32_t coords;   // coordinates in the head (2 or min(d, 4))
 };
 struct HeadPlan {
     double s, lo;  // scale (a power of two) and offset (a multiple of s)
     HeadArgs args;
 };
-bool head_plan(double lo, double hi, uint32_t d, double eps2, HeadPlan& p);
+bool head_plan(double lo, double hi, uint32_t d, double eps2, int kind, HeadPlan& p);
 cudaError_t launch_head_quantize(const float* pts, uint32_t stride, uint64_t n, const HeadPlan& p,
-                                 uint32_t* out, cudaStream_t s, int num_sms);
+                                 void* out, cudaStream_t s, int num_sms);
 cudaError_t launch_gather_head(const GatherArgs& a, const HeadArgs& h, cudaStream_t s, int num_sms);
 
 // ---- cluster stage (sngb_cluster.cu) ----
