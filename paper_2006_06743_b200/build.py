@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["sngb_api.cu", "sngb_kernels.cu", "sngb_quant.cu", "sngb_metric.cu", "sngb_head.cu", "sngb_sampler.cu",
            "sngb_cluster.cu"]
 HEADERS = ["sngb_internal.cuh", "sngb_rng.cuh", "sngb_device.cuh", "sngb_epstest.cuh",
-           "sngb_floyd_bitmap.cuh", "sngb_floyd_bloom.cuh"]
+           "sngb_floyd_bitmap.cuh", "sngb_floyd_bloom.cuh", "sngb_head.cuh"]
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -348,20 +348,24 @@ def _head_case(n, d, seed, k=12, spread=0.05, box=20.0):
     return np.ascontiguousarray(pts, np.float32)
 
 
+@pytest.mark.parametrize("bloom", [False, True])
 @pytest.mark.parametrize("mode,kind", [("0", "99"), ("2", "0"), ("2", "1"), ("2", "2")])
 @pytest.mark.parametrize("n,d,rate,seed,q", [(3000, 3, 0.05, 31, 0.3), (2500, 5, 0.06, 32, 0.5),
                                              (3000, 8, 0.05, 33, 0.2), (2800, 16, 0.05, 34, 0.6),
                                              (3000, 32, 0.04, 35, 0.3), (2000, 33, 0.06, 36, 0.9),
                                              (2200, 64, 0.05, 37, 0.4), (1800, 100, 0.06, 38, 0.5),
                                              (1500, 200, 0.08, 39, 0.3)])
-def test_head_filter_matches_oracle(oracle, monkeypatch, mode, kind, n, d, rate, seed, q):
+def test_head_filter_matches_oracle(oracle, monkeypatch, bloom, mode, kind, n, d, rate, seed, q):
     """SNGB_HEAD=2 forces the head filter (exact reject on a head of two 16-bit,
     four 8-bit or two 8-bit coordinates -- SNGB_HEAD_KIND 0/1/2 -- fp32 test for
     survivors) on every row width it serves; =0 is the plain fp32 gather.  eps at
     low and high within-cluster quantiles (few / many survivors): all identical
-    to the oracle."""
+    to the oracle.  bloom=True runs the large-n Floyd kernel beside it, False
+    the bitmap one."""
     monkeypatch.setenv("SNGB_HEAD", mode)
     monkeypatch.setenv("SNGB_HEAD_KIND", kind)
+    if bloom:
+        monkeypatch.setenv("SNGB_FLOYD_NO_BITMAP", "1")
     monkeypatch.setenv("SNGB_Q8", "0")
     pts = _head_case(n, d, seed)
     i = np.arange(0, n - 1, 5)
@@ -404,8 +408,10 @@ def test_head_filter_outlier_and_irregular_exact(oracle, monkeypatch):
     eps = 0.4
     keys, _ = oracle.sampled_edges(pts, eps, 0.04, 42)
     monkeypatch.setenv("SNGB_HEAD", "2")
-    for kind in ("0", "1", "2"):
+    for kind, bloom in (("0", False), ("1", False), ("2", False), ("0", True), ("2", True)):
         monkeypatch.setenv("SNGB_HEAD_KIND", kind)
+        if bloom:  # the large-n Floyd kernel
+            monkeypatch.setenv("SNGB_FLOYD_NO_BITMAP", "1")
         monkeypatch.delenv("SNGB_TEST_FORCE_IRREGULAR", raising=False)
         g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.04, seed=42)
         np.testing.assert_array_equal(g.keys, keys)
@@ -419,6 +425,7 @@ def test_head_filter_device_api_and_row_range(oracle, monkeypatch):
     import torch
     monkeypatch.setenv("SNGB_HEAD", "2")
     monkeypatch.setenv("SNGB_HEAD_KIND", "2")
+    monkeypatch.setenv("SNGB_FLOYD_NO_BITMAP", "1")
     pts = _head_case(6000, 32, 43)
     eps, rate, seed = 0.3, 0.03, 43
     labels, roles, gi = sng.sng_dbscan_device(torch.from_numpy(pts).cuda(), eps, 4, rate, seed)
