@@ -98,18 +98,18 @@ def load_gather_ceiling(d: int, n: int, row: int | None = None, read: int | None
     return best["bench"], best["rows_per_s"]
 
 
-def load_head_ceiling(n: int):
-    """Measured random 4-byte-row gather (the head table, n x 4 bytes) closest in
+def load_head_ceiling(n: int, hb: int = 4):
+    """Measured random hb-byte-row gather (the head table, n x hb bytes) closest in
     table size: (case name, rows/s) or (None, None)."""
     path = os.path.join(ROOT, "profiles", "r01_gather_ceilings.jsonl")
     try:
         cases = [json.loads(ln) for ln in open(path) if ln.strip().startswith("{")]
     except Exception:
         return None, None
-    same = [c for c in cases if c["bench"].startswith("ceiling_head4B")]
+    same = [c for c in cases if c["bench"].startswith(f"ceiling_head{hb}B")]
     if not same:
         return None, None
-    best = min(same, key=lambda c: abs(math.log(c["table_MB"] * 2**20 / max(4 * n, 1))))
+    best = min(same, key=lambda c: abs(math.log(c["table_MB"] * 2**20 / max(hb * n, 1))))
     return best["bench"], best["rows_per_s"]
 
 
@@ -438,10 +438,10 @@ def main():
         # HBM by table size): the ceiling is the time-weighted mix of the two
         # measured gathers; for an HBM-resident fp32 table the survivors' rows
         # come at the measured random-row rate of that table, not the copy peak
-        hcase, heads_per_s = load_head_ceiling(n)
-        rcase, frows_per_s = load_gather_ceiling(d, n)
         hb = getattr(info, "head_bytes", 4) or 4
         roofline["head_bytes"] = hb
+        hcase, heads_per_s = load_head_ceiling(n, hb)
+        rcase, frows_per_s = load_gather_ceiling(d, n)
         f = max(0.0, (bpp - hb) / (4 * d))
         roofline["tail_fraction"] = f
         if heads_per_s and frows_per_s:

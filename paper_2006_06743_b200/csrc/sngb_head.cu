@@ -35,6 +35,7 @@
 #include <cmath>
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sngb_device.cuh"
 #include "sngb_epstest.cuh"
@@ -244,6 +245,9 @@ cudaError_t head_one(const GatherArgs& a, const HeadArgs& h, cudaStream_t s, int
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
     if (per_sm < 1) per_sm = 1;
+    // SNGB_GATHER_BPSM: cap the persistent grid (co-residency with the sampler)
+    if (const char* e = std::getenv("SNGB_GATHER_BPSM"))
+        if (std::atoi(e) > 0 && std::atoi(e) < per_sm) per_sm = std::atoi(e);
     const uint64_t rows = a.row_end - a.row_begin;
     const uint64_t want = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const uint64_t cap = (uint64_t)num_sms * per_sm;

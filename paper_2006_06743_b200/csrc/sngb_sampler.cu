@@ -302,6 +302,9 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBloomBlock, smem);
         if (per_sm < 1) per_sm = 1;
+        // SNGB_SAMPLER_BPSM: cap the persistent grid (co-residency with the gather)
+        if (const char* e = std::getenv("SNGB_SAMPLER_BPSM"))
+            if (std::atoi(e) > 0 && std::atoi(e) < per_sm) per_sm = std::atoi(e);
         const uint64_t cap = (uint64_t)num_sms * per_sm;
         const unsigned grid = a.rows_per_block
                                   ? (unsigned)((rows + a.rows_per_block - 1) / a.rows_per_block)

@@ -62,9 +62,9 @@ __global__ void __launch_bounds__(256) k_lean(const float4* __restrict__ tab, ui
     if (acc == 1234.5f) sink[0] = acc;
 }
 
-// 4-byte rows (the head table of sngb_head.cu): one u32 per row per lane
-template <int UN>
-__global__ void __launch_bounds__(256) k_lean32(const uint32_t* __restrict__ tab, uint64_t rows,
+// 4- and 2-byte rows (the head tables of sngb_head.cu): one element per row per lane
+template <int UN, typename T = uint32_t>
+__global__ void __launch_bounds__(256) k_lean32(const T* __restrict__ tab, uint64_t rows,
                                                 uint32_t iters, float* sink) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t acc = 0;
@@ -101,15 +101,15 @@ float time_ms(F&& f) {
     return best;
 }
 
-template <int UN>
+template <int UN, typename T = uint32_t>
 double run32(size_t table_bytes, const float4* tab, float* sink, int sms, int bpsm) {
-    const uint64_t rows = table_bytes / 4;
+    const uint64_t rows = table_bytes / sizeof(T);
     const int blocks = sms * bpsm;
     const double threads = (double)blocks * 256;
     uint32_t iters = (uint32_t)(1e10 / (threads * UN * 32));
     if (iters < 4) iters = 4;
     const float ms = time_ms([&] {
-        k_lean32<UN><<<blocks, 256>>>(reinterpret_cast<const uint32_t*>(tab), rows, iters, sink);
+        k_lean32<UN, T><<<blocks, 256>>>(reinterpret_cast<const T*>(tab), rows, iters, sink);
     });
     return threads * iters * UN / (ms * 1e-3);  // rows per second
 }
@@ -196,22 +196,35 @@ int main(int argc, char** argv) {
         sweep<1, 1>(c5q4, tab, sink, sms);
         sweep<2, 1>(c5q8, tab, sink, sms);
         sweep<4, 1>(c5q16, tab, sink, sms);
-        // the head filter's 4-byte rows: cfg5 (20 M rows, 80 MB) and cfg3 (1 M rows, 4 MB)
-        for (size_t mb : {80, 4}) {
+        // the head filter's tables: 4-byte rows for cfg3 (1 M rows, 4 MB), cfg4 (5 M,
+        // 20 MB) and a 20 M-row 80 MB table; 2-byte rows for cfg5 (20 M rows, 40 MB)
+        auto head_case = [&](size_t bytes, int eb, const char* tag) {
             double best = 0;
             int bu = 0, bb = 0;
             for (int bpsm : {2, 4, 8}) {
-                const double r[3] = {run32<2>(mb << 20, tab, sink, sms, bpsm),
-                                     run32<4>(mb << 20, tab, sink, sms, bpsm),
-                                     run32<8>(mb << 20, tab, sink, sms, bpsm)};
+                double r[3];
+                if (eb == 4) {
+                    r[0] = run32<2>(bytes, tab, sink, sms, bpsm);
+                    r[1] = run32<4>(bytes, tab, sink, sms, bpsm);
+                    r[2] = run32<8>(bytes, tab, sink, sms, bpsm);
+                } else {
+                    r[0] = run32<2, unsigned short>(bytes, tab, sink, sms, bpsm);
+                    r[1] = run32<4, unsigned short>(bytes, tab, sink, sms, bpsm);
+                    r[2] = run32<8, unsigned short>(bytes, tab, sink, sms, bpsm);
+                }
                 for (int j = 0; j < 3; ++j)
                     if (r[j] > best) best = r[j], bu = 2 << j, bb = bpsm;
             }
-            printf("{\"bench\": \"ceiling_head4B_%zuMB\", \"row_bytes\": 4, \"read_bytes\": 4, "
+            printf("{\"bench\": \"ceiling_%s\", \"row_bytes\": %d, \"read_bytes\": %d, "
                    "\"table_MB\": %zu, \"GB_per_s\": %.1f, \"rows_per_s\": %.4g, "
                    "\"best_rows_in_flight_per_group\": %d, \"best_blocks_per_sm\": %d}\n",
-                   mb, mb, best * 4 / 1e9, best, bu, bb);
-        }
+                   tag, eb, eb, bytes >> 20, best * eb / 1e9, best, bu, bb);
+            fflush(stdout);
+        };
+        head_case(80ull << 20, 4, "head4B_80MB");
+        head_case(4ull << 20, 4, "head4B_4MB");
+        head_case(20ull << 20, 4, "head4B_20MB");
+        head_case(40ull << 20, 2, "head2B_40MB");
         return 0;
     }
     const Case c2q8h{"cfg2_q8_head256B_of_row800B_56MB", 56ull << 20, 800, 256};
