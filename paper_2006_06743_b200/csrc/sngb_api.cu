@@ -497,6 +497,14 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         }
         tm.mark_on(E_UPLOADED, c.copy);
     };
+    // side_pre: the sampler on the side stream while this stream prepares the
+    // points, waits for the filter plan and quantises; the gather then waits for
+    // the sampler (run together they slow the gather more than they gain).  The
+    // fork is recorded here, before the prepare pass.
+    const bool side_pre = !exhaustive && !h_src && (q8_try || head_try) &&
+                          !(stride <= 64 && (re - rb) >= 200000) &&  // not the overlap case
+                          env_u64("SNGB_OVERLAP", 2) != 1 && env_u64("SNGB_SIDE_PRE", 1) != 0;
+    if (side_pre) CK(cudaEventRecord(c.fork, s));
     if (!h_src && !f64) {
         prepare_rows(0, n);
         if (q8_try || head_try) minmax_to_host();
@@ -538,7 +546,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         const bool overlap =
             !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 200000));
         // host upload: the sampler reads no points, so it also runs while they arrive
-        const bool side = !exhaustive && (overlap || (h_src && attempt == 0));
+        const bool side = !exhaustive && (overlap || side_pre || (h_src && attempt == 0));
         if (!exhaustive) {
             SamplerArgs sa{};
             sa.n = n;
@@ -559,7 +567,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 // stream while the gather runs here; non-persistent grids let the
                 // block scheduler interleave the two kernels on every SM
                 sa.rows_per_block = (uint32_t)env_u64("SNGB_SAMPLER_RPB", overlap ? 32 : 0);
-                CK(cudaEventRecord(c.fork, s));
+                if (!(side_pre && attempt == 0)) CK(cudaEventRecord(c.fork, s));
                 CK(cudaStreamWaitEvent(c.side, c.fork, 0));
                 tm.mark_on(E_SIDE0, c.side);
                 CK(launch_sampler(sa, c.side, c.num_sms));
@@ -628,6 +636,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 }
             }
         }
+        if (side_pre) CK(cudaStreamWaitEvent(s, c.join, 0));  // gather after the sampler
         tm.mark(E_SAMPLED);
         GatherArgs ga{};
         ga.tp = tp;
@@ -775,8 +784,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     const size_t tb = std::max(sort_unique_temp_bytes(std::max<uint64_t>(gr.raw, 1), nb),
                                cluster_temp_bytes(n));
     c.temp.ensure(tb);
+    // the build's keys are canonical (a < b < n): 32-bit sort keys when they fit
+    // (SNGB_SORT32=0 keeps the 64-bit sort)
     CK(sort_unique(c.keys.as<unsigned long long>(), c.keys_alt.as<unsigned long long>(), gr.raw,
-                   nb, c.temp.p, c.temp.bytes, dc, &gr.ukeys, s));
+                   nb, c.temp.p, c.temp.bytes, dc, &gr.ukeys, s,
+                   env_u64("SNGB_SORT32", 1) ? n : 0));
     tm.mark(E_SORTED);
     return SNGB_OK;
 }

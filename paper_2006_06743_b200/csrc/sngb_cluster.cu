@@ -308,6 +308,39 @@ __global__ void k_import(const uint32_t* __restrict__ deg, const uint32_t* __res
     }
 }
 
+// 32-bit sort keys for small n (n(n-1)/2 <= 2^32: n <= 92 682, cfg1 and cfg2):
+// the canonical pair (a, b), a < b, as its upper-triangular index
+//     k = T(a) + (b - a - 1),  T(a) = a*n - a(a+1)/2,
+// which sorts exactly like (a << nb) | b, so the radix sort moves half the
+// bytes with one pass fewer (cfg2: 32 bits instead of 34 in u64 keys).
+__global__ void k_to_tri(const unsigned long long* __restrict__ in, uint32_t* __restrict__ out,
+                         uint64_t count, uint32_t nb, uint64_t n) {
+    const unsigned long long mask = (1ull << nb) - 1;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = in[i];
+        const uint64_t a = k >> nb, b = k & mask;
+        out[i] = (uint32_t)(a * n - a * (a + 1) / 2 + (b - a - 1));
+    }
+}
+__global__ void k_from_tri(const uint32_t* __restrict__ in, unsigned long long* __restrict__ out,
+                           const unsigned long long* __restrict__ m_ptr, uint32_t nb, uint64_t n) {
+    const uint64_t m = *m_ptr;
+    const double c = 2.0 * (double)n - 1.0;
+    auto T = [&](uint64_t a) { return a * n - a * (a + 1) / 2; };
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = in[i];
+        // a = floor((c - sqrt(c^2 - 8k)) / 2), then exact integer fix-ups
+        int64_t a = (int64_t)floor((c - sqrt(c * c - 8.0 * (double)k)) * 0.5);
+        if (a < 0) a = 0;
+        while (a > 0 && T((uint64_t)a) > k) --a;
+        while ((uint64_t)a + 1 < n && T((uint64_t)a + 1) <= k) ++a;
+        const uint64_t b = k - T((uint64_t)a) + (uint64_t)a + 1;
+        out[i] = ((unsigned long long)a << nb) | b;
+    }
+}
+
 unsigned grid_for(uint64_t items, int num_sms) {
     uint64_t b = (items + 255) / 256;
     const uint64_t cap = (uint64_t)num_sms * 8;
@@ -318,13 +351,20 @@ unsigned grid_for(uint64_t items, int num_sms) {
 }  // namespace
 
 size_t sort_unique_temp_bytes(uint64_t count, uint32_t nb) {
-    size_t a = 0, b = 0;
+    size_t a = 0, b = 0, a32 = 0, b32 = 0;
     cub::DoubleBuffer<unsigned long long> db(nullptr, nullptr);
     cub::DeviceRadixSort::SortKeys(nullptr, a, db, (int64_t)count, 0, (int)(2 * nb));
     cub::DeviceSelect::Unique(nullptr, b, (unsigned long long*)nullptr,
                               (unsigned long long*)nullptr, (unsigned long long*)nullptr,
                               (int64_t)count);
-    return (a > b ? a : b) + 256;
+    cub::DoubleBuffer<uint32_t> d32(nullptr, nullptr);
+    cub::DeviceRadixSort::SortKeys(nullptr, a32, d32, (int64_t)count, 0, 32);
+    cub::DeviceSelect::Unique(nullptr, b32, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                              (unsigned long long*)nullptr, (int64_t)count);
+    size_t m = a > b ? a : b;
+    m = m > a32 ? m : a32;
+    m = m > b32 ? m : b32;
+    return m + 256;
 }
 
 size_t cluster_temp_bytes(uint64_t n) {
@@ -336,10 +376,33 @@ size_t cluster_temp_bytes(uint64_t n) {
 
 cudaError_t sort_unique(unsigned long long* keys, unsigned long long* alt, uint64_t count,
                         uint32_t nb, void* temp, size_t temp_bytes, unsigned long long* counters,
-                        unsigned long long** unique_out, cudaStream_t s) {
+                        unsigned long long** unique_out, cudaStream_t s, uint64_t tri_n) {
     if (count == 0) {
         *unique_out = keys;
         return cudaMemsetAsync(&counters[C_UNIQUE], 0, sizeof(unsigned long long), s);
+    }
+    if (tri_n >= 2 && tri_n * (tri_n - 1) / 2 <= (1ull << 32)) {
+        // 32-bit triangular keys: keys -> alt (two u32 halves), sort, unique, decode -> keys
+        uint32_t* h0 = reinterpret_cast<uint32_t*>(alt);
+        uint32_t* h1 = h0 + count;
+        const unsigned g = grid_for(count, 148);
+        k_to_tri<<<g, 256, 0, s>>>(keys, h0, count, nb, tri_n);
+        const uint64_t kmax = tri_n * (tri_n - 1) / 2 - 1;
+        int bits = 1;
+        while (bits < 32 && (kmax >> bits) != 0) ++bits;
+        cub::DoubleBuffer<uint32_t> d32(h0, h1);
+        size_t tb = temp_bytes;
+        cudaError_t e = cub::DeviceRadixSort::SortKeys(temp, tb, d32, (int64_t)count, 0, bits, s);
+        if (e != cudaSuccess) return e;
+        uint32_t* sorted = d32.Current();
+        uint32_t* uq = (sorted == h0) ? h1 : h0;
+        tb = temp_bytes;
+        e = cub::DeviceSelect::Unique(temp, tb, sorted, uq, &counters[C_UNIQUE], (int64_t)count, s);
+        if (e != cudaSuccess) return e;
+        k_from_tri<<<g, 256, 0, s>>>(uq, keys, &counters[C_UNIQUE], nb, tri_n);
+        note_launch(2, 2 + (bits + 7) / 8 + 2);
+        *unique_out = keys;
+        return cudaGetLastError();
     }
     cub::DoubleBuffer<unsigned long long> db(keys, alt);
     size_t tb = temp_bytes;

@@ -47,16 +47,25 @@ __global__ void __launch_bounds__(256) k_floyd_bitmap(const SamplerArgs a) {
         clear();
         const uint64_t key = vertex_key(a.seed_mixed, u);
         bool replay = false;
+        // draws of the next chunk are computed one chunk ahead (independent of
+        // the bitmap operations, so the RNG overlaps their latency); the stream
+        // counter is carried incrementally and the test hook resolved per vertex
+        const uint32_t hook = (a.force_mod != 0 && (u % a.force_mod) == 0) ? D / 2 : 0xffffffffu;
+        uint64_t z = key + (uint64_t)(lane + 1) * kGamma;  // stream_at(key, i + 1), i = lane
+        bool fire_next;
+        uint32_t t_next = lemire32(mix(z), base + lane + 1, fire_next);
+        fire_next = (fire_next || (uint32_t)lane == hook) && (uint32_t)lane < D;
         for (uint32_t c0 = 0; c0 < D; c0 += 32) {
             const uint32_t i = c0 + lane;
             const bool valid = i < D;
-            bool fire = false;
-            uint32_t t = 0;
-            if (valid) {
-                t = lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fire);
-                fire |= test_fire(a.force_mod, u, i, D);
+            const bool fire = fire_next;
+            const uint32_t t = valid ? t_next : 0u;
+            z += 32ull * kGamma;
+            if (c0 + 32 < D) {
+                t_next = lemire32(mix(z), base + i + 33, fire_next);
+                fire_next = (fire_next || i + 32 == hook) && i + 32 < D;
             }
-            if (__ballot_sync(kFull, valid && fire)) {
+            if (__ballot_sync(kFull, fire)) {
                 replay = true;
                 break;
             }

@@ -253,7 +253,8 @@ struct ClusterBuffers {
 cudaError_t sort_unique(unsigned long long* keys, unsigned long long* alt, uint64_t count,
                         uint32_t nb, void* temp, size_t temp_bytes,
                         unsigned long long* counters, unsigned long long** unique_out,
-                        cudaStream_t s);
+                        cudaStream_t s, uint64_t tri_n = 0);  // tri_n: canonical keys of
+                                                              // n = tri_n points, 32-bit sort
 size_t sort_unique_temp_bytes(uint64_t count, uint32_t nb);
 size_t cluster_temp_bytes(uint64_t n);
 

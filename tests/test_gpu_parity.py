@@ -602,3 +602,18 @@ def test_edge_shapes_match_oracle(oracle, n, d, rate):
                        info)
     labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, 2, rate, 3)
     _assert_same(c, info, labels, roles, oinfo)
+
+
+@pytest.mark.parametrize("n", [92682, 92683])
+def test_sort32_triangular_keys_boundary(oracle, monkeypatch, n):
+    """n(n-1)/2 <= 2^32 (n <= 92 682) sorts the build's keys as 32-bit
+    upper-triangular indices, one more point takes the 64-bit sort: both give
+    the oracle's edge list, as does SNGB_SORT32=0."""
+    rng = np.random.default_rng(n)
+    pts = rng.random((n, 2), dtype=np.float32)
+    eps, rate, seed = 0.01, 40 / n, 7
+    keys, _ = oracle.sampled_edges(pts, eps, rate, seed)
+    for mode in ("1", "0"):
+        monkeypatch.setenv("SNGB_SORT32", mode)
+        g = sng.build_sampled_graph(sng.Dataset(pts), eps, rate, seed=seed)
+        np.testing.assert_array_equal(g.keys, keys)

@@ -1,6 +1,2 @@
-OUT=gpurun_out/r01k; mkdir -p $OUT
-./tools/gather_ceiling q5 > $OUT/ceil.jsonl 2>&1
-grep head $OUT/ceil.jsonl > $OUT/head_ceil.jsonl
-cat $OUT/head_ceil.jsonl >> profiles/r01_gather_ceilings.jsonl
-for c in 3 4; do timeout 900 python bench.py --config $c --steps 5 --warmup 3 > $OUT/bench_cfg$c.json 2> $OUT/bench_cfg$c.err; done
-timeout 900 python bench.py --config 5 --steps 3 --warmup 3 > $OUT/bench_cfg5.json 2> $OUT/bench_cfg5.err
+mkdir -p gpurun_out/fbn
+python tools/run_once.py --config 2 > gpurun_out/fbn/ro.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_floyd_bitmap -c 1 -o gpurun_out/fbn/bitmap_cfg2 python tools/run_once.py --config 2 --reps 0 > gpurun_out/fbn/ncu.log 2>&1
