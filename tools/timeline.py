@@ -19,15 +19,36 @@ from paper_2006_06743_b200 import synthetic  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--config", type=int, default=2)
 p.add_argument("--reps", type=int, default=3)
+p.add_argument("--host", action="store_true", help="the host C-ABI call from pinned memory (bench e2e)")
 a = p.parse_args()
 w = synthetic.CONFIGS[a.config]
-x = torch.from_numpy(synthetic.generate(a.config)).cuda()
+pts = synthetic.generate(a.config)
+if a.host:
+    import ctypes as C
+    from paper_2006_06743_b200 import _lib
+    host = torch.from_numpy(pts).pin_memory()
+    n, d = pts.shape
+    labels_h = torch.empty(n, dtype=torch.int32).pin_memory()
+    roles_h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    L = _lib.lib()
+    o = _lib.SngbOpts(0, 0, None, 0, 0)
+
+    def call():
+        sng._check(L.sngb_dbscan_f32(C.cast(host.data_ptr(), C.POINTER(C.c_float)), n, d, w.eps,
+                                     w.min_pts, w.rate, w.seed, C.byref(o),
+                                     C.cast(labels_h.data_ptr(), C.POINTER(C.c_int32)),
+                                     C.cast(roles_h.data_ptr(), C.POINTER(C.c_uint8)), None))
+else:
+    x = torch.from_numpy(pts).cuda()
+
+    def call():
+        sng.sng_dbscan_device(x, w.eps, w.min_pts, w.rate, w.seed)
 for _ in range(3):
-    sng.sng_dbscan_device(x, w.eps, w.min_pts, w.rate, w.seed)
+    call()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(a.reps):
-        sng.sng_dbscan_device(x, w.eps, w.min_pts, w.rate, w.seed)
+        call()
     torch.cuda.synchronize()
 evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 evs.sort(key=lambda e: e.time_range.start)
