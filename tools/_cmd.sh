@@ -1,11 +1,6 @@
-OUT=gpurun_out/r01l; mkdir -p $OUT
-timeout 1500 python -m pytest tests -q -m gpu -x > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
-timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
-timeout 600 python bench.py --config 1 > $OUT/bench_cfg1.json 2> $OUT/bench_cfg1.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
-python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/plain.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-      python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/ncu_launch.log 2>&1
-python tools/timeline.py --config 2 --reps 3 > $OUT/timeline_cfg2.txt 2>/dev/null
-python tools/timeline.py --config 2 --reps 2 --host > $OUT/timeline_cfg2_host.txt 2>/dev/null
-python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1
+mkdir -p gpurun_out/ff
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "fused_floyd or q8 or device_api" > gpurun_out/ff/pytest.log 2>&1
+python tools/timeline.py --config 2 --reps 3 > gpurun_out/ff/cfg2.txt 2> gpurun_out/ff/cfg2.err
+for v in "X=0" "SNGB_FUSE_FLOYD=0"; do
+  echo "$v $(env $v timeout 300 python bench.py --config 2 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"],3), round(d["roofline"]["kernel_ms"],3), d["stages_ms"])')" >> gpurun_out/ff/b.log
+done
