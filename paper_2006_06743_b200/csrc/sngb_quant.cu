@@ -244,8 +244,9 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8(const GatherArgs a, const 
     flush_stats(st, gpairs, a.counters, lane);
 }
 
-// Early-reject gather for wide rows.  Phase A: half a warp per pair reads the
-// pair's head (kHead chunks, the norm chunk first), UA pairs per half-warp step;
+// Early-reject gather for wide rows.  Phase A: a quarter warp per pair reads the
+// pair's head (kHead chunks, the norm chunk first; two chunks per lane), 32 pairs
+// per warp step;
 // pairs whose head sum already exceeds reject_min are rejected, the others are
 // queued with Q2h + Nta.  Phase B: the full warp finishes UB queued pairs per
 // step over the tail chunks plus the norm chunk (for Ntb = N - Nhead).  Both
@@ -261,7 +262,8 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
     static_assert(UA == 16, "phase A leaves one pair per lane");
     constexpr int SPANB = 32 / UB;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int hc = lane & 15;  // head chunk of this lane
+    // phase A: a quarter warp per pair, lane q of it holding head chunks q and q + 8
+    const int hc = lane & 7;
     const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
     const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerBlock;
     const uint4* __restrict__ Q = q8.rows;
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
     if (a.work) grab();
     for (; u < chunk_end; (a.work && u + 1 >= chunk_end) ? grab() : (void)(u += a.work ? 1 : nw)) {
         uint4 qh = __ldg(Q + u * RW + hc);
+        const uint4 qh8 = __ldg(Q + u * RW + hc + 8);
         const uint32_t nha = __shfl_sync(kFull, qh.x, 0), nfa = __shfl_sync(kFull, qh.y, 0);
         if (hc == 0) qh = make_uint4(0, 0, 0, 0);
         uint4 qt[VT];
@@ -350,19 +353,27 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
 
         // phase A over list[0, nA), nA <= 2*UA: heads, survivors appended to the queue
         auto head_step = [&](uint32_t nA) {
-            uint4 rows[UA];
+            // 8 pairs per quarter warp: two 16-byte chunks per lane per pair (one
+            // row address for both), a 3-level transposed reduce-scatter over the
+            // quarter warp -- half the address and shuffle work of a half warp
+            // per pair with one chunk per lane
+            constexpr int UQ = 8;
+            uint4 r0[UQ], r1[UQ];
 #pragma unroll
-            for (int k = 0; k < UA; ++k) {  // pairs past nA re-read pair 0's head (masked below)
-                const uint32_t j = (lane >> 4) * UA + k;
-                rows[k] = __ldg(Q + (uint64_t)list[j < nA ? j : 0] * RW + hc);
+            for (int k = 0; k < UQ; ++k) {  // pairs past nA re-read pair 0's head (masked below)
+                const uint32_t j = (lane >> 3) * UQ + k;
+                const uint4* rp = Q + (size_t)list[j < nA ? j : 0] * RW + hc;
+                r0[k] = __ldg(rp);
+                r1[k] = __ldg(rp + 8);
             }
             __syncwarp();
-            int ps[UA];
+            int ps[UQ];
 #pragma unroll
-            for (int k = 0; k < UA; ++k)
-                ps[k] = (hc == 0 ? (int)rows[k].x : 0) - 2 * (int)dot16(qh, rows[k], 0u);
+            for (int k = 0; k < UQ; ++k)
+                ps[k] = (hc == 0 ? (int)r0[k].x : 0) -
+                        2 * (int)dot16(qh8, r1[k], dot16(qh, r0[k], 0u));
 #pragma unroll
-            for (int o = 8, mm = UA; mm > 1; o >>= 1, mm >>= 1) {
+            for (int o = 4, mm = UQ; mm > 1; o >>= 1, mm >>= 1) {
                 const bool hi = (lane & o) != 0;
 #pragma unroll
                 for (int k = 0; k < mm / 2; ++k) {
