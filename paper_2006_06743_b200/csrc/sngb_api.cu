@@ -432,9 +432,13 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     } else {
         pairs = rows * draws;
     }
-    double exp_col = 0.0;
-    if (!exhaustive)
-        for (uint64_t i = 0; i < draws; ++i) exp_col += (double)i / (double)(base + i + 1);
+    // expected Floyd collisions per vertex, sum_i i / (base + i + 1), bounded above
+    // in closed form by D(D-1) / 2(base + 1) (a per-call loop over the draws
+    // cost ~15 us of host time on cfg2, 80 us on cfg5)
+    const double exp_col =
+        exhaustive ? 0.0
+                   : std::min((double)draws,
+                              (double)draws * ((double)draws - 1.0) / (2.0 * ((double)base + 1.0)));
     uint64_t extras_cap =
         exhaustive ? 0 : (uint64_t)(1.5 * exp_col * (double)rows) + 4096 + 4 * draws;
     uint64_t edge_cap = std::min<uint64_t>(pairs + extras_cap + 1, std::max<uint64_t>(1ull << 24, pairs / 8));
