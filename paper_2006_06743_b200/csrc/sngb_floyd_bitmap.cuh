@@ -22,7 +22,7 @@
 
 constexpr int kBitmapStage = 128;
 
-__global__ void __launch_bounds__(256) k_floyd_bitmap(const SamplerArgs a) {
+__global__ void __launch_bounds__(512) k_floyd_bitmap(const SamplerArgs a) {
     extern __shared__ __align__(16) uint32_t bsmem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;

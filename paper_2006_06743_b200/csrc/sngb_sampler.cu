@@ -30,7 +30,11 @@
 // of its partners become extras).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <cstdlib>
 
 #include "sngb_device.cuh"
@@ -260,6 +264,26 @@ size_t floyd_scratch_bytes(uint32_t draws, int num_sms) {
     return (size_t)num_sms * 2 * slots * 8;
 }
 
+// A kernel's dynamic shared-memory limit is raised once per device to the
+// opt-in maximum: concurrent callers (the batched API's host workers) with
+// different sizes must never lower it under another's launch.
+cudaError_t raise_smem_limit(const void* kernel) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0, mx = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({kernel, dev})) return cudaSuccess;
+    cudaError_t e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kernel);  // less its static shared memory
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 mx - (int)fa.sharedSizeBytes);
+    if (e == cudaSuccess) done.insert({kernel, dev});
+    return e;
+}
+
 cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
     const uint64_t rows = in.row_end - in.row_begin;
     if (rows == 0 || in.draws == 0) return cudaSuccess;
@@ -270,11 +294,24 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
     const uint64_t bm_words = (((a.n - 1) + 31) / 32 + 3) & ~3ull;
     if (bm_words * 4 <= 9216 && !std::getenv("SNGB_FLOYD_NO_BITMAP")) {
         a.col_words = (uint32_t)bm_words;
-        const int wpb = 8;
-        const size_t smem = (size_t)wpb * (bm_words * 4 + kBitmapStage * 8);
-        cudaError_t e = cudaFuncSetAttribute(k_floyd_bitmap,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
+        // warps per block: the most resident warps per SM for this bitmap size
+        // (shared memory bound for large bitmaps: 8-warp blocks fit 2 per SM at
+        // n = 70 k, i.e. 16 warps; 11-warp blocks fit 22), SNGB_BITMAP_WPB overrides
+        const size_t per_warp = bm_words * 4 + kBitmapStage * 8;
+        const cudaError_t attr_rc = raise_smem_limit(reinterpret_cast<const void*>(k_floyd_bitmap));
+        if (attr_rc != cudaSuccess) return attr_rc;
+        int wpb = 8, best = 0;
+        static thread_local uint64_t memo_words = 0;  // the search costs ~13 occupancy queries
+        static thread_local int memo_wpb = 8;
+        if (const char* ev = std::getenv("SNGB_BITMAP_WPB")) wpb = std::max(1, std::min(16, std::atoi(ev)));
+        else if (memo_words == bm_words) wpb = memo_wpb;
+        else
+            for (int w = 4; w <= 16; ++w) {
+                int pb = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_floyd_bitmap, w * 32, w * per_warp);
+                if (pb * w > best) best = pb * w, wpb = w, memo_wpb = w, memo_words = bm_words;
+            }
+        const size_t smem = (size_t)wpb * per_warp;
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_floyd_bitmap, wpb * 32, smem);
         if (per_sm < 1) per_sm = 1;
@@ -297,7 +334,7 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
                  : D <= 2560 ? k_floyd_bloom<10>
                  : D <= 3072 ? k_floyd_bloom<12>
                              : k_floyd_bloom<16>;
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(k));
         if (e != cudaSuccess) return e;
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBloomBlock, smem);
@@ -322,7 +359,7 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
     const bool sh = floyd_shared(D);
     const size_t smem = floyd_smem_bytes(D, sh);
     auto k = sh ? k_floyd<true> : k_floyd<false>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(k));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFloydThreads, smem);
