@@ -176,13 +176,22 @@ __device__ __forceinline__ uint32_t cluster_root(uint64_t v, const uint8_t* core
     return core[v] ? parent[v] : broot[v];
 }
 
+// first member of each cluster (clusterer.cpp:41-51: clusters are numbered by
+// their smallest member).  A component's root is its smallest core vertex
+// (hooking keeps parent[v] <= v), so among core members only the root itself
+// is a candidate: core non-roots skip the atomic (cfg2: all 70 k vertices are
+// core and hammered 10 addresses before), border vertices compete with it.
 __global__ void k_first(uint64_t n, const uint8_t* __restrict__ core,
                         const uint32_t* __restrict__ parent, const uint32_t* __restrict__ broot,
                         uint32_t* first) {
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
          v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t r = cluster_root(v, core, parent, broot);
-        if (r != kNone) atomicMin(&first[r], (uint32_t)v);
+        if (core[v]) {
+            if (parent[v] == (uint32_t)v) atomicMin(&first[v], (uint32_t)v);
+        } else {
+            const uint32_t r = broot[v];
+            if (r != kNone) atomicMin(&first[r], (uint32_t)v);
+        }
     }
 }
 
