@@ -497,6 +497,62 @@ __global__ void __launch_bounds__(256) k_extras_q8(const ExtrasArgs a, const Q8A
     flush_stats(st, 0, a.counters, lane);
 }
 
+// Floyd replacement pairs through the head/tail filter (rows that take
+// k_gather_q8s): half a warp per pair reads both heads (one chunk per lane,
+// the norm chunk first); only pairs the heads do not reject read their tails
+// (VT chunks per lane).  Nothing is shared between pairs, so every row is read
+// in full per pair: the early reject saves ~2/3 of the bytes.
+template <int VT>
+__global__ void __launch_bounds__(256) k_extras_q8s(const ExtrasArgs a, const Q8Args q8) {
+    __shared__ unsigned long long s_stage[kWarpsPerBlock][kStage];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int half = lane >> 4, hc = lane & 15;
+    const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
+    const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerBlock;
+    const uint4* __restrict__ Q = q8.rows;
+    const uint32_t RW = q8.nd + 1, T = RW - kHead;
+    WarpStage<kStage> stage{s_stage[wib], 0};
+    TestStats st;
+    uint64_t count = *a.count_ptr;
+    if (count > a.capacity) count = a.capacity;
+    for (uint64_t p0 = gw * 2; p0 < count; p0 += nw * 2) {
+        const uint64_t p = p0 + half;
+        const bool ok = p < count;
+        const unsigned long long rec = a.extras[ok ? p : p0];
+        const uint64_t u = rec >> 32, v = rec & 0xffffffffull;
+        const uint4 x = __ldg(Q + u * RW + hc), y = __ldg(Q + v * RW + hc);
+        int part = hc == 0 ? (int)(x.x + y.x) : -2 * (int)dot16(x, y, 0u);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+        const bool need_tail = ok && part <= q8.reject_min;  // else Q2 >= Q2h > B: reject
+        int q2 = part;
+        if (__any_sync(kFull, need_tail)) {
+            int t = hc == 0 ? (int)((x.y - x.x) + (y.y - y.x)) : 0;  // tail norms
+            uint32_t dot = 0;
+#pragma unroll
+            for (int k = 0; k < VT; ++k) {
+                const uint32_t sl = hc + 16 * k;
+                if (sl < T)
+                    dot = dot16(__ldg(Q + u * RW + kHead + sl), __ldg(Q + v * RW + kHead + sl), dot);
+            }
+            t -= 2 * (int)dot;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
+            q2 += t;
+        }
+        const bool leader = hc == 0 && ok;
+        const bool acc = leader && need_tail && q2 <= q8.accept_max;
+        if (leader && need_tail && q2 > q8.accept_max && q2 <= q8.reject_min) {  // k_band decides
+            band_push(a.tp, u, v, __int_as_float(0x7fc00000));
+            st.band++;
+        }
+        if (leader) st.pairs++;
+        stage.push(acc, edge_key(u, v, a.sink.nb), a.sink, lane);
+    }
+    stage.flush(a.sink, lane);
+    flush_stats(st, 0, a.counters, lane);
+}
+
 template <int V8>
 cudaError_t extras_q8_one(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
     auto k = k_extras_q8<V8>;
@@ -538,8 +594,33 @@ cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint3
     return cudaGetLastError();
 }
 
+template <int VT>
+cudaError_t extras_q8s_one(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
+    auto k = k_extras_q8s<VT>;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t want = (a.capacity + 2 * kWarpsPerBlock - 1) / (2 * kWarpsPerBlock);
+    const uint64_t cap = (uint64_t)num_sms * per_sm;
+    const uint64_t g = want < cap ? want : cap;
+    k<<<(unsigned)(g ? g : 1), 256, 0, s>>>(a, q);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_extras_q8(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {
     if (a.capacity == 0) return cudaSuccess;
+    if (q8_split(q.nd)) {
+        switch ((q.nd + 1 - kHead + 15) / 16) {  // tail chunks per lane of a half warp
+            case 1: return extras_q8s_one<1>(a, q, s, num_sms);
+            case 2: return extras_q8s_one<2>(a, q, s, num_sms);
+            case 3: return extras_q8s_one<3>(a, q, s, num_sms);
+            case 4: return extras_q8s_one<4>(a, q, s, num_sms);
+            case 5: return extras_q8s_one<5>(a, q, s, num_sms);
+            case 6: return extras_q8s_one<6>(a, q, s, num_sms);
+            default: break;  // wider rows: one pair per warp below
+        }
+    }
     switch ((q.nd + 1 + 31) / 32) {
         case 1: return extras_q8_one<1>(a, q, s, num_sms);
         case 2: return extras_q8_one<2>(a, q, s, num_sms);
