@@ -506,7 +506,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     // the sampler (run together they slow the gather more than they gain).  The
     // fork is recorded here, before the prepare pass.
     const bool side_pre = !exhaustive && !h_src && (q8_try || head_try) &&
-                          !(stride <= 64 && (re - rb) >= 200000) &&  // not the overlap case
+                          !(stride <= 64 && (re - rb) >= 10000) &&  // not the overlap case
                           env_u64("SNGB_OVERLAP", 2) != 1 && env_u64("SNGB_SIDE_PRE", 1) != 0;
     if (side_pre) CK(cudaEventRecord(c.fork, s));
     if (!h_src && !f64) {
@@ -541,14 +541,15 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             CK(cudaMemsetAsync(&dc[C_BAND_CURSOR], 0, sizeof(unsigned long long), s));
         }
         tm.mark(E_PREPARED);
-        // Overlap: the sampler on the side stream concurrently with a
-        // non-persistent gather (SNGB_OVERLAP 0 off, 1 on, 2 auto).  Auto for
-        // large narrow-row problems, where it measured 2-3 % better than the
-        // sequential order with dynamic row claiming (cfg3, cfg4; cfg5 equal);
-        // small and wide-row problems lose.
+        // Overlap: the sampler on the side stream concurrently with the
+        // persistent, dynamically claimed gather (SNGB_OVERLAP 0 off, 1 on, 2
+        // auto).  Auto for narrow-row problems of >= 10 k rows: cfg1 0.82 ->
+        // 0.79 ms, cfg3-5 within 1 % of sequential (cfg5 668 vs 686 ms with
+        // dynamic claiming, which a non-persistent gather grid lost); wide-row
+        // problems run the sampler beside prepare/plan/quantise instead.
         const uint64_t ov = env_u64("SNGB_OVERLAP", 2);
         const bool overlap =
-            !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 200000));
+            !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 10000));
         // host upload: the sampler reads no points, so it also runs while they arrive
         const bool side = !exhaustive && (overlap || side_pre || (h_src && attempt == 0));
         if (!exhaustive) {
@@ -653,7 +654,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         ga.base = (uint32_t)base;
         ga.seed_mixed = seed_mixed;
         ga.force_mod = test_force_mod();
-        ga.rows_per_block = (uint32_t)env_u64("SNGB_GATHER_RPB", overlap ? 8 * 16 : 0);
+        ga.rows_per_block = (uint32_t)env_u64("SNGB_GATHER_RPB", 0);
         // dynamic row claiming (persistent grid): one zeroed counter per launch
         constexpr uint32_t kWorkSlots = 256;
         const bool dyn = ga.rows_per_block == 0 && env_u64("SNGB_GATHER_DYN", 1) == 1;
