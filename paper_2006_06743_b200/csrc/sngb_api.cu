@@ -96,8 +96,9 @@ struct DevCtx {
     cudaEvent_t up_ev[kMaxChunks] = {};
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
-        flags, rank, temp, labels, roles, work, q8, upload64, rnorm, band;
+        flags, rank, temp, labels, roles, work, q8, upload64, rnorm, band, partners, poff;
     cudaEvent_t qev = nullptr;  // min/max of the points copied to the host (8-bit filter)
+    cudaEvent_t pev = nullptr;  // bucketed partner lists ready (host-upload 8-bit schedule)
     unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
     cudaEvent_t ev[12] = {};
     uint64_t edge_hint = 0;  // last needed edge capacity for this context
@@ -105,7 +106,7 @@ struct DevCtx {
 
     void release() {
         for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
-                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band})
+                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band, &partners, &poff})
             b->release();
     }
 };
@@ -160,6 +161,7 @@ DevCtx& get_ctx(int dev, int slot = 0) {
         CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->qev, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->pev, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->up_start, cudaEventDisableTiming));
         for (auto& e : c->up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaMallocHost(&c->h_counters, C_COUNT * sizeof(unsigned long long)));
@@ -488,6 +490,15 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         chunks = (uint32_t)std::min<uint64_t>(
             std::max<uint64_t>(env_u64("SNGB_Q8_CHUNKS", 8), 1), DevCtx::kMaxChunks);
     auto chunk_lo = [&](uint32_t k) { return n * k / chunks; };
+    // Host-upload 8-bit schedule: each landed slice k is tested against every
+    // earlier row, which regenerated all of their draws per launch; instead the
+    // draws' partners are bucketed by slice once, on the side stream while the
+    // first chunk uploads (no point data needed), and each launch reads only
+    // its slices' lists (SNGB_PARTNERS=0: regenerate)
+    const bool pre_partners = h_src && q8_try && chunks > 1 && !exhaustive &&
+                              q8_split((d + 15) / 16) && draws <= 1024 &&
+                              (re - rb) * draws * 4ull <= (2ull << 30) &&
+                              env_u64("SNGB_PARTNERS", 1) != 0;
     // issued after the sampler launch: a pageable source blocks the host while
     // it is staged, and the sampler should already be running by then
     auto start_upload = [&]() {
@@ -552,6 +563,22 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 10000));
         // host upload: the sampler reads no points, so it also runs while they arrive
         const bool side = !exhaustive && (overlap || side_pre || (h_src && attempt == 0));
+        if (pre_partners && attempt == 0) {  // before the sampler on the side stream
+            c.partners.ensure((re - rb) * draws * 4ull);
+            c.poff.ensure((re - rb) * (chunks + 1) * 4ull);
+            GatherArgs pa{};
+            pa.n = n;
+            pa.row_begin = rb;
+            pa.row_end = re;
+            pa.draws = (uint32_t)draws;
+            pa.base = (uint32_t)base;
+            pa.seed_mixed = seed_mixed;
+            pa.force_mod = test_force_mod();
+            pa.nbuckets = chunks;
+            CK(launch_partners(pa, c.partners.as<uint32_t>(), c.poff.as<uint32_t>(), c.side,
+                               c.num_sms));
+            CK(cudaEventRecord(c.pev, c.side));
+        }
         if (!exhaustive) {
             SamplerArgs sa{};
             sa.n = n;
@@ -655,6 +682,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         ga.seed_mixed = seed_mixed;
         ga.force_mod = test_force_mod();
         ga.rows_per_block = (uint32_t)env_u64("SNGB_GATHER_RPB", 0);
+        if (pre_partners && q8_on) CK(cudaStreamWaitEvent(gs, c.pev, 0));
         // dynamic row claiming (persistent grid): one zeroed counter per launch
         constexpr uint32_t kWorkSlots = 256;
         const bool dyn = ga.rows_per_block == 0 && env_u64("SNGB_GATHER_DYN", 1) == 1;
@@ -681,6 +709,19 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             ga.part_lo = plo;
             ga.part_hi = phi;
             if (ga.row_end <= ga.row_begin) return;
+            ga.partners = nullptr;
+            if (pre_partners && q8_on) {  // the launch's slices, if on bucket boundaries
+                const uint32_t blo = (uint32_t)((uint64_t)plo * chunks / n);
+                const uint32_t bhi = (uint32_t)((uint64_t)phi * chunks / n);
+                if (chunk_lo(blo) == plo && chunk_lo(bhi) == phi) {
+                    ga.partners = c.partners.as<uint32_t>();
+                    ga.poff = c.poff.as<uint32_t>();
+                    ga.partners_row0 = rb;
+                    ga.nbuckets = chunks;
+                    ga.blo = blo;
+                    ga.bhi = bhi;
+                }
+            }
             ga.work = nullptr;
             if (dyn && work_slot < kWorkSlots) {
                 ga.work = c.work.as<unsigned long long>() + work_slot++;

@@ -83,6 +83,15 @@ struct GatherArgs {
     uint32_t rows_per_block;    // 0: persistent grid; else one block per this many rows
     unsigned long long* work;   // non-null: warps claim `grab` rows at a time from *work (zeroed)
     uint32_t grab;
+    // Bucketed partner lists (k_partners; 8-bit head/tail gather only): row u's
+    // partners grouped by partner slice, slice b = [n*b/B, n*(b+1)/B), its list at
+    // partners[(u - partners_row0) * draws + poff[(u - partners_row0) * (B + 1) + b]];
+    // a launch reads slices [blo, bhi) instead of regenerating every draw.
+    // Draws from an irregular vertex's first fired draw on are left out.
+    const uint32_t* partners;
+    const uint32_t* poff;
+    uint64_t partners_row0;
+    uint32_t nbuckets, blo, bhi;
 };
 
 // Test hook (env SNGB_TEST_FORCE_IRREGULAR=m): pretend the Lemire reject
@@ -209,6 +218,10 @@ cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint3
                             const Q8Plan& p, uint4* out, cudaStream_t s, int num_sms,
                             const double* pts64 = nullptr);
 cudaError_t launch_gather_q8(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms);
+// bucketed partner lists of rows [a.row_begin, a.row_end) (a.nbuckets slices);
+// draws <= 1024; see GatherArgs::partners
+cudaError_t launch_partners(const GatherArgs& a, uint32_t* lists, uint32_t* offsets, cudaStream_t s,
+                            int num_sms);
 cudaError_t launch_extras_q8(const ExtrasArgs& a, const Q8Args& q, cudaStream_t s, int num_sms);
 cudaError_t launch_extras(const ExtrasArgs& a, cudaStream_t s, int num_sms);
 // Head filter for narrow rows (sngb_head.cu): a few coordinates per row in a

@@ -415,18 +415,31 @@ __global__ void __launch_bounds__(256, 2) k_gather_q8s(const GatherArgs a, const
         uint32_t nl = 0;  // live partners waiting for phase A (warp-uniform)
         uint32_t limit = a.draws;
         uint64_t z = vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
+        const uint32_t* pre = nullptr;  // bucketed partner list of this launch's slices
+        if (a.partners) {
+            const uint64_t r = u - a.partners_row0;
+            const uint32_t* o = a.poff + r * (a.nbuckets + 1);
+            const uint32_t lo = __ldg(o + a.blo);
+            pre = a.partners + r * a.draws + lo;
+            limit = __ldg(o + a.bhi) - lo;
+        }
         for (uint32_t i0 = 0; i0 < limit; i0 += 32, z += 32ull * kGamma) {
             const uint32_t i = i0 + lane;
-            const bool valid = i < limit;
-            bool fire = false;
-            uint32_t t = 0;
-            if (valid) {
-                t = lemire32(mix(z), a.base + i + 1, fire);
-                fire |= test_fire(a.force_mod, u, i, a.draws);
+            uint32_t p;
+            if (pre) {
+                p = i < limit ? __ldg(pre + i) : 0u;
+            } else {
+                const bool valid = i < limit;
+                bool fire = false;
+                uint32_t t = 0;
+                if (valid) {
+                    t = lemire32(mix(z), a.base + i + 1, fire);
+                    fire |= test_fire(a.force_mod, u, i, a.draws);
+                }
+                p = t + (t >= (uint32_t)u ? 1u : 0u);
+                const unsigned fm = __ballot_sync(kFull, valid && fire);
+                if (fm) limit = i0 + __ffs(fm) - 1;  // irregular vertex: cut here
             }
-            const uint32_t p = t + (t >= (uint32_t)u ? 1u : 0u);
-            const unsigned fm = __ballot_sync(kFull, valid && fire);
-            if (fm) limit = i0 + __ffs(fm) - 1;  // irregular vertex: cut here
             const bool live = i < limit && p >= plo && p < phi;
             const unsigned m = __ballot_sync(kFull, live);
             if (live) list[nl + __popc(m & lanemask_lt())] = p;
@@ -627,6 +640,74 @@ cudaError_t launch_extras_q8(const ExtrasArgs& a, const Q8Args& q, cudaStream_t 
         case 3: return extras_q8_one<3>(a, q, s, num_sms);
         default: return cudaErrorInvalidValue;
     }
+}
+
+namespace {
+// Bucketed partner lists, warp per row: every draw of k_gather (counter i+1,
+// Lemire, p = t + (t >= u)) held in registers (D <= 32 * MAXC), cut at an
+// irregular vertex's first fired draw, counted per partner slice, prefix-summed
+// and scattered slice by slice (ballot ranks keep draw order within a slice).
+template <int MAXC>
+__global__ void __launch_bounds__(256) k_partners(const GatherArgs a, uint32_t* __restrict__ lists,
+                                                  uint32_t* __restrict__ offsets) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t D = a.draws, B = a.nbuckets;
+    const uint64_t n = a.n;
+    auto bound = [&](uint32_t b) { return (uint32_t)(n * b / B); };
+    for (uint64_t u = a.row_begin + gw; u < a.row_end; u += nw) {
+        uint32_t pv[MAXC];
+        uint32_t limit = D;
+        uint64_t z = vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c, z += 32ull * kGamma) {
+            const uint32_t i = 32 * c + lane;
+            bool fire = false;
+            const uint32_t t = lemire32(mix(z), a.base + i + 1, fire);
+            fire = i < D && (fire || test_fire(a.force_mod, u, i, D));
+            const unsigned fm = __ballot_sync(kFull, fire);
+            if (fm && limit == D) limit = 32 * c + __ffs(fm) - 1;
+            pv[c] = t + (t >= (uint32_t)u ? 1u : 0u);
+        }
+        uint32_t bk[MAXC];  // slice of each draw, B = not live
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+            const uint32_t i = 32 * c + lane;
+            uint32_t b = (uint32_t)((uint64_t)pv[c] * B / n);
+            if (b + 1 < B && bound(b + 1) <= pv[c]) ++b;
+            if (b > 0 && bound(b) > pv[c]) --b;
+            bk[c] = i < limit ? b : B;
+        }
+        uint32_t* off = offsets + (u - a.row_begin) * (B + 1);
+        uint32_t* out = lists + (u - a.row_begin) * D;
+        uint32_t pos = 0;  // running offset of slice b
+        for (uint32_t b = 0; b < B; ++b) {
+            if (lane == 0) off[b] = pos;
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) {
+                const unsigned m = __ballot_sync(kFull, bk[c] == b);
+                if (bk[c] == b) out[pos + __popc(m & lanemask_lt())] = pv[c];
+                pos += __popc(m);
+            }
+        }
+        if (lane == 0) off[B] = pos;
+    }
+}
+}  // namespace
+
+cudaError_t launch_partners(const GatherArgs& a, uint32_t* lists, uint32_t* offsets, cudaStream_t s,
+                            int num_sms) {
+    if (a.row_end <= a.row_begin || a.draws == 0) return cudaSuccess;
+    uint64_t blocks = (a.row_end - a.row_begin + 7) / 8;
+    if (blocks > (uint64_t)num_sms * 8) blocks = (uint64_t)num_sms * 8;
+    const unsigned g = (unsigned)blocks;
+    if (a.draws <= 256) k_partners<8><<<g, 256, 0, s>>>(a, lists, offsets);
+    else if (a.draws <= 512) k_partners<16><<<g, 256, 0, s>>>(a, lists, offsets);
+    else if (a.draws <= 1024) k_partners<32><<<g, 256, 0, s>>>(a, lists, offsets);
+    else return cudaErrorInvalidValue;
+    note_launch(1);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_gather_q8(const GatherArgs& a, const Q8Args& q, cudaStream_t s, int num_sms) {

@@ -617,3 +617,33 @@ def test_sort32_triangular_keys_boundary(oracle, monkeypatch, n):
         monkeypatch.setenv("SNGB_SORT32", mode)
         g = sng.build_sampled_graph(sng.Dataset(pts), eps, rate, seed=seed)
         np.testing.assert_array_equal(g.keys, keys)
+
+
+@pytest.mark.parametrize("pre", ["1", "0"])
+@pytest.mark.parametrize("force", [None, "5"])
+@pytest.mark.parametrize("chunks", ["8", "3"])
+def test_q8_host_upload_bucketed_partners(oracle, monkeypatch, pre, force, chunks):
+    """Host-buffer calls with the 8-bit head/tail gather over upload chunks read
+    their draws' partners from lists bucketed by partner slice (SNGB_PARTNERS=1)
+    instead of regenerating every earlier row's draws in each triangle launch;
+    an irregular vertex's lists stop at its first fired draw; uneven slices
+    (3 chunks).  Identical to the oracle either way, also for a row range."""
+    monkeypatch.setenv("SNGB_Q8", "2")
+    monkeypatch.setenv("SNGB_PARTNERS", pre)
+    monkeypatch.setenv("SNGB_Q8_CHUNKS", chunks)
+    if force:
+        monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
+    n, d = 4001, 784
+    pts = _q8_case(n, d, 61)
+    i = np.arange(0, n - 1, 7)
+    eps = float(np.quantile(np.sqrt(((pts[i] - pts[i + 1]) ** 2).sum(1)), 0.2))
+    rate, seed = 0.05, 61
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=eps, min_pts=3, rate=rate, seed=seed),
+                       info)
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, 3, rate, seed)
+    _assert_same(c, info, labels, roles, oinfo)
+    assert info.gpu["filter_bits"] == 8
+    rb, re = 1000, 3100
+    okeys, _ = oracle.sampled_edges_rows(pts, eps, rate, seed, rb, re)
+    np.testing.assert_array_equal(_host_edges_rows(pts, eps, rate, seed, rb, re), okeys)
