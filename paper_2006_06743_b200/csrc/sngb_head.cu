@@ -43,6 +43,13 @@
 #include "sngb_internal.cuh"
 #include "sngb_rng.cuh"
 
+#ifndef SNGB_HEAD_UF
+#define SNGB_HEAD_UF 2
+#endif
+#ifndef SNGB_HEAD_R
+#define SNGB_HEAD_R 4
+#endif
+
 namespace sngb {
 
 bool head_plan(double lo, double hi, uint32_t d, double eps2, int kind, HeadPlan& p) {
@@ -100,7 +107,7 @@ __global__ void k_head_quantize(const float* __restrict__ pts, uint32_t stride, 
 template <int KIND, int G, int V, int R>
 __global__ void __launch_bounds__(256, V >= 4 ? 2 : 4) k_gather_head(const GatherArgs a, const HeadArgs h) {
     constexpr int NG = 32 / G;
-    constexpr int UF = 2;               // fp32 rows per group per step
+    constexpr int UF = SNGB_HEAD_UF;    // fp32 rows per group per step
     constexpr int STEP = NG * UF;       // survivors per fp32 step
     constexpr int QCAP = 32 * R + STEP;  // queue: < STEP left over + one chunk's worth
     __shared__ unsigned long long s_stage[kWarpsPerBlock][kStage];
@@ -277,12 +284,13 @@ namespace {
 template <int KIND>
 cudaError_t head_dispatch(const GatherArgs& a, const HeadArgs& h, cudaStream_t s, int num_sms) {
     const uint32_t W = a.tp.stride / 4;  // stride is a multiple of 4 for d >= 3
-    if (W <= 2) return head_one<KIND, 2, 1, 4>(a, h, s, num_sms);
-    if (W <= 4) return head_one<KIND, 4, 1, 4>(a, h, s, num_sms);
-    if (W <= 8) return head_one<KIND, 8, 1, 4>(a, h, s, num_sms);
-    if (W <= 16) return head_one<KIND, 16, 1, 4>(a, h, s, num_sms);
-    if (W <= 32) return head_one<KIND, 32, 1, 4>(a, h, s, num_sms);
-    if (W <= 64) return head_one<KIND, 32, 2, 4>(a, h, s, num_sms);
+    constexpr int R = SNGB_HEAD_R;  // 32-draw chunks per step
+    if (W <= 2) return head_one<KIND, 2, 1, R>(a, h, s, num_sms);
+    if (W <= 4) return head_one<KIND, 4, 1, R>(a, h, s, num_sms);
+    if (W <= 8) return head_one<KIND, 8, 1, R>(a, h, s, num_sms);
+    if (W <= 16) return head_one<KIND, 16, 1, R>(a, h, s, num_sms);
+    if (W <= 32) return head_one<KIND, 32, 1, R>(a, h, s, num_sms);
+    if (W <= 64) return head_one<KIND, 32, 2, R>(a, h, s, num_sms);
     if (W <= 128) return head_one<KIND, 32, 4, 2>(a, h, s, num_sms);
     if (W <= 256) return head_one<KIND, 32, 8, 2>(a, h, s, num_sms);
     return cudaErrorInvalidValue;
