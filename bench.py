@@ -460,10 +460,8 @@ def main():
         else:
             l2_peak = None
     if head and gather_pairs:
-        # every pair reads its 4-byte head (L2), a fraction f its fp32 row (L2 or
-        # HBM by table size): the ceiling is the time-weighted mix of the two
-        # measured gathers; for an HBM-resident fp32 table the survivors' rows
-        # come at the measured random-row rate of that table, not the copy peak
+        # every pair reads its 2/4-byte head (L2), a fraction f its fp32 row (L2 or
+        # HBM by table size), each at the measured random-row rate of its table
         hb = getattr(info, "head_bytes", 4) or 4
         roofline["head_bytes"] = hb
         hcase, heads_per_s = load_head_ceiling(n, hb)
@@ -471,8 +469,17 @@ def main():
         f = max(0.0, (bpp - hb) / (4 * d))
         roofline["tail_fraction"] = f
         if heads_per_s and frows_per_s:
-            l2_peak = bpp / (1.0 / heads_per_s + f / frows_per_s) / 1e9
-            case = f"{hcase} + {rcase}"
+            # heads come from L2; survivors' rows from L2 too when the fp32 table
+            # fits it (one resource: the times add), from HBM otherwise (two
+            # resources working concurrently: the slower one bounds)
+            t_head, t_rows = 1.0 / heads_per_s, f / frows_per_s
+            rows_in_hbm = n * 4 * ((d + 3) // 4) > 100 * 2**20
+            t_pair = max(t_head, t_rows) if rows_in_hbm else t_head + t_rows
+            l2_peak = bpp / t_pair / 1e9
+            case = f"{hcase} {'max' if rows_in_hbm else '+'} {rcase}"
+            roofline["ceiling_model"] = ("max(head time, survivor-row time): L2 and HBM in "
+                                         "parallel" if rows_in_hbm else
+                                         "head time + survivor-row time: both from L2")
             resident = True
     eff = l2_peak if resident else peak
     roofline.update({
