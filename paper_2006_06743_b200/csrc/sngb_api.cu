@@ -96,7 +96,7 @@ struct DevCtx {
     cudaEvent_t up_ev[kMaxChunks] = {};
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
-        flags, rank, temp, labels, roles, work, q8, upload64, rnorm, band, partners, poff;
+        flags, rank, temp, labels, roles, work, q8, upload64, rnorm, band, partners, poff, rstart;
     cudaEvent_t qev = nullptr;  // min/max of the points copied to the host (8-bit filter)
     cudaEvent_t pev = nullptr;  // bucketed partner lists ready (host-upload 8-bit schedule)
     unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
@@ -106,7 +106,7 @@ struct DevCtx {
 
     void release() {
         for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
-                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band, &partners, &poff})
+                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band, &partners, &poff, &rstart})
             b->release();
     }
 };
@@ -857,6 +857,8 @@ void ensure_cluster_bufs(DevCtx& c, uint64_t n, ClusterBuffers& b) {
     b.rank = c.rank.as<uint32_t>();
     b.temp = c.temp.p;
     b.temp_bytes = c.temp.bytes;
+    c.rstart.ensure(n * 4);
+    b.rstart = c.rstart.as<uint32_t>();
 }
 
 void fill_info(sngb_info* info, const unsigned long long* hc, uint64_t n, uint32_t d,

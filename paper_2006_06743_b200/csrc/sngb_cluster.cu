@@ -45,18 +45,22 @@ __device__ __forceinline__ void decode(unsigned long long k, uint32_t nb, uint32
 // for the degree, and union-find keeps a's root across the run.
 constexpr int kRun = 8;
 
+// rstart (optional): the index of each vertex's first key (the start of its
+// run), for the vertex-parallel Afforest rounds of k_union_nth.
 __global__ void k_degrees(const unsigned long long* __restrict__ keys, const unsigned long long* m_ptr,
-                          uint64_t m_host, uint32_t nb, uint32_t* deg) {
+                          uint64_t m_host, uint32_t nb, uint32_t* deg, uint32_t* rstart = nullptr) {
     const uint64_t m = m_ptr ? *m_ptr : m_host;
     for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c * kRun < m;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t e1 = (c + 1) * kRun < m ? (c + 1) * kRun : m;
         uint32_t run_a = 0xffffffffu, run = 0;
+        if (rstart && c > 0) run_a = (uint32_t)(keys[c * kRun - 1] >> nb);  // previous key's a
         for (uint64_t e = c * kRun; e < e1; ++e) {
             uint32_t a, b;
             decode(keys[e], nb, a, b);
             if (a != run_a) {
                 if (run) atomicAdd(&deg[run_a], run);
+                if (rstart) rstart[a] = (uint32_t)e;  // a run starts here
                 run_a = a;
                 run = 0;
             }
@@ -141,6 +145,31 @@ __global__ void k_union_first(const unsigned long long* __restrict__ keys,
         if (e < nth || (uint32_t)(keys[e - nth] >> nb) != a) continue;
         if (e > nth && (uint32_t)(keys[e - nth - 1] >> nb) == a) continue;
         if (!core[a] || !core[b]) continue;
+        for (;;) {
+            const uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
+            if (ra == rb) break;
+            const uint32_t lo = ra < rb ? ra : rb, hi = ra < rb ? rb : ra;
+            if (atomicCAS(&parent[hi], hi, lo) == hi) break;
+        }
+    }
+}
+
+// The same Afforest round, vertex-parallel: vertex v's nth neighbour is the key
+// at rstart[v] + nth when it still belongs to v's run (n threads instead of m).
+__global__ void k_union_nth(const unsigned long long* __restrict__ keys,
+                            const unsigned long long* m_ptr, uint64_t n, uint32_t nb,
+                            const uint32_t* __restrict__ rstart, const uint8_t* __restrict__ core,
+                            uint32_t* parent, uint32_t nth) {
+    const uint64_t m = *m_ptr;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s0 = rstart[v];
+        if (s0 == 0xffffffffu || !core[v]) continue;
+        const uint64_t e = (uint64_t)s0 + nth;
+        if (e >= m) continue;
+        uint32_t a, b;
+        decode(keys[e], nb, a, b);
+        if (a != (uint32_t)v || !core[b]) continue;
         for (;;) {
             const uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
             if (ra == rb) break;
@@ -449,7 +478,11 @@ cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned
     cudaError_t e = cudaMemsetAsync(b.deg, 0, n * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
     const unsigned ge = grid_for(m, num_sms), gn = grid_for(n + 1, num_sms);
-    if (m) k_degrees<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.deg);
+    if (b.rstart && m) {
+        e = cudaMemsetAsync(b.rstart, 0xff, n * sizeof(uint32_t), s);
+        if (e != cudaSuccess) return e;
+    }
+    if (m) k_degrees<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.deg, b.rstart);
     k_init<<<gn, 256, 0, s>>>(b.deg, n, (uint32_t)min_pts, b.core, b.parent, b.broot, b.first);
     if (m) {
         // Afforest-style sampling rounds, each vertex's first then second
@@ -460,7 +493,11 @@ cudaError_t cluster_unique_edges(const unsigned long long* ukeys, const unsigned
             return e ? std::max(0, std::atoi(e)) : 2;
         }();
         for (int r = 0; r < rounds; ++r) {
-            k_union_first<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.core, b.parent, (uint32_t)r);
+            if (b.rstart && m_ptr)
+                k_union_nth<<<gn, 256, 0, s>>>(ukeys, m_ptr, n, nb, b.rstart, b.core, b.parent,
+                                               (uint32_t)r);
+            else
+                k_union_first<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.core, b.parent, (uint32_t)r);
             k_compress<<<gn, 256, 0, s>>>(n, b.core, b.parent);
         }
         k_union<<<ge, 256, 0, s>>>(ukeys, m_ptr, 0, nb, b.core, b.parent);

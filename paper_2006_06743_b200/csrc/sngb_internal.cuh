@@ -259,6 +259,7 @@ struct ClusterBuffers {
     uint32_t* rank;               // n + 1
     void* temp;
     size_t temp_bytes;
+    uint32_t* rstart = nullptr;   // n: first key of each vertex's run (null: edge-based rounds)
 };
 
 // Sort + unique raw keys; returns pointer to the unique keys (one of the two
