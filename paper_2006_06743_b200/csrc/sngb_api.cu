@@ -428,9 +428,9 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     // ---- capacities ----
     uint64_t pairs;
     if (exhaustive) {
-        // rows [rb, re) pair with all v > u
+        // rows [rb, re) pair with all v > u, and (a partial range) with all v < rb
         const double sum = (double)rows * (double)(n - 1) - ((double)re * (re - 1) - (double)rb * (rb - 1)) / 2.0;
-        pairs = (uint64_t)std::max(0.0, sum);
+        pairs = (uint64_t)std::max(0.0, sum) + rows * rb;
     } else {
         pairs = rows * draws;
     }
@@ -763,6 +763,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             prepared = quantized = chunks;
             ensure_norms();
             for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
+        }
+        if (exhaustive && rb > 0) {  // a row range: its rows' pairs with every v < rb too
+            ga.exh_low = (uint32_t)rb;
+            for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
+            ga.exh_low = 0;
         }
         if (prio) {
             CK(cudaEventRecord(c.hi_join, c.hi));

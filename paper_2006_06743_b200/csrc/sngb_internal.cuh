@@ -81,6 +81,8 @@ struct GatherArgs {
     uint32_t force_mod;   // test hook (0 = off), see test_fire()
     uint32_t part_lo, part_hi;  // partner rows tested by this launch (L2-blocked phases)
     uint32_t rows_per_block;    // 0: persistent grid; else one block per this many rows
+    uint32_t exh_low;           // exhaustive, nonzero: partners are v < exh_low (the rows below a
+                                // row range: graph.cpp:157-159 pairs a row with every v != u)
     unsigned long long* work;   // non-null: warps claim `grab` rows at a time from *work (zeroed)
     uint32_t grab;
     // Bucketed partner lists (k_partners; 8-bit head/tail gather only): row u's

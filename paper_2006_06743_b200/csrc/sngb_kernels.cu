@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
                 else q2[vv] = to_x2(qv[vv]);
             }
         }
-        uint32_t limit = EXH ? (uint32_t)(a.n - 1 - u) : a.draws;
+        uint32_t limit = EXH ? (a.exh_low ? a.exh_low : (uint32_t)(a.n - 1 - u)) : a.draws;
         // stream_at(key, i + 1) for i = i0 + 32k + lane, carried incrementally
         // (nothing for ptxas to rematerialise from the vertex key per chunk)
         uint64_t z = EXH ? 0ull : vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const uint32_t i = i0 + 32 * k + lane;
-                    pvk[k] = EXH ? (uint32_t)u + 1 + i : pv[k];
+                    pvk[k] = EXH ? (a.exh_low ? i : (uint32_t)u + 1 + i) : pv[k];
                     vmk[k] = __ballot_sync(kFull, i < limit && pvk[k] >= plo && pvk[k] < phi);
                     any |= vmk[k];
                 }
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256, MinBlocks<G, V>::value) k_gather(const Ga
 #pragma unroll
             for (int k = 0; k < R; ++k) {
                 const uint32_t i = i0 + 32 * k + lane;
-                const uint32_t p = EXH ? (uint32_t)u + 1 + i : pv[k];
+                const uint32_t p = EXH ? (a.exh_low ? i : (uint32_t)u + 1 + i) : pv[k];
                 const bool live = i < limit && p >= plo && p < phi;
                 const unsigned m = __ballot_sync(kFull, live);
                 if (live) list[nlive + __popc(m & lanemask_lt())] = p;

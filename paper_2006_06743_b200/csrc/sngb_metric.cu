@@ -96,13 +96,13 @@ __global__ void __launch_bounds__(256) k_gather_metric(const GatherArgs a) {
     };
     if (a.work) grab();
     for (; u < chunk_end; (a.work && u + 1 >= chunk_end) ? grab() : (void)(u += a.work ? 1 : nw)) {
-        uint32_t limit = EXH ? (uint32_t)(a.n - 1 - u) : a.draws;
+        uint32_t limit = EXH ? (a.exh_low ? a.exh_low : (uint32_t)(a.n - 1 - u)) : a.draws;
         uint64_t z = EXH ? 0ull : vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
         for (uint32_t i0 = 0; i0 < limit; i0 += 32, z += 32ull * kGamma) {
             const uint32_t i = i0 + lane;
             uint32_t p;
             if (EXH) {
-                p = (uint32_t)u + 1 + i;
+                p = a.exh_low ? i : (uint32_t)u + 1 + i;
             } else {
                 const bool valid = i < limit;
                 bool fire = false;

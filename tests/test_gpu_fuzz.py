@@ -87,6 +87,12 @@ def test_fuzz_matches_oracle(oracle, monkeypatch, cid, n, d, kind, rate, q, env,
         keys, _ = sng.sampled_edges_device(x, eps, rate, seed)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(keys.cpu().numpy().view(np.uint64), okeys)
+        if n >= 8:  # a query-row range (the multi-GPU shard step)
+            rb, re = n // 4, n - n // 3
+            rkeys, _ = sng.sampled_edges_device(x, eps, rate, seed, row_begin=rb, row_end=re)
+            torch.cuda.synchronize()
+            orkeys, _ = oracle.sampled_edges_rows(pts, eps, rate, seed, rb, re)
+            np.testing.assert_array_equal(rkeys.cpu().numpy().view(np.uint64), orkeys)
         np.testing.assert_array_equal(gl.cpu().numpy(), labels)
         np.testing.assert_array_equal(gr.cpu().numpy(), roles)
         assert gi.edges == oinfo["edges"] and gi.distance_evals == oinfo["distance_evals"]
