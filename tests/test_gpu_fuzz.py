@@ -104,3 +104,75 @@ def test_fuzz_matches_oracle(oracle, monkeypatch, cid, n, d, kind, rate, q, env,
         np.testing.assert_array_equal(c.role, roles)
         assert info.edges == oinfo["edges"] and info.distance_evals == oinfo["distance_evals"]
         assert c.cluster_count == oinfo["cluster_count"]
+
+
+def _ref_cases():
+    rng = np.random.default_rng(7_2026)
+    out = []
+    for cid in range(60):
+        n = int(rng.choice([2, 5, 300, 2000, 6000]))
+        d = int(rng.choice([1, 2, 3, 7, 16, 33, 130, 784]))
+        metric = str(rng.choice(["euclidean", "manhattan", "cosine"]))
+        f64 = bool(rng.integers(0, 2))
+        rate = float(rng.choice([0.01, 0.05, 0.3, 1.0]))
+        pairs = n * max(1, min(int(np.ceil(rate * n)), n - 1))
+        d = max(1, min(d, 60_000_000 // pairs))
+        kind = str(rng.choice(["uniform", "blobs", "grid", "offset", "outlier"]))
+        q = float(rng.choice([0.01, 0.1, 0.4]))
+        env = ENVS[cid % len(ENVS)]
+        out.append(pytest.param(cid, n, d, metric, f64, rate, kind, q, env,
+                                id=f"r{cid}-n{n}-d{d}-{metric}-{'f64' if f64 else 'f32'}-r{rate}"))
+    return out
+
+
+@pytest.mark.parametrize("cid,n,d,metric,f64,rate,kind,q,env", _ref_cases())
+def test_fuzz_metrics_fp64_match_reference(monkeypatch, cid, n, d, metric, f64, rate, kind, q, env):
+    """Manhattan / cosine / Euclidean on fp32 and fp64 rows against the
+    reference compiled from its own sources (oracle/_ref): labels, roles,
+    counters and edge lists identical."""
+    import os
+    from oracle import REF_SO, Reference
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref/libsngref.so not built")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(5000 + cid)
+    pts = _data(rng, n, d, kind).astype(np.float64)
+    if metric == "cosine":
+        pts = pts + 0.5 + np.abs(pts).max()  # no row at the origin (the reference's error)
+    if f64:
+        pts = pts + rng.normal(0, 1e-7, pts.shape) * (np.abs(pts) + 1.0)
+    else:
+        pts = pts.astype(np.float32)
+    i = rng.integers(0, n, 256)
+    j = rng.integers(0, n, 256)
+    a, b = pts[i].astype(np.float64), pts[j].astype(np.float64)
+    if metric == "manhattan":
+        dist = np.abs(a - b).sum(1)
+    elif metric == "cosine":
+        dist = 1 - (a * b).sum(1) / np.linalg.norm(a, axis=1) / np.linalg.norm(b, axis=1)
+    else:
+        dist = np.sqrt(((a - b) ** 2).sum(1))
+    eps = float(np.quantile(dist, q))
+    if not eps > 0.0:
+        eps = 1e-3
+    min_pts = int(rng.integers(1, 5))
+    seed = int(rng.integers(0, 2**63))
+    ref = Reference()
+    ref.set_metric(metric)
+    try:
+        rds = ref.dataset(pts)
+        labels, roles, rinfo = ref.sng_dbscan(rds, eps, min_pts, rate, seed)
+        keys, _, _ = ref.sampled_edges(rds, eps, rate, seed)
+    finally:
+        ref.set_metric("euclidean")
+    ds = sng.Dataset(pts)
+    dm = sng.Distance.parse(metric)
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(ds, sng.SngParams(eps=eps, min_pts=min_pts, rate=rate, seed=seed, dist=dm),
+                       info)
+    np.testing.assert_array_equal(c.assignment, labels)
+    np.testing.assert_array_equal(c.role, roles)
+    assert info.edges == rinfo["edges"] and info.distance_evals == rinfo["distance_evals"]
+    g = sng.build_sampled_graph(ds, eps, rate, dist=dm, seed=seed)
+    np.testing.assert_array_equal(g.keys, keys)
