@@ -492,6 +492,28 @@ def main():
         "frac_of_effective_peak": (achieved / eff) if (achieved and eff) else None,
         "concurrent_with": ("the Floyd kernel on a side stream (in the step)" if overlapped
                             else None)})
+    # Two more bounds the gather is held against: the draws it
+    # regenerates against the measured RNG throughput (tools/microbench.cu
+    # rng_draw), and for rows narrower than an L2 sector (32 B) the share of
+    # each fetched sector that is algorithmic bytes.
+    rng_peak = None
+    try:
+        for ln in open(os.path.join(ROOT, "profiles", "r01_microbench.jsonl")):
+            rec = json.loads(ln)
+            if rec.get("bench") == "rng_draw":
+                rng_peak = rec["draws_per_s"]
+    except Exception:
+        pass
+    if g_ms > 0 and gather_pairs:
+        draws_s = gather_pairs / (g_ms / 1e3)
+        roofline["rng"] = {"draws_per_s": draws_s, "ceiling_draws_per_s": rng_peak,
+                           "frac": (draws_s / rng_peak) if rng_peak else None,
+                           "source": "profiles/r01_microbench.jsonl rng_draw (one SplitMix64 + "
+                                     "Lemire draw per lane, no memory traffic)"}
+    if not q8 and not head and 4 * d < 32:
+        row = 8 if d <= 2 else 16
+        roofline["sector_efficiency"] = {"row_bytes": row, "algorithmic_bytes": 4 * d,
+                                         "sector_bytes": 32, "frac": 4 * d / 32}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
