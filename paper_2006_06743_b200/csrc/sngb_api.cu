@@ -96,17 +96,20 @@ struct DevCtx {
     cudaEvent_t up_ev[kMaxChunks] = {};
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
-        flags, rank, temp, labels, roles, work, q8, upload64, rnorm, band, partners, poff, rstart;
+        flags, rank, temp, labels, roles, work, q8, upload64, rnorm, band, partners, poff, rstart,
+        colstats, perm;
     cudaEvent_t qev = nullptr;  // min/max of the points copied to the host (8-bit filter)
     cudaEvent_t pev = nullptr;  // bucketed partner lists ready (host-upload 8-bit schedule)
     unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
+    double* h_colstats = nullptr;  // pinned: per-column sums (8-bit filter column order)
+    uint32_t* h_perm = nullptr;    // pinned: that column order, uploaded per call
     cudaEvent_t ev[12] = {};
     uint64_t edge_hint = 0;  // last needed edge capacity for this context
     uint64_t band_hint = 0;  // last needed band-list capacity
 
     void release() {
         for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
-                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band, &partners, &poff, &rstart})
+                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band, &partners, &poff, &rstart, &colstats, &perm})
             b->release();
     }
 };
@@ -165,6 +168,8 @@ DevCtx& get_ctx(int dev, int slot = 0) {
         CK(cudaEventCreateWithFlags(&c->up_start, cudaEventDisableTiming));
         for (auto& e : c->up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaMallocHost(&c->h_counters, C_COUNT * sizeof(unsigned long long)));
+        CK(cudaMallocHost(&c->h_colstats, 2 * kQ8MaxD * sizeof(double)));
+        CK(cudaMallocHost(&c->h_perm, kQ8MaxD * sizeof(uint32_t)));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
         g_ctx[idx] = std::move(c);
     }
@@ -388,7 +393,21 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     };
     // after the last prepare: the min/max to the host, waited for only when the
     // 8-bit plan is made (the sampler is already running by then)
-    auto minmax_to_host = [&]() {
+    // With the 8-bit filter also the per-column statistics of the rows prepared so
+    // far (rows_ready): the head then holds the columns of largest variance.
+    bool perm_try = false;
+    uint64_t stats_rows = 0;
+    auto minmax_to_host = [&](uint64_t rows_ready) {
+        if (perm_try) {
+            // the order of the column variances from a sample of the rows (the
+            // first 8192: a full pass measured 60-110 us on cfg2's critical path)
+            rows_ready = std::min<uint64_t>(rows_ready, 8192);
+            CK(launch_colstats(pts, stride, rows_ready, d, d_pts64, c.colstats.as<double>(), gs,
+                               c.num_sms));
+            CK(cudaMemcpyAsync(c.h_colstats, c.colstats.p, 2ull * d * sizeof(double),
+                               cudaMemcpyDeviceToHost, gs));
+            stats_rows = rows_ready;
+        }
         CK(cudaMemcpyAsync(&c.h_counters[C_QMIN], &dc[C_QMIN], 2 * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, gs));
         CK(cudaEventRecord(c.qev, gs));
@@ -400,7 +419,9 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     // SNGB_Q8: 0 off, 1 auto (use when the band is narrow), 2 force (tests)
     const uint64_t q8_mode = env_u64("SNGB_Q8", 1);
     // the 8-bit gathers hold a row in <= 3 chunks per lane: d <= 16 * (3 * 32 - 1)
-    q8_try = metric == kMetricEuclid && !exhaustive && d >= 128 && d <= 1520 && q8_mode != 0;
+    q8_try = metric == kMetricEuclid && !exhaustive && d >= 128 && d <= kQ8MaxD && q8_mode != 0;
+    perm_try = q8_try && env_u64("SNGB_Q8_PERM", 1) != 0;  // variance-ordered columns
+    if (perm_try) c.colstats.ensure(2ull * d * sizeof(double));
     // SNGB_HEAD: 0 off, 1 auto, 2 force (tests); SNGB_HEAD_KIND picks the format.
     // Auto for large problems whose head table stays L2-resident (a table read
     // by every SM keeps about half the L2): 4-byte heads up to 0.4 L2, 2-byte
@@ -455,7 +476,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     double round_dist = 0.0, max_abs = 0.0;
     if (f64) {
         prepare_rows(0, n);
-        minmax_to_host();
+        minmax_to_host(n);
         CK(cudaEventSynchronize(c.qev));
         const double lo = ordered_value64(~c.h_counters[C_QMIN]);
         const double hi = ordered_value64(c.h_counters[C_QMAX]);
@@ -522,7 +543,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     if (side_pre) CK(cudaEventRecord(c.fork, s));
     if (!h_src && !f64) {
         prepare_rows(0, n);
-        if (q8_try || head_try) minmax_to_host();
+        if (q8_try || head_try) minmax_to_host(n);
     }
     tm.mark(E_PREPARED);
     bool q8_on = false, head_on = false;
@@ -626,7 +647,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                     prepare_rows(chunk_lo(k), chunk_lo(k + 1));
                 }
                 prepared = upto;
-                minmax_to_host();
+                minmax_to_host(chunk_lo(upto));
             }
             // a re-plan reads the global min/max kept in h_counters by the last sync
             if (!q8_replan) CK(cudaEventSynchronize(c.qev));
@@ -652,6 +673,42 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             q8_pipe = q8_on && pipe;
             q8_replan = false;
             if (!head_on) gphases = phases;
+            if (q8_on && perm_try && stats_rows > 0 && !q8_replan) {
+                // column order by decreasing variance (stable): the head's 240 values
+                // are the most spread-out coordinates (a real image's constant
+                // borders go last); any order is exact
+                const double m = (double)stats_rows;
+                std::vector<double> var(d);
+                for (uint32_t k = 0; k < d; ++k) {
+                    const double mu = c.h_colstats[k] / m;
+                    var[k] = c.h_colstats[d + k] / m - mu * mu;
+                }
+                std::vector<uint32_t> order(d);
+                for (uint32_t k = 0; k < d; ++k) order[k] = k;
+                std::stable_sort(order.begin(), order.end(),
+                                 [&](uint32_t x, uint32_t y) { return var[x] > var[y]; });
+                bool identity = true;
+                for (uint32_t k = 0; k < d; ++k) {
+                    c.h_perm[k] = order[k];
+                    identity = identity && order[k] == k;
+                }
+                // worth a permuted quantisation only if the natural head holds
+                // much less variance than the best one (an image's blank border;
+                // cfg2's iid columns: no -- there it costs the step 0.1 ms)
+                double nat = 0.0, best = 0.0;
+                for (uint32_t k = 0; k < std::min<uint32_t>(d, kHeadVals); ++k) {
+                    nat += std::max(0.0, var[k]);
+                    best += std::max(0.0, var[order[k]]);
+                }
+                if (nat >= 0.5 * best) identity = true;
+                q8p.perm = nullptr;
+                if (!identity) {
+                    c.perm.ensure(d * sizeof(uint32_t));
+                    CK(cudaMemcpyAsync(c.perm.p, c.h_perm, d * sizeof(uint32_t),
+                                       cudaMemcpyHostToDevice, gs));
+                    q8p.perm = c.perm.as<uint32_t>();
+                }
+            }
             if (q8_on) {
                 const uint32_t nd = (d + 15) / 16;
                 c.q8.ensure(n * (nd + 1) * 16ull);

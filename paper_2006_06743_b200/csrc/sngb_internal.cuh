@@ -210,10 +210,15 @@ struct Q8Args {
     int32_t accept_max;  // Q2 <= accept_max: the reference accepts
     int32_t reject_min;  // Q2 >  reject_min: the reference rejects (else exact recheck)
 };
+constexpr uint32_t kQ8MaxD = 1520;  // widest rows of the 8-bit filter (3 chunks per lane)
 struct Q8Plan {
     double s, lo;  // scale (a power of two) and offset (a multiple of s)
     Q8Args args;
+    const uint32_t* perm = nullptr;  // device: stored value k = column perm[k] (null: identity)
 };
+// per-column sums and sums of squares (stats[0..d) and stats[d..2d)), fp64
+cudaError_t launch_colstats(const float* pts, uint32_t stride, uint64_t n, uint32_t d,
+                            const double* pts64, double* stats, cudaStream_t s, int num_sms);
 bool q8_plan(double lo, double hi, uint32_t d, double eps2, Q8Plan& p);
 bool q8_split(uint32_t nd);  // rows of nd data chunks take the early-reject gather
 cudaError_t launch_quantize(const float* pts, uint32_t stride, uint64_t n, uint32_t d,

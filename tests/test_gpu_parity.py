@@ -647,3 +647,38 @@ def test_q8_host_upload_bucketed_partners(oracle, monkeypatch, pre, force, chunk
     rb, re = 1000, 3100
     okeys, _ = oracle.sampled_edges_rows(pts, eps, rate, seed, rb, re)
     np.testing.assert_array_equal(_host_edges_rows(pts, eps, rate, seed, rb, re), okeys)
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_q8_variance_ordered_head(oracle, monkeypatch, host):
+    """Rows whose first 300 coordinates are constant (an image's blank border):
+    with the columns stored in order of decreasing variance the 8-bit head
+    rejects as usual; in natural order it cannot (its values never differ).
+    Identical to the oracle either way; the head order reads far fewer bytes."""
+    import torch
+    rng = np.random.default_rng(71)
+    n, d = 6000, 784
+    centers = rng.random((10, d - 300), dtype=np.float32)
+    body = centers[rng.integers(0, 10, n)] + rng.normal(0, 0.1, (n, d - 300)).astype(np.float32)
+    pts = np.ascontiguousarray(np.concatenate([np.zeros((n, 300), np.float32), body], 1))
+    eps, rate, seed = 3.5, 0.05, 71
+    labels, roles, oinfo, keys = oracle.sng_dbscan(pts, eps, 5, rate, seed)
+    monkeypatch.setenv("SNGB_Q8", "2")
+    got = {}
+    for perm in ("1", "0"):
+        monkeypatch.setenv("SNGB_Q8_PERM", perm)
+        if host:
+            info = sng.ClusterRunInfo()
+            c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=eps, min_pts=5, rate=rate,
+                                                               seed=seed), info)
+            _assert_same(c, info, labels, roles, oinfo)
+            got[perm] = info.gpu["gather_bytes"]
+        else:
+            x = torch.from_numpy(pts).cuda()
+            gl, gr, gi = sng.sng_dbscan_device(x, eps, 5, rate, seed)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(gl.cpu().numpy(), labels)
+            np.testing.assert_array_equal(gr.cpu().numpy(), roles)
+            assert gi.edges == oinfo["edges"]
+            got[perm] = gi.gather_bytes
+    assert got["1"] < 0.6 * got["0"], got
