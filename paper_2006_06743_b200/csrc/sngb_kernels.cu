@@ -64,10 +64,19 @@ struct Unroll {
 #ifndef SNGB_WIDE_MINB
 #define SNGB_WIDE_MINB 1
 #endif
+// A/B build knobs (python -m paper_2006_06743_b200.build --variant ...): cfg1's
+// gather measured 0.191 ms at the defaults, 0.216 / 0.229 with 6 / 8 blocks per
+// SM, 0.195 / 0.211 with 2 / 8 draw chunks per step
+#ifndef SNGB_NARROW_MINB
+#define SNGB_NARROW_MINB 4
+#endif
+#ifndef SNGB_F2_R
+#define SNGB_F2_R 4
+#endif
 template <int G, int V>
 struct MinBlocks {
     static constexpr int value =
-        G == 32 ? (V == 8 ? 2 : SNGB_WIDE_MINB) : (G == 16 ? 2 : (G == 8 ? 3 : 4));
+        G == 32 ? (V == 8 ? 2 : SNGB_WIDE_MINB) : (G == 16 ? 2 : (G == 8 ? 3 : SNGB_NARROW_MINB));
 };
 
 template <int G, int V, int R, bool F2, bool EXH>
@@ -531,7 +540,7 @@ cudaError_t gather_one(const GatherArgs& a, cudaStream_t s, int num_sms) {
 
 template <bool EXH>
 cudaError_t gather_dispatch(const GatherArgs& a, cudaStream_t s, int num_sms) {
-    if (a.tp.stride == 2) return gather_one<1, 1, 4, true, EXH>(a, s, num_sms);
+    if (a.tp.stride == 2) return gather_one<1, 1, SNGB_F2_R, true, EXH>(a, s, num_sms);
     const uint32_t W = a.tp.stride / 4;
     // 16-byte rows: 2 chunks of 32 draws per step (R = 4 spilled at 64 registers
     // and measured 37 % slower on cfg4)
