@@ -538,7 +538,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     // the sampler (run together they slow the gather more than they gain).  The
     // fork is recorded here, before the prepare pass.
     const bool side_pre = !exhaustive && !h_src && (q8_try || head_try) &&
-                          !(stride <= 64 && (re - rb) >= 10000) &&  // not the overlap case
+                          !(stride <= 64 && (re - rb) >= 10000 && draws <= 1024) &&  // not overlap
                           env_u64("SNGB_OVERLAP", 2) != 1 && env_u64("SNGB_SIDE_PRE", 1) != 0;
     if (side_pre) CK(cudaEventRecord(c.fork, s));
     if (!h_src && !f64) {
@@ -580,8 +580,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         // dynamic claiming, which a non-persistent gather grid lost); wide-row
         // problems run the sampler beside prepare/plan/quantise instead.
         const uint64_t ov = env_u64("SNGB_OVERLAP", 2);
+        // (with the 4-block Floyd filter kernel, draws > 1024 lost: its blocks then
+        // crowd the gather's -- cfg5 876 vs 646 ms, cfg4 130 vs 96 ms)
         const bool overlap =
-            !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 10000));
+            !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 10000 &&
+                                        draws <= 1024));
         // host upload: the sampler reads no points, so it also runs while they arrive
         const bool side = !exhaustive && (overlap || side_pre || (h_src && attempt == 0));
         if (pre_partners && attempt == 0) {  // before the sampler on the side stream
@@ -619,7 +622,10 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 // the Floyd bookkeeping needs no point data: run it on the side
                 // stream while the gather runs here; non-persistent grids let the
                 // block scheduler interleave the two kernels on every SM
-                sa.rows_per_block = (uint32_t)env_u64("SNGB_SAMPLER_RPB", overlap ? 32 : 0);
+                // non-persistent beside the gather (and during a host upload, where the
+                // gather starts while it runs: cfg5 e2e 614 vs 943 ms persistent)
+                sa.rows_per_block =
+                    (uint32_t)env_u64("SNGB_SAMPLER_RPB", (overlap || h_src) ? 32 : 0);
                 if (!(side_pre && attempt == 0)) CK(cudaEventRecord(c.fork, s));
                 CK(cudaStreamWaitEvent(c.side, c.fork, 0));
                 tm.mark_on(E_SIDE0, c.side);

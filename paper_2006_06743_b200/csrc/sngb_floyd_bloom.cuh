@@ -136,7 +136,14 @@ constexpr int kBarFree = 4;     // + parity: resolver is done with that parity (
 constexpr int kBloomBlock = kBloomThreads + 32;
 
 template <int MAXR>
-__global__ void __launch_bounds__(kBloomBlock) k_floyd_bloom(const SamplerArgs a) {
+// Four resident blocks per SM (<= 56 registers, no spills): the kernel is
+// latency-bound on its shared-memory filter and barriers, and the fourth block
+// beats the heuristic's 72 registers / 3 blocks (cfg5 352 -> 321 ms, cfg4
+// 53.4 -> 51.4 ms, cfg3 5.26 -> 5.19 ms; 3 blocks measured no better).
+#ifndef SNGB_BLOOM_MINB
+#define SNGB_BLOOM_MINB 4
+#endif
+__global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_bloom(const SamplerArgs a) {
     constexpr int kT = kBloomThreads;
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t WB = a.hash_mask;  // filter words (2^B / 32)
