@@ -4,6 +4,11 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...     (rows sharded over N GPUs)
 
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself as
+N ranks (python -m torch.distributed.run --nproc-per-node N ...), one per GPU.
+The default workload is BASELINE.json's largest config that fits one GPU:
+cfg5 (n = 20 M, d = 32); --config 1..4 selects the other shapes.
+
 A "step" is one full sng::sng_dbscan (clusterer.cpp:54-65) over one synthetic
 workload: sample + eps-test every vertex's draws, symmetrise/dedup, degrees,
 core mask, union-find, border, relabel.  The metric is BASELINE.json's:
@@ -15,12 +20,18 @@ end-to-end clustering time, and the gather kernel's fraction of roofline.
             write) before every timed step, max over ranks.
   e2e       the public host API (sngb_dbscan_f32 through the C ABI) from
             pinned host memory: H2D of the points and D2H of labels+roles
-            inside the timed region.
-  roofline  gather kernel: algorithmic bytes (4*d per evaluated pair) over its
-            CUDA-event duration measured inside the library on the same stream,
-            against MEASURED_PEAKS.json hbm_gbs.
+            inside the timed region; its labels must equal the device-resident
+            run's (checked every run).  e2e_pageable: the same call from the
+            pageable numpy array the Python / C++ mirrors pass.
+  roofline  the dominant kernel's own algorithmic bytes over its CUDA-event
+            duration (measured inside the library on its stream) against the
+            measured random-gather ceiling of the memory level it reads
+            (tools/gather_ceiling.cu); frac_8d is SURVEY 8(d)'s 4*d bytes per
+            pair against MEASURED_PEAKS.json hbm_gbs -- an effective rate (the
+            filters read far fewer bytes), not a roofline fraction.
   cpu_baseline  the reference's own graph.cpp/clusterer.cpp (oracle/_ref,
-            compiled unmodified) on this host's cores, rank 0, N=1 only.
+            compiled unmodified) on this host's cores, rank 0, N=1 only, on the
+            FULL dataset with fewer draws per vertex (a bounded sample).
 """
 from __future__ import annotations
 
@@ -40,7 +51,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "sampled_pairs_per_sec"
 UNIT = "pairs/s"
-DEFAULT_CONFIG = 2  # BASELINE.json configs[1]
+DEFAULT_CONFIG = 5  # BASELINE.json configs[4]: the largest config that fits one GPU
 
 
 def parse():
@@ -52,6 +63,7 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-pageable", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=25.0,
                    help="CPU seconds allowed for the cpu_baseline sample")
     return p.parse_args()
@@ -111,6 +123,16 @@ def load_head_ceiling(n: int, hb: int = 4):
         return None, None
     best = min(same, key=lambda c: abs(math.log(c["table_MB"] * 2**20 / max(hb * n, 1))))
     return best["bench"], best["rows_per_s"]
+
+
+def load_ncu(workload: str):
+    """Key counters of the dominant kernel from the committed ncu --set full capture
+    (profiles/ncu_metrics.json, written by tools/ncu_summary.py --json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_metrics.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
 
 
 def load_traffic(workload: str):
@@ -175,54 +197,89 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
-def _ref_sample(pts, w, m):
-    """Row-prefix sample of m rows keeping each vertex's draws (same d, same per-pair work)."""
-    n, draws = pts.shape[0], w.draws
-    if m >= n:
-        return pts, w.rate, f"full workload (n={n}, draws={draws})"
-    rate = draws / m
-    return (np.ascontiguousarray(pts[:m]), rate,
-            f"first {m} rows of the workload, rate={rate:.6g} so each vertex keeps "
-            f"draws={draws} (same d, same per-pair work)")
+def _workload_config(w, n_gpus: int, extra: dict | None = None) -> dict:
+    """The config dict both arms print (same keys, so the driver can match them)."""
+    c = {"workload": w.name, "n": w.n, "d": w.d, "eps": w.eps, "rate": w.rate,
+         "min_pts": w.min_pts, "seed": w.seed, "draws": w.draws, "pairs": w.pairs,
+         "parallelism": f"rows sharded x{n_gpus}" if n_gpus > 1 else "1 GPU",
+         "l2": "256 MB L2 flush before every timed step"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+def _ref_rate(w, draws_s: int) -> float:
+    """A rate whose draws = min(ceil(rate*n), n-1) is exactly draws_s (graph.cpp:139-140)."""
+    n = w.n
+    rate = draws_s / n
+    while min(math.ceil(rate * float(n)), n - 1) > draws_s:
+        rate = math.nextafter(rate, 0.0)
+    while min(math.ceil(rate * float(n)), n - 1) < draws_s:
+        rate = math.nextafter(rate, 1.0)
+    return rate
+
+
+def _ref_draws(w, pairs_per_s: float, budget_s: float, fixed_s: float) -> int:
+    """Draws per vertex so one reference call on the full dataset takes ~budget_s."""
+    per_vertex = max(0.0, budget_s - fixed_s) * pairs_per_s / w.n
+    return int(max(1, min(w.draws, per_vertex)))
+
+
+def _ref_probe(ref, ds, w):
+    """Two short reference calls on the full dataset (1 and a few draws per
+    vertex) give its fixed per-call cost and its pairs/s."""
+    # ~2e8 pairs at d <= 16 (a second or two on 8-16 cores), fewer for wide rows
+    probe_pairs = 2e8 * 16 / max(w.d, 16)
+    d_lo, d_hi = 1, int(min(w.draws, max(2, probe_pairs // w.n)))
+    _, _, i_lo = ref.sng_dbscan(ds, w.eps, w.min_pts, _ref_rate(w, d_lo), w.seed, threads=0)
+    _, _, i_hi = ref.sng_dbscan(ds, w.eps, w.min_pts, _ref_rate(w, d_hi), w.seed, threads=0)
+    dt = max((i_hi["ms"] - i_lo["ms"]) / 1e3, 1e-6)
+    pairs_per_s = w.n * (d_hi - d_lo) / dt
+    fixed_s = max(0.0, i_lo["ms"] / 1e3 - w.n * d_lo / pairs_per_s)
+    return pairs_per_s, fixed_s
+
+
+def _sample_desc(w, draws_s: int) -> str:
+    if draws_s >= w.draws:
+        return f"full workload (n={w.n}, draws={w.draws})"
+    return (f"the full dataset (n={w.n}, d={w.d}, same eps/min_pts/seed) with "
+            f"draws={draws_s} per vertex instead of {w.draws} (rate={_ref_rate(w, draws_s):.6g}): "
+            f"every pair still gathers a random partner row from the whole table")
 
 
 def cpu_baseline(pts, w, budget_s: float):
     """The reference's own sng_dbscan (oracle/_ref) on all host cores, on the full
-    workload when it fits `budget_s`, else on a row-prefix sample sized from a
-    short probe run."""
+    dataset, with as many draws per vertex as fit `budget_s`."""
     from oracle import Reference
     ref = Reference()
     cores = ref.hw_threads()
-    n, draws = pts.shape[0], w.draws
-    m0 = min(n, max(4 * draws, 20000))
-    sp, rate, _ = _ref_sample(pts, w, m0)
-    _, _, pinfo = ref.sng_dbscan(ref.dataset(sp), w.eps, w.min_pts, rate, w.seed, threads=0)
-    probe_rate = pinfo["distance_evals"] / max(pinfo["ms"] / 1e3, 1e-6)
-    m = n if n * draws / probe_rate <= budget_s else max(m0, int(budget_s * probe_rate / draws))
-    sample_pts, rate, desc = _ref_sample(pts, w, m)
-    labels, roles, info = ref.sng_dbscan(ref.dataset(sample_pts), w.eps, w.min_pts, rate, w.seed,
-                                         threads=0)
+    ds = ref.dataset(pts)
+    pps, fixed = _ref_probe(ref, ds, w)
+    draws_s = _ref_draws(w, pps, budget_s, fixed)
+    rate = w.rate if draws_s >= w.draws else _ref_rate(w, draws_s)
+    _, _, info = ref.sng_dbscan(ds, w.eps, w.min_pts, rate, w.seed, threads=0)
     pairs = info["distance_evals"]
     return {"value": pairs / (info["ms"] / 1e3), "unit": UNIT, "cores": cores,
-            "kind": "reference", "sample": desc, "ms": info["ms"], "pairs": pairs}
+            "kind": "reference", "sample": _sample_desc(w, draws_s), "ms": info["ms"],
+            "pairs": pairs, "fixed_ms_per_call": fixed * 1e3}
 
 
 def run_reference_arm(args, w, pts):
+    """--impl reference: the reference's own code path (oracle/_ref), timed per
+    call on the host cores; every step is a bounded sample of the workload."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from oracle import Reference
     ref = Reference()
     cores = ref.hw_threads()
-    # Bound each step so (warmup + steps) finishes in a few minutes.
-    probe = cpu_baseline(pts, w, budget_s=max(1.0, 150.0 / max(1, args.steps + args.warmup)))
-    times = []
-    m_desc = probe["sample"]
-    m = probe["pairs"] // w.draws
-    sample_pts, rate, _ = _ref_sample(pts, w, m)
-    draws = w.draws
-    ds = ref.dataset(sample_pts)
-    pairs = None
+    ds = ref.dataset(pts)
+    pps, fixed = _ref_probe(ref, ds, w)
+    # bound each step so (warmup + steps) finishes in a few minutes
+    budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    draws_s = _ref_draws(w, pps, budget, fixed)
+    rate = w.rate if draws_s >= w.draws else _ref_rate(w, draws_s)
+    times, pairs = [], None
     for i in range(args.warmup + args.steps):
         _, _, info = ref.sng_dbscan(ds, w.eps, w.min_pts, rate, w.seed, threads=0)
         pairs = info["distance_evals"]
@@ -232,21 +289,42 @@ def run_reference_arm(args, w, pts):
     value = pairs / (ms / 1e3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": w.name, "n": w.n, "d": w.d, "eps": w.eps, "rate": w.rate,
-                       "min_pts": w.min_pts, "seed": w.seed, "draws": draws,
-                       "parallelism": f"{cores} host threads"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded generator, BASELINE.json shape)",
+            "impl": "reference",
+            "config": _workload_config(w, args.gpus, {
+                "parallelism": f"{cores} host threads (reference std::thread workers)",
+                "sample": _sample_desc(w, draws_s), "sample_draws": draws_s}),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                             "sample": m_desc},
+                             "sample": _sample_desc(w, draws_s)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def relaunch_cmd(argv: list[str], gpus: int, port: int) -> list[str]:
+    """`bench.py --gpus N` outside torchrun: the same command as N ranks."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={gpus}", "--master-addr", "127.0.0.1",
+            f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one rank per GPU: re-launch this command under torchrun (NCCL over NVLink)
+        sys.exit(subprocess.call(relaunch_cmd(sys.argv[1:], args.gpus, _free_port())))
     rank, world, local = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} ranks",
+              file=sys.stderr)
     from paper_2006_06743_b200 import synthetic
     w = synthetic.CONFIGS[args.config]
 
@@ -300,10 +378,11 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    dev_labels = dev_roles = None
     for k in range(args.steps):
         flush.zero_()  # L2 flush (outside the events)
         ev[k][0].record(stream)
-        _, _, info = step_device()
+        dev_labels, dev_roles, info = step_device()
         ev[k][1].record(stream)
         gather_ms.append(info.ms_gather)
         gather_bytes = info.gather_bytes
@@ -327,7 +406,7 @@ def main():
     value = pairs / (ms_per_step / 1e3)
 
     # ---- e2e through the public host API (pinned host buffers) ----
-    e2e = None
+    e2e = e2e_pageable = None
     if not args.no_e2e:
         labels_h = torch.empty(n, dtype=torch.int32).pin_memory()
         roles_h = torch.empty(n, dtype=torch.uint8).pin_memory()
@@ -342,9 +421,12 @@ def main():
             shard_in = torch.zeros((chunk, d), dtype=torch.float32, device=dev)
             replica = torch.empty((chunk * world, d), dtype=torch.float32, device=dev)
 
-        def step_e2e():
+        def step_e2e(src=None):
             if world == 1:
-                rc = L.sngb_dbscan_f32(C.cast(host.data_ptr(), C.POINTER(C.c_float)), n, d,
+                # src: the pageable numpy array (what the Python / C++ mirrors pass)
+                ptr = (src.ctypes.data_as(C.POINTER(C.c_float)) if src is not None
+                       else C.cast(host.data_ptr(), C.POINTER(C.c_float)))
+                rc = L.sngb_dbscan_f32(ptr, n, d,
                                        w.eps, w.min_pts, w.rate, w.seed, C.byref(o),
                                        C.cast(labels_h.data_ptr(), C.POINTER(C.c_int32)),
                                        C.cast(roles_h.data_ptr(), C.POINTER(C.c_uint8)),
@@ -381,8 +463,38 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_tot = float(t.item())
         e_step = e_tot / len(e_ms)
+        # the host call's results are the device-resident run's, bit for bit
+        same = True
+        if rank == 0:
+            same = (torch.equal(labels_h, dev_labels.cpu()) and
+                    torch.equal(roles_h, dev_roles.cpu()))
+            if not same:
+                raise SystemExit("bench.py: e2e labels/roles differ from the device-resident run")
         e2e = {"value": pairs / (e_step / 1e3), "unit": UNIT, "ms_per_step": e_step,
-               "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": n * 4 + n * 1}
+               "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": n * 4 + n * 1,
+               "source": "pinned host memory (torch pin_memory)",
+               "labels_equal_device_run": same}
+        if world == 1 and not args.no_pageable:
+            # pageable: the numpy array as the Python / C++ mirrors hand it over
+            step_e2e(pts)
+            torch.cuda.synchronize(dev)
+            p_ms = []
+            for _ in range(max(2, args.steps // 4)):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                step_e2e(pts)
+                b.record(stream)
+                b.synchronize()
+                p_ms.append(a.elapsed_time(b))
+            if not (torch.equal(labels_h, dev_labels.cpu()) and
+                    torch.equal(roles_h, dev_roles.cpu())):
+                raise SystemExit("bench.py: pageable e2e labels differ from the device run")
+            pm = statistics.mean(p_ms)
+            e2e_pageable = {"value": pairs / (pm / 1e3), "unit": UNIT, "ms_per_step": pm,
+                            "h2d_bytes_per_step": n * d * 4,
+                            "d2h_bytes_per_step": n * 4 + n * 1,
+                            "source": "pageable host memory (numpy)", "steps": len(p_ms)}
 
     # ---- roofline of the gather kernel ----
     peak, peak_kind = load_peaks()
@@ -416,10 +528,7 @@ def main():
     bpp = gather_bytes / gather_pairs if gather_pairs else 4 * d  # algorithmic bytes per pair
     kname = ("k_gather_q8s" if q8_split else "k_gather_q8") if q8 else (
         "k_gather_head" if head else "k_gather")
-    roofline = {"bound": "hbm", "kernel": kname,
-                "achieved": achieved, "peak": peak,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None,
+    roofline = {"kernel": kname, "achieved": achieved, "unit": "GB/s",
                 "traffic": load_traffic(w.name + ("_q8" if q8 else ("_head" if head else ""))),
                 "algorithmic_bytes_per_launch": gather_bytes,
                 "bytes_per_pair": bpp, "pairs_per_launch": gather_pairs,
@@ -482,16 +591,33 @@ def main():
                                          "head time + survivor-row time: both from L2")
             resident = True
     eff = l2_peak if resident else peak
+    # the fraction that means something: the kernel's own algorithmic bytes (what it
+    # must read: heads + survivor rows, or 8-bit heads + tails, or fp32 rows) against
+    # the measured random-gather ceiling of the memory level those rows come from
     roofline.update({
-        "effective_bound": ("l2 heads + survivor rows" if head else "l2 (random rows)")
-        if resident else "hbm",
-        "effective_peak": eff,
-        "effective_peak_source": (f"{case} in profiles/r01_gather_ceilings.jsonl "
-                                  "(tools/gather_ceiling.cu), in algorithmic bytes")
+        "bound": "l2" if resident else "hbm",
+        "bound_detail": ("l2 heads + survivor rows" if head else "l2 (random rows)")
+        if resident else "hbm (random rows)",
+        "peak": eff,
+        "peak_source": (f"{case} in profiles/r01_gather_ceilings.jsonl "
+                        "(tools/gather_ceiling.cu: lean random-row gather, measured on B200), "
+                        "in the kernel's algorithmic bytes")
         if resident else f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-        "frac_of_effective_peak": (achieved / eff) if (achieved and eff) else None,
+        "frac": (achieved / eff) if (achieved and eff) else None,
+        "hbm_gbs": peak,
         "concurrent_with": ("the Floyd kernel on a side stream (in the step)" if overlapped
                             else None)})
+    # SURVEY 8(d)'s figure: 4*d bytes per pair (one fp32 partner row) -- an effective
+    # rate against the HBM copy peak, not a roofline: the filters read far fewer bytes
+    if g_ms > 0 and gather_pairs:
+        a8 = 4.0 * d * gather_pairs / (g_ms / 1e3) / 1e9
+        roofline["frac_8d"] = {
+            "achieved": a8, "peak": peak, "unit": "GB/s", "value": a8 / peak,
+            "note": "effective rate: 4*d B per pair (SURVEY 8(d)) / kernel time / "
+                    "MEASURED_PEAKS hbm_gbs; > 1 means the filter avoided reading most rows"}
+    ncu = load_ncu(w.name)
+    if ncu:
+        roofline["ncu"] = ncu
     # Two more bounds the gather is held against: the draws it
     # regenerates against the measured RNG throughput (tools/microbench.cu
     # rng_draw), and for rows narrower than an L2 sector (32 B) the share of
@@ -527,16 +653,18 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8" if q8 else ("u16+f32" if head else "f32"),
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64-exact",
+            "filter": roofline["filter"],
             "data": "synthetic (seeded generator, BASELINE.json shape)",
-            "config": {"workload": w.name, "n": n, "d": d, "eps": w.eps, "rate": w.rate,
-                       "min_pts": w.min_pts, "seed": w.seed, "draws": w.draws, "pairs": pairs,
-                       "parallelism": f"rows sharded x{world}" if world > 1 else "1 GPU",
-                       "merge": "fixed-point union-find over NCCL all-reduce" if world > 1
-                       else None,
-                       "replica": "row-shard upload + NCCL all-gather" if world > 1 else None,
-                       "l2": "256 MB L2 flush before every timed step"},
+            "config": _workload_config(w, world, {
+                "merge": "fixed-point union-find over NCCL all-reduce" if world > 1 else None,
+                "replica": "row-shard upload + NCCL all-gather" if world > 1 else None}),
+            "dtype_note": "decisions are the reference's fp64 decisions, bit for bit: "
+                          "narrow filters (8-bit heads / rows, fp32 with a guard band) reject "
+                          "or accept only where their error bound proves the fp64 result, "
+                          "everything else is re-evaluated in fp64 in the reference's order",
             "e2e": e2e,
+            "e2e_pageable": e2e_pageable,
             "gpu_launches": launches,
             "library_launches": lib_launches,
             "roofline": roofline,

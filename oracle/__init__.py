@@ -192,6 +192,14 @@ class Reference:
                                               C.POINTER(C.c_int32), C.POINTER(C.c_uint8)]
         L.sngref_free.argtypes = [C.c_void_p]
         L.sngref_set_metric.argtypes = [C.c_int]
+        L.sngref_full_run.restype = C.c_int
+        L.sngref_full_run.argtypes = [C.c_void_p, C.c_double, C.c_int32, C.c_double, C.c_uint64,
+                                      C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_uint8), _u64p,
+                                      C.POINTER(_u64p), _u64p, C.POINTER(C.c_double)]
+        L.sngref_dbscan_exact.restype = C.c_int
+        L.sngref_dbscan_exact.argtypes = [C.c_void_p, C.c_double, C.c_int32, C.c_int,
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_uint8), _u64p,
+                                          C.POINTER(_u64p), _u64p, C.POINTER(C.c_double)]
         self.L = L
 
     def set_metric(self, name: str) -> None:
@@ -254,6 +262,47 @@ class Reference:
             np.empty(0, np.uint64)
         self.L.sngref_free(kp)
         return keys, int(ev.value), ms.value
+
+    def _keys(self, kp, nk):
+        keys = np.ctypeslib.as_array(kp, shape=(nk.value,)).copy() if nk.value else \
+            np.empty(0, np.uint64)
+        self.L.sngref_free(kp)
+        return keys
+
+    @staticmethod
+    def _info(info, ms):
+        return {"distance_evals": int(info[0]), "edges": int(info[1]),
+                "graph_bytes": int(info[2]), "cluster_count": int(info[3]), "ms": ms.value}
+
+    def full_run(self, ds: "_Dataset", eps, min_pts, rate, seed, threads=0):
+        """sng_dbscan with ONE graph build that also returns the canonical edge
+        keys: (labels, roles, info, keys).  Same code as sng_dbscan
+        (clusterer.cpp:54-65): build_sampled_graph then cluster_graph."""
+        labels = np.empty(ds.n, np.int32)
+        roles = np.empty(ds.n, np.uint8)
+        info = np.zeros(4, np.uint64)
+        kp, nk, ms = _u64p(), C.c_uint64(), C.c_double()
+        rc = self.L.sngref_full_run(ds.h, eps, min_pts, rate, seed, threads,
+                                    _ptr(labels, C.c_int32), _ptr(roles, C.c_uint8),
+                                    _ptr(info, C.c_uint64), C.byref(kp), C.byref(nk),
+                                    C.byref(ms))
+        if rc:
+            raise self._err()
+        return labels, roles, self._info(info, ms), self._keys(kp, nk)
+
+    def dbscan_exact(self, ds: "_Dataset", eps, min_pts, threads=0, with_keys=True):
+        """sng::dbscan_exact (clusterer.cpp:67-79): (labels, roles, info, keys|None)."""
+        labels = np.empty(ds.n, np.int32)
+        roles = np.empty(ds.n, np.uint8)
+        info = np.zeros(4, np.uint64)
+        kp, nk, ms = _u64p(), C.c_uint64(), C.c_double()
+        rc = self.L.sngref_dbscan_exact(ds.h, eps, min_pts, threads, _ptr(labels, C.c_int32),
+                                        _ptr(roles, C.c_uint8), _ptr(info, C.c_uint64),
+                                        C.byref(kp) if with_keys else None,
+                                        C.byref(nk), C.byref(ms))
+        if rc:
+            raise self._err()
+        return labels, roles, self._info(info, ms), (self._keys(kp, nk) if with_keys else None)
 
     def reference_dbscan(self, ds: "_Dataset", eps, min_pts):
         labels = np.empty(ds.n, np.int32)

@@ -142,6 +142,87 @@ int sngref_sampled_edges(void* ds, double eps, double rate, uint64_t seed, int t
     }
 }
 
+// One build_sampled_graph (graph.cpp:133-189) then cluster_graph
+// (clusterer.cpp:7-52) -- exactly what sng_dbscan (clusterer.cpp:54-65) does,
+// but also returning the canonical edge list, so full-size fixtures need one
+// (long) graph build instead of two.  *keys is malloc'ed (sngref_free).
+int sngref_full_run(void* ds, double eps, int32_t min_pts, double rate, uint64_t seed,
+                    int threads, int32_t* labels, uint8_t* roles, uint64_t* info,
+                    uint64_t** keys, uint64_t* nkeys, double* ms) {
+    try {
+        const auto& data = *static_cast<sng::Dataset*>(ds);
+        sng::SngParams p;
+        p.eps = eps;
+        p.min_pts = min_pts;
+        p.rate = rate;
+        p.seed = seed;
+        p.threads = threads;
+        p.dist = metric_dist();
+        p.validate();
+        sng::BuildStats st;
+        auto t0 = std::chrono::steady_clock::now();
+        sng::SampledGraph g = sng::build_sampled_graph(data, p.eps, p.rate, p.dist, p.seed,
+                                                       p.threads, &st);
+        sng::Clustering c = sng::cluster_graph(g, p.min_pts);
+        auto t1 = std::chrono::steady_clock::now();
+        if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        for (size_t i = 0; i < c.size(); ++i) {
+            labels[i] = c.assignment[i];
+            roles[i] = static_cast<uint8_t>(c.role[i]);
+        }
+        info[0] = st.distance_evals;
+        info[1] = g.edge_count();
+        info[2] = g.storage_bytes();
+        info[3] = static_cast<uint64_t>(c.cluster_count);
+        auto e = g.edges();
+        auto* out = static_cast<uint64_t*>(std::malloc((e.size() ? e.size() : 1) * sizeof(uint64_t)));
+        for (size_t i = 0; i < e.size(); ++i)
+            out[i] = (static_cast<uint64_t>(e[i].first) << 32) | e[i].second;
+        *keys = out;
+        *nkeys = e.size();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// sng::dbscan_exact (clusterer.hpp:46-48, clusterer.cpp:67-79) over
+// build_full_graph (graph.cpp:191-220); also returns its canonical edges.
+int sngref_dbscan_exact(void* ds, double eps, int32_t min_pts, int threads, int32_t* labels,
+                        uint8_t* roles, uint64_t* info, uint64_t** keys, uint64_t* nkeys,
+                        double* ms) {
+    try {
+        const auto& data = *static_cast<sng::Dataset*>(ds);
+        sng::ClusterRunInfo ri;
+        auto t0 = std::chrono::steady_clock::now();
+        sng::Clustering c = sng::dbscan_exact(data, eps, min_pts, metric_dist(), threads, &ri);
+        auto t1 = std::chrono::steady_clock::now();
+        if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        for (size_t i = 0; i < c.size(); ++i) {
+            labels[i] = c.assignment[i];
+            roles[i] = static_cast<uint8_t>(c.role[i]);
+        }
+        info[0] = ri.distance_evals;
+        info[1] = ri.edges;
+        info[2] = ri.graph_bytes;
+        info[3] = static_cast<uint64_t>(c.cluster_count);
+        if (keys) {
+            sng::BuildStats st;
+            sng::SampledGraph g = sng::build_full_graph(data, eps, metric_dist(), threads, &st);
+            auto e = g.edges();
+            auto* out = static_cast<uint64_t*>(
+                std::malloc((e.size() ? e.size() : 1) * sizeof(uint64_t)));
+            for (size_t i = 0; i < e.size(); ++i)
+                out[i] = (static_cast<uint64_t>(e[i].first) << 32) | e[i].second;
+            *keys = out;
+            *nkeys = e.size();
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 // tests/oracles.hpp:87-132: classical expand-cluster DBSCAN (the s=1 oracle).
 int sngref_reference_dbscan(void* ds, double eps, int32_t min_pts, int32_t* labels,
                             uint8_t* core) {

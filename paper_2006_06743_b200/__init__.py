@@ -319,6 +319,27 @@ def cluster_graph(g: SampledGraph, min_pts: int, device: int = -1) -> Clustering
 # ---------------------------------------------------------------------------
 # Device-tensor entry points (torch is plumbing only: memory + streams).
 # ---------------------------------------------------------------------------
+def _check_points(points) -> None:
+    import torch
+
+    if points.dtype != torch.float32 or not points.is_cuda or points.dim() != 2:
+        raise InvalidArgument("points must be a CUDA float32 [n, d] tensor")
+
+
+def _check_keys(keys) -> None:
+    import torch
+
+    if keys.dtype != torch.int64 or not keys.is_cuda or keys.dim() != 1:
+        raise InvalidArgument("keys must be a CUDA int64 1-D tensor (u<<32|v)")
+
+
+def _check_vertex_array(t, name: str) -> None:
+    import torch
+
+    if t.dtype != torch.int32 or not t.is_cuda or t.dim() != 1:
+        raise InvalidArgument(f"{name} must be a CUDA int32 1-D tensor")
+
+
 def _stream_handle(t) -> int:
     import torch
 
@@ -332,8 +353,7 @@ def sng_dbscan_device(points, eps: float, min_pts: int, rate: float, seed: int,
     Returns (labels int32[n], roles uint8[n], SngbInfo) as CUDA tensors."""
     import torch
 
-    if points.dtype != torch.float32 or not points.is_cuda or points.dim() != 2:
-        raise InvalidArgument("points must be a CUDA float32 [n, d] tensor")
+    _check_points(points)
     points = points.contiguous()
     n, d = points.shape
     if labels is None:
@@ -355,6 +375,7 @@ def sampled_edges_device(points, eps: float, rate: float, seed: int, row_begin: 
     """Canonical edge keys (int64 view of u<<32|v) sampled by rows [row_begin, row_end)."""
     import torch
 
+    _check_points(points)
     points = points.contiguous()
     n, d = points.shape
     L = _lib.lib()
@@ -381,6 +402,7 @@ def cluster_edges_device(keys, n: int, min_pts: int, timing: bool = False):
     """cluster_graph over CUDA int64 keys (u<<32|v, any order, duplicates allowed)."""
     import torch
 
+    _check_keys(keys)
     keys = keys.contiguous()
     labels = torch.empty(n, dtype=torch.int32, device=keys.device)
     roles = torch.empty(n, dtype=torch.uint8, device=keys.device)
@@ -402,6 +424,7 @@ def unique_keys_device(keys, n: int):
     """Sorted unique canonical keys (graph.cpp:34-40) of CUDA int64 keys."""
     import torch
 
+    _check_keys(keys)
     keys = keys.contiguous()
     out = torch.empty(max(keys.numel(), 1), dtype=torch.int64, device=keys.device)
     cnt = C.c_uint64(0)
@@ -415,9 +438,11 @@ def degrees_device(keys, n: int, degree=None):
     """degree[v] += keys incident to v (int32[n], created zeroed when None)."""
     import torch
 
+    _check_keys(keys)
     keys = keys.contiguous()
     if degree is None:
         degree = torch.zeros(n, dtype=torch.int32, device=keys.device)
+    _check_vertex_array(degree, "degree")
     o = _opts(keys.device.index, False, _stream_handle(keys))
     _check(_lib.lib().sngb_degrees_device(_ptr(keys), keys.numel(), n, C.byref(o),
                                           degree.data_ptr()))
@@ -427,6 +452,9 @@ def degrees_device(keys, n: int, degree=None):
 def components_device(keys, n: int, degree, min_pts: int, parent) -> int:
     """Union-find step over core-core keys into `parent` (in place); returns
     the number of vertices whose entry changed."""
+    _check_keys(keys)
+    _check_vertex_array(degree, "degree")
+    _check_vertex_array(parent, "parent")
     keys = keys.contiguous()
     changed = C.c_uint64(0)
     o = _opts(keys.device.index, False, _stream_handle(parent))
@@ -438,6 +466,9 @@ def components_device(keys, n: int, degree, min_pts: int, parent) -> int:
 
 def border_device(keys, n: int, degree, min_pts: int, parent, border) -> None:
     """border[b] = min(border[b], parent[a]) for core a -- non-core b edges."""
+    _check_keys(keys)
+    for t, nm in ((degree, "degree"), (parent, "parent"), (border, "border")):
+        _check_vertex_array(t, nm)
     keys = keys.contiguous()
     o = _opts(parent.device.index, False, _stream_handle(parent))
     _check(_lib.lib().sngb_border_device(_ptr(keys), keys.numel(), n, degree.data_ptr(),
@@ -449,6 +480,8 @@ def relabel_device(n: int, degree, min_pts: int, parent, border):
     """(labels int32[n], roles uint8[n], SngbInfo) from the merged arrays."""
     import torch
 
+    for t, nm in ((degree, "degree"), (parent, "parent"), (border, "border")):
+        _check_vertex_array(t, nm)
     labels = torch.empty(n, dtype=torch.int32, device=parent.device)
     roles = torch.empty(n, dtype=torch.uint8, device=parent.device)
     gi = SngbInfo()

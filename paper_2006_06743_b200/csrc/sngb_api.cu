@@ -289,12 +289,22 @@ bool metric_flags_ok(const sngb_opts* o) {
 }
 
 int validate(uint64_t n, uint32_t d, double eps, int32_t min_pts, double rate, bool need_minpts) {
-    // clusterer.hpp:19-23 order, then graph.cpp:17-21, then dataset shape.
-    if (!(eps > 0.0)) return SNGB_ERR_EPS;
-    if (need_minpts && min_pts < 1) return SNGB_ERR_MINPTS;
-    if (!(rate > 0.0) || rate > 1.0) return SNGB_ERR_RATE;
-    if (n == 0) return SNGB_ERR_EMPTY;
-    if (d == 0) return SNGB_ERR_DIM;
+    if (need_minpts) {
+        // sng_dbscan: SngParams::validate first (clusterer.hpp:19-23: eps, min_pts,
+        // rate), then build_sampled_graph's checks (graph.cpp:17-21: empty, dim)
+        if (!(eps > 0.0)) return SNGB_ERR_EPS;
+        if (min_pts < 1) return SNGB_ERR_MINPTS;
+        if (!(rate > 0.0) || rate > 1.0) return SNGB_ERR_RATE;
+        if (n == 0) return SNGB_ERR_EMPTY;
+        if (d == 0) return SNGB_ERR_DIM;
+    } else {
+        // build_sampled_graph alone: validate_graph_params (graph.cpp:17-21: empty,
+        // eps, dim), then the rate (graph.cpp:136)
+        if (n == 0) return SNGB_ERR_EMPTY;
+        if (!(eps > 0.0)) return SNGB_ERR_EPS;
+        if (d == 0) return SNGB_ERR_DIM;
+        if (!(rate > 0.0) || rate > 1.0) return SNGB_ERR_RATE;
+    }
     if (n >= 0xffffff00ull) return SNGB_ERR_TOO_LARGE;
     return SNGB_OK;
 }
@@ -410,6 +420,10 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         }
         CK(cudaMemcpyAsync(&c.h_counters[C_QMIN], &dc[C_QMIN], 2 * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, gs));
+        // this call's non-finite count too (the filter plans read it; a stale value
+        // from an earlier failed call must not switch the filters off)
+        CK(cudaMemcpyAsync(&c.h_counters[C_NONFINITE], &dc[C_NONFINITE],
+                           sizeof(unsigned long long), cudaMemcpyDeviceToHost, gs));
         CK(cudaEventRecord(c.qev, gs));
     };
 

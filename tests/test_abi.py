@@ -99,3 +99,24 @@ def test_no_cpu_fallback_without_gpu():
     assert _call(pts) == _lib.SNGB_ERR_NO_DEVICE
     with pytest.raises(sng.GpuError, match="no CUDA device"):
         sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=1.0, min_pts=1, rate=1.0))
+
+
+def _edges_call(n, d, eps, rate):
+    pts = np.zeros((max(n, 1), max(d, 1)), np.float32)
+    cnt = C.c_uint64(0)
+    keys = np.zeros(4, np.uint64)
+    return _lib.lib().sngb_sampled_edges_f32(
+        pts.ctypes.data_as(C.POINTER(C.c_float)), n, d, eps, rate, 0, None,
+        keys.ctypes.data_as(C.POINTER(C.c_uint64)), 4, C.byref(cnt), None)
+
+
+def test_sampled_edges_validation_order_is_build_sampled_graph():
+    """build_sampled_graph alone checks empty, eps, dim (graph.cpp:17-21), then the
+    rate (graph.cpp:136); sng_dbscan validates its params first (clusterer.hpp:19-23)."""
+    assert _edges_call(0, 2, -1.0, 7.0) == _lib.SNGB_ERR_EMPTY
+    assert _edges_call(4, 2, -1.0, 7.0) == _lib.SNGB_ERR_EPS
+    assert _edges_call(4, 0, 1.0, 7.0) == _lib.SNGB_ERR_DIM
+    assert _edges_call(4, 2, 1.0, 7.0) == _lib.SNGB_ERR_RATE
+    # sng_dbscan: params before the dataset
+    assert _call(np.zeros((0, 2), np.float32), eps=-1.0) == _lib.SNGB_ERR_EPS
+    assert _call(np.zeros((0, 2), np.float32), rate=2.0) == _lib.SNGB_ERR_RATE

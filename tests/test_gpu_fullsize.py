@@ -1,15 +1,26 @@
-"""Parity at BASELINE.json's full sizes.
+"""Parity at BASELINE.json's FULL sizes, all five configs, both entry points.
 
-cfg1-cfg3: the whole pipeline against the oracle run at full size.
-cfg4-cfg5 (oracle too slow for a test): size-independent properties --
-  * the clustering stage is exact: the oracle's cluster_graph restatement run
-    on the GPU's own edge list reproduces the GPU labels/roles bit for bit;
-  * the edge set is exact on a random sample of vertices: every sampled
-    vertex's Floyd partners (oracle restatement of graph.cpp:161-174) that pass
-    the fp64 eps-test are edges, and every GPU edge at a sampled vertex is
-    justified by one of the two endpoints' partner sets;
-  * determinism (two runs identical) and distance_evals == n * draws.
+tests/golden/golden_full.json holds the REFERENCE's own results on the five
+synthetic workloads at full size (tests/golden/make_golden_full.py: the
+reference's graph.cpp + clusterer.cpp compiled unmodified, one
+build_sampled_graph + cluster_graph per config = sng_dbscan,
+clusterer.cpp:54-65): SHA-256 digests of the points, the canonical edge keys,
+labels and roles, and the ClusterRunInfo counters.  Here the GPU path must
+reproduce them bit for bit through
+
+  * the device entry point   (sngb_dbscan_f32_device, points resident in HBM),
+  * the host-buffer entry    (sngb_dbscan_f32: chunked upload, the host-upload
+                              filter plans and schedules -- what bench.py's
+                              e2e times and sng::sng_dbscan / the Python
+                              mirror call),
+  * the edge builder         (sngb_sampled_edges_f32_device = SampledGraph::edges()).
+
+On a mismatch the 64 per-block digests say where the labels first differ.
 """
+import hashlib
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -18,91 +29,129 @@ pytestmark = pytest.mark.gpu
 import paper_2006_06743_b200 as sng  # noqa: E402
 from paper_2006_06743_b200 import synthetic  # noqa: E402
 
-
-@pytest.fixture(scope="module", autouse=True)
-def _need_gpu():
-    if sng.device_count() < 1:
-        pytest.fail("no CUDA device: the GPU path has no CPU fallback")
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_full.json")
 
 
-def _gpu(pts, w):
+def _golden(cfg):
+    with open(GOLDEN) as f:
+        g = json.load(f)["configs"]
+    if str(cfg) not in g:
+        pytest.fail(f"golden_full.json has no cfg{cfg}: run tests/golden/make_golden_full.py")
+    return g[str(cfg)]
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _first_bad_block(a, blocks):
+    n = len(a)
+    cuts = [(n * i) // len(blocks) for i in range(len(blocks) + 1)]
+    for i, want in enumerate(blocks):
+        if sha(a[cuts[i]:cuts[i + 1]])[:16] != want:
+            return i, cuts[i], cuts[i + 1]
+    return None
+
+
+def _check(g, labels, roles, info, where):
+    assert int(info.distance_evals) == g["distance_evals"], where
+    assert int(info.edges) == g["edges"], where
+    assert int(info.graph_bytes) == g["graph_bytes"], where
+    assert int(info.cluster_count) == g["cluster_count"], where
+    assert (int(info.core_count), int(info.border_count), int(info.noise_count)) == \
+        (g["core"], g["border"], g["noise"]), where
+    if sha(roles) != g["roles_sha256"]:
+        pytest.fail(f"{where}: roles differ, first bad block {_first_bad_block(roles, g['roles_blocks'])}")
+    if sha(labels) != g["labels_sha256"]:
+        pytest.fail(f"{where}: labels differ, first bad block "
+                    f"{_first_bad_block(labels, g['labels_blocks'])}")
+
+
+_PTS = {}
+
+
+def _points(cfg):
+    if cfg not in _PTS:
+        _PTS.clear()  # one full-size dataset in host memory at a time
+        _PTS[cfg] = synthetic.generate(cfg)
+    return _PTS[cfg]
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_generator_matches_golden_points(cfg):
+    g = _golden(cfg)
+    assert sha(_points(cfg)) == g["points_sha256"]
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_full_size_device_entry_equals_reference(cfg):
     import torch
-    x = torch.from_numpy(pts).cuda()
-    labels, roles, gi = sng.sng_dbscan_device(x, w.eps, w.min_pts, w.rate, w.seed)
-    keys, _ = sng.sampled_edges_device(x, w.eps, w.rate, w.seed)
-    torch.cuda.synchronize()
-    return labels.cpu().numpy(), roles.cpu().numpy(), gi, keys.cpu().numpy().view(np.uint64)
-
-
-@pytest.mark.parametrize("cfg", [1, 2, 3])
-def test_full_size_equals_oracle(oracle, cfg):
+    g = _golden(cfg)
     w = synthetic.CONFIGS[cfg]
-    pts = synthetic.generate(cfg)
-    labels, roles, gi, keys = _gpu(pts, w)
-    ol, orl, oinfo, okeys = oracle.sng_dbscan(pts, w.eps, w.min_pts, w.rate, w.seed)
-    assert gi.distance_evals == oinfo["distance_evals"] == w.pairs
-    assert gi.edges == oinfo["edges"]
-    np.testing.assert_array_equal(keys, okeys)
-    np.testing.assert_array_equal(roles, orl)
-    np.testing.assert_array_equal(labels, ol)
-    assert gi.cluster_count == oinfo["cluster_count"]
+    x = torch.from_numpy(_points(cfg)).cuda()
+    labels, roles, gi = sng.sng_dbscan_device(x, w.eps, w.min_pts, w.rate, w.seed)
+    torch.cuda.synchronize()
+    _check(g, labels.cpu().numpy(), roles.cpu().numpy(), gi, f"cfg{cfg} device entry")
+    keys, ki = sng.sampled_edges_device(x, w.eps, w.rate, w.seed)
+    torch.cuda.synchronize()
+    assert int(ki.edges) == g["edges"]
+    assert sha(keys.cpu().numpy().view(np.uint64)) == g["keys_sha256"], f"cfg{cfg} edge keys"
+    del x, labels, roles, keys
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_full_size_host_entry_equals_reference(cfg):
+    """The public host-buffer call (sngb_dbscan_f32 via the Python mirror), from
+    pageable numpy memory -- the chunked upload and its overlapped schedules."""
+    g = _golden(cfg)
+    w = synthetic.CONFIGS[cfg]
+    info = sng.ClusterRunInfo()
+    c = sng.sng_dbscan(sng.Dataset(_points(cfg)),
+                       sng.SngParams(eps=w.eps, min_pts=w.min_pts, rate=w.rate, seed=w.seed), info)
+
+    class _I:  # the fields _check reads
+        pass
+    gi = _I()
+    for k in ("distance_evals", "edges", "graph_bytes"):
+        setattr(gi, k, getattr(info, k))
+    gi.cluster_count = c.cluster_count
+    gi.core_count, gi.border_count, gi.noise_count = (c.count_role(sng.PointRole.Core),
+                                                      c.count_role(sng.PointRole.Border),
+                                                      c.count_role(sng.PointRole.Noise))
+    _check(g, c.assignment, c.role, gi, f"cfg{cfg} host entry")
 
 
 @pytest.mark.parametrize("cfg", [4, 5])
-def test_full_size_properties(oracle, cfg):
-    w = synthetic.CONFIGS[cfg]
-    pts = synthetic.generate(cfg)
-    n = pts.shape[0]
-    labels, roles, gi, keys = _gpu(pts, w)
-    assert gi.distance_evals == w.pairs
-    # canonical, sorted, unique, in range, no self loops
-    u = (keys >> np.uint64(32)).astype(np.int64)
-    v = (keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
-    assert len(keys) == gi.edges
-    assert np.all(np.diff(keys.astype(np.uint64)) > 0) if len(keys) > 1 else True
-    assert np.all(u < v) and np.all(v < n)
-    # clustering stage exact on the GPU's own edges
-    cl, cr, ccount = oracle.cluster_edges(keys, n, w.min_pts)
-    np.testing.assert_array_equal(cr, roles)
-    np.testing.assert_array_equal(cl, labels)
-    assert ccount == gi.cluster_count
-    # edge set exact on sampled vertices
-    rng = np.random.default_rng(cfg)
-    sample = rng.choice(n, size=64, replace=False)
-    eps2 = w.eps * w.eps
-    edge_set = set(keys.tolist())
-    partners = {}
-    for s in sample:
-        p = oracle.partners(n, w.draws, w.seed, int(s))
-        partners[int(s)] = set(p.tolist())
-        diff = pts[p].astype(np.float64) - pts[s].astype(np.float64)
-        d2 = np.zeros(len(p))
-        for k in range(pts.shape[1]):  # sequential in k, like distance.hpp:78-81
-            d2 = d2 + diff[:, k] * diff[:, k]
-        for vv, ok in zip(p.tolist(), (d2 <= eps2).tolist()):
-            key = (min(s, vv) << 32) | max(s, vv)
-            assert (key in edge_set) == ok, (s, vv, ok)  # within() is symmetric
-    # every GPU edge at a sampled vertex is justified by a partner set
-    for s in sample[:16]:
-        s = int(s)
-        inc = np.concatenate([v[u == s], u[v == s]])
-        for x in inc.tolist():
-            if x in partners[s]:
-                continue
-            assert s in set(oracle.partners(n, w.draws, w.seed, x).tolist()), (s, x)
-    # determinism
-    labels2, roles2, gi2, keys2 = _gpu(pts, w)
-    np.testing.assert_array_equal(keys2, keys)
-    np.testing.assert_array_equal(labels2, labels)
+def test_full_size_pinned_host_entry_equals_reference(cfg):
+    """Same through the raw C ABI from pinned memory (bench.py's e2e leg)."""
+    import ctypes as C
 
+    import torch
+    from paper_2006_06743_b200 import _lib
+    g = _golden(cfg)
+    w = synthetic.CONFIGS[cfg]
+    host = torch.from_numpy(_points(cfg)).pin_memory()
+    n, d = host.shape
+    labels = torch.empty(n, dtype=torch.int32).pin_memory()
+    roles = torch.empty(n, dtype=torch.uint8).pin_memory()
+    gi = _lib.SngbInfo()
+    rc = _lib.lib().sngb_dbscan_f32(C.cast(host.data_ptr(), C.POINTER(C.c_float)), n, d, w.eps,
+                                    w.min_pts, w.rate, w.seed, None,
+                                    C.cast(labels.data_ptr(), C.POINTER(C.c_int32)),
+                                    C.cast(roles.data_ptr(), C.POINTER(C.c_uint8)), C.byref(gi))
+    sng._check(rc)
+    _check(g, labels.numpy(), roles.numpy(), gi, f"cfg{cfg} pinned host entry")
 
 
 def test_cfg5_head_filter_equals_fp32_filter(monkeypatch):
     """cfg5 at full size: the auto path (head filter, 16) and the plain fp32
-    gather (SNGB_HEAD=0) give the same edge list, bit for bit."""
+    gather (SNGB_HEAD=0) give the same edge list, bit for bit -- and both the
+    reference's."""
     import torch
+    g = _golden(5)
     w = synthetic.CONFIGS[5]
-    x = torch.from_numpy(synthetic.generate(5)).cuda()
+    x = torch.from_numpy(_points(5)).cuda()
     k_auto, gi = sng.sampled_edges_device(x, w.eps, w.rate, w.seed)
     torch.cuda.synchronize()
     assert gi.filter_bits == 16
@@ -111,3 +160,4 @@ def test_cfg5_head_filter_equals_fp32_filter(monkeypatch):
     torch.cuda.synchronize()
     assert gi0.filter_bits == 32
     assert torch.equal(k_auto, k_fp32)
+    assert sha(k_fp32.cpu().numpy().view(np.uint64)) == g["keys_sha256"]

@@ -70,3 +70,44 @@ def test_workload_geometry_matches_baseline():
     assert got == {1: (20000, 2, 2000, 4.0e7), 2: (70000, 784, 700, 4.9e7),
                    3: (10**6, 16, 1000, 10**9), 4: (5 * 10**6, 3, 2500, 1.25e10),
                    5: (2 * 10**7, 32, 4000, 8.0e10)}
+
+
+def test_device_entry_points_reject_bad_tensors():
+    """CPU / wrong-dtype tensors fail with InvalidArgument before any library call
+    (a host pointer handed to a kernel would poison the CUDA context)."""
+    import torch
+    pts = torch.zeros((8, 2), dtype=torch.float32)  # CPU
+    with pytest.raises(sng.InvalidArgument, match="CUDA float32"):
+        sng.sampled_edges_device(pts, 1.0, 1.0, 0)
+    with pytest.raises(sng.InvalidArgument, match="CUDA float32"):
+        sng.sng_dbscan_device(pts, 1.0, 1, 1.0, 0)
+    keys = torch.zeros(4, dtype=torch.int64)
+    with pytest.raises(sng.InvalidArgument, match="CUDA int64"):
+        sng.cluster_edges_device(keys, 8, 1)
+    with pytest.raises(sng.InvalidArgument, match="CUDA int64"):
+        sng.unique_keys_device(keys, 8)
+    with pytest.raises(sng.InvalidArgument, match="CUDA int64"):
+        sng.degrees_device(keys.to(torch.int32), 8)
+
+
+def test_bench_relaunch_command():
+    """`bench.py --gpus N` outside torchrun re-launches itself as N local ranks."""
+    import bench
+    cmd = bench.relaunch_cmd(["--gpus", "4", "--steps", "3"], 4, 29511)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-port=29511" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"]
+    assert cmd[-5].endswith("bench.py")
+
+
+def test_bench_reference_sample_rate():
+    """The reference arm's bounded sample keeps the full dataset and picks a rate
+    whose draws (graph.cpp:139-140) are exactly the requested count."""
+    import math
+
+    import bench
+    w = synthetic.CONFIGS[5]
+    for k in (1, 7, 100, 3999):
+        r = bench._ref_rate(w, k)
+        assert min(math.ceil(r * float(w.n)), w.n - 1) == k

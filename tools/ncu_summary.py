@@ -2,7 +2,11 @@
 occupancy and stall metrics, plus the opcode mix).  Not part of the product.
 
     python tools/ncu_summary.py REPORT.ncu-rep "title" [units_of_work] [unit_name]
+        [--json WORKLOAD]   also merge the key counters into profiles/ncu_metrics.json
+                            (read by bench.py's roofline.ncu)
 """
+import json
+import os
 import collections
 import csv
 import io
@@ -23,7 +27,18 @@ METRICS = [
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput (% of peak)"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads per warp instruction"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "global load sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "global load requests"),
 ]
+
+
+def _num(v):
+    try:
+        return float(str(v).replace(",", ""))
+    except ValueError:
+        return None
 
 
 def ncu_csv(rep, *args):
@@ -33,9 +48,15 @@ def ncu_csv(rep, *args):
 
 
 def main():
-    rep, title = sys.argv[1], sys.argv[2]
-    units = float(sys.argv[3]) if len(sys.argv) > 3 else None
-    uname = sys.argv[4] if len(sys.argv) > 4 else "unit"
+    argv = list(sys.argv[1:])
+    workload = None
+    if "--json" in argv:
+        k = argv.index("--json")
+        workload = argv[k + 1]
+        del argv[k:k + 2]
+    rep, title = argv[0], argv[1]
+    units = float(argv[2]) if len(argv) > 2 else None
+    uname = argv[3] if len(argv) > 3 else "unit"
     raw = ncu_csv(rep, "--page", "raw")
     hdr, unit_row, vals = raw[0], raw[1], raw[2]
     kname = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
@@ -51,6 +72,40 @@ def main():
                 inst = float(v.replace(",", ""))
     if units and inst:
         print(f"| warp instructions per {uname} | {inst / units:.2f} |")
+    get = {m: _num(vals[hdr.index(m)]) for m, _ in METRICS if m in hdr}
+    sec, req = (get.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"),
+                get.get("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"))
+    tpi = get.get("smsp__thread_inst_executed_per_inst_executed.ratio")
+    if sec and req:
+        print(f"| global load sectors per request | {sec / req:.2f} |")
+    if tpi:
+        print(f"| warp execution efficiency (threads per instruction / 32) | {tpi / 32:.3f} |")
+    if workload:
+        path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "profiles", "ncu_metrics.json")
+        try:
+            with open(path) as f:
+                allm = json.load(f)
+        except Exception:
+            allm = {}
+        dram = (get.get("dram__bytes_read.sum") or 0) + (get.get("dram__bytes_write.sum") or 0)
+        allm[workload] = {
+            "kernel": kname, "report": os.path.basename(rep),
+            "duration_ns": get.get("gpu__time_duration.sum"),
+            "lts_throughput_pct": get.get("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "dram_throughput_pct": get.get("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "l2_hit_rate_pct": get.get("lts__t_sector_hit_rate.pct"),
+            "issue_active_pct": get.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "warps_active_pct": get.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
+            "sectors_per_request": (sec / req) if (sec and req) else None,
+            "warp_execution_efficiency": (tpi / 32) if tpi else None,
+            "dram_bytes": dram or None,
+            "warp_instructions": inst,
+            "warp_instructions_per_unit": (inst / units) if (units and inst) else None,
+            "unit": uname if units else None,
+        }
+        with open(path, "w") as f:
+            json.dump(allm, f, indent=1)
     stalls = []
     for i, h in enumerate(hdr):
         if "issue_stalled" in h and h.endswith("per_issue_active.ratio"):
