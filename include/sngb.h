@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SNGB_ABI_VERSION 3
+#define SNGB_ABI_VERSION 4
 
 /* Status codes.  1..6 carry the reference's std::invalid_argument messages. */
 enum {
@@ -69,6 +69,23 @@ typedef struct sngb_opts {
     void* stream;       /* cudaStream_t to run on; NULL = library-owned stream */
     uint64_t row_begin; /* sampled-edge entry only: query rows [row_begin, row_end) */
     uint64_t row_end;   /*   (row_end == 0 means n) -- the multi-GPU row shard */
+    /* ABI 4 -- several GPUs of this process (the reference's parallel_over_vertices
+     * row split, graph.cpp:45-63, across devices).  Used by
+     * sngb_dbscan_f32/_f64, sngb_dbscan_f32_device and sngb_dbscan_exact_f32[_device]:
+     *   num_gpus 0 or 1  one GPU (`device`), the single-GPU path;
+     *   num_gpus N > 1   query rows sharded over N GPUs: each uploads its row shard,
+     *                    the replica is assembled over NVLink peer copies, each GPU
+     *                    builds the edges of its rows, keys are routed to the owner
+     *                    of their smaller endpoint, and the union-find forests are
+     *                    merged to a fixed point by peer-memory all-reduces;
+     *   num_gpus -1      every visible GPU.
+     * devices: N CUDA ordinals (NULL: device, device+1, ... or 0.. when device is
+     * -1).  An ordinal may repeat: its shards then share that GPU (same results).
+     * The GPUs must have peer access to each other (NVLink / NVSwitch); the
+     * device-buffer entry takes its points / labels on devices[0].  Results are
+     * identical to the single-GPU call, bit for bit. */
+    int32_t num_gpus;
+    const int32_t* devices;
 } sngb_opts;
 
 /* ClusterRunInfo (clusterer.hpp:27-31) + BuildStats (graph.hpp:56-58) + GPU counters. */
@@ -103,6 +120,13 @@ typedef struct sngb_info {
      * head_bytes + survivors * 4d, survivors taking the fp32 test) */
     uint32_t filter_bits;
     uint32_t head_bytes;
+    /* ABI 4 -- multi-GPU calls: GPUs used, fixed-point merge rounds, keys moved by
+     * the owner routing (0 on one GPU); ms_merge: route + merge (SNGB_FLAG_TIMING) */
+    uint32_t num_gpus;
+    uint32_t merge_rounds;
+    uint64_t routed_keys;
+    float ms_merge;
+    uint32_t reserved;
 } sngb_info;
 
 /* sng::sng_dbscan (clusterer.hpp:42) on HOST buffers: pts[n*d] fp32 row-major,
@@ -134,6 +158,26 @@ int sngb_sampled_edges_f32_device(const float* d_pts, uint64_t n, uint32_t d, do
 int sngb_sampled_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps, double rate,
                            uint64_t seed, const sngb_opts* opts, uint64_t* keys_out,
                            uint64_t capacity, uint64_t* count_out, sngb_info* info_out);
+
+/* sng::dbscan_exact (clusterer.hpp:46-48, clusterer.cpp:67-79): classical DBSCAN
+ * on the exact eps-graph, build_full_graph (graph.cpp:191-220: every unordered
+ * pair once, distance_evals = n(n-1)/2), then cluster_graph.  Validation order:
+ * eps, min_pts (clusterer.cpp:69-70), then empty / dim (graph.cpp:17-21); no rate.
+ * Metric from opts->flags, multi-GPU from opts->num_gpus as above. */
+int sngb_dbscan_exact_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                          const sngb_opts* opts, int32_t* labels_out, uint8_t* roles_out,
+                          sngb_info* info_out);
+int sngb_dbscan_exact_f32_device(const float* d_pts, uint64_t n, uint32_t d, double eps,
+                                 int32_t min_pts, const sngb_opts* opts, int32_t* d_labels,
+                                 uint8_t* d_roles, sngb_info* info_out);
+int sngb_dbscan_exact_f64(const double* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                          const sngb_opts* opts, int32_t* labels_out, uint8_t* roles_out,
+                          sngb_info* info_out);
+/* sng::build_full_graph (graph.hpp:69-70): its canonical edges (SampledGraph::edges(),
+ * u << 32 | v, sorted) into keys_out (host); SNGB_ERR_CAPACITY as the sampled entry. */
+int sngb_full_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps,
+                        const sngb_opts* opts, uint64_t* keys_out, uint64_t capacity,
+                        uint64_t* count_out, sngb_info* info_out);
 
 /* Many small problems at once (the theory lab calls
  * sng_dbscan for many n <= 1e5 datasets, theory.cpp:239-256).  Each problem is

@@ -25,7 +25,8 @@ from ._lib import SNGB_FLAG_TIMING, SngbInfo, SngbOpts
 __all__ = [
     "InvalidArgument", "GpuError", "kNoiseLabel", "PointRole", "Dataset", "Distance",
     "SngParams", "ClusterRunInfo", "BuildStats", "Clustering", "SampledGraph",
-    "sng_dbscan", "build_sampled_graph", "cluster_graph", "sng_dbscan_device",
+    "sng_dbscan", "build_sampled_graph", "cluster_graph", "sng_dbscan_device", "dbscan_exact",
+    "build_full_graph", "dbscan_exact_device",
     "sampled_edges_device", "cluster_edges_device", "device_count",
 ]
 
@@ -166,6 +167,10 @@ class SngParams:  # clusterer.hpp:11-24
     dist: Distance = field(default_factory=Distance.euclidean)
     threads: int = 0  # CPU worker count in the reference; ignored by the GPU path
     device: int = -1  # extension: CUDA ordinal (-1 = current)
+    # extension: GPUs of this process to shard the rows over (0/1: one GPU, N, -1: all),
+    # optionally their ordinals (a repeated ordinal runs several shards on one GPU)
+    num_gpus: int = 0
+    devices: list | None = None
 
     def validate(self) -> None:
         if not (self.eps > 0.0):
@@ -235,9 +240,19 @@ class SampledGraph:
 
 
 def _opts(device: int = -1, timing: bool = False, stream: int = 0, row_begin: int = 0,
-          row_end: int = 0, dist: "Distance | None" = None) -> SngbOpts:
+          row_end: int = 0, dist: "Distance | None" = None, num_gpus: int = 0,
+          devices=None) -> SngbOpts:
     flags = (SNGB_FLAG_TIMING if timing else 0) | (dist.flags if dist is not None else 0)
-    return SngbOpts(device, flags, C.c_void_p(stream or None), row_begin, row_end)
+    o = SngbOpts(device, flags, C.c_void_p(stream or None), row_begin, row_end, int(num_gpus),
+                 None)
+    if devices is not None:
+        devs = list(devices)
+        if num_gpus in (0, 1) and len(devs) > 1:
+            o.num_gpus = len(devs)
+        arr = (C.c_int32 * max(len(devs), 1))(*devs)
+        o.devices = C.cast(arr, C.POINTER(C.c_int32))
+        o._keep = arr  # the array must outlive the call
+    return o
 
 
 def sng_dbscan(data: Dataset, params: SngParams, info: ClusterRunInfo | None = None,
@@ -253,7 +268,8 @@ def sng_dbscan(data: Dataset, params: SngParams, info: ClusterRunInfo | None = N
     labels = np.empty(n, np.int32)
     roles = np.empty(n, np.uint8)
     gi = SngbInfo()
-    o = _opts(params.device, timing, dist=params.dist)
+    o = _opts(params.device, timing, dist=params.dist, num_gpus=params.num_gpus,
+              devices=params.devices)
     if data.values64 is not None:
         fn, arg = _lib.lib().sngb_dbscan_f64, data.values64.ctypes.data_as(C.POINTER(C.c_double))
     else:
@@ -269,6 +285,76 @@ def sng_dbscan(data: Dataset, params: SngParams, info: ClusterRunInfo | None = N
         info.graph_bytes = gi.graph_bytes
         info.gpu = gi.as_dict()
     return Clustering(labels, roles, int(gi.cluster_count))
+
+
+def dbscan_exact(data: Dataset, eps: float, min_pts: int, dist: Distance | None = None,
+                 threads: int = 0, info: ClusterRunInfo | None = None, device: int = -1,
+                 num_gpus: int = 0, devices=None, timing: bool = False) -> Clustering:
+    """sng::dbscan_exact (clusterer.hpp:46-48, clusterer.cpp:67-79) on the GPU:
+    classical DBSCAN on the exact eps-graph (build_full_graph, graph.cpp:191-220),
+    distance_evals = n(n-1)/2."""
+    if not isinstance(data, Dataset):
+        data = Dataset(data)
+    if not (eps > 0.0):
+        raise InvalidArgument("eps must be > 0")
+    if min_pts < 1:
+        raise InvalidArgument("min_pts must be >= 1")
+    dist = dist or Distance.euclidean()
+    if not isinstance(dist, Distance):
+        raise NotImplementedError("a Python distance callback cannot run on the GPU path")
+    n, d = data.values.shape
+    labels = np.empty(n, np.int32)
+    roles = np.empty(n, np.uint8)
+    gi = SngbInfo()
+    o = _opts(device, timing, dist=dist, num_gpus=num_gpus, devices=devices)
+    L = _lib.lib()
+    if data.values64 is not None:
+        fn, arg = L.sngb_dbscan_exact_f64, data.values64.ctypes.data_as(C.POINTER(C.c_double))
+    else:
+        fn, arg = L.sngb_dbscan_exact_f32, data.values.ctypes.data_as(C.POINTER(C.c_float))
+    _check(fn(arg, n, d, float(eps), int(min_pts), C.byref(o),
+              labels.ctypes.data_as(C.POINTER(C.c_int32)),
+              roles.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(gi)))
+    if info is not None:
+        info.distance_evals = gi.distance_evals
+        info.edges = gi.edges
+        info.graph_bytes = gi.graph_bytes
+        info.gpu = gi.as_dict()
+    return Clustering(labels, roles, int(gi.cluster_count))
+
+
+def build_full_graph(data: Dataset, eps: float, dist: Distance | None = None, threads: int = 0,
+                     stats: BuildStats | None = None, device: int = -1) -> SampledGraph:
+    """sng::build_full_graph (graph.hpp:69-70, graph.cpp:191-220) on the GPU."""
+    if not isinstance(data, Dataset):
+        data = Dataset(data)
+    if dist is not None and not isinstance(dist, Distance):
+        raise NotImplementedError("a Python distance callback cannot run on the GPU path")
+    if data.values64 is not None:  # fp64 values: the exact graph is rate-1 sampling
+        g = build_sampled_graph(data, eps, 1.0, dist, 0, threads, None, device)
+        if stats is not None:
+            stats.distance_evals = g.n * (g.n - 1) // 2
+        return g
+    pts = data.values
+    n, d = pts.shape
+    L = _lib.lib()
+    gi = SngbInfo()
+    o = _opts(device, dist=dist)
+    cnt = C.c_uint64(0)
+    cap = 1 << 20
+    while True:
+        keys = np.empty(cap, np.uint64)
+        rc = L.sngb_full_edges_f32(pts.ctypes.data_as(C.POINTER(C.c_float)), n, d, float(eps),
+                                   C.byref(o), keys.ctypes.data_as(C.POINTER(C.c_uint64)), cap,
+                                   C.byref(cnt), C.byref(gi))
+        if rc == _lib.SNGB_ERR_CAPACITY:
+            cap = int(cnt.value)
+            continue
+        _check(rc)
+        break
+    if stats is not None:
+        stats.distance_evals = gi.distance_evals
+    return SampledGraph(n, keys[: cnt.value].copy())
 
 
 def build_sampled_graph(data: Dataset, eps: float, rate: float, dist: Distance | None = None,
@@ -347,8 +433,11 @@ def _stream_handle(t) -> int:
 
 
 def sng_dbscan_device(points, eps: float, min_pts: int, rate: float, seed: int,
-                      labels=None, roles=None, timing: bool = False):
-    """sng_dbscan over a CUDA float32 [n, d] tensor on torch's current stream.
+                      labels=None, roles=None, timing: bool = False, num_gpus: int = 0,
+                      devices=None):
+    """sng_dbscan over a CUDA float32 [n, d] tensor on torch's current stream
+    (num_gpus / devices: shard the rows over several GPUs of this process; the
+    points and the outputs stay on points.device, which must be devices[0]).
 
     Returns (labels int32[n], roles uint8[n], SngbInfo) as CUDA tensors."""
     import torch
@@ -361,12 +450,32 @@ def sng_dbscan_device(points, eps: float, min_pts: int, rate: float, seed: int,
     if roles is None:
         roles = torch.empty(n, dtype=torch.uint8, device=points.device)
     gi = SngbInfo()
-    o = _opts(points.device.index, timing, _stream_handle(points))
+    o = _opts(points.device.index, timing, _stream_handle(points), num_gpus=num_gpus,
+              devices=devices)
     rc = _lib.lib().sngb_dbscan_f32_device(points.data_ptr(), n, d, float(eps), int(min_pts),
                                            float(rate), int(seed) & 0xFFFFFFFFFFFFFFFF,
                                            C.byref(o), labels.data_ptr(), roles.data_ptr(),
                                            C.byref(gi))
     _check(rc)
+    return labels, roles, gi
+
+
+def dbscan_exact_device(points, eps: float, min_pts: int, timing: bool = False,
+                        num_gpus: int = 0, devices=None):
+    """dbscan_exact over a CUDA float32 [n, d] tensor: (labels, roles, SngbInfo)."""
+    import torch
+
+    _check_points(points)
+    points = points.contiguous()
+    n, d = points.shape
+    labels = torch.empty(n, dtype=torch.int32, device=points.device)
+    roles = torch.empty(n, dtype=torch.uint8, device=points.device)
+    gi = SngbInfo()
+    o = _opts(points.device.index, timing, _stream_handle(points), num_gpus=num_gpus,
+              devices=devices)
+    _check(_lib.lib().sngb_dbscan_exact_f32_device(points.data_ptr(), n, d, float(eps),
+                                                   int(min_pts), C.byref(o), labels.data_ptr(),
+                                                   roles.data_ptr(), C.byref(gi)))
     return labels, roles, gi
 
 

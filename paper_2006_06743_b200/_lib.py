@@ -40,12 +40,16 @@ EXPORTS = [
     "sngb_border_device", "sngb_relabel_device",
     "sngb_dbscan_f64", "sngb_dbscan_f64_device", "sngb_sampled_edges_f64",
     "sngb_dbscan_batch_f32",
+    "sngb_dbscan_exact_f32", "sngb_dbscan_exact_f32_device", "sngb_dbscan_exact_f64",
+    "sngb_full_edges_f32",
 ]
 
 
 class SngbOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("flags", C.c_uint32), ("stream", C.c_void_p),
-                ("row_begin", C.c_uint64), ("row_end", C.c_uint64)]
+                ("row_begin", C.c_uint64), ("row_end", C.c_uint64),
+                # ABI 4: GPUs of this process (0/1: one; N; -1: all) and their ordinals
+                ("num_gpus", C.c_int32), ("devices", C.POINTER(C.c_int32))]
 
 
 class SngbInfo(C.Structure):
@@ -62,6 +66,8 @@ class SngbInfo(C.Structure):
         ("gather_pairs", C.c_uint64), ("gather_bytes", C.c_uint64),
         ("kernel_launches", C.c_uint64), ("library_launches", C.c_uint64),
         ("filter_bits", C.c_uint32), ("head_bytes", C.c_uint32),
+        ("num_gpus", C.c_uint32), ("merge_rounds", C.c_uint32), ("routed_keys", C.c_uint64),
+        ("ms_merge", C.c_float), ("reserved", C.c_uint32),
     ]
 
     def as_dict(self) -> dict:
@@ -132,6 +138,18 @@ def lib() -> C.CDLL:
                                              infop]
         L.sngb_dbscan_batch_f32.restype = C.c_int
         L.sngb_dbscan_batch_f32.argtypes = [C.POINTER(SngbProblem), C.c_uint64, optp]
+        L.sngb_dbscan_exact_f32.restype = C.c_int
+        L.sngb_dbscan_exact_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                            optp, i32p, u8p, infop]
+        L.sngb_dbscan_exact_f32_device.restype = C.c_int
+        L.sngb_dbscan_exact_f32_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double,
+                                                   C.c_int32, optp, vp, vp, infop]
+        L.sngb_dbscan_exact_f64.restype = C.c_int
+        L.sngb_dbscan_exact_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                            optp, i32p, u8p, infop]
+        L.sngb_full_edges_f32.restype = C.c_int
+        L.sngb_full_edges_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double, optp, u64p,
+                                          C.c_uint64, u64p, infop]
         L.sngb_strerror.restype = C.c_char_p
         L.sngb_strerror.argtypes = [C.c_int]
         L.sngb_last_error_detail.restype = C.c_char_p

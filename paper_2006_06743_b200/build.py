@@ -22,10 +22,12 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libsngb.so")
+CLI_SRC = os.path.join(PKG, "cpp", "tools", "sngb_cluster.cpp")
+CLI = os.path.join(PKG, "bin", "sngb_cluster")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["sngb_api.cu", "sngb_kernels.cu", "sngb_quant.cu", "sngb_metric.cu", "sngb_head.cu", "sngb_sampler.cu",
-           "sngb_cluster.cu"]
-HEADERS = ["sngb_internal.cuh", "sngb_rng.cuh", "sngb_device.cuh", "sngb_epstest.cuh",
+           "sngb_cluster.cu", "sngb_multi.cu"]
+HEADERS = ["sngb_internal.cuh", "sngb_host.cuh", "sngb_rng.cuh", "sngb_device.cuh", "sngb_epstest.cuh",
            "sngb_floyd_bitmap.cuh", "sngb_floyd_bloom.cuh", "sngb_head.cuh"]
 
 FLAGS = [
@@ -73,7 +75,24 @@ def build(verbose: bool = False, variant: str | None = None, extra: tuple = ()) 
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs,
                "-lcudart", "-lpthread"]
         subprocess.run(cmd, check=True)
+    if not variant:
+        build_cli(lib)
     return lib
+
+
+def build_cli(lib: str = LIB) -> str:
+    """The `cluster` front-end (SPEC cmd_cluster) over the C++ mirror -> bin/sngb_cluster."""
+    inc = os.path.join(PKG, "cpp", "include")
+    deps = [CLI_SRC, lib, os.path.join(ROOT, "include", "sngb.h"),
+            os.path.join(inc, "sngb", "sng.hpp"), os.path.join(inc, "sngb", "io.hpp")]
+    if _stale(CLI, deps):
+        os.makedirs(os.path.dirname(CLI), exist_ok=True)
+        libdir = os.path.dirname(lib)
+        subprocess.run([os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-Wall",
+                        "-I" + os.path.join(ROOT, "include"), "-I" + inc, CLI_SRC,
+                        "-L" + libdir, "-lsngb", "-Wl,-rpath,$ORIGIN/../lib", "-o", CLI],
+                       check=True)
+    return CLI
 
 
 if __name__ == "__main__":

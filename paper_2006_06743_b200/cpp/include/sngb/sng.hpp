@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "sngb.h"
@@ -105,6 +106,11 @@ struct SngParams {
     Distance dist = Distance::euclidean();
     int threads = 0;  // CPU workers in the reference; unused by the GPU path
     int device = -1;  // CUDA ordinal (-1 = current)
+    // extension (ABI 4): shard the rows over several GPUs of this process --
+    // 0/1: one GPU, N: N GPUs, -1: every visible GPU; `devices` optionally lists
+    // the ordinals (a repeated ordinal runs several shards on one GPU)
+    int num_gpus = 0;
+    std::vector<std::int32_t> devices;
 
     void validate() const {
         if (!(eps > 0.0)) throw std::invalid_argument("eps must be > 0");
@@ -140,6 +146,37 @@ inline void check(int rc) {
     if (rc == SNGB_ERR_CUDA) m += std::string(": ") + sngb_last_error_detail();
     throw std::runtime_error(m);
 }
+inline sngb_opts opts(int device, std::uint32_t flags, int num_gpus,
+                      const std::vector<std::int32_t>& devices) {
+    sngb_opts o{};
+    o.device = device;
+    o.flags = flags;
+    o.num_gpus = devices.empty() ? num_gpus
+                                 : (num_gpus == 0 || num_gpus == 1
+                                        ? static_cast<int>(devices.size())
+                                        : num_gpus);
+    o.devices = devices.empty() ? nullptr : devices.data();
+    return o;
+}
+
+inline Clustering to_clustering(std::vector<std::int32_t>&& labels,
+                                const std::vector<std::uint8_t>& roles, const sngb_info& gi) {
+    Clustering c;
+    const std::size_t n = labels.size();
+    c.assignment = std::move(labels);
+    c.role.resize(n);
+    for (std::size_t i = 0; i < n; ++i) c.role[i] = static_cast<PointRole>(roles[i]);
+    c.cluster_count = gi.cluster_count;
+    return c;
+}
+
+inline void to_info(ClusterRunInfo* info, const sngb_info& gi) {
+    if (!info) return;
+    info->distance_evals = gi.distance_evals;
+    info->edges = gi.edges;
+    info->graph_bytes = gi.graph_bytes;
+    info->gpu = gi;
+}
 }  // namespace detail
 
 inline Clustering sng_dbscan(const Dataset& data, const SngParams& params,
@@ -149,7 +186,8 @@ inline Clustering sng_dbscan(const Dataset& data, const SngParams& params,
     const std::size_t n = data.size();
     std::vector<std::int32_t> labels(n);
     std::vector<std::uint8_t> roles(n);
-    sngb_opts o{params.device, params.dist.flags(), nullptr, 0, 0};
+    sngb_opts o = detail::opts(params.device, params.dist.flags(), params.num_gpus,
+                               params.devices);
     sngb_info gi{};
     const auto d = static_cast<std::uint32_t>(data.dim());
     detail::check(data.is_fp64()
@@ -171,6 +209,63 @@ inline Clustering sng_dbscan(const Dataset& data, const SngParams& params,
         info->gpu = gi;
     }
     return c;
+}
+
+// Classical DBSCAN on the exact eps-graph (clusterer.hpp:46-48,
+// clusterer.cpp:67-79): distance_evals = n(n-1)/2.
+inline Clustering dbscan_exact(const Dataset& data, double eps, int min_pts,
+                               const Distance& dist = Distance::euclidean(), int threads = 0,
+                               ClusterRunInfo* info = nullptr, int device = -1,
+                               int num_gpus = 0,
+                               const std::vector<std::int32_t>& devices = {}) {
+    (void)threads;
+    if (!(eps > 0.0)) throw std::invalid_argument("eps must be > 0");
+    if (min_pts < 1) throw std::invalid_argument("min_pts must be >= 1");
+    if (data.empty()) throw std::invalid_argument("dataset is empty");
+    const std::size_t n = data.size();
+    std::vector<std::int32_t> labels(n);
+    std::vector<std::uint8_t> roles(n);
+    sngb_opts o = detail::opts(device, dist.flags(), num_gpus, devices);
+    sngb_info gi{};
+    const auto d = static_cast<std::uint32_t>(data.dim());
+    detail::check(data.is_fp64()
+                      ? sngb_dbscan_exact_f64(data.values_f64().data(), n, d, eps, min_pts, &o,
+                                              labels.data(), roles.data(), &gi)
+                      : sngb_dbscan_exact_f32(data.values_f32().data(), n, d, eps, min_pts, &o,
+                                              labels.data(), roles.data(), &gi));
+    detail::to_info(info, gi);
+    return detail::to_clustering(std::move(labels), roles, gi);
+}
+
+// The canonical edge list of build_full_graph (graph.hpp:69-70, SampledGraph::edges():
+// u < v, sorted) for fp32-exact data.
+inline std::vector<std::pair<std::uint32_t, std::uint32_t>> full_graph_edges(
+    const Dataset& data, double eps, const Distance& dist = Distance::euclidean(),
+    std::uint64_t* distance_evals = nullptr, int device = -1) {
+    if (data.empty()) throw std::invalid_argument("dataset is empty");
+    if (data.is_fp64())
+        throw std::invalid_argument("full_graph_edges: fp32-exact data only (use dbscan_exact)");
+    sngb_opts o = detail::opts(device, dist.flags(), 0, {});
+    sngb_info gi{};
+    std::uint64_t cap = 1u << 20, cnt = 0;
+    std::vector<std::uint64_t> keys;
+    for (;;) {
+        keys.resize(cap);
+        const int rc = sngb_full_edges_f32(data.values_f32().data(), data.size(),
+                                           static_cast<std::uint32_t>(data.dim()), eps, &o,
+                                           keys.data(), cap, &cnt, &gi);
+        if (rc == SNGB_ERR_CAPACITY) {
+            cap = cnt;
+            continue;
+        }
+        detail::check(rc);
+        break;
+    }
+    if (distance_evals) *distance_evals = gi.distance_evals;
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> e(cnt);
+    for (std::uint64_t i = 0; i < cnt; ++i)
+        e[i] = {static_cast<std::uint32_t>(keys[i] >> 32), static_cast<std::uint32_t>(keys[i])};
+    return e;
 }
 
 }  // namespace sng

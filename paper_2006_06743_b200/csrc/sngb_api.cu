@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "sngb.h"
+#include "sngb_host.cuh"
 #include "sngb_internal.cuh"
 #include "sngb_rng.cuh"
 
@@ -36,99 +37,24 @@ void sngb::note_launch(int hand_written, int library) {
     sngb_t_launch_lib += library;
 }
 
-namespace {
+namespace sngb {
+namespace host {
 
 thread_local std::string g_detail;
+std::string& detail() { return g_detail; }
+void reset_launches() {
+    sngb_t_launch_hand = 0;
+    sngb_t_launch_lib = 0;
+}
+uint64_t hand_launches() { return sngb_t_launch_hand; }
+uint64_t lib_launches() { return sngb_t_launch_lib; }
 
-struct CudaFail {
-    cudaError_t err;
-};
 
-#define CK(expr)                                                                      \
-    do {                                                                              \
-        cudaError_t _e = (expr);                                                      \
-        if (_e != cudaSuccess) {                                                      \
-            char _b[512];                                                             \
-            snprintf(_b, sizeof(_b), "%s at %s:%d (%s)", cudaGetErrorString(_e),      \
-                     __FILE__, __LINE__, #expr);                                      \
-            g_detail = _b;                                                            \
-            throw CudaFail{_e};                                                       \
-        }                                                                             \
-    } while (0)
 
-struct Buf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    template <typename T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-    void ensure(size_t want) {
-        if (want == 0) want = 16;
-        if (bytes >= want) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-        CK(cudaMalloc(&p, want));
-        bytes = want;
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-    }
-};
-
-struct DevCtx {
-    int dev = 0;
-    int num_sms = 148;
-    uint64_t l2_bytes = 126ull << 20;
-    cudaStream_t stream = nullptr;
-    cudaStream_t side = nullptr;          // sampler runs here, concurrently with the gather
-    cudaStream_t hi = nullptr;            // high-priority stream for the gather (SNGB_PRIO)
-    cudaEvent_t hi_fork = nullptr, hi_join = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    // host-buffer calls: the points are uploaded in row chunks on `copy`,
-    // chunk k's arrival is up_ev[k]; compute starts on the first chunk
-    static constexpr int kMaxChunks = 16;
-    cudaStream_t copy = nullptr;
-    cudaEvent_t up_start = nullptr;
-    cudaEvent_t up_ev[kMaxChunks] = {};
-    std::mutex mu;
-    Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
-        flags, rank, temp, labels, roles, work, q8, upload64, rnorm, band, partners, poff, rstart,
-        colstats, perm;
-    cudaEvent_t qev = nullptr;  // min/max of the points copied to the host (8-bit filter)
-    cudaEvent_t pev = nullptr;  // bucketed partner lists ready (host-upload 8-bit schedule)
-    unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
-    double* h_colstats = nullptr;  // pinned: per-column sums (8-bit filter column order)
-    uint32_t* h_perm = nullptr;    // pinned: that column order, uploaded per call
-    cudaEvent_t ev[12] = {};
-    uint64_t edge_hint = 0;  // last needed edge capacity for this context
-    uint64_t band_hint = 0;  // last needed band-list capacity
-
-    void release() {
-        for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
-                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band, &partners, &poff, &rstart, &colstats, &perm})
-            b->release();
-    }
-};
 
 std::mutex g_ctx_mu;
 std::vector<std::unique_ptr<DevCtx>> g_ctx;
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) CK(cudaSetDevice(dev));
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
 
 int device_count() {
     int n = 0;
@@ -139,10 +65,7 @@ int device_count() {
     return n;
 }
 
-// One context per (device, slot): slot 0 serves the single-problem calls,
-// slots 1.. the concurrent workers of sngb_dbscan_batch_f32.
-constexpr int kMaxSlots = 16;
-DevCtx& get_ctx(int dev, int slot = 0) {
+DevCtx& get_ctx(int dev, int slot) {
     std::lock_guard<std::mutex> lk(g_ctx_mu);
     const size_t idx = (size_t)dev * kMaxSlots + (size_t)slot;
     if (g_ctx.size() <= idx) g_ctx.resize(idx + 1);
@@ -309,31 +232,7 @@ int validate(uint64_t n, uint32_t d, double eps, int32_t min_pts, double rate, b
     return SNGB_OK;
 }
 
-struct Timer {
-    DevCtx& c;
-    cudaStream_t s;
-    bool on;
-    int next = 0;
-    void mark(int i) {
-        if (on) CK(cudaEventRecord(c.ev[i], s));
-    }
-    void mark_on(int i, cudaStream_t st) {
-        if (on) CK(cudaEventRecord(c.ev[i], st));
-    }
-    bool side = false;  // the sampler ran on the side stream (E_SIDE0..E_SIDE1)
-    float between(int a, int b) {
-        if (!on) return 0.f;
-        float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, c.ev[a], c.ev[b]) != cudaSuccess) {
-            cudaGetLastError();
-            return 0.f;
-        }
-        return ms;
-    }
-};
 
-enum Ev { E_START = 0, E_UPLOADED, E_PREPARED, E_SAMPLED, E_GATHERED, E_EXTRAS, E_SORTED,
-          E_CLUSTERED, E_DOWNLOADED, E_END, E_SIDE0, E_SIDE1 };
 
 // Number of L2-blocked gather phases.  A phase re-generates every draw
 // (~0.35 SM-cycles each) and re-streams the query rows, and in exchange turns
@@ -353,16 +252,6 @@ uint32_t gather_phases(const DevCtx& c, uint64_t n, uint32_t stride, uint64_t dr
     return p <= cap ? (uint32_t)p : 1u;
 }
 
-struct GraphResult {
-    unsigned long long* ukeys = nullptr;  // device, compact keys
-    uint64_t m = 0;                       // unique count (valid after sync)
-    uint32_t nb = 1;
-    uint64_t draws = 0;
-    bool exhaustive = false;
-    uint64_t raw = 0;
-    bool q8 = false;  // the gather ran the 8-bit filter
-    uint32_t head = 0;  // the gather ran the head filter (sngb_head.cu): its bytes per row
-};
 
 // Prepare points and run the graph build for rows [rb, re).  Leaves sorted
 // unique compact keys in c.keys/keys_alt and their count in
@@ -372,8 +261,8 @@ struct GraphResult {
 // the sampler and (L2-blocked case) with the gather of the chunks already in.
 int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64_t n, uint32_t d,
                 double eps, double rate, uint64_t seed, uint64_t rb, uint64_t re,
-                GraphResult& gr, const float* h_src = nullptr, const double* d_pts64 = nullptr,
-                int32_t metric = kMetricEuclid) {
+                GraphResult& gr, const float* h_src, const double* d_pts64, int32_t metric,
+                bool upper_only) {
     unsigned long long* dc = nullptr;
     c.counters.ensure(C_COUNT * sizeof(unsigned long long));
     dc = c.counters.as<unsigned long long>();
@@ -465,7 +354,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     if (exhaustive) {
         // rows [rb, re) pair with all v > u, and (a partial range) with all v < rb
         const double sum = (double)rows * (double)(n - 1) - ((double)re * (re - 1) - (double)rb * (rb - 1)) / 2.0;
-        pairs = (uint64_t)std::max(0.0, sum) + rows * rb;
+        pairs = (uint64_t)std::max(0.0, sum) + (upper_only ? 0 : rows * rb);
     } else {
         pairs = rows * draws;
     }
@@ -841,7 +730,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             ensure_norms();
             for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
         }
-        if (exhaustive && rb > 0) {  // a row range: its rows' pairs with every v < rb too
+        if (exhaustive && rb > 0 && !upper_only) {  // a row range: its rows' pairs with every v < rb too
             ga.exh_low = (uint32_t)rb;
             for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
             ga.exh_low = 0;
@@ -1051,7 +940,10 @@ const unsigned long long* ull(const uint64_t* p) {
     return reinterpret_cast<const unsigned long long*>(p);
 }
 
-}  // namespace
+}  // namespace host
+}  // namespace sngb
+
+using namespace sngb::host;
 
 extern "C" {
 
@@ -1059,7 +951,7 @@ int sngb_abi_version(void) { return SNGB_ABI_VERSION; }
 
 int sngb_device_count(void) { return device_count(); }
 
-const char* sngb_last_error_detail(void) { return g_detail.c_str(); }
+const char* sngb_last_error_detail(void) { return detail().c_str(); }
 
 const char* sngb_strerror(int code) {
     switch (code) {
@@ -1101,6 +993,19 @@ int sngb_dbscan_f32_device(const float* d_pts, uint64_t n, uint32_t d, double ep
     if (!d_pts || !d_labels || !d_roles) return SNGB_ERR_ARG;
     if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    std::vector<int> devs;
+    const int w = multi_devices(opts, devs);
+    if (w < 0) return SNGB_ERR_ARG;
+    if (w > 1)
+        return guarded([&]() -> int {
+            if (opts->stream) {  // the caller's prior work on the points is complete
+                DeviceGuard dg(devs[0]);
+                CK(cudaStreamSynchronize((cudaStream_t)opts->stream));
+            }
+            return multi_dbscan(devs, 2, d_pts, n, d, eps, min_pts, rate, seed, metric_of(opts),
+                                false, (opts->flags & SNGB_FLAG_TIMING) != 0, d_labels, d_roles,
+                                info);
+        });
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
         DeviceGuard dg(dev);
@@ -1162,6 +1067,23 @@ static int dbscan_f32_host(int slot, const float* pts, uint64_t n, uint32_t d, d
 int sngb_dbscan_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
                     double rate, uint64_t seed, const sngb_opts* opts, int32_t* labels_out,
                     uint8_t* roles_out, sngb_info* info) {
+    std::vector<int> devs;
+    if (opts && opts->num_gpus != 0 && opts->num_gpus != 1) {
+        int rc = validate(n, d, eps, min_pts, rate, true);
+        if (rc) return rc;
+        if (!pts || !labels_out || !roles_out) return SNGB_ERR_ARG;
+        if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
+        if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    }
+    const int w = multi_devices(opts, devs);
+    if (w < 0) return SNGB_ERR_ARG;
+    if (w > 1) {
+        return guarded([&]() -> int {
+            return multi_dbscan(devs, 0, pts, n, d, eps, min_pts, rate, seed, metric_of(opts),
+                                false, (opts->flags & SNGB_FLAG_TIMING) != 0, labels_out,
+                                roles_out, info);
+        });
+    }
     return dbscan_f32_host(0, pts, n, d, eps, min_pts, rate, seed, opts, labels_out, roles_out,
                            info);
 }
@@ -1381,6 +1303,15 @@ int sngb_dbscan_f64(const double* pts, uint64_t n, uint32_t d, double eps, int32
     if (!pts || !labels_out || !roles_out) return SNGB_ERR_ARG;
     if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
     if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    std::vector<int> devs;
+    const int w = multi_devices(opts, devs);
+    if (w < 0) return SNGB_ERR_ARG;
+    if (w > 1)
+        return guarded([&]() -> int {
+            return multi_dbscan(devs, 1, pts, n, d, eps, min_pts, rate, seed, metric_of(opts),
+                                false, (opts->flags & SNGB_FLAG_TIMING) != 0, labels_out,
+                                roles_out, info);
+        });
     return guarded([&]() -> int {
         const int dev = resolve_device(opts);
         DeviceGuard dg(dev);
@@ -1583,6 +1514,106 @@ int sngb_relabel_device(uint64_t n, const int32_t* d_degree, int32_t min_pts,
         info->kernel_launches = sngb_t_launch_hand;
         info->library_launches = sngb_t_launch_lib;
     }
+    return rc;
+}
+
+
+// ---- sng::dbscan_exact / build_full_graph (clusterer.cpp:67-79, graph.cpp:191-220) ----
+// The exact eps-graph is the exhaustive branch of the graph build (every v > u
+// tested once: the GPU path already evaluates each unordered pair once);
+// dbscan_exact differs from sng_dbscan(rate = 1) only in its validation (no
+// rate) and in counting n(n-1)/2 distance evaluations (graph.cpp:206-210).
+}  // extern "C"
+
+static int validate_exact(uint64_t n, uint32_t d, double eps, int32_t min_pts) {
+    if (!(eps > 0.0)) return SNGB_ERR_EPS;      // clusterer.cpp:69
+    if (min_pts < 1) return SNGB_ERR_MINPTS;    // clusterer.cpp:70
+    if (n == 0) return SNGB_ERR_EMPTY;          // graph.cpp:18
+    if (d == 0) return SNGB_ERR_DIM;            // dataset.hpp:22
+    if (n >= 0xffffff00ull) return SNGB_ERR_TOO_LARGE;
+    return SNGB_OK;
+}
+
+static void exact_info(sngb_info* info, uint64_t n) {
+    if (!info) return;
+    info->draws = n - 1;
+    info->distance_evals = n * (n - 1) / 2;  // build_full_graph: v > u only
+}
+
+template <class Single>
+static int exact_call(uint64_t n, uint32_t d, double eps, int32_t min_pts, const void* pts,
+                      const void* labels, const void* roles, const sngb_opts* opts, int src_kind,
+                      int32_t* lab, uint8_t* rol, sngb_info* info, Single&& single) {
+    int rc = validate_exact(n, d, eps, min_pts);
+    if (rc) return rc;
+    if (!pts || !labels || !roles) return SNGB_ERR_ARG;
+    if (!metric_flags_ok(opts)) return SNGB_ERR_ARG;
+    if (device_count() == 0) return SNGB_ERR_NO_DEVICE;
+    std::vector<int> devs;
+    const int w = multi_devices(opts, devs);
+    if (w < 0) return SNGB_ERR_ARG;
+    if (w > 1) {
+        rc = guarded([&]() -> int {
+            if (src_kind == 2 && opts->stream) {
+                DeviceGuard dg(devs[0]);
+                CK(cudaStreamSynchronize((cudaStream_t)opts->stream));
+            }
+            return multi_dbscan(devs, src_kind, pts, n, d, eps, min_pts, 1.0, 0, metric_of(opts),
+                                true, (opts->flags & SNGB_FLAG_TIMING) != 0, lab, rol, info);
+        });
+        return rc;
+    }
+    rc = single();
+    if (rc == SNGB_OK) exact_info(info, n);
+    return rc;
+}
+
+extern "C" {
+
+int sngb_dbscan_exact_f32(const float* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                          const sngb_opts* opts, int32_t* labels_out, uint8_t* roles_out,
+                          sngb_info* info) {
+    return exact_call(n, d, eps, min_pts, pts, labels_out, roles_out, opts, 0, labels_out,
+                      roles_out, info, [&]() {
+                          return dbscan_f32_host(0, pts, n, d, eps, min_pts, 1.0, 0, opts,
+                                                 labels_out, roles_out, info);
+                      });
+}
+
+int sngb_dbscan_exact_f32_device(const float* d_pts, uint64_t n, uint32_t d, double eps,
+                                 int32_t min_pts, const sngb_opts* opts, int32_t* d_labels,
+                                 uint8_t* d_roles, sngb_info* info) {
+    return exact_call(n, d, eps, min_pts, d_pts, d_labels, d_roles, opts, 2, d_labels, d_roles,
+                      info, [&]() {
+                          sngb_opts o = opts ? *opts : sngb_opts{-1, 0u, nullptr, 0, 0, 0, nullptr};
+                          o.num_gpus = 0;
+                          return sngb_dbscan_f32_device(d_pts, n, d, eps, min_pts, 1.0, 0, &o,
+                                                        d_labels, d_roles, info);
+                      });
+}
+
+int sngb_dbscan_exact_f64(const double* pts, uint64_t n, uint32_t d, double eps, int32_t min_pts,
+                          const sngb_opts* opts, int32_t* labels_out, uint8_t* roles_out,
+                          sngb_info* info) {
+    return exact_call(n, d, eps, min_pts, pts, labels_out, roles_out, opts, 1, labels_out,
+                      roles_out, info, [&]() {
+                          sngb_opts o = opts ? *opts : sngb_opts{-1, 0u, nullptr, 0, 0, 0, nullptr};
+                          o.num_gpus = 0;
+                          return sngb_dbscan_f64(pts, n, d, eps, min_pts, 1.0, 0, &o, labels_out,
+                                                 roles_out, info);
+                      });
+}
+
+int sngb_full_edges_f32(const float* pts, uint64_t n, uint32_t d, double eps, const sngb_opts* opts,
+                        uint64_t* keys_out, uint64_t capacity, uint64_t* count_out,
+                        sngb_info* info) {
+    sngb_opts o = opts ? *opts : sngb_opts{-1, 0u, nullptr, 0, 0, 0, nullptr};
+    o.row_begin = 0;
+    o.row_end = 0;
+    o.num_gpus = 0;
+    const int rc = sngb_sampled_edges_f32(pts, n, d, eps, 1.0, 0, &o, keys_out, capacity,
+                                          count_out, info);
+    if (rc == SNGB_OK || rc == SNGB_ERR_CAPACITY) exact_info(info, n);
     return rc;
 }
 

@@ -1,10 +1,12 @@
 // Builds against the C++ mirror (sngb/sng.hpp) exactly as a reference user
 // would against sng/clusterer.hpp.  Exit codes: 0 ok, 2 wrong result,
 // 3 no GPU (std::runtime_error), 4 unexpected exception text.
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "sngb/io.hpp"
@@ -52,7 +54,25 @@ int main() {
         p.dist = sng::Distance::parse("manhattan");
         sng::Clustering cm = sng::sng_dbscan(ds, p, &info);
         std::printf("manhattan: clusters=%d\n", cm.cluster_count);
-        return cm.assignment == c.assignment ? 0 : 2;
+        if (cm.assignment != c.assignment) return 2;
+        // dbscan_exact (clusterer.cpp:67-79): same clusters, n(n-1)/2 = 6 evaluations
+        sng::ClusterRunInfo ei;
+        sng::Clustering ce = sng::dbscan_exact(ds, 1.0, 1, sng::Distance::euclidean(), 0, &ei);
+        std::uint64_t fe = 0;
+        const auto edges = sng::full_graph_edges(ds, 1.0, sng::Distance::euclidean(), &fe);
+        std::printf("exact: clusters=%d evals=%llu full_edges=%zu\n", ce.cluster_count,
+                    (unsigned long long)ei.distance_evals, edges.size());
+        if (ce.assignment != c.assignment || ei.distance_evals != 6 || fe != 6 ||
+            edges.size() != 2 || edges[0] != std::make_pair(0u, 1u))
+            return 2;
+        // two row shards on GPU 0 (ABI 4 multi-GPU path, a repeated ordinal)
+        sng::SngParams pm = p;
+        pm.dist = sng::Distance::euclidean();
+        pm.devices = {0, 0};
+        sng::ClusterRunInfo mi;
+        sng::Clustering cmg = sng::sng_dbscan(ds, pm, &mi);
+        std::printf("multi: clusters=%d gpus=%u\n", cmg.cluster_count, mi.gpu.num_gpus);
+        return (cmg.assignment == c.assignment && mi.gpu.num_gpus == 2) ? 0 : 2;
     } catch (const std::runtime_error& e) {
         std::printf("runtime_error: %s\n", e.what());
         return 3;

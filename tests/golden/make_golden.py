@@ -62,6 +62,27 @@ CASES = [
 ]
 
 
+# dbscan_exact (clusterer.cpp:67-79) / build_full_graph (graph.cpp:191-220) cases:
+# (name, recipe, eps, min_pts, metric)
+EXACT_CASES = [
+    ("exact_spec_line", {"kind": "explicit", "values": [[0.0], [0.5], [10.0], [10.5]]}, 1.0, 1,
+     "euclidean"),
+    ("exact_coincident5", {"kind": "explicit", "values": [[1.0, 1.0]] * 5}, 1.0, 4, "euclidean"),
+    ("exact_single", {"kind": "explicit", "values": [[3.0, 4.0]]}, 0.5, 1, "euclidean"),
+    ("exact_rand_500x3", {"kind": "random", "n": 500, "d": 3, "seed": 3, "scale": 1.0}, 0.15, 4,
+     "euclidean"),
+    ("exact_rand_3000x16", {"kind": "random", "n": 3000, "d": 16, "seed": 11, "scale": 3.0}, 3.6,
+     5, "euclidean"),
+    ("exact_rand_1200x784", {"kind": "random", "n": 1200, "d": 784, "seed": 2, "scale": 1.0},
+     11.2, 5, "euclidean"),
+    ("exact_cfg1_n6000", {"kind": "synthetic", "cfg": 1, "n": 6000}, 0.03, 10, "euclidean"),
+    ("exact_manhattan_800x5", {"kind": "random", "n": 800, "d": 5, "seed": 8, "scale": 1.0}, 0.6,
+     3, "manhattan"),
+    ("exact_cosine_800x8", {"kind": "random", "n": 800, "d": 8, "seed": 9, "scale": 1.0}, 0.05,
+     3, "cosine"),
+]
+
+
 def build_points(recipe):
     k = recipe["kind"]
     if k == "arange":
@@ -124,6 +145,26 @@ def main():
             c["labels"] = labels.tolist()
             c["roles"] = roles.tolist()
         g["cases"].append(c)
+        print(name, c["edges"], c["cluster_count"], flush=True)
+    g["exact_cases"] = []
+    for name, recipe, eps, min_pts, metric in EXACT_CASES:
+        pts = build_points(recipe)
+        ds = ref.dataset(pts)
+        ref.set_metric(metric)
+        labels, roles, info, keys = ref.dbscan_exact(ds, eps, min_pts)
+        ref.set_metric("euclidean")
+        c = {"name": name, "recipe": recipe, "eps": eps, "min_pts": min_pts, "metric": metric,
+             "n": int(pts.shape[0]), "d": int(pts.shape[1]),
+             "distance_evals": info["distance_evals"], "edges": info["edges"],
+             "graph_bytes": info["graph_bytes"], "cluster_count": info["cluster_count"],
+             "points_sha256": sha(pts), "keys_sha256": sha(keys), "labels_sha256": sha(labels),
+             "roles_sha256": sha(roles), "core": int((roles == 0).sum()),
+             "border": int((roles == 1).sum()), "noise": int((roles == 2).sum())}
+        if pts.shape[0] <= 64:
+            c["keys"] = [str(int(k)) for k in keys]
+            c["labels"] = labels.tolist()
+            c["roles"] = roles.tolist()
+        g["exact_cases"].append(c)
         print(name, c["edges"], c["cluster_count"], flush=True)
     with open(OUT, "w") as f:
         json.dump(g, f, indent=1)

@@ -68,7 +68,7 @@ def test_strerror_carries_reference_messages():
     assert _lib.strerror(4) == "dataset is empty"
     assert _lib.strerror(5) == "dataset dimension must be >= 1"
     assert _lib.strerror(6) == "dataset contains a non-finite value"
-    assert int(_lib.lib().sngb_abi_version()) == 3
+    assert int(_lib.lib().sngb_abi_version()) == 4
 
 
 def _call(pts, eps=1.0, min_pts=1, rate=1.0, seed=0):

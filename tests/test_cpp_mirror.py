@@ -39,3 +39,5 @@ def test_cpp_mirror_on_gpu(tmp_path):
                        env={**os.environ, "DEMO_DIR": str(tmp_path)})
     assert r.returncode == 0, r.stdout + r.stderr
     assert "fp64 via SNGD: clusters=2 ok=1" in r.stdout
+    assert "exact: clusters=2 evals=6 full_edges=2" in r.stdout
+    assert "multi: clusters=2 gpus=2" in r.stdout

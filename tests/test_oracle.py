@@ -104,3 +104,22 @@ def test_oracle_errors(oracle):
         oracle.sng_dbscan(pts, 1.0, 0, 1.0, 0)
     with pytest.raises(ValueError, match=r"rate must lie in \(0, 1\]"):
         oracle.sng_dbscan(pts, 1.0, 1, 0.0, 0)
+
+
+def test_oracle_rate1_reproduces_reference_dbscan_exact(oracle):
+    """dbscan_exact (clusterer.cpp:67-79) clusters build_full_graph; for a symmetric
+    metric that is the rate-1 sampled graph (graph.cpp:157-159), so the oracle's
+    rate-1 run must reproduce the reference's dbscan_exact fixtures bit for bit."""
+    from tests import _golden
+    g = _golden.load()
+    for c in g["exact_cases"]:
+        if c["metric"] != "euclidean":
+            continue
+        pts = _golden.points(c["recipe"])
+        labels, roles, info, keys = oracle.sng_dbscan(pts, c["eps"], c["min_pts"], 1.0, 0)
+        assert _golden.sha(keys) == c["keys_sha256"], c["name"]
+        assert _golden.sha(labels) == c["labels_sha256"], c["name"]
+        assert _golden.sha(roles) == c["roles_sha256"], c["name"]
+        assert info["edges"] == c["edges"]
+        n = c["n"]
+        assert c["distance_evals"] == n * (n - 1) // 2
