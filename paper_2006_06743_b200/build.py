@@ -26,7 +26,7 @@ CLI_SRC = os.path.join(PKG, "cpp", "tools", "sngb_cluster.cpp")
 CLI = os.path.join(PKG, "bin", "sngb_cluster")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["sngb_api.cu", "sngb_kernels.cu", "sngb_quant.cu", "sngb_metric.cu", "sngb_head.cu", "sngb_sampler.cu",
-           "sngb_cluster.cu", "sngb_multi.cu"]
+           "sngb_cluster.cu", "sngb_multi.cu", "sngb_fused.cu"]
 HEADERS = ["sngb_internal.cuh", "sngb_host.cuh", "sngb_rng.cuh", "sngb_device.cuh", "sngb_epstest.cuh",
            "sngb_floyd_bitmap.cuh", "sngb_floyd_bloom.cuh", "sngb_head.cuh"]
 
@@ -77,7 +77,32 @@ def build(verbose: bool = False, variant: str | None = None, extra: tuple = ()) 
         subprocess.run(cmd, check=True)
     if not variant:
         build_cli(lib)
+        build_pymod(lib)
     return lib
+
+
+PYMOD_SRC = os.path.join(PKG, "cpp", "python", "sngdbscan_module.cpp")
+PYMOD_DIR = os.path.join(ROOT, "sngdbscan")
+
+
+def build_pymod(lib: str = LIB) -> str:
+    """The `sngdbscan` pybind11 module (reference proj/CMakeLists.txt:11) ->
+    sngdbscan/_sngdbscan<EXT_SUFFIX>, linked against libsngb.so."""
+    import sysconfig
+
+    import pybind11
+
+    out = os.path.join(PYMOD_DIR, "_sngdbscan" + sysconfig.get_config_var("EXT_SUFFIX"))
+    deps = [PYMOD_SRC, lib, os.path.join(ROOT, "include", "sngb.h")]
+    if _stale(out, deps):
+        libdir = os.path.dirname(lib)
+        rel = os.path.relpath(libdir, PYMOD_DIR)
+        subprocess.run([os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-shared", "-fPIC",
+                        "-fvisibility=hidden", "-I" + pybind11.get_include(),
+                        "-I" + sysconfig.get_paths()["include"],
+                        "-I" + os.path.join(ROOT, "include"), PYMOD_SRC, "-L" + libdir, "-lsngb",
+                        f"-Wl,-rpath,$ORIGIN/{rel}", "-o", out], check=True)
+    return out
 
 
 def build_cli(lib: str = LIB) -> str:

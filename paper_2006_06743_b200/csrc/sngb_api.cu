@@ -440,7 +440,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     // points, waits for the filter plan and quantises; the gather then waits for
     // the sampler (run together they slow the gather more than they gain).  The
     // fork is recorded here, before the prepare pass.
-    const bool side_pre = !exhaustive && !h_src && (q8_try || head_try) &&
+    // Floyd bookkeeping fused into the head gather (sngb_fused.cu: every draw
+    // generated once) when the head filter runs; the head plan decides, so the
+    // sampler launch is held back until then
+    const bool fuse_try = head_try && !exhaustive && fused_eligible(n, draws, stride);
+    const bool side_pre = !exhaustive && !fuse_try && !h_src && (q8_try || head_try) &&
                           !(stride <= 64 && (re - rb) >= 10000 && draws <= 1024) &&  // not overlap
                           env_u64("SNGB_OVERLAP", 2) != 1 && env_u64("SNGB_SIDE_PRE", 1) != 0;
     if (side_pre) CK(cudaEventRecord(c.fork, s));
@@ -489,7 +493,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 10000 &&
                                         draws <= 1024));
         // host upload: the sampler reads no points, so it also runs while they arrive
-        const bool side = !exhaustive && (overlap || side_pre || (h_src && attempt == 0));
+        const bool side =
+            !exhaustive && !fuse_try && (overlap || side_pre || (h_src && attempt == 0));
         if (pre_partners && attempt == 0) {  // before the sampler on the side stream
             c.partners.ensure((re - rb) * draws * 4ull);
             c.poff.ensure((re - rb) * (chunks + 1) * 4ull);
@@ -506,7 +511,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                                c.num_sms));
             CK(cudaEventRecord(c.pev, c.side));
         }
-        if (!exhaustive) {
+        auto make_sa = [&]() {
             SamplerArgs sa{};
             sa.n = n;
             sa.row_begin = rb;
@@ -521,6 +526,10 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             sa.extras = c.extras.as<unsigned long long>();
             sa.extras_capacity = extras_cap;
             sa.counters = dc;
+            return sa;
+        };
+        if (!exhaustive && !fuse_try) {
+            SamplerArgs sa = make_sa();
             if (side) {
                 // the Floyd bookkeeping needs no point data: run it on the side
                 // stream while the gather runs here; non-persistent grids let the
@@ -635,6 +644,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             }
         }
         if (side_pre) CK(cudaStreamWaitEvent(s, c.join, 0));  // gather after the sampler
+        const bool fused = fuse_try && head_on;
+        if (fuse_try && !head_on) CK(launch_sampler(make_sa(), s, c.num_sms));  // unfused after all
         tm.mark(E_SAMPLED);
         GatherArgs ga{};
         ga.tp = tp;
@@ -653,7 +664,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         constexpr uint32_t kWorkSlots = 256;
         const bool dyn = ga.rows_per_block == 0 && env_u64("SNGB_GATHER_DYN", 1) == 1;
         uint32_t work_slot = 0;
-        if (dyn) {
+        if (dyn || fused) {
             c.work.ensure(kWorkSlots * 8);
             CK(cudaMemsetAsync(c.work.p, 0, kWorkSlots * 8, s));
         }
@@ -728,7 +739,17 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 for (uint32_t k = 0; k < chunks; ++k) land_chunk(k);
             prepared = quantized = chunks;
             ensure_norms();
-            for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
+            if (fused) {  // Floyd bookkeeping + head gather in one kernel
+                ga.row_begin = rb;
+                ga.row_end = re;
+                ga.part_lo = 0;
+                ga.part_hi = (uint32_t)n;
+                ga.partners = nullptr;
+                ga.work = c.work.as<unsigned long long>() + work_slot++;
+                CK(launch_floyd_head(make_sa(), ga, hp.args, gs, c.num_sms));
+            } else {
+                for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
+            }
         }
         if (exhaustive && rb > 0 && !upper_only) {  // a row range: its rows' pairs with every v < rb too
             ga.exh_low = (uint32_t)rb;

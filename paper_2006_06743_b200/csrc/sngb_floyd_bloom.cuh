@@ -124,6 +124,9 @@ __device__ __forceinline__ void red_or_sh_if(uint32_t addr, uint32_t v, uint32_t
         "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}"
         ::"r"(addr), "r"(v), "r"(pred) : "memory");
 }
+__device__ __forceinline__ void st_sh(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_sh(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");

@@ -252,6 +252,11 @@ bool head_plan(double lo, double hi, uint32_t d, double eps2, int kind, HeadPlan
 cudaError_t launch_head_quantize(const float* pts, uint32_t stride, uint64_t n, const HeadPlan& p,
                                  void* out, cudaStream_t s, int num_sms);
 cudaError_t launch_gather_head(const GatherArgs& a, const HeadArgs& h, cudaStream_t s, int num_sms);
+// sngb_fused.cu: Floyd bookkeeping + head gather in one pass (large n, narrow rows);
+// a.work must point at a zeroed counter (dynamic vertex claiming)
+bool fused_eligible(uint64_t n, uint32_t draws, uint32_t stride);
+cudaError_t launch_floyd_head(const SamplerArgs& sa, const GatherArgs& ga, const HeadArgs& h,
+                              cudaStream_t s, int num_sms);
 
 // ---- cluster stage (sngb_cluster.cu) ----
 struct ClusterBuffers {

@@ -348,7 +348,7 @@ def _head_case(n, d, seed, k=12, spread=0.05, box=20.0):
     return np.ascontiguousarray(pts, np.float32)
 
 
-@pytest.mark.parametrize("bloom", [False, True])
+@pytest.mark.parametrize("bloom", [False, True, "unfused"])
 @pytest.mark.parametrize("mode,kind", [("0", "99"), ("2", "0"), ("2", "1"), ("2", "2")])
 @pytest.mark.parametrize("n,d,rate,seed,q", [(3000, 3, 0.05, 31, 0.3), (2500, 5, 0.06, 32, 0.5),
                                              (3000, 8, 0.05, 33, 0.2), (2800, 16, 0.05, 34, 0.6),
@@ -360,12 +360,15 @@ def test_head_filter_matches_oracle(oracle, monkeypatch, bloom, mode, kind, n, d
     four 8-bit or two 8-bit coordinates -- SNGB_HEAD_KIND 0/1/2 -- fp32 test for
     survivors) on every row width it serves; =0 is the plain fp32 gather.  eps at
     low and high within-cluster quantiles (few / many survivors): all identical
-    to the oracle.  bloom=True runs the large-n Floyd kernel beside it, False
-    the bitmap one."""
+    to the oracle.  bloom=True runs the large-n Floyd bookkeeping fused into the
+    head gather (sngb_fused.cu), "unfused" the same as two kernels
+    (k_floyd_bloom + k_gather_head), False the bitmap Floyd kernel."""
     monkeypatch.setenv("SNGB_HEAD", mode)
     monkeypatch.setenv("SNGB_HEAD_KIND", kind)
     if bloom:
         monkeypatch.setenv("SNGB_FLOYD_NO_BITMAP", "1")
+    if bloom == "unfused":
+        monkeypatch.setenv("SNGB_FUSED", "0")
     monkeypatch.setenv("SNGB_Q8", "0")
     pts = _head_case(n, d, seed)
     i = np.arange(0, n - 1, 5)
@@ -408,10 +411,13 @@ def test_head_filter_outlier_and_irregular_exact(oracle, monkeypatch):
     eps = 0.4
     keys, _ = oracle.sampled_edges(pts, eps, 0.04, 42)
     monkeypatch.setenv("SNGB_HEAD", "2")
-    for kind, bloom in (("0", False), ("1", False), ("2", False), ("0", True), ("2", True)):
+    for kind, bloom in (("0", False), ("1", False), ("2", False), ("0", True), ("2", True),
+                        ("1", "unfused"), ("2", "unfused")):
         monkeypatch.setenv("SNGB_HEAD_KIND", kind)
-        if bloom:  # the large-n Floyd kernel
+        if bloom:  # the large-n Floyd bookkeeping (fused into the head gather)
             monkeypatch.setenv("SNGB_FLOYD_NO_BITMAP", "1")
+        if bloom == "unfused":
+            monkeypatch.setenv("SNGB_FUSED", "0")
         monkeypatch.delenv("SNGB_TEST_FORCE_IRREGULAR", raising=False)
         g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.04, seed=42)
         np.testing.assert_array_equal(g.keys, keys)
@@ -438,9 +444,13 @@ def test_head_filter_device_api_and_row_range(oracle, monkeypatch):
     np.testing.assert_array_equal(_host_edges_rows(pts, eps, rate, seed, rb, re), okeys)
 
 
-def test_head_filter_auto_on_cfg5_shape(oracle):
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_head_filter_auto_on_cfg5_shape(oracle, monkeypatch, fused):
     """cfg5's row shape (d = 32) with the fp32 table beyond half the L2: auto
-    selects the head filter; labels identical to the oracle."""
+    selects the head filter (fused with the Floyd bookkeeping, or the two
+    kernels with SNGB_FUSED=0); labels identical to the oracle."""
+    if fused == "0":
+        monkeypatch.setenv("SNGB_FUSED", "0")
     n = 600_000
     pts = synthetic.generate(5, n=n)
     w = synthetic.CONFIGS[5]
@@ -682,3 +692,29 @@ def test_q8_variance_ordered_head(oracle, monkeypatch, host):
             assert gi.edges == oinfo["edges"]
             got[perm] = gi.gather_bytes
     assert got["1"] < 0.6 * got["0"], got
+
+
+@pytest.mark.parametrize("cfg,n", [(3, 200_000), (4, 400_000), (5, 300_000)])
+def test_fused_floyd_head_equals_two_kernels(monkeypatch, cfg, n):
+    """k_floyd_head (Floyd bookkeeping + head gather in one pass) against the two
+    kernels it replaces, on reduced BASELINE shapes (the bloom regime): the same
+    edge list, collisions and pair counts; also with forced Lemire replays."""
+    import torch
+    w = synthetic.CONFIGS[cfg]
+    x = torch.from_numpy(synthetic.generate(cfg, n=n)).cuda()
+    rate = w.draws / n
+    for force in (None, "9"):
+        if force:
+            monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
+        monkeypatch.delenv("SNGB_FUSED", raising=False)
+        kf, gf = sng.sampled_edges_device(x, w.eps, rate, w.seed)
+        monkeypatch.setenv("SNGB_FUSED", "0")
+        k2, g2 = sng.sampled_edges_device(x, w.eps, rate, w.seed)
+        torch.cuda.synchronize()
+        assert gf.filter_bits == g2.filter_bits == 16
+        assert torch.equal(kf, k2), (cfg, force)
+        assert gf.collisions == g2.collisions
+        assert gf.irregular_vertices == g2.irregular_vertices
+        if not force:
+            assert gf.gather_pairs == g2.gather_pairs == gf.draws * n
+            assert gf.pairs_evaluated == g2.pairs_evaluated
