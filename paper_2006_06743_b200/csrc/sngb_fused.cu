@@ -423,12 +423,18 @@ cudaError_t fused_kind(const SamplerArgs& sa, const GatherArgs& ga, const HeadAr
 
 }  // namespace
 
+#ifndef SNGB_FUSED_DEFAULT
+#define SNGB_FUSED_DEFAULT 0
+#endif
+constexpr int kFusedDefault = SNGB_FUSED_DEFAULT;
+
 bool fused_eligible(uint64_t n, uint32_t draws, uint32_t stride) {
-    // SNGB_FUSED=0 keeps the two kernels.  Fused wherever launch_sampler would
+    // SNGB_FUSED=0 keeps the two kernels, 1 fuses (default: SNGB_FUSED_DEFAULT).  Fused wherever launch_sampler would
     // pick k_floyd_bloom (n beyond the per-warp bitmap kernel's 73 k, or
     // SNGB_FLOYD_NO_BITMAP; draws <= 4096) for rows of <= 32 float4
     const char* e = std::getenv("SNGB_FUSED");
-    if ((e && std::atoi(e) == 0) || draws < 1 || draws > 4096 || n - 2 >= 0xffffffffull ||
+    const int mode = e ? std::atoi(e) : kFusedDefault;
+    if (mode == 0 || draws < 1 || draws > 4096 || n - 2 >= 0xffffffffull ||
         stride / 4 > 32)
         return false;
     const uint64_t bm_words = (((n - 1) + 31) / 32 + 3) & ~3ull;

@@ -367,8 +367,7 @@ def test_head_filter_matches_oracle(oracle, monkeypatch, bloom, mode, kind, n, d
     monkeypatch.setenv("SNGB_HEAD_KIND", kind)
     if bloom:
         monkeypatch.setenv("SNGB_FLOYD_NO_BITMAP", "1")
-    if bloom == "unfused":
-        monkeypatch.setenv("SNGB_FUSED", "0")
+    monkeypatch.setenv("SNGB_FUSED", "0" if bloom == "unfused" else "1")
     monkeypatch.setenv("SNGB_Q8", "0")
     pts = _head_case(n, d, seed)
     i = np.arange(0, n - 1, 5)
@@ -416,8 +415,7 @@ def test_head_filter_outlier_and_irregular_exact(oracle, monkeypatch):
         monkeypatch.setenv("SNGB_HEAD_KIND", kind)
         if bloom:  # the large-n Floyd bookkeeping (fused into the head gather)
             monkeypatch.setenv("SNGB_FLOYD_NO_BITMAP", "1")
-        if bloom == "unfused":
-            monkeypatch.setenv("SNGB_FUSED", "0")
+        monkeypatch.setenv("SNGB_FUSED", "0" if bloom == "unfused" else "1")
         monkeypatch.delenv("SNGB_TEST_FORCE_IRREGULAR", raising=False)
         g = sng.build_sampled_graph(sng.Dataset(pts), eps, 0.04, seed=42)
         np.testing.assert_array_equal(g.keys, keys)
@@ -449,8 +447,7 @@ def test_head_filter_auto_on_cfg5_shape(oracle, monkeypatch, fused):
     """cfg5's row shape (d = 32) with the fp32 table beyond half the L2: auto
     selects the head filter (fused with the Floyd bookkeeping, or the two
     kernels with SNGB_FUSED=0); labels identical to the oracle."""
-    if fused == "0":
-        monkeypatch.setenv("SNGB_FUSED", "0")
+    monkeypatch.setenv("SNGB_FUSED", fused)
     n = 600_000
     pts = synthetic.generate(5, n=n)
     w = synthetic.CONFIGS[5]
@@ -706,7 +703,7 @@ def test_fused_floyd_head_equals_two_kernels(monkeypatch, cfg, n):
     for force in (None, "9"):
         if force:
             monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
-        monkeypatch.delenv("SNGB_FUSED", raising=False)
+        monkeypatch.setenv("SNGB_FUSED", "1")
         kf, gf = sng.sampled_edges_device(x, w.eps, rate, w.seed)
         monkeypatch.setenv("SNGB_FUSED", "0")
         k2, g2 = sng.sampled_edges_device(x, w.eps, rate, w.seed)

@@ -21,7 +21,7 @@ import paper_2006_06743_b200 as sng  # noqa: E402
 from paper_2006_06743_b200 import synthetic  # noqa: E402
 
 cfgs = [int(a) for a in sys.argv[1:]] or [3, 4, 5]
-variants = [("fused", {}), ("two_kernels", {"SNGB_FUSED": "0"})]
+variants = [("fused", {"SNGB_FUSED": "1"}), ("two_kernels", {"SNGB_FUSED": "0"})]
 lib = os.path.basename(os.environ.get("SNGB_LIBRARY", "libsngb.so"))
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 for cfg in cfgs:
