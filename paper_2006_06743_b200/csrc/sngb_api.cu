@@ -579,7 +579,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 gr.head = head_on ? (head_kind == kHeadU8x2 ? 2u : 4u) : 0u;
                 if (head_on) {
                     // the head table (exclusive with the 8-bit rows)
-                    c.q8.ensure(n * (head_kind == kHeadU8x2 ? 2ull : 4ull));
+                    // (+16: the fused kernel copies 2-byte heads as aligned 4-byte words)
+                    c.q8.ensure(n * (head_kind == kHeadU8x2 ? 2ull : 4ull) + 16);
                     hp.args.head = c.q8.p;
                     CK(launch_head_quantize(pts, stride, n, hp, c.q8.p, gs, c.num_sms));
                     gphases = 1;  // the fp32 rows are read by survivors only

@@ -57,7 +57,20 @@ namespace {
 constexpr int kFusedStage = 64;     // edge staging per warp (accepts are rare here)
 constexpr int kFusedHash = 1024;    // resolver hash slots (group lists: <= kGroupCap)
 constexpr int kFusedHashLog2 = 10;
-constexpr int kHeadGroup = 2;       // draw slots tested per survivor flush
+constexpr int kDefCap = 128;        // survivors per warp a vertex may defer to the next
+
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 template <int KIND, int G, int V, int MAXR>
 __global__ void __launch_bounds__(kBloomBlock, SNGB_FUSED_MINB)
@@ -66,7 +79,6 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_FUSED_MINB)
     constexpr int NG = 32 / G;
     constexpr int UF = SNGB_FUSED_UF;
     constexpr int STEP = NG * UF;
-    constexpr int QCAP = 32 * kHeadGroup + STEP;
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t WB = a.hash_mask;  // filter words (2^B / 32)
     const uint32_t shift = 32 - a.key_bits;
@@ -82,8 +94,9 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_FUSED_MINB)
     __shared__ uint32_t s_cnt[2][2];  // [parity][group, chain]
     __shared__ unsigned long long s_u[3];  // claimed vertices: ring of the last three
     __shared__ unsigned long long s_stage[kBloomThreads / 32][kFusedStage];
-    __shared__ uint32_t s_queue[kBloomThreads / 32][QCAP];
     __shared__ uint32_t s_t[MAXR * kBloomThreads];  // this vertex's draws, slot-major
+    __shared__ uint32_t s_h[MAXR * kBloomThreads];  // their partners' head words (cp.async)
+    __shared__ uint32_t s_defq[kBloomThreads / 32][2][kDefCap];  // deferred survivors per warp
 
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     const bool resolver = tid >= kT;
@@ -182,16 +195,67 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_FUSED_MINB)
         }
     } else {
         const float4* __restrict__ P = reinterpret_cast<const float4*>(g.tp.pts);
-        const void* __restrict__ H = h.head;
+        const char* __restrict__ H = static_cast<const char*>(h.head);
         const uint32_t Wr = g.tp.stride / 4;
         const float reject = h.reject;
         const int q = lane % G, grp = lane / G;
         const bool leader = (q == 0);
-        uint32_t* queue = s_queue[wib];
         const uint64_t pol = evict_first_policy();  // survivor rows must not evict the heads
         WarpStage<kFusedStage> stage{s_stage[wib], 0};
         TestStats st;
         uint32_t gpairs = 0, tails = 0;
+        // this thread's draw slot r lives at +4 kT r from these (slot-major: conflict-free)
+        const uint32_t ta = smem_addr(s_t) + 4u * tid, ha = smem_addr(s_h) + 4u * tid;
+        // the warp's slots, numbered j = 32 r + lane, double as its survivor queue in H
+        const uint32_t qa = smem_addr(s_t) + 4u * (wib * 32);
+        auto qaddr = [&](uint32_t j) { return qa + 4u * ((j >> 5) * kT + (j & 31)); };
+        // deferred survivors: vertex k's are tested during vertex k + 1's draws, their
+        // rows prefetched to L2 in between (HBM latency off the vertex's critical path)
+        uint32_t dn = 0, dcur = 0;
+        uint64_t u_prev = 0;
+        F4x2 qv_prev[V];
+#pragma unroll
+        for (int vv = 0; vv < V; ++vv) qv_prev[vv] = F4x2{0, 0};
+
+        // fp32 test of survivors [e0, e0 + STEP) of `qend` (entry e read by ld(e))
+        // against query row qvx of vertex ux: G lanes per row, UF rows per group
+        auto fp32_step = [&](auto ld, uint32_t e0, uint32_t qend, const F4x2* qvx, uint64_t ux) {
+            F4x2 rows[UF][V];
+            uint32_t pe[UF];
+            bool oke[UF];
+#pragma unroll
+            for (int uu = 0; uu < UF; ++uu) {
+                const uint32_t e = e0 + grp + NG * uu;
+                oke[uu] = e < qend;
+                pe[uu] = ld(oke[uu] ? e : e0);
+#pragma unroll
+                for (int vv = 0; vv < V; ++vv) {
+                    const uint32_t c = q + G * vv;
+                    const uint64_t row = (oke[uu] && c < Wr) ? pe[uu] : ux;
+                    rows[uu][vv] = ldg_row2_ef(P + row * Wr + (c < Wr ? c : Wr - 1), pol);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int uu = 0; uu < UF; ++uu) {
+                Acc2 acc;
+#pragma unroll
+                for (int vv = 0; vv < V; ++vv) diff2x2(qvx[vv], rows[uu][vv], acc);
+                float sum = acc2_sum(acc);
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+                const bool accd = decide(sum, oke[uu], leader, grp * G, g.tp, ux, pe[uu], st);
+                tails += (oke[uu] && leader) ? 1u : 0u;
+                stage.push(leader && accd, edge_key(ux, pe[uu], g.sink.nb), g.sink, lane);
+            }
+        };
+        auto run_deferred = [&]() {
+            const uint32_t* dq = s_defq[wib][dcur];
+#pragma unroll 1
+            for (uint32_t e0 = 0; e0 < dn; e0 += STEP)
+                fp32_step([&](uint32_t e) { return dq[e]; }, e0, dn, qv_prev, u_prev);
+            dn = 0;
+        };
 
         uint32_t par = 0;
         const uint64_t dz = (uint64_t)kT * kGamma;  // counter step between a thread's draws
@@ -233,17 +297,12 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_FUSED_MINB)
             const uint32_t forced_i =
                 (a.force_mod != 0 && (u % a.force_mod) == 0) ? D / 2 : 0xffffffffu;
 
-            // ---- P1: draw, filter bit, chain candidate, head load ----
-            // (the draw values wait in shared memory for P2 and H: re-deriving them
-            // for the few lanes that need one costs the whole warp an RNG pass)
-            uint32_t hb[MAXR];  // the partners' heads (loads in flight)
+            // ---- P1: draw, filter bit, chain candidate, async head copy ----
             uint32_t chain = 0;
             bool fired = false;
-            const uint32_t ta = smem_addr(s_t) + 4u * tid;  // slot r at ta + 4 kT r
 #pragma unroll
             for (int r = 0; r < MAXR; ++r, z += dz) {
                 const uint32_t i = tid + kT * r;
-                hb[r] = 0;
                 if ((uint32_t)r < nfull || i < D) {
                     bool fi;
                     const uint32_t t = lemire32(mix(z), base + i + 1, fi);
@@ -253,9 +312,14 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_FUSED_MINB)
                     red_or_sh_if(sa + off, bit, atom_or_sh(fa + off, bit) & bit);
                     chain |= (t - base < i ? 1u : 0u) << r;
                     st_sh(ta + 4u * kT * r, t);
-                    hb[r] = head_load<KIND>(H, t + (t >= (uint32_t)u ? 1u : 0u));
+                    const uint32_t p = t + (t >= (uint32_t)u ? 1u : 0u);
+                    // the 4-byte word holding p's head (2-byte heads: the aligned pair)
+                    const uint64_t hoff = KIND == kHeadU8x2 ? (uint64_t)(p & ~1u) * 2u
+                                                            : (uint64_t)p * 4u;
+                    cp_async4(ha + 4u * kT * r, H + hoff);
                 }
             }
+            cp_async_commit();
             if (chain) {  // rare (about draws/n per draw)
 #pragma unroll
                 for (int r = 0; r < MAXR; ++r)
@@ -264,7 +328,10 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_FUSED_MINB)
                         if (p < kChainCap) cl[p] = tid + kT * r;
                     }
             }
+            // the previous vertex's survivors, while this vertex's heads arrive
+            if (dn) run_deferred();
             auto replay = [&]() {  // exact sequential replay (k_floyd_bloom), rare
+                cp_async_wait_all();  // no copy of this vertex may land after the next one's
                 bar_sync(kBarWorkers, kT);
                 if (tid == 0) {
                     ++nrep;
@@ -281,7 +348,7 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_FUSED_MINB)
                 continue;
             }
             // ---- P2: draws on a shared filter bit -> the group list ----
-#pragma unroll
+#pragma unroll 4
             for (int r = 0; r < MAXR; ++r) {
                 const uint32_t i = tid + kT * r;
                 if ((uint32_t)r * kT >= D) break;
@@ -301,70 +368,50 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_FUSED_MINB)
             }
             bar_arrive(kBarReady + par, kBloomBlock);
 
-            // ---- H: head tests, survivors' fp32 test (the resolver runs meanwhile) ----
+            // ---- H: head tests (the resolver runs meanwhile) ----
+            cp_async_wait_all();
+            __syncwarp();
             uint32_t qn = 0;
-            auto fp32_step = [&](uint32_t e0, uint32_t qend) {
-                F4x2 rows[UF][V];
-                uint32_t pe[UF];
-                bool oke[UF];
-#pragma unroll
-                for (int uu = 0; uu < UF; ++uu) {
-                    const uint32_t e = e0 + grp + NG * uu;
-                    oke[uu] = e < qend;
-                    pe[uu] = queue[oke[uu] ? e : e0];
-#pragma unroll
-                    for (int vv = 0; vv < V; ++vv) {
-                        const uint32_t c = q + G * vv;
-                        const uint64_t row = (oke[uu] && c < Wr) ? pe[uu] : u;
-                        rows[uu][vv] = ldg_row2_ef(P + row * Wr + (c < Wr ? c : Wr - 1), pol);
-                    }
-                }
-                __syncwarp();
-#pragma unroll
-                for (int uu = 0; uu < UF; ++uu) {
-                    Acc2 acc;
-#pragma unroll
-                    for (int vv = 0; vv < V; ++vv) diff2x2(qv[vv], rows[uu][vv], acc);
-                    float s = acc2_sum(acc);
-#pragma unroll
-                    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-                    const bool accd = decide(s, oke[uu], leader, grp * G, g.tp, u, pe[uu], st);
-                    tails += (oke[uu] && leader) ? 1u : 0u;
-                    stage.push(leader && accd, edge_key(u, pe[uu], g.sink.nb), g.sink, lane);
-                }
-            };
-#pragma unroll
-            for (int r0 = 0; r0 < MAXR; r0 += kHeadGroup) {
-                if ((uint32_t)r0 * kT >= D) break;  // uniform
-#pragma unroll
-                for (int r = r0; r < r0 + kHeadGroup && r < MAXR; ++r) {
-                    const uint32_t i = tid + kT * r;
-                    const bool valid = (uint32_t)r < nfull || i < D;
-                    gpairs += valid ? 1u : 0u;
-                    const bool keep = valid && !(head_q<KIND>(hq, hb[r]) > reject);
-                    const unsigned km = __ballot_sync(kFull, keep);
-                    if (keep) {
-                        const uint32_t t = ld_sh(ta + 4u * kT * r);
-                        queue[qn + __popc(km & lanemask_lt())] = t + (t >= (uint32_t)u ? 1u : 0u);
-                    }
-                    qn += __popc(km);
-                }
-                __syncwarp();
-                if (qn >= (uint32_t)STEP) {
-                    uint32_t e0 = 0;
-#pragma unroll 1
-                    for (; e0 + STEP <= qn; e0 += STEP) fp32_step(e0, qn);
-                    const uint32_t rem = qn - e0;  // < STEP: move them to the front
-                    const uint32_t mp = (uint32_t)lane < rem ? queue[e0 + lane] : 0u;
-                    __syncwarp();
-                    if ((uint32_t)lane < rem) queue[lane] = mp;
-                    qn = rem;
-                    __syncwarp();
-                }
+#pragma unroll 2
+            for (int r = 0; r < MAXR; ++r) {
+                if ((uint32_t)r * kT >= D) break;  // uniform
+                const uint32_t i = tid + kT * r;
+                const bool valid = (uint32_t)r < nfull || i < D;
+                gpairs += valid ? 1u : 0u;
+                const uint32_t t = ld_sh(ta + 4u * kT * r);
+                const uint32_t p = t + (t >= (uint32_t)u ? 1u : 0u);
+                const uint32_t w = ld_sh(ha + 4u * kT * r);
+                const uint32_t hv = KIND == kHeadU8x2 ? ((p & 1u) ? (w >> 16) : (w & 0xffffu)) : w;
+                const bool keep = valid && !(head_q<KIND>(hq, hv) > reject);
+                const unsigned km = __ballot_sync(kFull, keep);
+                __syncwarp();  // every lane read slot r before the queue overwrites it
+                if (keep) st_sh(qaddr(qn + __popc(km & lanemask_lt())), p);
+                qn += __popc(km);
             }
-            if (qn) fp32_step(0, qn);
+            __syncwarp();
+            if (qn <= (uint32_t)kDefCap) {
+                // defer: copy to the idle deferred queue, prefetch the rows into L2
+                uint32_t* dq = s_defq[wib][dcur ^ 1u];
+                for (uint32_t e = lane; e < qn; e += 32) {
+                    const uint32_t p = ld_sh(qaddr(e));
+                    dq[e] = p;
+                    const char* row = reinterpret_cast<const char*>(P + (uint64_t)p * Wr);
+                    for (uint32_t b = 0; b < Wr * 16; b += 128) prefetch_l2(row + b);
+                }
+                __syncwarp();
+                dcur ^= 1u;
+                dn = qn;
+                u_prev = u;
+#pragma unroll
+                for (int vv = 0; vv < V; ++vv) qv_prev[vv] = qv[vv];
+            } else {  // a dense vertex: test its survivors now
+#pragma unroll 1
+                for (uint32_t e0 = 0; e0 < qn; e0 += STEP)
+                    fp32_step([&](uint32_t e) { return ld_sh(qaddr(e)); }, e0, qn, qv, u);
+            }
             __syncwarp();
         }
+        if (dn) run_deferred();
         stage.flush(g.sink, lane);
         st.pairs = gpairs;
         flush_stats(st, gpairs, g.counters, lane);
