@@ -88,76 +88,82 @@ def lib() -> C.CDLL:
     """Load libsngb.so once.  Raises if it has not been built (no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(
-                f"{LIB_PATH} is missing: build it with `python -m paper_2006_06743_b200.build` "
-                "(there is no CPU fallback)")
-        L = C.CDLL(LIB_PATH)
-        f32p, u64p, i32p, u8p = (C.POINTER(C.c_float), C.POINTER(C.c_uint64),
-                                 C.POINTER(C.c_int32), C.POINTER(C.c_uint8))
-        optp, infop = C.POINTER(SngbOpts), C.POINTER(SngbInfo)
-        vp = C.c_void_p
-        L.sngb_dbscan_f32.restype = C.c_int
-        L.sngb_dbscan_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
-                                      C.c_double, C.c_uint64, optp, i32p, u8p, infop]
-        L.sngb_dbscan_f32_device.restype = C.c_int
-        L.sngb_dbscan_f32_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
-                                             C.c_double, C.c_uint64, optp, vp, vp, infop]
-        L.sngb_sampled_edges_f32_device.restype = C.c_int
-        L.sngb_sampled_edges_f32_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double,
-                                                    C.c_double, C.c_uint64, optp, vp, C.c_uint64,
-                                                    u64p, infop]
-        L.sngb_sampled_edges_f32.restype = C.c_int
-        L.sngb_sampled_edges_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double,
-                                             C.c_double, C.c_uint64, optp, u64p, C.c_uint64, u64p,
-                                             infop]
-        L.sngb_cluster_edges_device.restype = C.c_int
-        L.sngb_cluster_edges_device.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_int32, optp, vp,
-                                                vp, infop]
-        L.sngb_unique_keys_device.restype = C.c_int
-        L.sngb_unique_keys_device.argtypes = [vp, C.c_uint64, C.c_uint64, optp, vp, u64p]
-        L.sngb_degrees_device.restype = C.c_int
-        L.sngb_degrees_device.argtypes = [vp, C.c_uint64, C.c_uint64, optp, vp]
-        L.sngb_components_device.restype = C.c_int
-        L.sngb_components_device.argtypes = [vp, C.c_uint64, C.c_uint64, vp, C.c_int32, optp, vp,
-                                             u64p]
-        L.sngb_border_device.restype = C.c_int
-        L.sngb_border_device.argtypes = [vp, C.c_uint64, C.c_uint64, vp, C.c_int32, vp, optp, vp]
-        L.sngb_relabel_device.restype = C.c_int
-        L.sngb_relabel_device.argtypes = [C.c_uint64, vp, C.c_int32, vp, vp, optp, vp, vp, infop]
-        f64p = C.POINTER(C.c_double)
-        L.sngb_dbscan_f64.restype = C.c_int
-        L.sngb_dbscan_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
-                                      C.c_double, C.c_uint64, optp, i32p, u8p, infop]
-        L.sngb_dbscan_f64_device.restype = C.c_int
-        L.sngb_dbscan_f64_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
-                                             C.c_double, C.c_uint64, optp, vp, vp, infop]
-        L.sngb_sampled_edges_f64.restype = C.c_int
-        L.sngb_sampled_edges_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double,
-                                             C.c_double, C.c_uint64, optp, u64p, C.c_uint64, u64p,
-                                             infop]
-        L.sngb_dbscan_batch_f32.restype = C.c_int
-        L.sngb_dbscan_batch_f32.argtypes = [C.POINTER(SngbProblem), C.c_uint64, optp]
-        L.sngb_dbscan_exact_f32.restype = C.c_int
-        L.sngb_dbscan_exact_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
-                                            optp, i32p, u8p, infop]
-        L.sngb_dbscan_exact_f32_device.restype = C.c_int
-        L.sngb_dbscan_exact_f32_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double,
-                                                   C.c_int32, optp, vp, vp, infop]
-        L.sngb_dbscan_exact_f64.restype = C.c_int
-        L.sngb_dbscan_exact_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
-                                            optp, i32p, u8p, infop]
-        L.sngb_full_edges_f32.restype = C.c_int
-        L.sngb_full_edges_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double, optp, u64p,
-                                          C.c_uint64, u64p, infop]
-        L.sngb_strerror.restype = C.c_char_p
-        L.sngb_strerror.argtypes = [C.c_int]
-        L.sngb_last_error_detail.restype = C.c_char_p
-        L.sngb_abi_version.restype = C.c_int
-        L.sngb_device_count.restype = C.c_int
-        L.sngb_release_pools.restype = None
-        _lib = L
+        _lib = load(LIB_PATH)
     return _lib
+
+
+def load(path: str) -> C.CDLL:
+    """Load and declare one build of the library (the product, or an A/B or
+    test-hook build of the same sources)."""
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build it with `python -m paper_2006_06743_b200.build` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    f32p, u64p, i32p, u8p = (C.POINTER(C.c_float), C.POINTER(C.c_uint64),
+                             C.POINTER(C.c_int32), C.POINTER(C.c_uint8))
+    optp, infop = C.POINTER(SngbOpts), C.POINTER(SngbInfo)
+    vp = C.c_void_p
+    L.sngb_dbscan_f32.restype = C.c_int
+    L.sngb_dbscan_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                  C.c_double, C.c_uint64, optp, i32p, u8p, infop]
+    L.sngb_dbscan_f32_device.restype = C.c_int
+    L.sngb_dbscan_f32_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                         C.c_double, C.c_uint64, optp, vp, vp, infop]
+    L.sngb_sampled_edges_f32_device.restype = C.c_int
+    L.sngb_sampled_edges_f32_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double,
+                                                C.c_double, C.c_uint64, optp, vp, C.c_uint64,
+                                                u64p, infop]
+    L.sngb_sampled_edges_f32.restype = C.c_int
+    L.sngb_sampled_edges_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double,
+                                         C.c_double, C.c_uint64, optp, u64p, C.c_uint64, u64p,
+                                         infop]
+    L.sngb_cluster_edges_device.restype = C.c_int
+    L.sngb_cluster_edges_device.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_int32, optp, vp,
+                                            vp, infop]
+    L.sngb_unique_keys_device.restype = C.c_int
+    L.sngb_unique_keys_device.argtypes = [vp, C.c_uint64, C.c_uint64, optp, vp, u64p]
+    L.sngb_degrees_device.restype = C.c_int
+    L.sngb_degrees_device.argtypes = [vp, C.c_uint64, C.c_uint64, optp, vp]
+    L.sngb_components_device.restype = C.c_int
+    L.sngb_components_device.argtypes = [vp, C.c_uint64, C.c_uint64, vp, C.c_int32, optp, vp,
+                                         u64p]
+    L.sngb_border_device.restype = C.c_int
+    L.sngb_border_device.argtypes = [vp, C.c_uint64, C.c_uint64, vp, C.c_int32, vp, optp, vp]
+    L.sngb_relabel_device.restype = C.c_int
+    L.sngb_relabel_device.argtypes = [C.c_uint64, vp, C.c_int32, vp, vp, optp, vp, vp, infop]
+    f64p = C.POINTER(C.c_double)
+    L.sngb_dbscan_f64.restype = C.c_int
+    L.sngb_dbscan_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                  C.c_double, C.c_uint64, optp, i32p, u8p, infop]
+    L.sngb_dbscan_f64_device.restype = C.c_int
+    L.sngb_dbscan_f64_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                         C.c_double, C.c_uint64, optp, vp, vp, infop]
+    L.sngb_sampled_edges_f64.restype = C.c_int
+    L.sngb_sampled_edges_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double,
+                                         C.c_double, C.c_uint64, optp, u64p, C.c_uint64, u64p,
+                                         infop]
+    L.sngb_dbscan_batch_f32.restype = C.c_int
+    L.sngb_dbscan_batch_f32.argtypes = [C.POINTER(SngbProblem), C.c_uint64, optp]
+    L.sngb_dbscan_exact_f32.restype = C.c_int
+    L.sngb_dbscan_exact_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                        optp, i32p, u8p, infop]
+    L.sngb_dbscan_exact_f32_device.restype = C.c_int
+    L.sngb_dbscan_exact_f32_device.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_double,
+                                               C.c_int32, optp, vp, vp, infop]
+    L.sngb_dbscan_exact_f64.restype = C.c_int
+    L.sngb_dbscan_exact_f64.argtypes = [f64p, C.c_uint64, C.c_uint32, C.c_double, C.c_int32,
+                                        optp, i32p, u8p, infop]
+    L.sngb_full_edges_f32.restype = C.c_int
+    L.sngb_full_edges_f32.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_double, optp, u64p,
+                                      C.c_uint64, u64p, infop]
+    L.sngb_strerror.restype = C.c_char_p
+    L.sngb_strerror.argtypes = [C.c_int]
+    L.sngb_last_error_detail.restype = C.c_char_p
+    L.sngb_abi_version.restype = C.c_int
+    L.sngb_device_count.restype = C.c_int
+    L.sngb_release_pools.restype = None
+    return L
 
 
 def strerror(code: int) -> str:

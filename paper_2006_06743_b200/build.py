@@ -76,9 +76,27 @@ def build(verbose: bool = False, variant: str | None = None, extra: tuple = ()) 
                "-lcudart", "-lpthread"]
         subprocess.run(cmd, check=True)
     if not variant:
+        build_testhooks(objs)
         build_cli(lib)
         build_pymod(lib)
     return lib
+
+
+TESTHOOKS_LIB = os.path.join(PKG, "lib", "libsngb_testhooks.so")
+
+
+def build_testhooks(objs: list[str]) -> str:
+    """lib/libsngb_testhooks.so: the product objects with sngb_api.cu recompiled
+    with -DSNGB_TEST_HOOKS (SNGB_TEST_FORCE_IRREGULAR forces the exact replay
+    path).  Loaded only by tests/conftest.py, never by the package."""
+    hook_dir = os.path.join(OBJ, "testhooks")
+    os.makedirs(hook_dir, exist_ok=True)
+    api = _compile("sngb_api.cu", False, hook_dir, ("-DSNGB_TEST_HOOKS=1",))
+    others = [o for o in objs if os.path.basename(o) != "sngb_api.o"]
+    if _stale(TESTHOOKS_LIB, [api, *others]):
+        subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
+                        TESTHOOKS_LIB, api, *others, "-lcudart", "-lpthread"], check=True)
+    return TESTHOOKS_LIB
 
 
 PYMOD_SRC = os.path.join(PKG, "cpp", "python", "sngdbscan_module.cpp")

@@ -106,9 +106,17 @@ int resolve_device(const sngb_opts* o) {
     return d;
 }
 
-uint32_t test_force_mod() {  // see test_fire() in sngb_internal.cuh
+// Test hook (see test_fire() in sngb_internal.cuh): forces the exact sequential
+// replay on every m-th vertex so the parity tests reach it.  Compiled only into
+// the test build lib/libsngb_testhooks.so (-DSNGB_TEST_HOOKS, build.py); the
+// product library always returns 0 and never reads the variable.
+uint32_t test_force_mod() {
+#ifdef SNGB_TEST_HOOKS
     const char* v = std::getenv("SNGB_TEST_FORCE_IRREGULAR");
     return v ? (uint32_t)std::strtoul(v, nullptr, 10) : 0u;
+#else
+    return 0u;
+#endif
 }
 
 uint64_t env_u64(const char* name, uint64_t dflt) {

@@ -31,3 +31,26 @@ def ref():
     if not os.path.exists(REF_SO):
         pytest.skip("oracle/_ref/libsngref.so not built")
     return Reference()
+
+
+def _route_test_hooks():
+    """Calls made while SNGB_TEST_FORCE_IRREGULAR is set go to the test build
+    lib/libsngb_testhooks.so (the product library compiles the hook out)."""
+    try:
+        from paper_2006_06743_b200 import _lib
+    except Exception:
+        return
+    product = _lib.lib
+    hooked = {}
+
+    def lib():
+        if os.environ.get("SNGB_TEST_FORCE_IRREGULAR"):
+            if "L" not in hooked:
+                hooked["L"] = _lib.load(os.path.join(_lib.PKG, "lib", "libsngb_testhooks.so"))
+            return hooked["L"]
+        return product()
+
+    _lib.lib = lib
+
+
+_route_test_hooks()

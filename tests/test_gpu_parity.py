@@ -154,6 +154,27 @@ def test_forced_irregular_vertices_exact(oracle, monkeypatch, n, d, eps, rate, s
     np.testing.assert_array_equal(c.assignment, ol)
 
 
+def test_product_library_has_no_test_hook(monkeypatch):
+    """The product libsngb.so compiles SNGB_TEST_FORCE_IRREGULAR out; only the
+    test build (lib/libsngb_testhooks.so, routed by conftest.py) honours it."""
+    import ctypes as C
+    from paper_2006_06743_b200 import _lib
+    rng = np.random.default_rng(3)
+    pts = np.ascontiguousarray(rng.random((5000, 3), dtype=np.float32))
+    monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", "7")
+    counts = []
+    for L in (_lib.load(_lib.LIB_PATH), _lib.lib()):
+        gi = _lib.SngbInfo()
+        lab = np.empty(5000, np.int32)
+        rol = np.empty(5000, np.uint8)
+        rc = L.sngb_dbscan_f32(pts.ctypes.data_as(C.POINTER(C.c_float)), 5000, 3, 0.05, 3, 0.05,
+                               1, None, lab.ctypes.data_as(C.POINTER(C.c_int32)),
+                               rol.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(gi))
+        assert rc == 0
+        counts.append(gi.irregular_vertices)
+    assert counts[0] == 0 and counts[1] >= 5000 // 7
+
+
 def _host_edges_rows(pts, eps, rate, seed, rb, re):
     """sngb_sampled_edges_f32 (host buffers) over the query rows [rb, re)."""
     import ctypes as C
