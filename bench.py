@@ -219,24 +219,24 @@ def _ref_rate(w, draws_s: int) -> float:
     return rate
 
 
-def _ref_draws(w, pairs_per_s: float, budget_s: float, fixed_s: float) -> int:
-    """Draws per vertex so one reference call on the full dataset takes ~budget_s."""
-    per_vertex = max(0.0, budget_s - fixed_s) * pairs_per_s / w.n
-    return int(max(1, min(w.draws, per_vertex)))
-
-
-def _ref_probe(ref, ds, w):
-    """Two short reference calls on the full dataset (1 and a few draws per
-    vertex) give its fixed per-call cost and its pairs/s."""
-    # ~2e8 pairs at d <= 16 (a second or two on 8-16 cores), fewer for wide rows
-    probe_pairs = 2e8 * 16 / max(w.d, 16)
-    d_lo, d_hi = 1, int(min(w.draws, max(2, probe_pairs // w.n)))
-    _, _, i_lo = ref.sng_dbscan(ds, w.eps, w.min_pts, _ref_rate(w, d_lo), w.seed, threads=0)
-    _, _, i_hi = ref.sng_dbscan(ds, w.eps, w.min_pts, _ref_rate(w, d_hi), w.seed, threads=0)
-    dt = max((i_hi["ms"] - i_lo["ms"]) / 1e3, 1e-6)
-    pairs_per_s = w.n * (d_hi - d_lo) / dt
-    fixed_s = max(0.0, i_lo["ms"] / 1e3 - w.n * d_lo / pairs_per_s)
-    return pairs_per_s, fixed_s
+def _ref_calibrate(ref, ds, w, budget_s: float) -> int:
+    """Draws per vertex so one reference call on the full dataset takes at most
+    ~0.8 budget_s: a tiny call (d0 draws), then one of about a quarter of the
+    budget (d1), and the line through the two (fixed per-call cost + cost per
+    draw).  The second point is far from the first, so a noisy fixed cost
+    cannot inflate the slope's estimate (a 1-vs-5-draw probe once mistook
+    noise for throughput and ran the full workload)."""
+    d0 = int(min(w.draws, max(1, (1e8 * 16 / max(w.d, 16)) // w.n)))
+    t0 = ref.sng_dbscan(ds, w.eps, w.min_pts, _ref_rate(w, d0), w.seed, threads=0)[2]["ms"] / 1e3
+    d1 = int(min(w.draws, max(d0 + 1, d0 * (0.25 * budget_s) / max(t0, 1e-3))))
+    if d1 <= d0:
+        return d0
+    t1 = ref.sng_dbscan(ds, w.eps, w.min_pts, _ref_rate(w, d1), w.seed, threads=0)[2]["ms"] / 1e3
+    slope = (t1 - t0) / (d1 - d0)
+    if slope <= 0:  # no measurable per-draw cost: stay at the measured point
+        return d1
+    fixed = max(0.0, t0 - slope * d0)
+    return int(max(1, min(w.draws, (0.8 * budget_s - fixed) / slope)))
 
 
 def _sample_desc(w, draws_s: int) -> str:
@@ -254,14 +254,13 @@ def cpu_baseline(pts, w, budget_s: float):
     ref = Reference()
     cores = ref.hw_threads()
     ds = ref.dataset(pts)
-    pps, fixed = _ref_probe(ref, ds, w)
-    draws_s = _ref_draws(w, pps, budget_s, fixed)
+    draws_s = _ref_calibrate(ref, ds, w, budget_s)
     rate = w.rate if draws_s >= w.draws else _ref_rate(w, draws_s)
     _, _, info = ref.sng_dbscan(ds, w.eps, w.min_pts, rate, w.seed, threads=0)
     pairs = info["distance_evals"]
     return {"value": pairs / (info["ms"] / 1e3), "unit": UNIT, "cores": cores,
             "kind": "reference", "sample": _sample_desc(w, draws_s), "ms": info["ms"],
-            "pairs": pairs, "fixed_ms_per_call": fixed * 1e3}
+            "pairs": pairs}
 
 
 def run_reference_arm(args, w, pts):
@@ -274,10 +273,9 @@ def run_reference_arm(args, w, pts):
     ref = Reference()
     cores = ref.hw_threads()
     ds = ref.dataset(pts)
-    pps, fixed = _ref_probe(ref, ds, w)
     # bound each step so (warmup + steps) finishes in a few minutes
     budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))
-    draws_s = _ref_draws(w, pps, budget, fixed)
+    draws_s = _ref_calibrate(ref, ds, w, budget)
     rate = w.rate if draws_s >= w.draws else _ref_rate(w, draws_s)
     times, pairs = [], None
     for i in range(args.warmup + args.steps):

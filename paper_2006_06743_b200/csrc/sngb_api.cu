@@ -486,6 +486,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         {
             CK(cudaMemsetAsync(dc, 0, C_UNIQUE * sizeof(unsigned long long), s));
             CK(cudaMemsetAsync(&dc[C_BAND_CURSOR], 0, sizeof(unsigned long long), s));
+            CK(cudaMemsetAsync(&dc[C_IRR_CURSOR], 0, sizeof(unsigned long long), s));
         }
         tm.mark(E_PREPARED);
         // Overlap: the sampler on the side stream concurrently with the
@@ -528,7 +529,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             sa.base = (uint32_t)base;
             sa.seed_mixed = seed_mixed;
             sa.force_mod = test_force_mod();
-            const size_t scratch = floyd_scratch_bytes((uint32_t)draws, c.num_sms);
+            const size_t scratch = fuse_try ? fused_scratch_bytes((uint32_t)draws, re - rb, c.num_sms)
+                                            : floyd_scratch_bytes((uint32_t)draws, c.num_sms);
             if (scratch) c.scratch.ensure(scratch);
             sa.scratch64 = scratch ? c.scratch.as<unsigned long long>() : nullptr;
             sa.extras = c.extras.as<unsigned long long>();

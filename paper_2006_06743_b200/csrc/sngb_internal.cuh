@@ -34,6 +34,7 @@ enum Counter : int {
     C_QMIN,              // max of ~ordered(value): the dataset minimum (8-bit filter scale)
     C_QMAX,              // max of ordered(value): the dataset maximum
     C_TAIL_PAIRS,        // 8-bit filter: pairs the head did not reject (read their tail)
+    C_IRR_CURSOR,        // fused sampler: vertices listed for the exact sequential replay
     C_COUNT
 };
 
@@ -255,6 +256,8 @@ cudaError_t launch_gather_head(const GatherArgs& a, const HeadArgs& h, cudaStrea
 // sngb_fused.cu: Floyd bookkeeping + head gather in one pass (large n, narrow rows);
 // a.work must point at a zeroed counter (dynamic vertex claiming)
 bool fused_eligible(uint64_t n, uint32_t draws, uint32_t stride);
+// global scratch of the fused kernel (per-warp draw / group lists, replay list)
+size_t fused_scratch_bytes(uint32_t draws, uint64_t rows, int num_sms);
 cudaError_t launch_floyd_head(const SamplerArgs& sa, const GatherArgs& ga, const HeadArgs& h,
                               cudaStream_t s, int num_sms);
 

@@ -712,11 +712,13 @@ def test_q8_variance_ordered_head(oracle, monkeypatch, host):
     assert got["1"] < 0.6 * got["0"], got
 
 
-@pytest.mark.parametrize("cfg,n", [(3, 200_000), (4, 400_000), (5, 300_000)])
+@pytest.mark.parametrize("cfg,n", [(3, 200_000), (4, 400_000), (5, 300_000), (4, 1_000_000),
+                                   (5, 2_500_000)])
 def test_fused_floyd_head_equals_two_kernels(monkeypatch, cfg, n):
-    """k_floyd_head (Floyd bookkeeping + head gather in one pass) against the two
-    kernels it replaces, on reduced BASELINE shapes (the bloom regime): the same
-    edge list, collisions and pair counts; also with forced Lemire replays."""
+    """k_sample_head (Floyd bookkeeping + head gather in one pass, sngb_fused.cu)
+    against the two kernels it replaces, on reduced BASELINE shapes (the bloom
+    regime; the two largest with cfg4/cfg5's chain density): the same edge list,
+    collisions and pair counts; also with forced Lemire replays."""
     import torch
     w = synthetic.CONFIGS[cfg]
     x = torch.from_numpy(synthetic.generate(cfg, n=n)).cuda()
