@@ -195,6 +195,82 @@ __global__ void __launch_bounds__(256) k_bulk(const uint16_t* __restrict__ tab, 
     if (acc == 0x7fffu && gid == 0u) sink[0] = acc;
 }
 
+
+// Wide rows (the 8-bit gather's heads: the first 256 B of random 800-B rows,
+// cfg2's 56 MB table).  ldg: half a warp per row (16 lanes x 16 B), UN rows
+// in flight per half warp.  g4w: lanes 0..7 each issue one gather4 (4 rows x
+// 256 B) per stage, so a stage is 32 rows = 8 KB; the warp then reads them
+// back from shared memory (16 B per lane per row).
+template <int UN>
+__global__ void __launch_bounds__(256) k_ldg_wide(const uint4* __restrict__ tab, uint32_t rows,
+                                                  uint32_t row16, uint32_t iters, uint32_t* sink) {
+    const uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t half = gid >> 4, q = threadIdx.x & 15;
+    uint32_t acc = 0;
+    for (uint32_t it = 0; it < iters; ++it) {
+        uint4 v[UN];
+#pragma unroll
+        for (int k = 0; k < UN; ++k) {
+            const uint32_t h = hash32(half * 0x9E3779B1u + it * UN + k);
+            const uint32_t r = (uint32_t)(((uint64_t)h * rows) >> 32);
+            v[k] = __ldg(tab + (size_t)r * row16 + q);
+        }
+#pragma unroll
+        for (int k = 0; k < UN; ++k) acc ^= v[k].x ^ v[k].y ^ v[k].z ^ v[k].w;
+    }
+    if (acc == 0x7fffu && gid == 0u) sink[0] = acc;
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) k_g4_wide(const __grid_constant__ CUtensorMap tm, uint32_t rows,
+                                                 uint32_t iters, uint32_t* sink) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) unsigned long long mb[4][S];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned char* buf = sm + (size_t)w * S * 8192;
+    if (lane == 0)
+        for (int s = 0; s < S; ++s) mbar_init(smem_u32(&mb[w][s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    uint32_t acc = 0;
+    auto issue = [&](uint32_t it, int s) {
+        const uint32_t mbar = smem_u32(&mb[w][s]);
+        if (lane == 0) mbar_expect_tx(mbar, 8192);
+        __syncwarp();
+        if (lane < 8) {
+            uint32_t r[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t h = hash32(gid * 0x9E3779B1u + it * 4 + k);
+                r[k] = (uint32_t)(((uint64_t)h * rows) >> 32);
+            }
+            g4(smem_u32(buf + s * 8192 + lane * 1024), &tm, mbar, 0, r[0], r[1], r[2], r[3]);
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < S; ++s) issue(s, s);
+    uint32_t ph = 0;
+    for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            mbar_wait(smem_u32(&mb[w][s]), ph);
+            const uint4* st = reinterpret_cast<const uint4*>(buf + s * 8192);
+#pragma unroll 4
+            for (int k = 0; k < 16; ++k) {
+                const uint4 v = st[k * 32 + lane];
+                acc ^= v.x ^ v.y ^ v.z ^ v.w;
+            }
+            __syncwarp();
+            issue((it + 1) * S + s, s);
+        }
+        ph ^= 1u;
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_wait(smem_u32(&mb[w][s]), ph);
+    if (acc == 0x7fffu && gid == 0u) sink[0] = acc;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -224,7 +300,52 @@ static double time_ms(F launch, int reps = 5) {
     return best;
 }
 
-int main() {
+static int wide(int sms, int clk, PFN_cuTensorMapEncodeTiled_v12000 encode, uint32_t* sink) {
+    const uint32_t rows = 70000, row_bytes = 800;
+    unsigned char* tab;
+    CK(cudaMalloc(&tab, (size_t)rows * row_bytes));
+    CK(cudaMemset(tab, 0x5a, (size_t)rows * row_bytes));
+    CUtensorMap tm;
+    cuuint64_t gdim[2] = {row_bytes, rows};
+    cuuint64_t gstr[1] = {row_bytes};
+    cuuint32_t box[2] = {256, 1};
+    cuuint32_t es[2] = {1, 1};
+    if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, tab, gdim, gstr, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        fprintf(stderr, "encode (wide) failed\n");
+        return 1;
+    }
+    for (int bpsm : {2, 4, 8}) {
+        const int grid = sms * bpsm;
+        const uint32_t it = 64;
+        double ms = time_ms([&] { k_ldg_wide<4><<<grid, 256>>>(reinterpret_cast<const uint4*>(tab), rows, row_bytes / 16, it, sink); });
+        CK(cudaGetLastError());
+        double rps = (double)grid * 16 * it * 4 / (ms * 1e-3);
+        printf("{\"case\": \"ldg_wide256\", \"table_mb\": 56, \"bpsm\": %d, \"rows_per_s\": %.4g, \"per_sm_cycle\": %.3f}\n",
+               bpsm, rps, rps / (sms * (clk * 1e3)));
+        for (int S : {1, 2}) {
+            const size_t smem = (size_t)4 * S * 8192;
+            const int g2 = sms * bpsm * 2;
+            if (S == 1) {
+                cudaFuncSetAttribute(k_g4_wide<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                ms = time_ms([&] { k_g4_wide<1><<<g2, 128, smem>>>(tm, rows, it, sink); });
+            } else {
+                cudaFuncSetAttribute(k_g4_wide<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                ms = time_ms([&] { k_g4_wide<2><<<g2, 128, smem>>>(tm, rows, it, sink); });
+            }
+            CK(cudaGetLastError());
+            rps = (double)g2 * 4 * 32 * it * S / (ms * 1e-3);
+            printf("{\"case\": \"tma_gather4_wide256\", \"table_mb\": 56, \"bpsm\": %d, \"stages\": %d, \"rows_per_s\": %.4g, \"per_sm_cycle\": %.3f}\n",
+                   bpsm * 2, S, rps, rps / (sms * (clk * 1e3)));
+            fflush(stdout);
+        }
+    }
+    cudaFree(tab);
+    return 0;
+}
+
+int main(int argc, char** argv) {
     int sms = 0, clk = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
@@ -235,6 +356,7 @@ int main() {
     }
     uint32_t* sink;
     CK(cudaMalloc(&sink, 4));
+    if (argc > 1 && argv[1][0] == 'w') return wide(sms, clk, encode, sink);
     for (uint64_t mb : {2ull, 40ull, 80ull, 400ull}) {
         const uint64_t heads = mb * 1000000ull / 2;  // u16 heads
         const uint32_t rows16 = (uint32_t)(heads / 8);
