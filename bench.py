@@ -222,19 +222,26 @@ def _ref_rate(w, draws_s: int) -> float:
 def _ref_calibrate(ref, ds, w, budget_s: float) -> int:
     """Draws per vertex so one reference call on the full dataset takes at most
     ~0.8 budget_s: a tiny call (d0 draws), then one of about a quarter of the
-    budget (d1), and the line through the two (fixed per-call cost + cost per
-    draw).  The second point is far from the first, so a noisy fixed cost
-    cannot inflate the slope's estimate (a 1-vs-5-draw probe once mistook
-    noise for throughput and ran the full workload)."""
+    budget (d1, grown 4x at a time until it takes >= budget/8), and the line
+    through the last two (fixed per-call cost + cost per draw).  The points
+    are far apart, so a noisy fixed cost cannot skew the slope (a 1-vs-5-draw
+    probe once mistook noise for throughput and ran the full workload)."""
+    def timed(dr):
+        t = ref.sng_dbscan(ds, w.eps, w.min_pts, _ref_rate(w, dr), w.seed, threads=0)[2]["ms"] / 1e3
+        print(f"bench.py: reference calibration draws={dr} {t:.3f} s", file=sys.stderr)
+        return t
+
     d0 = int(min(w.draws, max(1, (1e8 * 16 / max(w.d, 16)) // w.n)))
-    t0 = ref.sng_dbscan(ds, w.eps, w.min_pts, _ref_rate(w, d0), w.seed, threads=0)[2]["ms"] / 1e3
-    d1 = int(min(w.draws, max(d0 + 1, d0 * (0.25 * budget_s) / max(t0, 1e-3))))
-    if d1 <= d0:
-        return d0
-    t1 = ref.sng_dbscan(ds, w.eps, w.min_pts, _ref_rate(w, d1), w.seed, threads=0)[2]["ms"] / 1e3
-    slope = (t1 - t0) / (d1 - d0)
-    if slope <= 0:  # no measurable per-draw cost: stay at the measured point
+    t0 = timed(d0)
+    # grow the second point until its draw work clearly dominates the fixed cost
+    d1, t1 = d0, t0
+    while t1 < 0.125 * budget_s and d1 < w.draws:
+        d0, t0 = d1, t1
+        d1 = int(min(w.draws, d1 * 4))
+        t1 = timed(d1)
+    if d1 <= d0 or t1 <= t0:  # no measurable per-draw cost: stay at the measured point
         return d1
+    slope = (t1 - t0) / (d1 - d0)
     fixed = max(0.0, t0 - slope * d0)
     return int(max(1, min(w.draws, (0.8 * budget_s - fixed) / slope)))
 

@@ -1,36 +1,38 @@
 // sngb_fused.cu -- k_sample_head: the Floyd bookkeeping (graph.cpp:161-174) and
-// the head-filter gather (sngb_head.cu) of large narrow-row problems in ONE
-// pass over the draws, one warp per vertex (cfg3, cfg4, cfg5).
+// the head-filter gather (sngb_head.cu) of large narrow-row problems in one
+// kernel, one warp per vertex (cfg3, cfg4, cfg5).
 //
-// Why.  As two kernels (k_floyd_bloom + k_gather_head) every draw
+// Why.  As two kernels (k_floyd_bloom + k_gather_head) each draw
 //   t_i = Lemire(mix(key + (i+1) gamma), base + i + 1)   (rng.hpp:26,35-48)
-// is generated twice and each kernel spends ~95 SASS instructions per draw
-// (ncu, profiles/r02_ncu_floyd_cfg5.md, r01_ncu_head_cfg5.md); the gather
-// also waits on one random L2 sector per pair.  Here a warp owns a vertex and
-// generates each draw once; the only per-draw work besides the RNG is one
-// shared-memory atomic, one coalesced store and the head test.  No block
-// barriers: the warps of a block are independent.
+// costs ~100 SASS instructions in each (ncu: profiles/r02_ncu_floyd_cfg5.md,
+// r01_ncu_head_cfg5.md), and the Floyd kernel's block barriers and the
+// gather's L2 latency each leave the SM a third idle.  A one-pass fusion with
+// the draws kept in global scratch (v4, profiles/r02_ncu_fused_v4_cfg5.md) was
+// slower: 5.5 warp-instructions per draw and 318 GB of scratch write-back.
+// Here every warp owns a vertex and makes TWO lean passes over its draws,
+// regenerating them (a draw is ~26 integer instructions; storing it costs
+// more in L2/DRAM traffic than it saves):
 //
-// Per vertex u (warp-private shared memory, global scratch for the draws):
-//   P1  draw i (lane i mod 32, slot-major): t_i; the partner's head load;
-//       t_i -> scratch[i]; OR bit h(t_i) into a 2^B-bit filter F -- a draw that
-//       finds its bit already set records h in the second-comer list SL;
-//       t_i in [base, base + i) (may equal an earlier replacement j_k) goes
-//       to the chain list CL; the head test (exact reject, sngb_head.cu) and
-//       survivors' fp32 test (sngb_epstest.cuh) as in k_gather_head.
-//   P2  F := the bits of SL (every bit hit by >= 2 draws); scan the stored
-//       draws, the ones on such a bit -> group list GL (scratch);
-//   R   GL in a small hash (F's memory) keyed by t with the minimum index:
-//       a draw whose value has a smaller index collides (graph.cpp:168-169:
-//       its replacement j_i = base + i is inserted instead); then the chain
+//   P1  filter pass (no memory traffic): t_i, OR bit h(t_i) into a warp-
+//       private 2^B-bit filter F; a draw that finds its bit already set
+//       records h in its lane's second-comer list SL; the running minimum of
+//       Lemire's low word flags a possible reject pre-condition (rng.hpp:43).
+//   ->  F := the bits in SL (exactly the bits hit by >= 2 draws).
+//   P2  gather pass: t_i again, the partner's head load (exact reject,
+//       sngb_head.cu), survivors queued for the fp32 test (sngb_epstest.cuh);
+//       draws on a shared bit -> the lane's group list GL (their indices, in
+//       SL's slots), t_i in [base, base + i) -> the lane's chain list CL.
+//   R   GL's values (regenerated) in a small hash (F's memory) keyed by t with
+//       the minimum index: a
+//       draw whose value has a smaller index collides (graph.cpp:168-169, its
+//       replacement j_i = base + i is inserted instead); then the chain
 //       candidates in index order against the collided set.  Every collided
 //       draw's replacement is emitted as an extra pair (tested by k_extras).
-// A Lemire reject pre-condition (rng.hpp:43, ~1e-12 per draw) or a list
-// overflow sends the vertex to the exact sequential replay (k_replay_list,
-// true Stream semantics; every partner becomes an extra); its gather stops at
-// the first fired draw, as k_gather_head does.  Every decision is the
-// two-kernel path's, so the results are identical (tests/test_gpu_parity.py
-// -k fused).
+// A Lemire reject pre-condition (~1e-12 per draw) or a list overflow sends
+// the vertex to the exact sequential replay (k_replay_list: true Stream
+// semantics, every partner an extra); its gather stops at the first fired
+// draw, as k_gather_head's does.  Results are the two-kernel path's bit for
+// bit (tests/test_gpu_parity.py -k "fused or head").
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -57,20 +59,20 @@ namespace {
 #include "sngb_floyd_bloom.cuh"
 
 constexpr int kFWarps = 4;       // warps per block (independent vertices)
-constexpr int kSLCap = 256;      // second-comer bits per vertex (D^2 / 2^(B+1): 122 at D = 4000)
-constexpr int kCLCap = 64;       // chain candidates per vertex (~D^2 / 2n)
+constexpr int kSLL = 32;         // per lane: second-comer bits (P1; mean D^2/2^(B+1)/32 = 3.8 at D = 4000),
+                                 // then group-list draws (P2; mean D^2/2^B/32 = 7.6)
+constexpr int kCLL = 4;          // chain candidates per lane (mean D^2 / 2n / 32: 0.01 on cfg5)
 constexpr int kFStage = 64;      // edge staging per warp (accepts are rare here)
 constexpr int kMaxWarpsPerSM = 32;
 
-// per-warp geometry: filter F of 2^B bits (FW words), its reuse as the
-// resolution hash (FW / 2 u64 slots), collided bitmap (CW words)
+// per-warp geometry: filter F of 2^B bits (FW words, reused as the resolution
+// hash of FW / 2 u64 slots), collided bitmap (CW words)
 struct FGeom {
-    uint32_t B, FW, CW, gl_cap, dpad;
+    uint32_t B, FW, CW;
     __host__ __device__ uint32_t q_cap(int R, int step) const { return ((32 * R + step) + 3) & ~3u; }
     __host__ __device__ uint32_t warp_bytes(int R, int step) const {
-        return FW * 4 + kSLCap * 4 + kCLCap * 8 + CW * 4 + q_cap(R, step) * 4 + kFStage * 8;
+        return FW * 4 + 32 * kSLL * 2 + 32 * kCLL * 8 + CW * 4 + q_cap(R, step) * 4 + kFStage * 8;
     }
-    __host__ __device__ uint64_t scratch_words() const { return dpad + 2ull * gl_cap; }
 };
 
 inline FGeom fgeom(uint32_t draws) {
@@ -79,13 +81,36 @@ inline FGeom fgeom(uint32_t draws) {
     g.B = bg.bits_log2;
     g.FW = bg.words;
     g.CW = bg.col_words;
-    g.gl_cap = (g.FW / 2) * 3 / 4;
-    g.dpad = (draws + 31) & ~31u;
     return g;
+}
+
+#ifndef SNGB_FUSED_PF
+#define SNGB_FUSED_PF 0  // measured slower on cfg5 (861 vs 845 ms)
+#endif
+constexpr bool kPrefetch = SNGB_FUSED_PF != 0;
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 __device__ __forceinline__ void red_or_sh(uint32_t addr, uint32_t v) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// first draw index < D whose Lemire step meets the reject pre-condition
+// (lo < bound, rng.hpp:43), or D: the exact test behind the slo == 0 flag
+__device__ __noinline__ uint32_t first_fire(uint64_t key, uint32_t D, uint32_t base, int lane) {
+    uint32_t f = D;
+    for (uint32_t i = lane; i < D; i += 32) {
+        bool fire;
+        (void)lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fire);
+        if (fire) {
+            f = i;
+            break;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f = min(f, __shfl_xor_sync(kFull, f, o));
+    return f;
 }
 
 template <int KIND, int G, int V, int R>
@@ -94,6 +119,7 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
     constexpr int NG = 32 / G;
     constexpr int UF = 2;            // fp32 rows per group per step
     constexpr int STEP = NG * UF;    // survivors per fp32 step
+    constexpr uint32_t ITER = 32 * R;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int q = lane % G, grp = lane / G;
@@ -107,19 +133,19 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
     unsigned char* wsm = smem + (size_t)wib * fg.warp_bytes(R, STEP);
     uint32_t* F = reinterpret_cast<uint32_t*>(wsm);
     unsigned long long* HT = reinterpret_cast<unsigned long long*>(wsm);  // F's memory in R
-    uint32_t* SL = F + FW;
-    unsigned long long* CL = reinterpret_cast<unsigned long long*>(SL + kSLCap);
-    uint32_t* colbits = reinterpret_cast<uint32_t*>(CL + kCLCap);
+    uint16_t* SL = reinterpret_cast<uint16_t*>(F + FW);       // [32][kSLL], lane-major (B <= 16)
+    unsigned long long* CL = reinterpret_cast<unsigned long long*>(SL + 32 * kSLL);  // [32][kCLL]
+    uint32_t* colbits = reinterpret_cast<uint32_t*>(CL + 32 * kCLL);
     uint32_t* Q = colbits + fg.CW;
     unsigned long long* stg = reinterpret_cast<unsigned long long*>(Q + fg.q_cap(R, STEP));
     const uint32_t Fa = smem_addr(F);
+    uint16_t* mySL = SL + lane * kSLL;
+    unsigned long long* myCL = CL + lane * kCLL;
 
-    // warp-private global scratch: the draws, then the group list
-    const uint64_t gw = (uint64_t)blockIdx.x * kFWarps + wib;
-    uint32_t* scr = reinterpret_cast<uint32_t*>(a.scratch64) + gw * fg.scratch_words();
-    unsigned long long* GL = reinterpret_cast<unsigned long long*>(scr + fg.dpad);
-    uint32_t* irr_list = reinterpret_cast<uint32_t*>(a.scratch64) +
-                         (uint64_t)gridDim.x * kFWarps * fg.scratch_words();
+    // the lane's group list (draw indices) reuses its SL slots: SL is consumed
+    // (F rebuilt) before P2 pushes the first group entry
+    uint16_t* myGL = mySL;
+    uint32_t* irr_list = reinterpret_cast<uint32_t*>(a.scratch64);  // the replay list
 
     const float4* __restrict__ P = reinterpret_cast<const float4*>(g.tp.pts);
     const void* __restrict__ H = h.head;
@@ -133,6 +159,7 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
     unsigned long long gpairs = 0, tails = 0, ncol = 0;
 
     for (uint32_t w = lane; w < fg.CW; w += 32) colbits[w] = 0;
+    for (int j = 0; j < kCLL; ++j) myCL[j] = 0ull;  // chain lists start empty (0 = no entry)
 
     uint64_t u = 0, chunk_end = 0;
     auto grab = [&]() {
@@ -141,6 +168,16 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
         b0 = __shfl_sync(kFull, b0, 0);
         u = a.row_begin + b0;
         chunk_end = u + g.grab < a.row_end ? u + g.grab : a.row_end;
+    };
+    auto zeroF = [&]() {
+        uint4* f4 = reinterpret_cast<uint4*>(F);
+        for (uint32_t w = lane; w < FW / 4; w += 32) f4[w] = make_uint4(0, 0, 0, 0);
+    };
+    auto emit_extra = [&](uint32_t i) {  // collided draw i: its replacement j_i = base + i
+        const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
+        const uint32_t e2 = base + i;
+        if (s2 < xs.capacity) xs.keys[s2] = (u << 32) | (e2 + (e2 >= (uint32_t)u ? 1u : 0u));
+        ++ncol;
     };
     grab();
     for (; u < chunk_end; (u + 1 >= chunk_end) ? grab() : (void)(++u)) {
@@ -151,11 +188,59 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
             qv[vv] = to_x2(ldg_row(P + u * W + (c < W ? c : W - 1)));
         }
         const uint32_t hq = head_load<KIND>(H, (uint32_t)u);
-        // test hook (test_fire) resolved once per vertex
-        const uint32_t hook = (a.force_mod != 0 && (u % a.force_mod) == 0) ? D / 2 : 0xffffffffu;
-        {  // F := 0 (the previous vertex left its resolution hash here)
-            uint4* f4 = reinterpret_cast<uint4*>(F);
-            for (uint32_t w = lane; w < FW / 4; w += 32) f4[w] = make_uint4(0, 0, 0, 0);
+        const uint64_t key = vertex_key(a.seed_mixed, u);
+        const uint64_t z0 = key + (uint64_t)(lane + 1) * kGamma;
+        zeroF();
+        __syncwarp();
+
+        // ---- P1: the filter pass ----
+        uint32_t nsl = 0, mn = 0xffffffffu;
+        auto p1 = [&](uint32_t i0, uint64_t z, bool tail) {
+            uint32_t hk[R], old[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const uint32_t i = i0 + 32 * k + lane;
+                uint32_t slo;
+                const uint32_t t = lemire32_slo(mix(z + (uint64_t)(32 * k) * kGamma), base + i + 1, slo);
+                hk[k] = (t * 0x9E3779B1u) >> shift;
+                if (!tail || i < D) mn = min(mn, slo);
+            }
+            // all R atomics in flight before any result is used
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const uint32_t i = i0 + 32 * k + lane;
+                old[k] = (!tail || i < D) ? atom_or_sh(Fa + (hk[k] >> 5) * 4u, 1u << (hk[k] & 31)) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                if ((old[k] >> (hk[k] & 31)) & 1u) {  // a second comer
+                    if (nsl < (uint32_t)kSLL) mySL[nsl] = (uint16_t)hk[k];
+                    ++nsl;
+                }
+            }
+        };
+        {
+            const uint32_t nfull = D / ITER;
+            uint64_t z = z0;
+            for (uint32_t it = 0; it < nfull; ++it, z += (uint64_t)ITER * kGamma) p1(it * ITER, z, false);
+            if (nfull * ITER < D) p1(nfull * ITER, z, true);
+        }
+        // a possible reject pre-condition (or the test hook): the exact first fire
+        uint32_t limit = D;
+        const bool hooked = a.force_mod != 0 && (u % a.force_mod) == 0;
+        if (__any_sync(kFull, mn == 0u) || hooked) {
+            limit = first_fire(key, D, base, lane);
+            if (hooked) limit = min(limit, D / 2);
+        }
+        const bool irregular = limit < D;
+        bool replay = irregular || __any_sync(kFull, nsl > (uint32_t)kSLL);
+        // F := the shared bits
+        __syncwarp();
+        zeroF();
+        __syncwarp();
+        {
+            const uint32_t ns = min(nsl, (uint32_t)kSLL);
+            for (uint32_t j = 0; j < ns; ++j) red_or_sh(Fa + (mySL[j] >> 5) * 4u, 1u << (mySL[j] & 31));
         }
         __syncwarp();
 
@@ -191,80 +276,49 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
             }
         };
 
-        // ---- P1: draws, head tests, filter ----
-        uint32_t limit = D, qn = 0, nsl = 0, ncl = 0;
-        bool irregular = false;
-        uint64_t z = vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
-        for (uint32_t i0 = 0; i0 < limit; i0 += 32 * R, z += (uint64_t)(32 * R) * kGamma) {
+        // ---- P2: the gather pass (draws below limit) ----
+        uint32_t qn = 0, ngl = 0, ncl = 0;
+        auto p2 = [&](uint32_t i0, uint64_t z, bool tail) {
             uint32_t tv[R], pv[R];
-            unsigned fires = 0;
 #pragma unroll
             for (int k = 0; k < R; ++k) {
                 const uint32_t i = i0 + 32 * k + lane;
-                bool fire;
-                const uint32_t t = lemire32(mix(z + (uint64_t)(32 * k) * kGamma), base + i + 1, fire);
-                const bool valid = i < limit;
-                fires |= ((fire || i == hook) && valid) ? (1u << k) : 0u;
-                tv[k] = t;
-                pv[k] = valid ? t + (t >= (uint32_t)u ? 1u : 0u) : (uint32_t)u;
+                uint32_t slo;
+                tv[k] = lemire32_slo(mix(z + (uint64_t)(32 * k) * kGamma), base + i + 1, slo);
+                const uint32_t p = tv[k] + (tv[k] >= (uint32_t)u ? 1u : 0u);
+                pv[k] = (!tail || i < limit) ? p : (uint32_t)u;
             }
             uint32_t hb[R];
 #pragma unroll
             for (int k = 0; k < R; ++k) hb[k] = head_load<KIND>(H, pv[k]);  // in flight from here
-            unsigned sec = 0, chn = 0;
-            uint32_t hk[R];
+            uint32_t fw[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) fw[k] = ld_sh(Fa + ((tv[k] * 0x9E3779B1u) >> shift >> 5) * 4u);
 #pragma unroll
             for (int k = 0; k < R; ++k) {
                 const uint32_t i = i0 + 32 * k + lane;
                 const uint32_t t = tv[k];
-                hk[k] = (t * 0x9E3779B1u) >> shift;
-                if (i < limit) {
-                    scr[i] = t;
-                    const uint32_t bit = 1u << (hk[k] & 31);
-                    sec |= (atom_or_sh(Fa + (hk[k] >> 5) * 4u, bit) & bit) ? (1u << k) : 0u;
-                    chn |= (t - base < i) ? (1u << k) : 0u;  // t <= base + i always
+                const bool ok = !tail || i < limit;
+                if (ok && ((fw[k] >> (((t * 0x9E3779B1u) >> shift) & 31)) & 1u)) {  // on a shared bit
+                    if (ngl < (uint32_t)kSLL) myGL[ngl] = (uint16_t)i;
+                    ++ngl;
                 }
-            }
-            if (__any_sync(kFull, fires != 0)) {  // rare: irregular vertex, cut at the first fire
-                irregular = true;
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const unsigned fm = __ballot_sync(kFull, (fires >> k) & 1u);
-                    if (fm) {
-                        limit = i0 + 32 * k + __ffs(fm) - 1;
-                        break;
-                    }
-                }
-            }
-            if (__any_sync(kFull, sec != 0)) {
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const bool b = (sec >> k) & 1u;
-                    const unsigned m = __ballot_sync(kFull, b);
-                    const uint32_t slot = nsl + __popc(m & lanemask_lt());
-                    if (b && slot < (uint32_t)kSLCap) SL[slot] = hk[k];
-                    nsl += __popc(m);
-                }
-            }
-            if (__any_sync(kFull, chn != 0)) {  // rare (about draws/n per draw)
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const bool b = (chn >> k) & 1u;
-                    const unsigned m = __ballot_sync(kFull, b);
-                    const uint32_t slot = ncl + __popc(m & lanemask_lt());
-                    if (b && slot < (uint32_t)kCLCap)
-                        CL[slot] = ((unsigned long long)tv[k] << 32) | (i0 + 32 * k + lane);
-                    ncl += __popc(m);
+                if (ok && t - base < i) {  // may equal an earlier replacement (t <= base + i)
+                    if (ncl < (uint32_t)kCLL) myCL[ncl] = ((unsigned long long)t << 32) | i;
+                    ++ncl;
                 }
             }
 #pragma unroll
             for (int k = 0; k < R; ++k) {
                 const uint32_t i = i0 + 32 * k + lane;
-                const bool live = i < limit;
-                gpairs += live ? 1u : 0u;
-                const bool keep = live && !(head_q<KIND>(hq, hb[k]) > reject);
+                const bool keep = (!tail || i < limit) && !(head_q<KIND>(hq, hb[k]) > reject);
                 const unsigned km = __ballot_sync(kFull, keep);
-                if (keep) Q[qn + __popc(km & lanemask_lt())] = pv[k];
+                if (keep) {
+                    Q[qn + __popc(km & lanemask_lt())] = pv[k];
+                    // wide rows come from HBM: start the fetch into L2 now, the
+                    // fp32 test reads it a queue-fill later (SNGB_FUSED_PF)
+                    if (kPrefetch && G >= 8) prefetch_l2(P + (uint64_t)pv[k] * W);
+                }
                 qn += __popc(km);
             }
             __syncwarp();
@@ -279,100 +333,91 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
                 qn = rem;
                 __syncwarp();
             }
+        };
+        {
+            const uint32_t nfull = limit / ITER;
+            uint64_t z = z0;
+            for (uint32_t it = 0; it < nfull; ++it, z += (uint64_t)ITER * kGamma) p2(it * ITER, z, false);
+            if (nfull * ITER < limit) p2(nfull * ITER, z, true);
         }
         if (qn) fp32_step(0, qn);
+        if (lane == 0) gpairs += limit;
         __syncwarp();
 
-        // ---- P2 + R: the Floyd collisions of this vertex ----
-        bool replay = irregular || nsl > (uint32_t)kSLCap || ncl > (uint32_t)kCLCap;
-        if (!replay && nsl > 0) {
-            {  // F := the shared bits
-                uint4* f4 = reinterpret_cast<uint4*>(F);
-                for (uint32_t w = lane; w < FW / 4; w += 32) f4[w] = make_uint4(0, 0, 0, 0);
+        // ---- R: the collided draws of this vertex ----
+        replay = replay || __any_sync(kFull, ngl > (uint32_t)kSLL || ncl > (uint32_t)kCLL) ||
+                 (__any_sync(kFull, ncl != 0) && warp_sum(ncl) > FW / 2);  // chain sort room
+        if (!replay && __any_sync(kFull, ngl != 0)) {
+            zeroF();  // F's memory := an empty (t + 1, min index) hash
+            __syncwarp();
+            // the group draws' values are regenerated (cheaper than keeping them)
+            auto draw_t = [&](uint32_t i) {
+                bool f;
+                return lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, f);
+            };
+            for (uint32_t e = 0; e < ngl; ++e) {
+                const uint32_t i = myGL[e], t = draw_t(i);
+                const unsigned long long kk = ((unsigned long long)(t + 1u) << 32) | i;  // never 0
+                uint32_t sl = (t * 0x85EBCA6Bu) >> (32 - hs_log);
+                for (;;) {
+                    const unsigned long long old = atomicCAS(&HT[sl], 0ull, kk);
+                    if (old == 0ull) break;
+                    if ((old >> 32) == (kk >> 32)) {
+                        atomicMin(&HT[sl], kk);
+                        break;
+                    }
+                    sl = (sl + 1) & hs_mask;
+                }
             }
             __syncwarp();
-            for (uint32_t e = lane; e < nsl; e += 32) red_or_sh(Fa + (SL[e] >> 5) * 4u, 1u << (SL[e] & 31));
-            __syncwarp();
-            uint32_t ng = 0;
-            for (uint32_t i0 = 0; i0 < D; i0 += 32) {
-                const uint32_t i = i0 + lane;
-                const uint32_t t = i < D ? scr[i] : 0u;
-                const uint32_t hh = (t * 0x9E3779B1u) >> shift;
-                const bool hit = i < D && ((ld_sh(Fa + (hh >> 5) * 4u) >> (hh & 31)) & 1u);
-                const unsigned m = __ballot_sync(kFull, hit);
-                const uint32_t slot = ng + __popc(m & lanemask_lt());
-                if (hit && slot < fg.gl_cap) GL[slot] = ((unsigned long long)t << 32) | i;
-                ng += __popc(m);
+            for (uint32_t e = 0; e < ngl; ++e) {
+                const uint32_t i = myGL[e], t = draw_t(i);
+                uint32_t sl = (t * 0x85EBCA6Bu) >> (32 - hs_log);
+                while ((uint32_t)(HT[sl] >> 32) != t + 1u) sl = (sl + 1) & hs_mask;
+                if ((uint32_t)HT[sl] != i) {  // an earlier draw has the same value
+                    atomicOr(&colbits[i >> 5], 1u << (i & 31));
+                    emit_extra(i);
+                }
             }
-            if (ng > fg.gl_cap) {
-                replay = true;
-            } else {
-                __syncwarp();
-                {  // F's memory := an empty (t + 1, min index) hash
-                    uint4* f4 = reinterpret_cast<uint4*>(F);
-                    for (uint32_t w = lane; w < FW / 4; w += 32) f4[w] = make_uint4(0, 0, 0, 0);
-                }
-                __syncwarp();
-                for (uint32_t e = lane; e < ng; e += 32) {
-                    const unsigned long long en = GL[e];
-                    const unsigned long long kk = en + (1ull << 32);  // (t + 1) << 32 | i, never 0
-                    uint32_t sl = ((uint32_t)(en >> 32) * 0x85EBCA6Bu) >> (32 - hs_log);
-                    for (;;) {
-                        const unsigned long long old = atomicCAS(&HT[sl], 0ull, kk);
-                        if (old == 0ull) break;
-                        if ((old >> 32) == (kk >> 32)) {
-                            atomicMin(&HT[sl], kk);
-                            break;
-                        }
-                        sl = (sl + 1) & hs_mask;
-                    }
-                }
-                __syncwarp();
-                for (uint32_t e = lane; e < ng; e += 32) {
-                    const unsigned long long en = GL[e];
-                    const uint32_t t1 = (uint32_t)(en >> 32) + 1u, i = (uint32_t)en;
-                    uint32_t sl = ((uint32_t)(en >> 32) * 0x85EBCA6Bu) >> (32 - hs_log);
-                    while ((uint32_t)(HT[sl] >> 32) != t1) sl = (sl + 1) & hs_mask;
-                    if ((uint32_t)HT[sl] != i) {  // an earlier draw has the same value
-                        atomicOr(&colbits[i >> 5], 1u << (i & 31));
-                        const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
-                        const uint32_t e2 = base + i;
-                        if (s2 < xs.capacity)
-                            xs.keys[s2] = (u << 32) | (e2 + (e2 >= (uint32_t)u ? 1u : 0u));
-                        ++ncol;
-                    }
-                }
-                __syncwarp();
-                if (lane == 0 && ncl) {
-                    for (uint32_t x = 1; x < ncl; ++x) {  // insertion sort by index (tiny list)
-                        const unsigned long long v = CL[x];
-                        uint32_t y = x;
-                        while (y > 0 && (uint32_t)CL[y - 1] > (uint32_t)v) {
-                            CL[y] = CL[y - 1];
+            __syncwarp();
+        }
+        if (!replay && __any_sync(kFull, ncl != 0)) {
+            // chain candidates of all lanes in index order (tiny), against the
+            // collided set; a collision makes its replacement visible to later ones
+            const unsigned cm = __ballot_sync(kFull, ncl != 0);
+            if (lane == 0) {
+                unsigned long long* cl = HT;  // F's memory is free now
+                uint32_t nc = 0;
+                for (unsigned m = cm; m; m &= m - 1) {
+                    const int l = __ffs(m) - 1;
+                    for (int j = 0; j < kCLL; ++j) {
+                        const unsigned long long v = CL[l * kCLL + j];
+                        if (v == 0ull) break;  // empty slot (a chain entry has i > 0)
+                        uint32_t y = nc++;
+                        while (y > 0 && (uint32_t)cl[y - 1] > (uint32_t)v) {
+                            cl[y] = cl[y - 1];
                             --y;
                         }
-                        CL[y] = v;
-                    }
-                    for (uint32_t x = 0; x < ncl; ++x) {
-                        const uint32_t i = (uint32_t)CL[x];
-                        if ((colbits[i >> 5] >> (i & 31)) & 1u) continue;  // already collided
-                        const uint32_t kx = (uint32_t)(CL[x] >> 32) - base;
-                        if ((colbits[kx >> 5] >> (kx & 31)) & 1u) {  // t_i = j_k, k collided
-                            colbits[i >> 5] |= 1u << (i & 31);
-                            const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
-                            const uint32_t e2 = base + i;
-                            if (s2 < xs.capacity)
-                                xs.keys[s2] = (u << 32) | (e2 + (e2 >= (uint32_t)u ? 1u : 0u));
-                            ++ncol;
-                        }
+                        cl[y] = v;
                     }
                 }
-                __syncwarp();
-                for (uint32_t e = lane; e < ng; e += 32) colbits[(uint32_t)GL[e] >> 5] = 0;
-                for (uint32_t e = lane; e < ncl; e += 32) colbits[(uint32_t)CL[e] >> 5] = 0;
-                __syncwarp();
+                for (uint32_t x = 0; x < nc; ++x) {
+                    const uint32_t i = (uint32_t)cl[x];
+                    if ((colbits[i >> 5] >> (i & 31)) & 1u) continue;  // already collided
+                    const uint32_t kx = (uint32_t)(cl[x] >> 32) - base;
+                    if ((colbits[kx >> 5] >> (kx & 31)) & 1u) {  // t_i = j_k, draw k collided
+                        colbits[i >> 5] |= 1u << (i & 31);
+                        emit_extra(i);
+                    }
+                }
             }
-        }  // nsl == 0: all values distinct, no replacement exists, no chain can collide
+            __syncwarp();
+        }
+        if (!replay) {  // clear the touched collided-bitmap words
+            for (uint32_t e = 0; e < ngl; ++e) colbits[(uint32_t)myGL[e] >> 5] = 0;
+            for (uint32_t e = 0; e < ncl; ++e) colbits[(uint32_t)myCL[e] >> 5] = 0;
+        }
+        for (int j = 0; j < kCLL; ++j) myCL[j] = 0ull;  // chain lists start empty
         if (replay && lane == 0) {
             const unsigned long long s2 = atomicAdd(&a.counters[C_IRR_CURSOR], 1ull);
             irr_list[s2] = (uint32_t)u;  // capacity: one slot per row
@@ -436,7 +481,7 @@ cudaError_t fused_one(SamplerArgs a, GatherArgs ga, const HeadArgs& h, cudaStrea
     const size_t rsmem = (size_t)cap_slots * 4;
     e = cudaFuncSetAttribute(k_replay_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
     if (e != cudaSuccess) return e;
-    const uint32_t* list = reinterpret_cast<const uint32_t*>(a.scratch64) + warps * fg.scratch_words();
+    const uint32_t* list = reinterpret_cast<const uint32_t*>(a.scratch64);
     k_replay_list<<<num_sms * 8, 32, rsmem, s>>>(a, list, cap_slots);
     note_launch(1);
     return cudaGetLastError();
@@ -477,8 +522,9 @@ bool fused_eligible(uint64_t n, uint32_t draws, uint32_t stride) {
 }
 
 size_t fused_scratch_bytes(uint32_t draws, uint64_t rows, int num_sms) {
-    const FGeom fg = fgeom(draws);
-    return ((uint64_t)num_sms * kMaxWarpsPerSM * fg.scratch_words() + rows) * 4;
+    (void)draws;
+    (void)num_sms;
+    return rows * 4;  // the replay list: at most one entry per row
 }
 
 cudaError_t launch_floyd_head(const SamplerArgs& in, const GatherArgs& ga, const HeadArgs& h,

@@ -50,6 +50,16 @@ __device__ __forceinline__ uint32_t lemire32(uint64_t x, uint32_t b, bool& fire)
     return (uint32_t)(s >> 32);
 }
 
+// Same, returning the low word of s instead of the pre-condition: a draw can
+// fire only if slo == 0, so a running minimum of slo over many draws is a one-
+// instruction superset test (the exact test is redone on the rare hit).
+__device__ __forceinline__ uint32_t lemire32_slo(uint64_t x, uint32_t b, uint32_t& slo) {
+    const uint64_t p1 = (uint64_t)(uint32_t)x * b;
+    const uint64_t s = (uint64_t)(uint32_t)(x >> 32) * b + (p1 >> 32);
+    slo = (uint32_t)s;
+    return (uint32_t)(s >> 32);
+}
+
 // Exact sequential Stream (rng.hpp:21-48) for the rare irregular vertices.
 struct SeqStream {
     uint64_t key;
