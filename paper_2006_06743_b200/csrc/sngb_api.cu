@@ -530,7 +530,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             sa.seed_mixed = seed_mixed;
             sa.force_mod = test_force_mod();
             const size_t scratch = fuse_try ? fused_scratch_bytes((uint32_t)draws, re - rb, c.num_sms)
-                                            : floyd_scratch_bytes((uint32_t)draws, c.num_sms);
+                                            : floyd_scratch_bytes((uint32_t)draws, c.num_sms, re - rb);
             if (scratch) c.scratch.ensure(scratch);
             sa.scratch64 = scratch ? c.scratch.as<unsigned long long>() : nullptr;
             sa.extras = c.extras.as<unsigned long long>();

@@ -360,3 +360,22 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_bloom(co
         if (nrep) atomicAdd(&a.counters[C_IRREGULAR], nrep);
     }
 }
+
+// The exact sequential replay (bloom_replay: graph.cpp:163-174 with true Stream
+// semantics) of the vertices k_floyd_warp / k_sample_head listed; every partner is an extra.
+__global__ void __launch_bounds__(32) k_replay_list(const SamplerArgs a, const uint32_t* list,
+                                                    uint32_t cap) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* tab = reinterpret_cast<uint32_t*>(smem);
+    const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
+    const unsigned long long cnt = a.counters[C_IRR_CURSOR];
+    unsigned long long nrep = 0;
+    for (unsigned long long x = blockIdx.x; x < cnt; x += gridDim.x) {
+        if (threadIdx.x == 0) {
+            const uint64_t u = list[x];
+            bloom_replay(vertex_key(a.seed_mixed, u), u, a.n, a.base, tab, cap, xs);
+            ++nrep;
+        }
+    }
+    if (threadIdx.x == 0 && nrep) atomicAdd(&a.counters[C_IRREGULAR], nrep);
+}

@@ -1,38 +1,36 @@
 // sngb_fused.cu -- k_sample_head: the Floyd bookkeeping (graph.cpp:161-174) and
 // the head-filter gather (sngb_head.cu) of large narrow-row problems in one
-// kernel, one warp per vertex (cfg3, cfg4, cfg5).
+// kernel, one warp per vertex, each draw generated once (cfg3, cfg4, cfg5).
 //
 // Why.  As two kernels (k_floyd_bloom + k_gather_head) each draw
 //   t_i = Lemire(mix(key + (i+1) gamma), base + i + 1)   (rng.hpp:26,35-48)
-// costs ~100 SASS instructions in each (ncu: profiles/r02_ncu_floyd_cfg5.md,
-// r01_ncu_head_cfg5.md), and the Floyd kernel's block barriers and the
-// gather's L2 latency each leave the SM a third idle.  A one-pass fusion with
-// the draws kept in global scratch (v4, profiles/r02_ncu_fused_v4_cfg5.md) was
-// slower: 5.5 warp-instructions per draw and 318 GB of scratch write-back.
-// Here every warp owns a vertex and makes TWO lean passes over its draws,
-// regenerating them (a draw is ~26 integer instructions; storing it costs
-// more in L2/DRAM traffic than it saves):
+// is generated twice and costs ~100 SASS instructions in each (ncu:
+// profiles/r02_ncu_floyd_cfg5.md, r01_ncu_head_cfg5.md).  Earlier fusions:
+// v3 block per vertex (barriers: 831 ms on cfg5), v4 one pass with the draws
+// in global scratch (318 GB of write-back: 978 ms), v6 two regenerating passes
+// (5.2 warp-instructions per draw: 750 ms), against 654 ms for the two kernels.
+// Here a warp owns a vertex and keeps only each draw's 16-bit filter hash in
+// shared memory (D x 2 bytes), so the one pass over the draws does everything:
 //
-//   P1  filter pass (no memory traffic): t_i, OR bit h(t_i) into a warp-
-//       private 2^B-bit filter F; a draw that finds its bit already set
-//       records h in its lane's second-comer list SL; the running minimum of
-//       Lemire's low word flags a possible reject pre-condition (rng.hpp:43).
-//   ->  F := the bits in SL (exactly the bits hit by >= 2 draws).
-//   P2  gather pass: t_i again, the partner's head load (exact reject,
-//       sngb_head.cu), survivors queued for the fp32 test (sngb_epstest.cuh);
-//       draws on a shared bit -> the lane's group list GL (their indices, in
-//       SL's slots), t_i in [base, base + i) -> the lane's chain list CL.
-//   R   GL's values (regenerated) in a small hash (F's memory) keyed by t with
-//       the minimum index: a
-//       draw whose value has a smaller index collides (graph.cpp:168-169, its
-//       replacement j_i = base + i is inserted instead); then the chain
-//       candidates in index order against the collided set.  Every collided
-//       draw's replacement is emitted as an extra pair (tested by k_extras).
-// A Lemire reject pre-condition (~1e-12 per draw) or a list overflow sends
-// the vertex to the exact sequential replay (k_replay_list: true Stream
-// semantics, every partner an extra); its gather stops at the first fired
-// draw, as k_gather_head's does.  Results are the two-kernel path's bit for
-// bit (tests/test_gpu_parity.py -k "fused or head").
+//   P1  draw i (lane i mod 32, R slots per step): t_i; a running test of the
+//       Lemire reject pre-condition (rng.hpp:43, ~1e-12 per draw) that cuts
+//       the vertex at its first fired draw; the partner's head load (exact
+//       reject, sngb_head.cu) and survivors' fp32 test (sngb_epstest.cuh);
+//       h_i = hash(t_i) -> HS[i]; OR bit h_i into a warp-private 2^B-bit filter
+//       F -- a draw finding its bit already set records h_i in its lane's
+//       second-comer list SL; t_i in [base, base + i) -> the lane's chain list.
+//   P2  F := the bits in SL (exactly the bits hit by >= 2 draws); scan HS: the
+//       draws on such a bit -> the lane's group list GL (indices, SL's slots).
+//   R   GL's values (regenerated: ~6 % of the draws) in a small hash (F's
+//       memory) keyed by t with the minimum index: a draw whose value has a
+//       smaller index collides (graph.cpp:168-169: its replacement
+//       j_i = base + i is inserted instead); then the chain candidates in index
+//       order against the collided set.  Every collided draw's replacement is
+//       emitted as an extra pair (tested by k_extras).
+// A fired draw or a list overflow sends the vertex to the exact sequential
+// replay (k_replay_list: true Stream semantics, every partner an extra); its
+// gather stops at the first fired draw, as k_gather_head's does.  Results are
+// the two-kernel path's bit for bit (tests/test_gpu_parity.py -k "fused or head").
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -46,10 +44,10 @@
 #include "sngb_rng.cuh"
 
 #ifndef SNGB_FUSED_MINB
-#define SNGB_FUSED_MINB 4
+#define SNGB_FUSED_MINB 8
 #endif
 #ifndef SNGB_FUSED_R
-#define SNGB_FUSED_R 4
+#define SNGB_FUSED_R 8
 #endif
 
 namespace sngb {
@@ -57,94 +55,39 @@ namespace sngb {
 namespace {
 
 #include "sngb_floyd_bloom.cuh"
+#include "sngb_floyd_warp.cuh"
 
-constexpr int kFWarps = 4;       // warps per block (independent vertices)
-constexpr int kSLL = 32;         // per lane: second-comer bits (P1; mean D^2/2^(B+1)/32 = 3.8 at D = 4000),
-                                 // then group-list draws (P2; mean D^2/2^B/32 = 7.6)
-constexpr int kCLL = 4;          // chain candidates per lane (mean D^2 / 2n / 32: 0.01 on cfg5)
-constexpr int kFStage = 64;      // edge staging per warp (accepts are rare here)
-constexpr int kMaxWarpsPerSM = 32;
+constexpr int kFStage = 64;  // edge staging per warp (accepts are rare here)
 
-// per-warp geometry: filter F of 2^B bits (FW words, reused as the resolution
-// hash of FW / 2 u64 slots), collided bitmap (CW words)
-struct FGeom {
-    uint32_t B, FW, CW;
-    __host__ __device__ uint32_t q_cap(int R, int step) const { return ((32 * R + step) + 3) & ~3u; }
-    __host__ __device__ uint32_t warp_bytes(int R, int step) const {
-        return FW * 4 + 32 * kSLL * 2 + 32 * kCLL * 8 + CW * 4 + q_cap(R, step) * 4 + kFStage * 8;
-    }
-};
-
-inline FGeom fgeom(uint32_t draws) {
-    const BloomGeom bg = bloom_geometry(draws);
-    FGeom g;
-    g.B = bg.bits_log2;
-    g.FW = bg.words;
-    g.CW = bg.col_words;
-    return g;
-}
-
-#ifndef SNGB_FUSED_PF
-#define SNGB_FUSED_PF 0  // measured slower on cfg5 (861 vs 845 ms)
-#endif
-constexpr bool kPrefetch = SNGB_FUSED_PF != 0;
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-__device__ __forceinline__ void red_or_sh(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-
-// first draw index < D whose Lemire step meets the reject pre-condition
-// (lo < bound, rng.hpp:43), or D: the exact test behind the slo == 0 flag
-__device__ __noinline__ uint32_t first_fire(uint64_t key, uint32_t D, uint32_t base, int lane) {
-    uint32_t f = D;
-    for (uint32_t i = lane; i < D; i += 32) {
-        bool fire;
-        (void)lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fire);
-        if (fire) {
-            f = i;
-            break;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) f = min(f, __shfl_xor_sync(kFull, f, o));
-    return f;
+__host__ __device__ inline uint32_t fused_q_cap(int R, int step) { return ((32 * R + step) + 3) & ~3u; }
+__host__ __device__ inline uint32_t fused_warp_bytes(const FwGeom& fg, int R, int step) {
+    return fg.warp_bytes() + fused_q_cap(R, step) * 4 + kFStage * 8;
 }
 
 template <int KIND, int G, int V, int R>
-__global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
-    k_sample_head(const SamplerArgs a, const GatherArgs g, const HeadArgs h, const FGeom fg) {
+__global__ void __launch_bounds__(32, 8)
+    k_sample_head(const SamplerArgs a, const GatherArgs g, const HeadArgs h, const FwGeom fg) {
     constexpr int NG = 32 / G;
     constexpr int UF = 2;            // fp32 rows per group per step
     constexpr int STEP = NG * UF;    // survivors per fp32 step
     constexpr uint32_t ITER = 32 * R;
     extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
     const int q = lane % G, grp = lane / G;
     const bool leader = (q == 0);
     const uint32_t D = a.draws, base = a.base;
     const uint32_t shift = 32 - fg.B, FW = fg.FW;
-    const uint32_t hs_log = fg.B - 6;  // resolution hash: 2^B / 64 u64 slots
-    const uint32_t hs_mask = (1u << hs_log) - 1;
 
-    // warp-private shared memory
-    unsigned char* wsm = smem + (size_t)wib * fg.warp_bytes(R, STEP);
-    uint32_t* F = reinterpret_cast<uint32_t*>(wsm);
-    unsigned long long* HT = reinterpret_cast<unsigned long long*>(wsm);  // F's memory in R
-    uint16_t* SL = reinterpret_cast<uint16_t*>(F + FW);       // [32][kSLL], lane-major (B <= 16)
-    unsigned long long* CL = reinterpret_cast<unsigned long long*>(SL + 32 * kSLL);  // [32][kCLL]
-    uint32_t* colbits = reinterpret_cast<uint32_t*>(CL + 32 * kCLL);
-    uint32_t* Q = colbits + fg.CW;
-    unsigned long long* stg = reinterpret_cast<unsigned long long*>(Q + fg.q_cap(R, STEP));
-    const uint32_t Fa = smem_addr(F);
-    uint16_t* mySL = SL + lane * kSLL;
-    unsigned long long* myCL = CL + lane * kCLL;
-
-    // the lane's group list (draw indices) reuses its SL slots: SL is consumed
-    // (F rebuilt) before P2 pushes the first group entry
-    uint16_t* myGL = mySL;
+    // the warp's shared memory (one warp per block): k_floyd_warp's layout + queue + stage
+    uint32_t* F = reinterpret_cast<uint32_t*>(smem);
+    uint16_t* HS = reinterpret_cast<uint16_t*>(F + FW);
+    uint16_t* SL = HS + 2 * fg.hs_words;  // [32][kFwSLL]
+    uint16_t* CLs = SL + 32 * kFwSLL;     // [32][kFwCLL]
+    uint32_t* Q = reinterpret_cast<uint32_t*>(CLs + 32 * kFwCLL);
+    unsigned long long* stg = reinterpret_cast<unsigned long long*>(Q + fused_q_cap(R, STEP));
+    const uint32_t Fa = smem_addr(F), HSa = smem_addr(HS), Qa = smem_addr(Q);
+    const uint32_t SLa = smem_addr(SL + lane * kFwSLL), CLa = smem_addr(CLs + lane * kFwCLL);
+    uint16_t* myCL = CLs + lane * kFwCLL;
     uint32_t* irr_list = reinterpret_cast<uint32_t*>(a.scratch64);  // the replay list
 
     const float4* __restrict__ P = reinterpret_cast<const float4*>(g.tp.pts);
@@ -152,14 +95,11 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
     const uint32_t W = g.tp.stride / 4;
     const float reject = h.reject;
     const uint64_t pol = evict_first_policy();  // survivor rows must not evict the heads
-    const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
 
     WarpStage<kFStage> stage{stg, 0};
     TestStats st;
     unsigned long long gpairs = 0, tails = 0, ncol = 0;
-
-    for (uint32_t w = lane; w < fg.CW; w += 32) colbits[w] = 0;
-    for (int j = 0; j < kCLL; ++j) myCL[j] = 0ull;  // chain lists start empty (0 = no entry)
+    for (int j = 0; j < kFwCLL; ++j) myCL[j] = 0;  // chain lists start empty (0 = no entry)
 
     uint64_t u = 0, chunk_end = 0;
     auto grab = [&]() {
@@ -168,16 +108,6 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
         b0 = __shfl_sync(kFull, b0, 0);
         u = a.row_begin + b0;
         chunk_end = u + g.grab < a.row_end ? u + g.grab : a.row_end;
-    };
-    auto zeroF = [&]() {
-        uint4* f4 = reinterpret_cast<uint4*>(F);
-        for (uint32_t w = lane; w < FW / 4; w += 32) f4[w] = make_uint4(0, 0, 0, 0);
-    };
-    auto emit_extra = [&](uint32_t i) {  // collided draw i: its replacement j_i = base + i
-        const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
-        const uint32_t e2 = base + i;
-        if (s2 < xs.capacity) xs.keys[s2] = (u << 32) | (e2 + (e2 >= (uint32_t)u ? 1u : 0u));
-        ++ncol;
     };
     grab();
     for (; u < chunk_end; (u + 1 >= chunk_end) ? grab() : (void)(++u)) {
@@ -189,59 +119,7 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
         }
         const uint32_t hq = head_load<KIND>(H, (uint32_t)u);
         const uint64_t key = vertex_key(a.seed_mixed, u);
-        const uint64_t z0 = key + (uint64_t)(lane + 1) * kGamma;
-        zeroF();
-        __syncwarp();
-
-        // ---- P1: the filter pass ----
-        uint32_t nsl = 0, mn = 0xffffffffu;
-        auto p1 = [&](uint32_t i0, uint64_t z, bool tail) {
-            uint32_t hk[R], old[R];
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-                const uint32_t i = i0 + 32 * k + lane;
-                uint32_t slo;
-                const uint32_t t = lemire32_slo(mix(z + (uint64_t)(32 * k) * kGamma), base + i + 1, slo);
-                hk[k] = (t * 0x9E3779B1u) >> shift;
-                if (!tail || i < D) mn = min(mn, slo);
-            }
-            // all R atomics in flight before any result is used
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-                const uint32_t i = i0 + 32 * k + lane;
-                old[k] = (!tail || i < D) ? atom_or_sh(Fa + (hk[k] >> 5) * 4u, 1u << (hk[k] & 31)) : 0u;
-            }
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-                if ((old[k] >> (hk[k] & 31)) & 1u) {  // a second comer
-                    if (nsl < (uint32_t)kSLL) mySL[nsl] = (uint16_t)hk[k];
-                    ++nsl;
-                }
-            }
-        };
-        {
-            const uint32_t nfull = D / ITER;
-            uint64_t z = z0;
-            for (uint32_t it = 0; it < nfull; ++it, z += (uint64_t)ITER * kGamma) p1(it * ITER, z, false);
-            if (nfull * ITER < D) p1(nfull * ITER, z, true);
-        }
-        // a possible reject pre-condition (or the test hook): the exact first fire
-        uint32_t limit = D;
-        const bool hooked = a.force_mod != 0 && (u % a.force_mod) == 0;
-        if (__any_sync(kFull, mn == 0u) || hooked) {
-            limit = first_fire(key, D, base, lane);
-            if (hooked) limit = min(limit, D / 2);
-        }
-        const bool irregular = limit < D;
-        bool replay = irregular || __any_sync(kFull, nsl > (uint32_t)kSLL);
-        // F := the shared bits
-        __syncwarp();
-        zeroF();
-        __syncwarp();
-        {
-            const uint32_t ns = min(nsl, (uint32_t)kSLL);
-            for (uint32_t j = 0; j < ns; ++j) red_or_sh(Fa + (mySL[j] >> 5) * 4u, 1u << (mySL[j] & 31));
-        }
+        for (uint32_t w = lane; w < FW / 4; w += 32) st_sh_zero16(Fa + 16 * w);
         __syncwarp();
 
         // fp32 test of queue entries [e0, e0 + STEP) of which those < qend are real
@@ -253,7 +131,7 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
             for (int uu = 0; uu < UF; ++uu) {
                 const uint32_t e = e0 + grp + NG * uu;
                 oke[uu] = e < qend;
-                pe[uu] = Q[oke[uu] ? e : e0];
+                pe[uu] = ld_sh(Qa + 4 * (oke[uu] ? e : e0));
 #pragma unroll
                 for (int vv = 0; vv < V; ++vv) {
                     const uint32_t c = q + G * vv;
@@ -276,49 +154,82 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
             }
         };
 
-        // ---- P2: the gather pass (draws below limit) ----
-        uint32_t qn = 0, ngl = 0, ncl = 0;
-        auto p2 = [&](uint32_t i0, uint64_t z, bool tail) {
-            uint32_t tv[R], pv[R];
+        // ---- P1: every draw once (test hook: a hooked vertex fires at draw D/2) ----
+        uint32_t limit = (a.force_mod != 0 && (u % a.force_mod) == 0) ? D / 2 : D;
+        bool replay = limit < D;
+        uint32_t qn = 0, nsl = 0, ncl = 0;
+        // one step of R slots; TAIL masks the draws >= limit.  Returns true when a
+        // draw of this step fired (limit cut): the step is then redone as a tail.
+        auto step = [&](uint32_t i0, uint64_t z, auto tail_c) -> bool {
+            constexpr bool TAIL = decltype(tail_c)::value;
+            const uint32_t b0 = base + i0 + lane + 1;  // Lemire bound of slot 0
+            uint32_t tv[R], mn = 0xffffffffu;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                uint32_t slo;
+                tv[k] = lemire32_slo(mix(z + (uint64_t)(32 * k) * kGamma), b0 + 32 * k, slo);
+                const bool valid = !TAIL || i0 + 32 * k + lane < limit;
+                mn = valid ? min(mn, slo) : mn;
+            }
+            if (__any_sync(kFull, mn == 0u)) {  // rare: the exact pre-condition, first fired draw
+                uint32_t f = limit;
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    bool fire;
+                    (void)lemire32(mix(z + (uint64_t)(32 * k) * kGamma), b0 + 32 * k, fire);
+                    const uint32_t i = i0 + 32 * k + lane;
+                    if (fire && i < f) f = i;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) f = min(f, __shfl_xor_sync(kFull, f, o));
+                if (f < limit) {
+                    limit = f;
+                    replay = true;
+                    if (!TAIL) return true;  // redo this step as a tail
+                }
+            }
+            uint32_t pv[R];
 #pragma unroll
             for (int k = 0; k < R; ++k) {
                 const uint32_t i = i0 + 32 * k + lane;
-                uint32_t slo;
-                tv[k] = lemire32_slo(mix(z + (uint64_t)(32 * k) * kGamma), base + i + 1, slo);
                 const uint32_t p = tv[k] + (tv[k] >= (uint32_t)u ? 1u : 0u);
-                pv[k] = (!tail || i < limit) ? p : (uint32_t)u;
+                pv[k] = (!TAIL || i < limit) ? p : (uint32_t)u;
             }
             uint32_t hb[R];
 #pragma unroll
             for (int k = 0; k < R; ++k) hb[k] = head_load<KIND>(H, pv[k]);  // in flight from here
-            uint32_t fw[R];
+            if (!replay) {  // the Floyd bookkeeping (skipped once the vertex will be replayed)
+                uint32_t hk[R], old[R];
 #pragma unroll
-            for (int k = 0; k < R; ++k) fw[k] = ld_sh(Fa + ((tv[k] * 0x9E3779B1u) >> shift >> 5) * 4u);
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-                const uint32_t i = i0 + 32 * k + lane;
-                const uint32_t t = tv[k];
-                const bool ok = !tail || i < limit;
-                if (ok && ((fw[k] >> (((t * 0x9E3779B1u) >> shift) & 31)) & 1u)) {  // on a shared bit
-                    if (ngl < (uint32_t)kSLL) myGL[ngl] = (uint16_t)i;
-                    ++ngl;
+                for (int k = 0; k < R; ++k) {
+                    const uint32_t i = i0 + 32 * k + lane;
+                    hk[k] = (tv[k] * 0x9E3779B1u) >> shift;
+                    if (TAIL) st_sh_u16_if(HSa + 2 * i, hk[k], i < limit);
+                    else st_sh_u16(HSa + 2 * i, hk[k]);
                 }
-                if (ok && t - base < i) {  // may equal an earlier replacement (t <= base + i)
-                    if (ncl < (uint32_t)kCLL) myCL[ncl] = ((unsigned long long)t << 32) | i;
-                    ++ncl;
+#pragma unroll
+                for (int k = 0; k < R; ++k) {  // all R atomics in flight before any result is used
+                    const uint32_t i = i0 + 32 * k + lane;
+                    const uint32_t addr = Fa + ((hk[k] >> 5) << 2), bit = 1u << (hk[k] & 31);
+                    old[k] = TAIL ? atom_or_sh_if(addr, bit, i < limit) : atom_or_sh(addr, bit);
+                }
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    const uint32_t i = i0 + 32 * k + lane;
+                    const bool sec = (old[k] >> (hk[k] & 31)) & 1u;  // a second comer (0 if masked)
+                    st_sh_u16_if(SLa + 2 * min(nsl, (uint32_t)kFwSLL - 1), hk[k], sec);
+                    nsl += sec ? 1u : 0u;
+                    const bool ch = (!TAIL || i < limit) && tv[k] - base < i;  // t <= base + i
+                    st_sh_u16_if(CLa + 2 * min(ncl, (uint32_t)kFwCLL - 1), i, ch);
+                    ncl += ch ? 1u : 0u;
                 }
             }
 #pragma unroll
             for (int k = 0; k < R; ++k) {
                 const uint32_t i = i0 + 32 * k + lane;
-                const bool keep = (!tail || i < limit) && !(head_q<KIND>(hq, hb[k]) > reject);
+                const bool keep = (!TAIL || i < limit) && !(head_q<KIND>(hq, hb[k]) > reject);
                 const unsigned km = __ballot_sync(kFull, keep);
-                if (keep) {
-                    Q[qn + __popc(km & lanemask_lt())] = pv[k];
-                    // wide rows come from HBM: start the fetch into L2 now, the
-                    // fp32 test reads it a queue-fill later (SNGB_FUSED_PF)
-                    if (kPrefetch && G >= 8) prefetch_l2(P + (uint64_t)pv[k] * W);
-                }
+                if (keep) st_sh(Qa + 4 * (qn + __popc(km & lanemask_lt())), pv[k]);
                 qn += __popc(km);
             }
             __syncwarp();
@@ -327,97 +238,29 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
 #pragma unroll 1
                 for (; e0 + STEP <= qn; e0 += STEP) fp32_step(e0, qn);
                 const uint32_t rem = qn - e0;  // < STEP: move them to the front
-                const uint32_t mp = (uint32_t)lane < rem ? Q[e0 + lane] : 0u;
+                const uint32_t mp = lane < rem ? ld_sh(Qa + 4 * (e0 + lane)) : 0u;
                 __syncwarp();
-                if ((uint32_t)lane < rem) Q[lane] = mp;
+                if (lane < rem) st_sh(Qa + 4 * lane, mp);
                 qn = rem;
                 __syncwarp();
             }
+            return false;
         };
         {
-            const uint32_t nfull = limit / ITER;
-            uint64_t z = z0;
-            for (uint32_t it = 0; it < nfull; ++it, z += (uint64_t)ITER * kGamma) p2(it * ITER, z, false);
-            if (nfull * ITER < limit) p2(nfull * ITER, z, true);
+            uint64_t z = key + (uint64_t)(lane + 1) * kGamma;
+            uint32_t i0 = 0;
+            for (; i0 + ITER <= limit; i0 += ITER, z += (uint64_t)ITER * kGamma)
+                if (step(i0, z, std::false_type{})) break;  // fired: redo as the tail below
+            if (i0 < limit) step(i0, z, std::true_type{});
         }
         if (qn) fp32_step(0, qn);
         if (lane == 0) gpairs += limit;
-        __syncwarp();
 
-        // ---- R: the collided draws of this vertex ----
-        replay = replay || __any_sync(kFull, ngl > (uint32_t)kSLL || ncl > (uint32_t)kCLL) ||
-                 (__any_sync(kFull, ncl != 0) && warp_sum(ncl) > FW / 2);  // chain sort room
-        if (!replay && __any_sync(kFull, ngl != 0)) {
-            zeroF();  // F's memory := an empty (t + 1, min index) hash
-            __syncwarp();
-            // the group draws' values are regenerated (cheaper than keeping them)
-            auto draw_t = [&](uint32_t i) {
-                bool f;
-                return lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, f);
-            };
-            for (uint32_t e = 0; e < ngl; ++e) {
-                const uint32_t i = myGL[e], t = draw_t(i);
-                const unsigned long long kk = ((unsigned long long)(t + 1u) << 32) | i;  // never 0
-                uint32_t sl = (t * 0x85EBCA6Bu) >> (32 - hs_log);
-                for (;;) {
-                    const unsigned long long old = atomicCAS(&HT[sl], 0ull, kk);
-                    if (old == 0ull) break;
-                    if ((old >> 32) == (kk >> 32)) {
-                        atomicMin(&HT[sl], kk);
-                        break;
-                    }
-                    sl = (sl + 1) & hs_mask;
-                }
-            }
-            __syncwarp();
-            for (uint32_t e = 0; e < ngl; ++e) {
-                const uint32_t i = myGL[e], t = draw_t(i);
-                uint32_t sl = (t * 0x85EBCA6Bu) >> (32 - hs_log);
-                while ((uint32_t)(HT[sl] >> 32) != t + 1u) sl = (sl + 1) & hs_mask;
-                if ((uint32_t)HT[sl] != i) {  // an earlier draw has the same value
-                    atomicOr(&colbits[i >> 5], 1u << (i & 31));
-                    emit_extra(i);
-                }
-            }
-            __syncwarp();
-        }
-        if (!replay && __any_sync(kFull, ncl != 0)) {
-            // chain candidates of all lanes in index order (tiny), against the
-            // collided set; a collision makes its replacement visible to later ones
-            const unsigned cm = __ballot_sync(kFull, ncl != 0);
-            if (lane == 0) {
-                unsigned long long* cl = HT;  // F's memory is free now
-                uint32_t nc = 0;
-                for (unsigned m = cm; m; m &= m - 1) {
-                    const int l = __ffs(m) - 1;
-                    for (int j = 0; j < kCLL; ++j) {
-                        const unsigned long long v = CL[l * kCLL + j];
-                        if (v == 0ull) break;  // empty slot (a chain entry has i > 0)
-                        uint32_t y = nc++;
-                        while (y > 0 && (uint32_t)cl[y - 1] > (uint32_t)v) {
-                            cl[y] = cl[y - 1];
-                            --y;
-                        }
-                        cl[y] = v;
-                    }
-                }
-                for (uint32_t x = 0; x < nc; ++x) {
-                    const uint32_t i = (uint32_t)cl[x];
-                    if ((colbits[i >> 5] >> (i & 31)) & 1u) continue;  // already collided
-                    const uint32_t kx = (uint32_t)(cl[x] >> 32) - base;
-                    if ((colbits[kx >> 5] >> (kx & 31)) & 1u) {  // t_i = j_k, draw k collided
-                        colbits[i >> 5] |= 1u << (i & 31);
-                        emit_extra(i);
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        if (!replay) {  // clear the touched collided-bitmap words
-            for (uint32_t e = 0; e < ngl; ++e) colbits[(uint32_t)myGL[e] >> 5] = 0;
-            for (uint32_t e = 0; e < ncl; ++e) colbits[(uint32_t)myCL[e] >> 5] = 0;
-        }
-        for (int j = 0; j < kCLL; ++j) myCL[j] = 0ull;  // chain lists start empty
+        // ---- P2 + R: the collided draws (k_floyd_warp's resolution) ----
+        replay = replay || __any_sync(kFull, nsl > (uint32_t)kFwSLL || ncl > (uint32_t)kFwCLL);
+        __syncwarp();
+        fw_resolve(a, fg, u, key, F, HS, SL, CLs, nsl, ncl, replay, ncol);
+        for (int j = 0; j < kFwCLL; ++j) myCL[j] = 0;
         if (replay && lane == 0) {
             const unsigned long long s2 = atomicAdd(&a.counters[C_IRR_CURSOR], 1ull);
             irr_list[s2] = (uint32_t)u;  // capacity: one slot per row
@@ -433,46 +276,24 @@ __global__ void __launch_bounds__(kFWarps * 32, SNGB_FUSED_MINB)
     if (lane == 0 && ncol) atomicAdd(&a.counters[C_COLLISIONS], ncol);
 }
 
-// The exact sequential replay (bloom_replay: graph.cpp:163-174 with true Stream
-// semantics) of the vertices k_sample_head listed; every partner is an extra.
-__global__ void __launch_bounds__(32) k_replay_list(const SamplerArgs a, const uint32_t* list,
-                                                    uint32_t cap) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    uint32_t* tab = reinterpret_cast<uint32_t*>(smem);
-    const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
-    const unsigned long long cnt = a.counters[C_IRR_CURSOR];
-    unsigned long long nrep = 0;
-    for (unsigned long long x = blockIdx.x; x < cnt; x += gridDim.x) {
-        if (threadIdx.x == 0) {
-            const uint64_t u = list[x];
-            bloom_replay(vertex_key(a.seed_mixed, u), u, a.n, a.base, tab, cap, xs);
-            ++nrep;
-        }
-    }
-    if (threadIdx.x == 0 && nrep) atomicAdd(&a.counters[C_IRREGULAR], nrep);
-}
-
 template <int KIND, int G, int V>
 cudaError_t fused_one(SamplerArgs a, GatherArgs ga, const HeadArgs& h, cudaStream_t s,
                       int num_sms) {
     constexpr int R = SNGB_FUSED_R;
     constexpr int STEP = (32 / G) * 2;
     auto k = k_sample_head<KIND, G, V, R>;
-    const FGeom fg = fgeom(a.draws);
-    const size_t smem = (size_t)kFWarps * fg.warp_bytes(R, STEP);
+    const FwGeom fg = fw_geometry(a.draws);
+    const size_t smem = fused_warp_bytes(fg, R, STEP);  // one warp per block
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem);
     if (per_sm < 1) per_sm = 1;
-    if (per_sm > kMaxWarpsPerSM / kFWarps) per_sm = kMaxWarpsPerSM / kFWarps;
     const uint64_t rows = a.row_end - a.row_begin;
-    const uint64_t want = (rows + kFWarps - 1) / kFWarps;
     const uint64_t cap = (uint64_t)num_sms * per_sm;
-    const unsigned grid = (unsigned)(want < cap ? want : cap);
-    const uint64_t warps = (uint64_t)grid * kFWarps;
-    ga.grab = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, rows / (warps * 16)));
-    k<<<grid, kFWarps * 32, smem, s>>>(a, ga, h, fg);
+    const unsigned grid = (unsigned)(rows < cap ? rows : cap);
+    ga.grab = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, rows / ((uint64_t)grid * 16)));
+    k<<<grid, 32, smem, s>>>(a, ga, h, fg);
     note_launch(1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // the listed vertices' exact replays (usually none: one small launch)
@@ -481,8 +302,8 @@ cudaError_t fused_one(SamplerArgs a, GatherArgs ga, const HeadArgs& h, cudaStrea
     const size_t rsmem = (size_t)cap_slots * 4;
     e = cudaFuncSetAttribute(k_replay_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
     if (e != cudaSuccess) return e;
-    const uint32_t* list = reinterpret_cast<const uint32_t*>(a.scratch64);
-    k_replay_list<<<num_sms * 8, 32, rsmem, s>>>(a, list, cap_slots);
+    k_replay_list<<<num_sms * 8, 32, rsmem, s>>>(a, reinterpret_cast<const uint32_t*>(a.scratch64),
+                                                 cap_slots);
     note_launch(1);
     return cudaGetLastError();
 }

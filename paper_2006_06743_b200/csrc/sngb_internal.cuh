@@ -186,7 +186,7 @@ __host__ __device__ __forceinline__ float ordered_value(uint32_t k) {
 }
 // sngb_sampler.cu
 void floyd_geometry(uint32_t draws, uint32_t& slots, uint32_t& col_words);
-size_t floyd_scratch_bytes(uint32_t draws, int num_sms);
+size_t floyd_scratch_bytes(uint32_t draws, int num_sms, uint64_t rows);
 cudaError_t launch_sampler(const SamplerArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_gather(const GatherArgs& a, bool exhaustive, cudaStream_t s, int num_sms);
 // exact fp64 decision of the band pairs; accepted ones go to `sink`

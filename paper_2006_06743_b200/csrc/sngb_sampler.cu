@@ -32,8 +32,10 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <mutex>
 #include <set>
+#include <type_traits>
 #include <utility>
 #include <cstdlib>
 
@@ -237,6 +239,7 @@ __global__ void __launch_bounds__(kFloydThreads) k_floyd(const SamplerArgs a) {
 
 #include "sngb_floyd_bitmap.cuh"
 #include "sngb_floyd_bloom.cuh"
+#include "sngb_floyd_warp.cuh"
 
 }  // namespace
 
@@ -257,11 +260,12 @@ size_t floyd_smem_bytes(uint32_t draws, bool shared_table) {
 
 bool floyd_shared(uint32_t draws) { return floyd_smem_bytes(draws, true) <= 200 * 1024; }
 
-size_t floyd_scratch_bytes(uint32_t draws, int num_sms) {
-    if (floyd_shared(draws)) return 0;
+size_t floyd_scratch_bytes(uint32_t draws, int num_sms, uint64_t rows) {
+    // k_floyd_warp's replay list (one u32 per row); k_floyd's L2 tables
+    if (floyd_shared(draws)) return rows * 4;
     uint32_t slots, cw;
     floyd_geometry(draws, slots, cw);
-    return (size_t)num_sms * 2 * slots * 8;
+    return std::max<size_t>((size_t)num_sms * 2 * slots * 8, rows * 4);
 }
 
 // A kernel's dynamic shared-memory limit is raised once per device to the
@@ -317,6 +321,38 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
         if (per_sm < 1) per_sm = 1;
         const uint64_t want = (rows + wpb - 1) / wpb, cap = (uint64_t)num_sms * per_sm;
         k_floyd_bitmap<<<(unsigned)(want < cap ? want : cap), wpb * 32, smem, s>>>(a);
+        note_launch(1);
+        return cudaGetLastError();
+    }
+    // large n, draws <= 4096: a warp per vertex (k_floyd_warp) with SNGB_FLOYD_WARP=1
+    // (cfg5: 330 ms vs 321 for k_floyd_bloom, profiles/r02_ab_floyd_warp.jsonl);
+    // SNGB_FLOYD_BLOOM=1 forces the block-per-vertex filter kernel
+    const char* fwenv = std::getenv("SNGB_FLOYD_WARP");
+    if (D <= 4096 && a.n - 2 < 0xffffffffull && a.scratch64 && fwenv && std::atoi(fwenv) == 1 &&
+        !std::getenv("SNGB_FLOYD_BLOOM")) {
+        const FwGeom fg = fw_geometry(D);
+        const size_t smem = fg.warp_bytes();
+        auto k = D <= 512 ? k_floyd_warp<4> : k_floyd_warp<8>;
+        cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(k));
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem);
+        if (per_sm < 1) per_sm = 1;
+        if (const char* ev = std::getenv("SNGB_SAMPLER_BPSM"))
+            if (std::atoi(ev) > 0 && std::atoi(ev) < per_sm) per_sm = std::atoi(ev);
+        const uint64_t cap = (uint64_t)num_sms * per_sm;
+        const unsigned grid = a.rows_per_block
+                                  ? (unsigned)((rows + a.rows_per_block - 1) / a.rows_per_block)
+                                  : (unsigned)(rows < cap ? rows : cap);
+        k<<<grid, 32, smem, s>>>(a, fg);
+        note_launch(1);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        uint32_t cap_slots = 1;
+        while (cap_slots < 2 * D + 2) cap_slots <<= 1;
+        e = raise_smem_limit(reinterpret_cast<const void*>(k_replay_list));
+        if (e != cudaSuccess) return e;
+        k_replay_list<<<num_sms * 8, 32, (size_t)cap_slots * 4, s>>>(
+            a, reinterpret_cast<const uint32_t*>(a.scratch64), cap_slots);
         note_launch(1);
         return cudaGetLastError();
     }

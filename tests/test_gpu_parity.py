@@ -738,3 +738,34 @@ def test_fused_floyd_head_equals_two_kernels(monkeypatch, cfg, n):
         if not force:
             assert gf.gather_pairs == g2.gather_pairs == gf.draws * n
             assert gf.pairs_evaluated == g2.pairs_evaluated
+
+
+@pytest.mark.parametrize("cfg,n,head", [(3, 200_000, "1"), (4, 400_000, "1"), (5, 300_000, "1"),
+                                        (5, 300_000, "0"), (2, 120_000, "1")])
+def test_floyd_warp_equals_bloom(monkeypatch, cfg, n, head):
+    """k_floyd_warp (warp per vertex, sngb_floyd_warp.cuh, SNGB_FLOYD_WARP=1) against
+    k_floyd_bloom (SNGB_FLOYD_BLOOM=1) on reduced BASELINE shapes: the same edge list, the same
+    Floyd collisions and replayed vertices; with forced Lemire replays too, and
+    draws <= 512 (cfg2 shape at n = 120 k: D = 700; cfg3: D = 1000)."""
+    import torch
+    w = synthetic.CONFIGS[cfg]
+    x = torch.from_numpy(synthetic.generate(cfg, n=n)).cuda()
+    rate = w.draws / n
+    monkeypatch.setenv("SNGB_FUSED", "0")
+    monkeypatch.setenv("SNGB_HEAD", head)
+    monkeypatch.setenv("SNGB_Q8", "0")
+    for force in (None, "7"):
+        if force:
+            monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
+        monkeypatch.delenv("SNGB_FLOYD_BLOOM", raising=False)
+        monkeypatch.setenv("SNGB_FLOYD_WARP", "1")
+        kw, gw = sng.sampled_edges_device(x, w.eps, rate, w.seed)
+        monkeypatch.delenv("SNGB_FLOYD_WARP", raising=False)
+        monkeypatch.setenv("SNGB_FLOYD_BLOOM", "1")
+        kb, gb = sng.sampled_edges_device(x, w.eps, rate, w.seed)
+        torch.cuda.synchronize()
+        assert torch.equal(kw, kb), (cfg, force)
+        assert gw.collisions == gb.collisions
+        assert gw.irregular_vertices == gb.irregular_vertices
+        if force:
+            assert gw.irregular_vertices >= n // 7

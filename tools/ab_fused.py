@@ -21,14 +21,17 @@ import paper_2006_06743_b200 as sng  # noqa: E402
 from paper_2006_06743_b200 import synthetic  # noqa: E402
 
 cfgs = [int(a) for a in sys.argv[1:]] or [3, 4, 5]
-variants = [("fused", {"SNGB_FUSED": "1"}), ("two_kernels", {"SNGB_FUSED": "0"})]
+variants = [("fused", {"SNGB_FUSED": "1"}), ("two_kernels", {"SNGB_FUSED": "0"}),
+            ("two_kernels_bloom", {"SNGB_FUSED": "0", "SNGB_FLOYD_BLOOM": "1"})]
+if os.environ.get("AB_VARIANTS"):
+    variants = [v for v in variants if v[0] in os.environ["AB_VARIANTS"].split(",")]
 lib = os.path.basename(os.environ.get("SNGB_LIBRARY", "libsngb.so"))
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 for cfg in cfgs:
     w = synthetic.CONFIGS[cfg]
     x = torch.from_numpy(synthetic.generate(cfg)).cuda()
     for name, env in variants:
-        for k in ("SNGB_FUSED",):
+        for k in ("SNGB_FUSED", "SNGB_FLOYD_BLOOM"):
             os.environ.pop(k, None)
         os.environ.update(env)
         for _ in range(2):
