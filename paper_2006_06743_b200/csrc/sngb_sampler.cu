@@ -240,6 +240,9 @@ __global__ void __launch_bounds__(kFloydThreads) k_floyd(const SamplerArgs a) {
 #include "sngb_floyd_bitmap.cuh"
 #include "sngb_floyd_bloom.cuh"
 #include "sngb_floyd_warp.cuh"
+#ifndef SNGB_FW_R
+#define SNGB_FW_R 8  // draw slots per lane per step of k_floyd_warp
+#endif
 
 }  // namespace
 
@@ -324,15 +327,17 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
         note_launch(1);
         return cudaGetLastError();
     }
-    // large n, draws <= 4096: a warp per vertex (k_floyd_warp) with SNGB_FLOYD_WARP=1
-    // (cfg5: 330 ms vs 321 for k_floyd_bloom, profiles/r02_ab_floyd_warp.jsonl);
-    // SNGB_FLOYD_BLOOM=1 forces the block-per-vertex filter kernel
+    // large n, draws <= 1024: a warp per vertex (k_floyd_warp; its shared memory is
+    // small enough for ~30 warps per SM: cfg3 3.9 vs 5.2 ms for k_floyd_bloom); larger
+    // draws keep k_floyd_bloom (cfg4 52 vs 51 ms, cfg5 335 vs 322 ms:
+    // profiles/r02_floyd_warp_r_sweep.jsonl).  SNGB_FLOYD_WARP=0 never, 1 always.
     const char* fwenv = std::getenv("SNGB_FLOYD_WARP");
-    if (D <= 4096 && a.n - 2 < 0xffffffffull && a.scratch64 && fwenv && std::atoi(fwenv) == 1 &&
-        !std::getenv("SNGB_FLOYD_BLOOM")) {
+    const int fwmode = fwenv ? std::atoi(fwenv) : 2;
+    if (D <= 4096 && a.n - 2 < 0xffffffffull && a.scratch64 && !std::getenv("SNGB_FLOYD_BLOOM") &&
+        (fwmode == 1 || (fwmode == 2 && D <= 1024))) {
         const FwGeom fg = fw_geometry(D);
         const size_t smem = fg.warp_bytes();
-        auto k = D <= 512 ? k_floyd_warp<4> : k_floyd_warp<8>;
+        auto k = D <= 1024 ? k_floyd_warp<4> : k_floyd_warp<SNGB_FW_R>;
         cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(k));
         if (e != cudaSuccess) return e;
         int per_sm = 0;
