@@ -496,11 +496,12 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         // dynamic claiming, which a non-persistent gather grid lost); wide-row
         // problems run the sampler beside prepare/plan/quantise instead.
         const uint64_t ov = env_u64("SNGB_OVERLAP", 2);
-        // (with the 4-block Floyd filter kernel, draws > 1024 lost: its blocks then
-        // crowd the gather's -- cfg5 876 vs 646 ms, cfg4 130 vs 96 ms)
+        // (with the 4-block Floyd filter kernel and 32 rows per sampler block, draws >
+        // 1024 lost: its blocks then crowd the gather's -- cfg5 876 vs 646 ms, cfg4 130
+        // vs 96 ms; 8 rows per block win: cfg5 636 vs 656 ms, cfg4 92.5 vs 95.9 ms,
+        // profiles/r02_overlap_rpb_cfg*.jsonl)
         const bool overlap =
-            !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 10000 &&
-                                        draws <= 1024));
+            !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 10000));
         // host upload: the sampler reads no points, so it also runs while they arrive
         const bool side =
             !exhaustive && !fuse_try && (overlap || side_pre || (h_src && attempt == 0));
@@ -545,9 +546,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 // stream while the gather runs here; non-persistent grids let the
                 // block scheduler interleave the two kernels on every SM
                 // non-persistent beside the gather (and during a host upload, where the
-                // gather starts while it runs: cfg5 e2e 614 vs 943 ms persistent)
+                // gather starts while it runs: cfg5 e2e 614 vs 943 ms persistent; 32
+                // rows per block there, 625 vs 639 ms with 8)
                 sa.rows_per_block =
-                    (uint32_t)env_u64("SNGB_SAMPLER_RPB", (overlap || h_src) ? 32 : 0);
+                    (uint32_t)env_u64("SNGB_SAMPLER_RPB",
+                                      h_src ? 32 : (overlap ? (draws > 1024 ? 8 : 32) : 0));
                 if (!(side_pre && attempt == 0)) CK(cudaEventRecord(c.fork, s));
                 CK(cudaStreamWaitEvent(c.side, c.fork, 0));
                 tm.mark_on(E_SIDE0, c.side);

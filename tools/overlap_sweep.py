@@ -21,8 +21,8 @@ KNOBS = ("SNGB_OVERLAP", "SNGB_SAMPLER_RPB", "SNGB_SAMPLER_BPSM", "SNGB_GATHER_B
          "SNGB_FLOYD_WARP", "SNGB_FUSED", "SNGB_GATHER_RPB")
 if os.environ.get("SWEEP") == "rpb":
     SETTINGS = [("sequential_bloom", {"SNGB_OVERLAP": "0"})]
-    for gb in ("4", "3", "2", "1"):
-        for srpb in ("32", "8"):
+    for gb in (os.environ.get("SWEEP_G", "4,3,2,1").split(",")):
+        for srpb in (os.environ.get("SWEEP_RPB", "32,8").split(",")):
             SETTINGS.append((f"overlap_bloom_rpb{srpb}_g{gb}",
                              {"SNGB_OVERLAP": "1", "SNGB_SAMPLER_RPB": srpb, "SNGB_GATHER_BPSM": gb}))
     SETTINGS.append(("overlap_bloom_rpb32_gather_rpb128",
