@@ -58,9 +58,12 @@ inline size_t bloom_smem_bytes(const BloomGeom& g) {
 }
 
 // Exact sequential replay (graph.cpp:163-174) with a u32 open-addressing set
-// in `tab` (cap slots, power of two); every partner becomes an extra.
-__device__ void bloom_replay(uint64_t key, uint64_t u, uint64_t n, uint32_t base, uint32_t* tab,
-                             uint32_t cap, const EdgeSink& xs) {
+// in `tab` (cap slots, power of two); every partner becomes an extra.  Returns
+// the vertex's Floyd collisions (draws replaced by j), so the collision count
+// does not depend on which vertices a kernel replays.
+__device__ unsigned long long bloom_replay(uint64_t key, uint64_t u, uint64_t n, uint32_t base,
+                                           uint32_t* tab, uint32_t cap, const EdgeSink& xs) {
+    unsigned long long ncol = 0;
     for (uint32_t s = 0; s < cap; ++s) tab[s] = kEmpty;
     const uint32_t mask = cap - 1;
     auto insert = [&](uint32_t t) -> bool {
@@ -81,11 +84,13 @@ __device__ void bloom_replay(uint64_t key, uint64_t u, uint64_t n, uint32_t base
         if (!insert(t)) {
             insert((uint32_t)jj);
             e = (uint32_t)jj;
+            ++ncol;
         }
         const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
         if (s2 < xs.capacity)
             xs.keys[s2] = ((unsigned long long)u << 32) | (e + (e >= (uint32_t)u ? 1u : 0u));
     }
+    return ncol;
 }
 
 // Named barriers (bar.sync/arrive with a thread count): the 8 worker warps
@@ -138,6 +143,107 @@ constexpr int kBarReady = 2;    // + parity: lists of a vertex are complete (288
 constexpr int kBarFree = 4;     // + parity: resolver is done with that parity (288)
 constexpr int kBloomBlock = kBloomThreads + 32;
 
+// P3 of one vertex (the resolver warp of k_floyd_bloom / k_floyd_lean /
+// k_floyd_head): the vertex's group list (every draw on a bloom bit hit by >= 2
+// draws) and chain list (parity `par`) become collided draws, whose
+// replacements are emitted as extras; the lists are left empty.
+__device__ __forceinline__ void bloom_resolve_vertex(const SamplerArgs& a, uint64_t u, uint32_t par,
+                                                     unsigned long long* glist, uint32_t* clist,
+                                                     uint32_t (*s_cnt)[2], uint32_t* colbits,
+                                                     unsigned long long* htab, const EdgeSink& xs,
+                                                     int lane, unsigned long long& ncol) {
+    const uint32_t base = a.base;
+    auto emit = [&](uint64_t u, uint32_t e) {  // extra pair (u, partner of value e)
+        const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
+        if (s2 < xs.capacity)
+            xs.keys[s2] = ((unsigned long long)u << 32) | (e + (e >= (uint32_t)u ? 1u : 0u));
+    };
+    unsigned long long* gl = glist + par * kGroupCap;
+    uint32_t* cl = clist + par * kChainCap;
+    uint32_t* cnt = s_cnt[par];
+    const uint32_t ng = cnt[0], nc = cnt[1];
+    if (ng || nc) {
+        // first occurrence per value: (t, min index) in a small hash
+        for (uint32_t p = lane; p < ng; p += 32) {
+            const unsigned long long e = gl[p];
+            const uint32_t t = (uint32_t)(e >> 32);
+            uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
+            for (;;) {
+                const unsigned long long old = atomicCAS(&htab[h], ~0ull, e);
+                if (old == ~0ull) break;
+                if ((uint32_t)(old >> 32) == t) {
+                    atomicMin(&htab[h], e);
+                    break;
+                }
+                h = (h + 1) & (kHashSlots - 1);
+            }
+        }
+        __syncwarp();
+        for (uint32_t p = lane; p < ng; p += 32) {
+            const unsigned long long e = gl[p];
+            const uint32_t t = (uint32_t)(e >> 32), i = (uint32_t)e;
+            uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
+            while ((uint32_t)(htab[h] >> 32) != t) h = (h + 1) & (kHashSlots - 1);
+            if ((uint32_t)htab[h] != i) {  // an earlier draw has the same value
+                atomicOr(&colbits[i >> 5], 1u << (i & 31));
+                emit(u, base + i);
+                ++ncol;
+            }
+        }
+        __syncwarp();  // all lookups done: reset the whole (8 KB) hash
+        for (uint32_t s2 = lane; s2 < kHashSlots; s2 += 32) htab[s2] = ~0ull;
+        __syncwarp();
+        if (lane == 0 && nc) {
+            const uint64_t key = vertex_key(a.seed_mixed, u);
+            for (uint32_t x = 1; x < nc; ++x) {  // insertion sort (tiny list)
+                const uint32_t v = cl[x];
+                uint32_t y = x;
+                while (y > 0 && cl[y - 1] > v) {
+                    cl[y] = cl[y - 1];
+                    --y;
+                }
+                cl[y] = v;
+            }
+            for (uint32_t x = 0; x < nc; ++x) {
+                const uint32_t i = cl[x];
+                if ((colbits[i >> 5] >> (i & 31)) & 1u) continue;  // already collided
+                bool fi;
+                const uint32_t k =
+                    lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fi) - base;
+                if ((colbits[k >> 5] >> (k & 31)) & 1u) {
+                    colbits[i >> 5] |= 1u << (i & 31);
+                    emit(u, base + i);
+                    ++ncol;
+                }
+            }
+        }
+        __syncwarp();
+        for (uint32_t p = lane; p < ng + nc; p += 32) {  // clear the touched words
+            const uint32_t i = p < ng ? (uint32_t)gl[p] : cl[p - ng];
+            colbits[i >> 5] = 0;
+        }
+        __syncwarp();
+        if (lane == 0) cnt[0] = cnt[1] = 0;
+    }
+    __syncwarp();
+}
+
+// P3 loop of the resolver warp, one vertex behind the workers.
+__device__ __forceinline__ void bloom_resolver(const SamplerArgs& a, unsigned long long* glist,
+                                               uint32_t* clist, uint32_t (*s_cnt)[2],
+                                               uint32_t* colbits, unsigned long long* htab,
+                                               const EdgeSink& xs, int lane,
+                                               unsigned long long& ncol) {
+    uint32_t par = 0;
+    for (uint64_t u = a.row_begin + blockIdx.x; u < a.row_end; u += gridDim.x) {
+        par ^= 1u;
+        bar_sync(kBarReady + par, kBloomBlock);
+        bloom_resolve_vertex(a, u, par, glist, clist, s_cnt, colbits, htab, xs, lane, ncol);
+        bar_arrive(kBarFree + par, kBloomBlock);
+    }
+}
+
+
 template <int MAXR>
 // Four resident blocks per SM (<= 56 registers, no spills): the kernel is
 // latency-bound on its shared-memory filter and barriers, and the fourth block
@@ -162,7 +268,7 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_bloom(co
         reinterpret_cast<unsigned long long*>(clist + 2 * kChainCap);  // [kHashSlots]
     __shared__ uint32_t s_cnt[2][2];  // [parity][group, chain]
 
-    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     const bool resolver = tid >= kT;
     const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
     const uint32_t D = a.draws, base = a.base;
@@ -173,88 +279,8 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_bloom(co
     if (tid < 4) (&s_cnt[0][0])[tid] = 0;
     __syncthreads();
 
-    auto emit = [&](uint64_t u, uint32_t e) {  // extra pair (u, partner of value e)
-        const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
-        if (s2 < xs.capacity)
-            xs.keys[s2] = ((unsigned long long)u << 32) | (e + (e >= (uint32_t)u ? 1u : 0u));
-    };
-
     if (resolver) {
-        // ---- P3 (resolver warp), one vertex behind the workers ----
-        uint32_t par = 0;
-        for (uint64_t u = a.row_begin + blockIdx.x; u < a.row_end; u += gridDim.x) {
-            par ^= 1u;
-            bar_sync(kBarReady + par, kBloomBlock);
-            unsigned long long* gl = glist + par * kGroupCap;
-            uint32_t* cl = clist + par * kChainCap;
-            uint32_t* cnt = s_cnt[par];
-            const uint32_t ng = cnt[0], nc = cnt[1];
-            if (ng || nc) {
-                // first occurrence per value: (t, min index) in a small hash
-                for (uint32_t p = lane; p < ng; p += 32) {
-                    const unsigned long long e = gl[p];
-                    const uint32_t t = (uint32_t)(e >> 32);
-                    uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
-                    for (;;) {
-                        const unsigned long long old = atomicCAS(&htab[h], ~0ull, e);
-                        if (old == ~0ull) break;
-                        if ((uint32_t)(old >> 32) == t) {
-                            atomicMin(&htab[h], e);
-                            break;
-                        }
-                        h = (h + 1) & (kHashSlots - 1);
-                    }
-                }
-                __syncwarp();
-                for (uint32_t p = lane; p < ng; p += 32) {
-                    const unsigned long long e = gl[p];
-                    const uint32_t t = (uint32_t)(e >> 32), i = (uint32_t)e;
-                    uint32_t h = (t * 0x85EBCA6Bu) >> (32 - kHashLog2);
-                    while ((uint32_t)(htab[h] >> 32) != t) h = (h + 1) & (kHashSlots - 1);
-                    if ((uint32_t)htab[h] != i) {  // an earlier draw has the same value
-                        atomicOr(&colbits[i >> 5], 1u << (i & 31));
-                        emit(u, base + i);
-                        ++ncol;
-                    }
-                }
-                __syncwarp();  // all lookups done: reset the whole (8 KB) hash
-                for (uint32_t s2 = lane; s2 < kHashSlots; s2 += 32) htab[s2] = ~0ull;
-                __syncwarp();
-                if (lane == 0 && nc) {
-                    const uint64_t key = vertex_key(a.seed_mixed, u);
-                    for (uint32_t x = 1; x < nc; ++x) {  // insertion sort (tiny list)
-                        const uint32_t v = cl[x];
-                        uint32_t y = x;
-                        while (y > 0 && cl[y - 1] > v) {
-                            cl[y] = cl[y - 1];
-                            --y;
-                        }
-                        cl[y] = v;
-                    }
-                    for (uint32_t x = 0; x < nc; ++x) {
-                        const uint32_t i = cl[x];
-                        if ((colbits[i >> 5] >> (i & 31)) & 1u) continue;  // already collided
-                        bool fi;
-                        const uint32_t k =
-                            lemire32(stream_at(key, (uint64_t)i + 1), base + i + 1, fi) - base;
-                        if ((colbits[k >> 5] >> (k & 31)) & 1u) {
-                            colbits[i >> 5] |= 1u << (i & 31);
-                            emit(u, base + i);
-                            ++ncol;
-                        }
-                    }
-                }
-                __syncwarp();
-                for (uint32_t p = lane; p < ng + nc; p += 32) {  // clear the touched words
-                    const uint32_t i = p < ng ? (uint32_t)gl[p] : cl[p - ng];
-                    colbits[i >> 5] = 0;
-                }
-                __syncwarp();
-                if (lane == 0) cnt[0] = cnt[1] = 0;
-            }
-            __syncwarp();
-            bar_arrive(kBarFree + par, kBloomBlock);
-        }
+        bloom_resolver(a, glist, clist, s_cnt, colbits, htab, xs, lane, ncol);
     } else {
         // ---- workers: P1 filter bits + chain candidates, P2 group list ----
         uint32_t par = 0, vcount = 0;
@@ -318,7 +344,7 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_bloom(co
                 bar_sync(kBarWorkers, kT);
                 if (tid == 0) {
                     ++nrep;
-                    bloom_replay(key, u, a.n, base, filt, 4 * WB, xs);
+                    ncol += bloom_replay(key, u, a.n, base, filt, 4 * WB, xs);
                     cnt[0] = cnt[1] = 0;
                 }
                 bar_sync(kBarWorkers, kT);
@@ -369,13 +395,14 @@ __global__ void __launch_bounds__(32) k_replay_list(const SamplerArgs a, const u
     uint32_t* tab = reinterpret_cast<uint32_t*>(smem);
     const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
     const unsigned long long cnt = a.counters[C_IRR_CURSOR];
-    unsigned long long nrep = 0;
+    unsigned long long nrep = 0, ncol = 0;
     for (unsigned long long x = blockIdx.x; x < cnt; x += gridDim.x) {
         if (threadIdx.x == 0) {
             const uint64_t u = list[x];
-            bloom_replay(vertex_key(a.seed_mixed, u), u, a.n, a.base, tab, cap, xs);
+            ncol += bloom_replay(vertex_key(a.seed_mixed, u), u, a.n, a.base, tab, cap, xs);
             ++nrep;
         }
     }
     if (threadIdx.x == 0 && nrep) atomicAdd(&a.counters[C_IRREGULAR], nrep);
+    if (threadIdx.x == 0 && ncol) atomicAdd(&a.counters[C_COLLISIONS], ncol);
 }

@@ -56,6 +56,8 @@ namespace {
 
 #include "sngb_floyd_bloom.cuh"
 #include "sngb_floyd_warp.cuh"
+#include "sngb_floyd_lean.cuh"
+#include "sngb_floyd_head.cuh"
 
 constexpr int kFStage = 64;  // edge staging per warp (accepts are rare here)
 
@@ -320,6 +322,53 @@ cudaError_t fused_kind(const SamplerArgs& sa, const GatherArgs& ga, const HeadAr
     return cudaErrorInvalidValue;
 }
 
+// k_floyd_head (sngb_floyd_head.cuh): block per vertex, draws 1024 < D <= 4096
+template <int KIND, int G, int V>
+cudaError_t fh_one(SamplerArgs a, const GatherArgs& ga, const HeadArgs& h, cudaStream_t s,
+                   int num_sms) {
+    const BloomGeom bg = bloom_geometry(a.draws);
+    a.hash_mask = bg.words;
+    a.key_bits = bg.bits_log2;
+    a.col_words = bg.col_words;
+    const uint32_t scap = (a.draws + 3) & ~3u;  // every draw may survive the head
+    const size_t smem = fh_smem_bytes(bg, scap);
+    auto k = k_floyd_head<KIND, G, V>;
+    // the opt-in maximum, never lowered under a concurrent caller's launch
+    int dev = 0, mx = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFhBlock, smem);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t rows = a.row_end - a.row_begin;
+    const uint64_t cap = (uint64_t)num_sms * per_sm;
+    k<<<(unsigned)(rows < cap ? rows : cap), kFhBlock, smem, s>>>(a, ga, h, scap);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t fh_kind(const SamplerArgs& sa, const GatherArgs& ga, const HeadArgs& h,
+                    cudaStream_t s, int num_sms) {
+    // the testers' row shape: one or two lanes per survivor row, so a warp has
+    // 32-256 rows in flight and reduces with at most one shuffle
+    const uint32_t W = ga.tp.stride / 4;
+    if (W <= 1) return fh_one<KIND, 1, 1>(sa, ga, h, s, num_sms);
+    if (W <= 2) return fh_one<KIND, 1, 2>(sa, ga, h, s, num_sms);
+    if (W <= 4) return fh_one<KIND, 1, 4>(sa, ga, h, s, num_sms);
+    return fh_one<KIND, 2, 4>(sa, ga, h, s, num_sms);
+}
+
+bool fh_eligible(uint32_t draws, uint32_t stride) {
+    const char* e = std::getenv("SNGB_FH");
+    return draws > 1024 && draws <= 4096 && stride / 4 <= 8 && !(e && std::atoi(e) == 0);
+}
+
 }  // namespace
 
 #ifndef SNGB_FUSED_DEFAULT
@@ -352,6 +401,13 @@ cudaError_t launch_floyd_head(const SamplerArgs& in, const GatherArgs& ga, const
                               cudaStream_t s, int num_sms) {
     const uint64_t rows = in.row_end - in.row_begin;
     if (rows == 0 || in.draws == 0) return cudaSuccess;
+    if (fh_eligible(in.draws, ga.tp.stride)) {  // block per vertex, survivors off the workers' path
+        switch (h.kind) {
+            case kHeadU16x2: return fh_kind<kHeadU16x2>(in, ga, h, s, num_sms);
+            case kHeadU8x4: return fh_kind<kHeadU8x4>(in, ga, h, s, num_sms);
+            default: return fh_kind<kHeadU8x2>(in, ga, h, s, num_sms);
+        }
+    }
     if (!ga.work || !in.scratch64) return cudaErrorInvalidValue;  // zeroed counter, scratch
     switch (h.kind) {
         case kHeadU16x2: return fused_kind<kHeadU16x2>(in, ga, h, s, num_sms);

@@ -34,4 +34,15 @@ __device__ __forceinline__ uint32_t head_load(const void* h, uint32_t r) {
     else return __ldg(static_cast<const uint32_t*>(h) + r);
 }
 
+// The same load with a 32-bit row index scaled in one IMAD.WIDE (the plain
+// pointer arithmetic above compiles to a 64-bit add chain when r is a select).
+template <int KIND>
+__device__ __forceinline__ uint32_t head_load32(const void* h, uint32_t r) {
+    const unsigned long long base = reinterpret_cast<unsigned long long>(h);
+    unsigned long long a;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(r), "r"(KIND == kHeadU8x2 ? 2u : 4u), "l"(base));
+    if constexpr (KIND == kHeadU8x2) return __ldg(reinterpret_cast<const unsigned short*>(a));
+    else return __ldg(reinterpret_cast<const uint32_t*>(a));
+}
+
 }  // namespace sngb

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kFloydThreads) k_floyd(const SamplerArgs a) {
 #include "sngb_floyd_bitmap.cuh"
 #include "sngb_floyd_bloom.cuh"
 #include "sngb_floyd_warp.cuh"
+#include "sngb_floyd_lean.cuh"
 #ifndef SNGB_FW_R
 #define SNGB_FW_R 8  // draw slots per lane per step of k_floyd_warp
 #endif
@@ -368,13 +369,23 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
         a.key_bits = bg.bits_log2;
         a.col_words = bg.col_words;
         const size_t smem = bloom_smem_bytes(bg);
-        // draws per worker thread = ceil(D / 256), every slot computed
-        auto k = D <= 768    ? k_floyd_bloom<3>
-                 : D <= 1024 ? k_floyd_bloom<4>
-                 : D <= 2048 ? k_floyd_bloom<8>
-                 : D <= 2560 ? k_floyd_bloom<10>
-                 : D <= 3072 ? k_floyd_bloom<12>
-                             : k_floyd_bloom<16>;
+        // draws per worker thread = ceil(D / 256), every slot computed.  Above
+        // 1024 draws k_floyd_lean (same tables and resolver, ~half the worker
+        // instructions); SNGB_FLOYD_LEAN=0 keeps k_floyd_bloom for A/B runs.
+        const char* lenv = std::getenv("SNGB_FLOYD_LEAN");
+        const bool lean = D > 1024 && !(lenv && std::atoi(lenv) == 0);
+        using KFn = void (*)(const SamplerArgs);
+        static constexpr KFn kLean[12] = {k_floyd_lean<5>,  k_floyd_lean<6>,  k_floyd_lean<7>,
+                                          k_floyd_lean<8>,  k_floyd_lean<9>,  k_floyd_lean<10>,
+                                          k_floyd_lean<11>, k_floyd_lean<12>, k_floyd_lean<13>,
+                                          k_floyd_lean<14>, k_floyd_lean<15>, k_floyd_lean<16>};
+        KFn k = lean ? kLean[(D + kBloomThreads - 1) / kBloomThreads - 5]
+                : D <= 768    ? k_floyd_bloom<3>
+                : D <= 1024   ? k_floyd_bloom<4>
+                : D <= 2048   ? k_floyd_bloom<8>
+                : D <= 2560   ? k_floyd_bloom<10>
+                : D <= 3072   ? k_floyd_bloom<12>
+                              : k_floyd_bloom<16>;
         cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(k));
         if (e != cudaSuccess) return e;
         int per_sm = 0;

@@ -712,17 +712,20 @@ def test_q8_variance_ordered_head(oracle, monkeypatch, host):
     assert got["1"] < 0.6 * got["0"], got
 
 
-@pytest.mark.parametrize("cfg,n", [(3, 200_000), (4, 400_000), (5, 300_000), (4, 1_000_000),
-                                   (5, 2_500_000)])
-def test_fused_floyd_head_equals_two_kernels(monkeypatch, cfg, n):
-    """k_sample_head (Floyd bookkeeping + head gather in one pass, sngb_fused.cu)
-    against the two kernels it replaces, on reduced BASELINE shapes (the bloom
+@pytest.mark.parametrize("cfg,n,fh", [(3, 200_000, "1"), (4, 400_000, "1"), (5, 300_000, "1"),
+                                      (4, 1_000_000, "1"), (5, 2_500_000, "1"), (4, 400_000, "0"),
+                                      (5, 300_000, "0")])
+def test_fused_floyd_head_equals_two_kernels(monkeypatch, cfg, n, fh):
+    """The fused paths (sngb_fused.cu: k_floyd_head, block per vertex, for
+    draws > 1024; k_sample_head, warp per vertex, below that or with SNGB_FH=0)
+    against the two kernels they replace, on reduced BASELINE shapes (the bloom
     regime; the two largest with cfg4/cfg5's chain density): the same edge list,
     collisions and pair counts; also with forced Lemire replays."""
     import torch
     w = synthetic.CONFIGS[cfg]
     x = torch.from_numpy(synthetic.generate(cfg, n=n)).cuda()
     rate = w.draws / n
+    monkeypatch.setenv("SNGB_FH", fh)
     for force in (None, "9"):
         if force:
             monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
@@ -738,6 +741,33 @@ def test_fused_floyd_head_equals_two_kernels(monkeypatch, cfg, n):
         if not force:
             assert gf.gather_pairs == g2.gather_pairs == gf.draws * n
             assert gf.pairs_evaluated == g2.pairs_evaluated
+
+
+@pytest.mark.parametrize("cfg,n", [(4, 400_000), (5, 300_000), (4, 1_000_000), (5, 2_500_000)])
+def test_floyd_lean_equals_bloom(monkeypatch, cfg, n):
+    """k_floyd_lean (sngb_floyd_lean.cuh, the default above 1024 draws) against
+    k_floyd_bloom (SNGB_FLOYD_LEAN=0) on reduced cfg4/cfg5 shapes: the same edge
+    list, Floyd collisions and replayed vertices, with forced Lemire replays too."""
+    import torch
+    w = synthetic.CONFIGS[cfg]
+    x = torch.from_numpy(synthetic.generate(cfg, n=n)).cuda()
+    rate = w.draws / n
+    monkeypatch.setenv("SNGB_FUSED", "0")
+    monkeypatch.setenv("SNGB_FLOYD_WARP", "0")
+    for force in (None, "7"):
+        if force:
+            monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
+        monkeypatch.delenv("SNGB_FLOYD_LEAN", raising=False)
+        kl, gl = sng.sampled_edges_device(x, w.eps, rate, w.seed)
+        monkeypatch.setenv("SNGB_FLOYD_LEAN", "0")
+        kb, gb = sng.sampled_edges_device(x, w.eps, rate, w.seed)
+        torch.cuda.synchronize()
+        assert gl.draws > 1024
+        assert torch.equal(kl, kb), (cfg, force)
+        assert gl.collisions == gb.collisions > 0
+        assert gl.irregular_vertices == gb.irregular_vertices
+        if force:
+            assert gl.irregular_vertices >= n // 7
 
 
 @pytest.mark.parametrize("cfg,n,head", [(3, 200_000, "1"), (4, 400_000, "1"), (5, 300_000, "1"),
