@@ -541,8 +541,11 @@ def main():
                            "integer accept/reject thresholds, fp64 recheck in the band"
                            + ("; exact early reject on the 240-value head, survivors read "
                               "the tail" if q8_split else ""))
-                if q8 else ("exact reject on a 4-byte head (two 16-bit coordinates, L2-resident); "
-                            "survivors: fp32 rows, fp32 guard band, fp64 recheck in the band"
+                if q8 else (("exact reject on a 2-byte head (two 8-bit coordinates, L2-resident); "
+                             if (getattr(info, "head_bytes", 4) or 4) == 2 else
+                             "exact reject on a 4-byte head (two 16-bit or four 8-bit coordinates, "
+                             "L2-resident); ")
+                            + "survivors: fp32 rows, fp32 guard band, fp64 recheck in the band"
                             if head else "fp32 rows, fp32 guard band, fp64 recheck in the band"),
                 "kernel_ms": g_ms,
                 "kernel_ms_in_step": g_ms_overlapped if g_ms_overlapped is not None else g_ms,

@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(kFloydThreads) k_floyd(const SamplerArgs a) {
 #include "sngb_floyd_bloom.cuh"
 #include "sngb_floyd_warp.cuh"
 #include "sngb_floyd_lean.cuh"
+#include "sngb_floyd_pipe.cuh"
 #ifndef SNGB_FW_R
 #define SNGB_FW_R 8  // draw slots per lane per step of k_floyd_warp
 #endif
@@ -379,6 +380,32 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
                                           k_floyd_lean<8>,  k_floyd_lean<9>,  k_floyd_lean<10>,
                                           k_floyd_lean<11>, k_floyd_lean<12>, k_floyd_lean<13>,
                                           k_floyd_lean<14>, k_floyd_lean<15>, k_floyd_lean<16>};
+        // k_floyd_pipe: k_floyd_lean's workers resolve their own group entries,
+        // pipelined over the vertex loop (no resolver warp); SNGB_FLOYD_PIPE=0|1
+        const char* penv = std::getenv("SNGB_FLOYD_PIPE");
+        const bool pipe = D > 1024 && (penv ? std::atoi(penv) != 0 : kPipeDefault);
+        if (pipe) {
+            static constexpr KFn kPipe[12] = {k_floyd_pipe<5>,  k_floyd_pipe<6>,  k_floyd_pipe<7>,
+                                              k_floyd_pipe<8>,  k_floyd_pipe<9>,  k_floyd_pipe<10>,
+                                              k_floyd_pipe<11>, k_floyd_pipe<12>, k_floyd_pipe<13>,
+                                              k_floyd_pipe<14>, k_floyd_pipe<15>, k_floyd_pipe<16>};
+            KFn kp = kPipe[(D + kBloomThreads - 1) / kBloomThreads - 5];
+            const size_t psmem = pipe_smem_bytes(bg);
+            cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(kp));
+            if (e != cudaSuccess) return e;
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, kBloomThreads, psmem);
+            if (per_sm < 1) per_sm = 1;
+            if (const char* ev = std::getenv("SNGB_SAMPLER_BPSM"))
+                if (std::atoi(ev) > 0 && std::atoi(ev) < per_sm) per_sm = std::atoi(ev);
+            const uint64_t cap = (uint64_t)num_sms * per_sm;
+            const unsigned grid = a.rows_per_block
+                                      ? (unsigned)((rows + a.rows_per_block - 1) / a.rows_per_block)
+                                      : (unsigned)(rows < cap ? rows : cap);
+            kp<<<grid, kBloomThreads, psmem, s>>>(a);
+            note_launch(1);
+            return cudaGetLastError();
+        }
         KFn k = lean ? kLean[(D + kBloomThreads - 1) / kBloomThreads - 5]
                 : D <= 768    ? k_floyd_bloom<3>
                 : D <= 1024   ? k_floyd_bloom<4>

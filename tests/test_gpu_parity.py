@@ -770,6 +770,63 @@ def test_floyd_lean_equals_bloom(monkeypatch, cfg, n):
             assert gl.irregular_vertices >= n // 7
 
 
+@pytest.mark.parametrize("cfg,n,draws", [(4, 400_000, None), (5, 300_000, None), (4, 1_000_000, None),
+                                         (5, 2_500_000, None), (5, 300_000, 4096), (5, 300_000, 1025),
+                                         (4, 300_000, 1281), (3, 60_000, 3000)])
+def test_floyd_pipe_equals_bloom(monkeypatch, cfg, n, draws):
+    """k_floyd_pipe (sngb_floyd_pipe.cuh: the workers resolve their own group
+    entries, pipelined over the vertex loop) against k_floyd_bloom on reduced
+    cfg3/cfg4/cfg5 shapes and the draw counts at the ends of its range: the same
+    edge list, Floyd collisions and replayed vertices, with forced Lemire replays
+    and a row range too."""
+    import torch
+    w = synthetic.CONFIGS[cfg]
+    x = torch.from_numpy(synthetic.generate(cfg, n=n)).cuda()
+    rate = (draws or w.draws) / n
+    monkeypatch.setenv("SNGB_FUSED", "0")
+    monkeypatch.setenv("SNGB_FLOYD_WARP", "0")
+    for force, rows in ((None, (0, 0)), ("7", (0, 0)), (None, (n // 3, n // 2 + 5))):
+        if force:
+            monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
+        else:
+            monkeypatch.delenv("SNGB_TEST_FORCE_IRREGULAR", raising=False)
+        monkeypatch.setenv("SNGB_FLOYD_PIPE", "1")
+        kp, gp = sng.sampled_edges_device(x, w.eps, rate, w.seed, rows[0], rows[1])
+        monkeypatch.setenv("SNGB_FLOYD_PIPE", "0")
+        monkeypatch.setenv("SNGB_FLOYD_LEAN", "0")
+        kb, gb = sng.sampled_edges_device(x, w.eps, rate, w.seed, rows[0], rows[1])
+        monkeypatch.delenv("SNGB_FLOYD_LEAN", raising=False)
+        torch.cuda.synchronize()
+        assert gp.draws > 1024
+        assert torch.equal(kp, kb), (cfg, force, rows)
+        assert gp.collisions == gb.collisions > 0
+        assert gp.irregular_vertices == gb.irregular_vertices
+        if force:
+            assert gp.irregular_vertices >= n // 7
+
+
+def test_floyd_pipe_matches_oracle(monkeypatch, oracle):
+    """k_floyd_pipe end to end against the oracle (labels, roles, counters) at
+    1200 draws per vertex, with and without forced Lemire replays."""
+    n = 40_000
+    pts = synthetic.generate(3, n=n)
+    w = synthetic.CONFIGS[3]
+    rate = 0.03
+    monkeypatch.setenv("SNGB_FLOYD_PIPE", "1")
+    monkeypatch.setenv("SNGB_FLOYD_WARP", "0")
+    monkeypatch.setenv("SNGB_FUSED", "0")
+    labels, roles, oinfo, _ = oracle.sng_dbscan(pts, w.eps, w.min_pts, rate, w.seed)
+    for force in (None, "5"):
+        if force:
+            monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
+        info = sng.ClusterRunInfo()
+        c = sng.sng_dbscan(sng.Dataset(pts), sng.SngParams(eps=w.eps, min_pts=w.min_pts, rate=rate,
+                                                           seed=w.seed, device=0), info)
+        assert np.array_equal(c.assignment, labels) and np.array_equal(c.role, roles)
+        assert info.edges == oinfo["edges"] and info.distance_evals == oinfo["distance_evals"]
+        assert info.gpu["draws"] == 1200 and info.gpu["collisions"] > 0
+
+
 @pytest.mark.parametrize("cfg,n,head", [(3, 200_000, "1"), (4, 400_000, "1"), (5, 300_000, "1"),
                                         (5, 300_000, "0"), (2, 120_000, "1")])
 def test_floyd_warp_equals_bloom(monkeypatch, cfg, n, head):
