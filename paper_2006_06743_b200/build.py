@@ -28,8 +28,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["sngb_api.cu", "sngb_kernels.cu", "sngb_quant.cu", "sngb_metric.cu", "sngb_head.cu", "sngb_sampler.cu",
            "sngb_cluster.cu", "sngb_multi.cu", "sngb_fused.cu"]
 HEADERS = ["sngb_internal.cuh", "sngb_host.cuh", "sngb_rng.cuh", "sngb_device.cuh", "sngb_epstest.cuh",
-           "sngb_floyd_bitmap.cuh", "sngb_floyd_bloom.cuh", "sngb_floyd_warp.cuh", "sngb_floyd_lean.cuh", "sngb_floyd_pipe.cuh", "sngb_floyd_head.cuh",
-           "sngb_head.cuh"]
+           "sngb_floyd_bitmap.cuh", "sngb_floyd_bloom.cuh", "sngb_floyd_warp.cuh", "sngb_floyd_lean.cuh", "sngb_floyd_pipe.cuh", "sngb_floyd_headpipe.cuh", "sngb_floyd_head.cuh",
+           "sngb_head.cuh", "sngb_gather_head.cuh"]
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -548,9 +548,12 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 // non-persistent beside the gather (and during a host upload, where the
                 // gather starts while it runs: cfg5 e2e 614 vs 943 ms persistent; 32
                 // rows per block there, 625 vs 639 ms with 8)
-                sa.rows_per_block =
-                    (uint32_t)env_u64("SNGB_SAMPLER_RPB",
-                                      h_src ? 32 : (overlap ? (draws > 1024 ? 8 : 32) : 0));
+                // (k_floyd_pipe: 64 rows per block, two drain steps each; cfg5 602 vs
+                // 609 ms with 8, 630 ms persistent)
+                sa.rows_per_block = (uint32_t)env_u64(
+                    "SNGB_SAMPLER_RPB", sampler_uses_pipe(n, (uint32_t)draws)
+                                            ? 64
+                                            : (h_src ? 32 : (overlap ? (draws > 1024 ? 8 : 32) : 0)));
                 if (!(side_pre && attempt == 0)) CK(cudaEventRecord(c.fork, s));
                 CK(cudaStreamWaitEvent(c.side, c.fork, 0));
                 tm.mark_on(E_SIDE0, c.side);
@@ -559,6 +562,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 tm.side = true;
                 CK(cudaEventRecord(c.join, c.side));
             } else {
+                if (sampler_uses_pipe(n, (uint32_t)draws))
+                    sa.rows_per_block = (uint32_t)env_u64("SNGB_SAMPLER_RPB", 64);
                 CK(launch_sampler(sa, s, c.num_sms));
             }
         }
@@ -760,6 +765,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 ga.part_hi = (uint32_t)n;
                 ga.partners = nullptr;
                 ga.work = c.work.as<unsigned long long>() + work_slot++;
+                ++work_slot;  // k_duo's Floyd chunk counter (ga.work + 1)
                 CK(launch_floyd_head(make_sa(), ga, hp.args, gs, c.num_sms));
             } else {
                 for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));

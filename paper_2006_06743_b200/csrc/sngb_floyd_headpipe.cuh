@@ -1,64 +1,54 @@
-// sngb_floyd_pipe.cuh -- k_floyd_pipe: k_floyd_lean's Floyd bookkeeping with the
-// exact resolution done by the worker warps themselves, software-pipelined over
-// the vertex loop (large n, 1024 < draws <= 4096: cfg4, cfg5).  Included by
-// sngb_sampler.cu after sngb_floyd_bloom.cuh and sngb_floyd_lean.cuh.
+// sngb_floyd_headpipe.cuh -- k_floyd_headpipe: k_floyd_pipe's Floyd bookkeeping and
+// the head-filter gather (sngb_head.cu) in one block-per-vertex kernel, each draw
+// generated once (large n, 1024 < draws <= 4096, rows of <= 8 float4: cfg4, cfg5).
+// Included by sngb_fused.cu after sngb_floyd_pipe.cuh.
 //
-// Why.  ncu on k_floyd_lean (cfg5, profiles/r02_ncu_floyd_lean_src_cfg5.md): a
-// third of all warp samples sit at the top-of-vertex barrier waiting for the
-// resolver warp, which is busy all the time -- one warp walks each vertex's
-// ~240 group entries (6 % of the draws share a filter bit at B = 16) through a
-// CAS hash at ~17 cycles per dependent instruction, 9 us per vertex.  The
-// resolution is tiny but serial.  Here the 256 threads that found the entries
-// resolve them, one or two entries per thread, and the three steps of a
-// vertex's resolution ride on the barriers the next two vertices need anyway:
+// Why.  As two kernels, k_floyd_pipe (2.8 warp-instructions per draw) and
+// k_gather_head (2.9) each regenerate every draw
+//   t_i = Lemire(mix(key + (i+1) gamma), base + i + 1)   (rng.hpp:26,35-48)
+// and, run side by side (k_duo), they queue on the same in-order L1TEX pipe and
+// lose.  k_floyd_head fused them around a resolver warp and tester warps and was
+// bound by those consumers' serial latency (46 % issue).  Here the eight worker
+// warps of k_floyd_pipe do everything themselves:
 //
-//   step s (vertex s of this block, parity s & 1), all 256 threads:
-//     C  vertex s-2: empty the hash slots it used; thread 0 settles its chain
-//        candidates (t_i in [base, base + i): graph.cpp:168 may meet an earlier
-//        replacement j_k) against its collided bitmap, in index order
-//     A  vertex s-1: insert my group entries (t, i) into its first-occurrence
-//        hash (minimum index per value)
-//     P1 vertex s: draws, filter bits, running tests        (k_floyd_lean)
-//     -- barrier (with the OR of the threads' Lemire pre-condition) --
-//     B  vertex s-1: look my entries up: an entry whose index is not the
-//        minimum of its value collided (graph.cpp:168-170): its replacement j_i
-//        becomes an extra, its bit goes to the collided bitmap
-//     P2 vertex s: draws on a shared bit -> my warp's segment of the group
-//        list, by ballot + popc (no atomics, no divergent push); chain
-//        candidates -> the chain list
-//     -- barrier --
+//   P1(s)  as k_floyd_pipe, plus the partner's head load (p = t + (t >= u),
+//          graph.cpp:172-173), issued here and consumed in P2 so its L2 latency
+//          hides behind the rest of P1;
+//   P2(s)  as k_floyd_pipe, plus the exact head reject (sngb_head.cu): survivors'
+//          partners -> the warp's own queue (ballot + popc);
+//   T(s)   each warp tests the survivors it found on their fp32 rows (G lanes per
+//          row, UF rows per group in flight, evict-first loads): the same
+//          decision code as k_gather_head (sngb_epstest.cuh: accept, reject, or
+//          the band list for k_band), edges through the warp's stage;
+//   A/B/C  the group entries' exact resolution, pipelined as in k_floyd_pipe.
 //
-// so a vertex costs two block barriers and no producer/consumer hand-off; the
-// block is 8 worker warps (no resolver warp).  Lists, hashes and bitmaps are
-// double-buffered by parity; two drain steps finish the last two vertices.
-// List overflow and the Lemire reject pre-condition replay the vertex exactly
-// (bloom_replay), as in k_floyd_lean.  Results equal k_floyd_bloom's bit for
-// bit (tests/test_gpu_parity.py -k floyd_pipe).
+// A vertex whose stream meets the Lemire reject pre-condition (or the test hook)
+// is replayed exactly by one thread (bloom_replay: every partner an extra) and
+// skips its head tests; its gather-pair count is the draws before the first
+// fired one, as k_gather_head counts them.  Results equal the two-kernel path
+// bit for bit (tests/test_gpu_parity.py -k headpipe).
 #pragma once
 
-constexpr int kPipeSeg = 64;          // group entries per warp and vertex
-constexpr int kPipeHashLog2 = 9;
-constexpr int kPipeSlots = 1 << kPipeHashLog2;
-constexpr uint32_t kPipeMaxGroup = 384;  // entries per vertex the 512-slot hash takes
-constexpr uint32_t kPipeNone = 0xffffffffu;
+#ifndef SNGB_FHP_UF
+#define SNGB_FHP_UF 4
+#endif
+constexpr int kFhpQueue = 32 * 16;  // survivors per warp and vertex: every draw may survive
+constexpr int kFhpStage = 64;       // edge staging per warp
 
-inline size_t pipe_smem_bytes(const BloomGeom& g) {
-    return 4ull * g.words * 4                          // filter + shared-bit filter, x2 parity
-           + 2ull * g.col_words * 4                    // collided bitmaps, x2 parity
-           + 2ull * (kBloomThreads / 32) * kPipeSeg * 8  // group segments, x2 parity
-           + 2ull * kChainCap * 4                      // chain lists, x2 parity
-           + 2ull * kPipeSlots * 8;                    // first-occurrence hashes, x2 parity
+inline size_t fhp_smem_bytes(const BloomGeom& g) {
+    return pipe_smem_bytes(g) + (size_t)(kBloomThreads / 32) * (kFhpQueue * 4 + kFhpStage * 8);
 }
 
-// The vertices first, first + stride, ... (nv of them) of one block; `smem` is
-// pipe_smem_bytes() of dynamic shared memory.  Called once per block by
-// k_floyd_pipe and once per claimed chunk by k_duo (sngb_fused.cu).
-template <int MAXR>
-__device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned char* smem,
-                                               const uint64_t first, const uint64_t stride,
-                                               const uint32_t nv) {
+template <int KIND, int G, int MAXR>
+__device__ __forceinline__ void floyd_headpipe_run(const SamplerArgs& a, const GatherArgs& g,
+                                                   const HeadArgs& hd, unsigned char* smem,
+                                                   const uint64_t first, const uint64_t stride,
+                                                   const uint32_t nv) {
     constexpr int kT = kBloomThreads;
     constexpr int kW = kT / 32;
+    constexpr int NG = 32 / G;
+    constexpr int UF = SNGB_FHP_UF;  // fp32 rows per G-lane group per survivor step
+    constexpr int STEP = NG * UF;
     const uint32_t WB = a.hash_mask;  // filter words (2^B / 32)
     const uint32_t W = a.col_words;
     uint32_t* filt = reinterpret_cast<uint32_t*>(smem);          // [2][WB]
@@ -69,6 +59,10 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
     uint32_t* clist = reinterpret_cast<uint32_t*>(glist + 2 * kW * kPipeSeg);  // [2][kChainCap]
     unsigned long long* htab =
         reinterpret_cast<unsigned long long*>(clist + 2 * kChainCap);  // [2][kPipeSlots]
+    uint32_t* squeue = reinterpret_cast<uint32_t*>(htab + 2 * kPipeSlots);  // [kW][kFhpQueue]
+    unsigned long long* stages =
+        reinterpret_cast<unsigned long long*>(squeue + kW * kFhpQueue);  // [kW][kFhpStage]
+    __shared__ uint32_t s_lim;  // first fired draw of a vertex being replayed
     __shared__ uint32_t s_wc[2][kW];  // [parity][warp] group entries
     __shared__ uint32_t s_ng[2];      // [parity] group entries of the vertex
     __shared__ uint32_t s_cc[2];      // [parity] chain candidates
@@ -77,7 +71,17 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const EdgeSink xs{a.extras, a.extras_capacity, &a.counters[C_EXTRA_CURSOR], 0};
     const uint32_t D = a.draws, base = a.base;
-    unsigned long long ncol = 0, nrep = 0;
+    unsigned long long ncol = 0, nrep = 0, gpairs = 0, tails = 0;
+    const void* __restrict__ H = hd.head;
+    const float reject = hd.reject;
+    const float4* __restrict__ P = reinterpret_cast<const float4*>(g.tp.pts);
+    const uint32_t RW = g.tp.stride / 4;
+    const int q = lane % G, grp = lane / G;
+    const bool leader = q == 0;
+    const uint64_t pol = evict_first_policy();  // survivor rows must not evict the heads
+    uint32_t* myq = squeue + warp * kFhpQueue;
+    WarpStage<kFhpStage> stage{stages + warp * kFhpStage, 0};
+    TestStats st;
     auto emit = [&](uint64_t u, uint32_t e) {  // extra pair (u, partner of value e)
         const unsigned long long s2 = atomicAdd(xs.cursor, 1ull);
         if (s2 < xs.capacity)
@@ -88,6 +92,7 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
     for (uint32_t s = tid; s < 2 * kPipeSlots; s += kT) htab[s] = ~0ull;
     if (tid < 2 * kW) (&s_wc[0][0])[tid] = 0;
     if (tid < 2) s_ng[tid] = s_cc[tid] = s_ovf[tid] = 0;
+    if (tid == 0) s_lim = D;
     __syncthreads();
 
     const uint64_t dz = (uint64_t)kT * kGamma;  // counter step between a thread's draws
@@ -172,11 +177,12 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
         __syncwarp();  // reconverge after the divergent probe loops (else P1 runs per fragment)
 
         // ---- P1: vertex s ----
-        uint32_t tr[MAXR];
+        uint32_t tr[MAXR], hb[MAXR];
         uint32_t tmax = 0;
         bool fired = false;
         uint64_t key = 0;
-        uint32_t sa = 0;
+        uint32_t sa = 0, hq = 0;
+        const uint32_t u32 = (uint32_t)u;
         if (has_v) {
             {  // clear the other parity's filters (last used by vertex s - 1)
                 uint4* fo = reinterpret_cast<uint4*>(filt + (par ^ 1u) * WB);
@@ -192,11 +198,15 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
             const uint32_t fa = smem_addr(filt + par * WB);
             sa = smem_addr(shared_bits + par * WB);
             uint32_t smin = 0xffffffffu;
+            hq = head_load<KIND>(H, u32);
 #pragma unroll
             for (int r = 0; r < MAXR; ++r) {
                 uint32_t slo;
                 const uint32_t t = lemire32_slo(mix(z0 + (uint64_t)r * dz), b0 + kT * r, slo);
                 tr[r] = t;
+                // the partner's head (partner p = t + (t >= u), graph.cpp:172-173): issued
+                // here, consumed in P2, so its L2 latency hides behind the rest of P1
+                hb[r] = head_load32<KIND>(H, (r < MAXR - 1 || in_tail) ? t + (t >= u32 ? 1u : 0u) : u32);
                 if (r < MAXR - 1 || in_tail) {
                     smin = min(smin, slo);
                     tmax = max(tmax, t);
@@ -204,15 +214,18 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
                     red_or_sh(sa + off, atom_or_sh(fa + off, bit) & bit);
                 }
             }
-            fired = hook_thread && (u % a.force_mod) == 0;
+            uint32_t first_fire = hook_thread && (u % a.force_mod) == 0 ? D / 2 : D;
             if (smin == 0u) {  // rare (2^-32 per draw): the exact pre-condition, lo < bound
 #pragma unroll 1
                 for (int r = 0; r < MAXR; ++r) {
                     bool fi;
                     lemire32(mix(z0 + (uint64_t)r * dz), b0 + kT * r, fi);
-                    fired |= fi && (r < MAXR - 1 || in_tail);
+                    const uint32_t i = (uint32_t)tid + kT * r;
+                    if (fi && (r < MAXR - 1 || in_tail) && i < first_fire) first_fire = i;
                 }
             }
+            fired = first_fire < D;
+            if (fired) atomicMin(&s_lim, first_fire);
         }
         const bool any_fired = __syncthreads_or(fired);
 
@@ -246,12 +259,16 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
 
         // exact sequential replay of vertex s (rare); the filter memory (4 * WB >=
         // 4 * draws words) serves as its hash set, then is re-zeroed; its lists stay empty
-        auto replay = [&]() {
+        auto replay = [&](bool fired_vertex) {
             __syncthreads();
             if (tid == 0) {
                 ++nrep;
                 ncol += bloom_replay(key, u, a.n, base, filt, 4 * WB, xs);
                 s_cc[par] = s_ovf[par] = 0;
+                if (fired_vertex) {  // the head tests stop at the first fired draw
+                    gpairs += s_lim;  // (k_gather_head's limit); every partner is an extra
+                    s_lim = D;
+                }
             }
             if (tid < kW) s_wc[par][tid] = 0;
             __syncthreads();
@@ -260,22 +277,29 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
 
         if (has_v) {
             if (any_fired) {
-                replay();
+                replay(true);
             } else {
                 // ---- P2: vertex s ----
                 unsigned long long* wl = glist + (par * kW + warp) * kPipeSeg;
-                uint32_t wpos = 0;
+                uint32_t wpos = 0, qn = 0;
 #pragma unroll
                 for (int r = 0; r < MAXR; ++r) {
                     const uint32_t t = tr[r];
+                    const bool valid = r < MAXR - 1 || in_tail;
                     const uint32_t off = (t >> 3) & wmask, bit = 1u << (t & 31);
-                    const bool hit = (ld_sh(sa + off) & bit) && (r < MAXR - 1 || in_tail);
+                    const bool hit = (ld_sh(sa + off) & bit) && valid;
                     const uint32_t m = __ballot_sync(kFull, hit);
                     const uint32_t pos = wpos + __popc(m & lt);
                     if (hit && pos < kPipeSeg)
                         wl[pos] = ((unsigned long long)t << 32) | ((uint32_t)tid + kT * r);
                     wpos += __popc(m);
+                    // the exact head reject (sngb_head.cu); survivors -> my warp's queue
+                    const bool keep = valid && !(head_q<KIND>(hq, hb[r]) > reject);
+                    const uint32_t km = __ballot_sync(kFull, keep);
+                    if (keep) myq[qn + __popc(km & lt)] = t + (t >= u32 ? 1u : 0u);
+                    qn += __popc(km);
                 }
+                if (tid == 0) gpairs += D;
                 if (lane == 0) {
                     s_wc[par][warp] = wpos < kPipeSeg ? wpos : kPipeSeg;
                     if (wpos > kPipeSeg) s_ovf[par] = 1;
@@ -293,14 +317,52 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
                         }
                     }
                 }
+                // ---- T: vertex s: my warp's survivors take the fp32 test on their rows
+                // (G lanes per row, UF rows per group in flight; sngb_epstest.cuh decides) ----
+                __syncwarp();
+                if (qn) {
+                    const uint32_t c = (uint32_t)q < RW ? (uint32_t)q : RW - 1;
+                    const F4x2 qv = to_x2(ldg_row(P + u * RW + c));
+                    for (uint32_t e0 = 0; e0 < qn; e0 += STEP) {
+                        F4x2 rows[UF];
+                        uint32_t pe[UF];
+                        bool oke[UF];
+#pragma unroll
+                        for (int uu = 0; uu < UF; ++uu) {
+                            const uint32_t e = e0 + grp + NG * uu;
+                            oke[uu] = e < qn;
+                            pe[uu] = myq[oke[uu] ? e : e0];
+                            const uint64_t row = (oke[uu] && (uint32_t)q < RW) ? pe[uu] : u;
+                            rows[uu] = ldg_row2_ef(P + row * RW + c, pol);
+                        }
+                        __syncwarp();  // scheduling fence: all UF loads in flight together
+#pragma unroll
+                        for (int uu = 0; uu < UF; ++uu) {
+                            Acc2 acc;
+                            diff2x2(qv, rows[uu], acc);
+                            float sum = acc2_sum(acc);
+#pragma unroll
+                            for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+                            const bool accd = decide(sum, oke[uu], leader, grp * G, g.tp, u, pe[uu], st);
+                            tails += (oke[uu] && leader) ? 1u : 0u;
+                            stage.push(leader && accd, edge_key(u, pe[uu], g.sink.nb), g.sink, lane);
+                        }
+                    }
+                    __syncwarp();
+                }
             }
         }
         __syncthreads();
         if (has_v && !any_fired && s_ovf[par]) {  // list overflow: exact replay
-            replay();
+            replay(false);  // the survivors were tested: every draw took the head test
             __syncthreads();
         }
     }
+    stage.flush(g.sink, lane);
+    st.pairs = gpairs;
+    flush_stats(st, gpairs, g.counters, lane);
+    tails = warp_sum(tails);
+    if (lane == 0 && tails) atomicAdd(&g.counters[C_TAIL_PAIRS], tails);
     ncol = warp_sum(ncol);
     nrep = warp_sum(nrep);
     if (lane == 0) {
@@ -309,11 +371,20 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
     }
 }
 
-template <int MAXR>
-__global__ void __launch_bounds__(kBloomThreads, 4) k_floyd_pipe(const SamplerArgs a) {
+
+template <int KIND, int G, int MAXR>
+__global__ void __launch_bounds__(kBloomThreads, 3)
+    k_floyd_headpipe(const SamplerArgs a, const GatherArgs g, const HeadArgs hd, uint32_t grab) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const uint64_t first = a.row_begin + blockIdx.x;
-    const uint32_t nv =
-        first < a.row_end ? (uint32_t)((a.row_end - first + gridDim.x - 1) / gridDim.x) : 0u;
-    floyd_pipe_run<MAXR>(a, smem, first, gridDim.x, nv);
+    __shared__ unsigned long long s_c0;
+    const uint64_t rows = a.row_end - a.row_begin;
+    for (;;) {  // chunks of `grab` consecutive vertices, claimed from g.work (zeroed)
+        if (threadIdx.x == 0) s_c0 = atomicAdd(g.work, (unsigned long long)grab);
+        __syncthreads();
+        const unsigned long long c0 = s_c0;
+        __syncthreads();
+        if (c0 >= rows) break;
+        const uint32_t nv = (uint32_t)(rows - c0 < grab ? rows - c0 : grab);
+        floyd_headpipe_run<KIND, G, MAXR>(a, g, hd, smem, a.row_begin + c0, 1, nv);
+    }
 }

@@ -40,6 +40,7 @@
 #include "sngb_device.cuh"
 #include "sngb_epstest.cuh"
 #include "sngb_head.cuh"
+#include "sngb_gather_head.cuh"
 #include "sngb_internal.cuh"
 #include "sngb_rng.cuh"
 
@@ -58,6 +59,8 @@ namespace {
 #include "sngb_floyd_warp.cuh"
 #include "sngb_floyd_lean.cuh"
 #include "sngb_floyd_head.cuh"
+#include "sngb_floyd_pipe.cuh"
+#include "sngb_floyd_headpipe.cuh"
 
 constexpr int kFStage = 64;  // edge staging per warp (accepts are rare here)
 
@@ -364,6 +367,132 @@ cudaError_t fh_kind(const SamplerArgs& sa, const GatherArgs& ga, const HeadArgs&
     return fh_one<KIND, 2, 4>(sa, ga, h, s, num_sms);
 }
 
+// ---- k_duo: the Floyd bookkeeping (floyd_pipe_run) and the head gather
+// (gather_head_body) as two roles of ONE launch, so both are resident on every
+// SM for the whole step.  As two launches the gather's persistent blocks fill
+// the register file and the sampler only runs in its drain; yet the two bodies
+// lean on different units -- the gather on the L1TEX tag stage (one random head
+// per SM-cycle, issue 63 %), the Floyd workers on the issue slots and the
+// shared-memory data stage -- so side by side they overlap.  Blocks start in
+// the role their index picks (half and half per SM under breadth-first block
+// placement), claim work dynamically (gather: ga.work rows; Floyd: fwork chunks
+// of fgrab consecutive vertices) and switch role when their queue is empty.
+// Every draw is still generated twice; the results are those of the two kernels.
+template <int KIND, int G, int V, int R, int MAXR>
+__global__ void __launch_bounds__(kBloomThreads, 4)
+    k_duo(const SamplerArgs sa, const GatherArgs ga, const HeadArgs h, unsigned long long* fwork,
+          uint32_t fgrab, uint32_t split) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned long long s_c0;
+    const bool floyd_first = split ? ((blockIdx.x / split) & 1u) != 0 : (blockIdx.x & 1u) != 0;
+    const uint64_t rows = sa.row_end - sa.row_begin;
+    for (int pass = 0; pass < 2; ++pass) {
+        if ((pass == 0) == floyd_first) {
+            for (;;) {
+                if (threadIdx.x == 0) s_c0 = atomicAdd(fwork, (unsigned long long)fgrab);
+                __syncthreads();
+                const unsigned long long c0 = s_c0;
+                __syncthreads();
+                if (c0 >= rows) break;
+                const uint32_t nv = (uint32_t)(rows - c0 < fgrab ? rows - c0 : fgrab);
+                floyd_pipe_run<MAXR>(sa, smem, sa.row_begin + c0, 1, nv);
+            }
+        } else {
+            unsigned long long* stage_mem = reinterpret_cast<unsigned long long*>(smem);
+            uint32_t* queue_mem =
+                reinterpret_cast<uint32_t*>(smem + (size_t)kWarpsPerBlock * kStage * 8);
+            gather_head_body<KIND, G, V, R>(ga, h, stage_mem, queue_mem);
+        }
+        __syncthreads();
+    }
+}
+
+template <int KIND, int G, int MAXR>
+cudaError_t duo_one(SamplerArgs a, GatherArgs ga, const HeadArgs& h, cudaStream_t s, int num_sms) {
+    constexpr int R = SNGB_HEAD_R;
+    const BloomGeom bg = bloom_geometry(a.draws);
+    a.hash_mask = bg.words;
+    a.key_bits = bg.bits_log2;
+    a.col_words = bg.col_words;
+    const size_t gsmem = (size_t)kWarpsPerBlock * (kStage * 8 + gather_head_qcap<G, R>() * 4);
+    const size_t smem = std::max(pipe_smem_bytes(bg), gsmem);
+    auto k = k_duo<KIND, G, 1, R, MAXR>;
+    int dev = 0, mx = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBloomThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t rows = a.row_end - a.row_begin;
+    // gather: ~16 claims per resident warp, at most 32 rows per claim (as launch_gather_head's caller)
+    const uint64_t warps = (uint64_t)num_sms * 64;
+    ga.grab = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, rows / (warps * 16)));
+    const char* ge = std::getenv("SNGB_DUO_GRAB");
+    const uint32_t fgrab = ge && std::atoi(ge) > 0 ? (uint32_t)std::atoi(ge) : 64u;
+    const char* se = std::getenv("SNGB_DUO_SPLIT");  // 0: roles alternate by block index
+    const uint32_t split = se ? (uint32_t)std::atoi(se) : (uint32_t)num_sms;
+    k<<<(unsigned)(num_sms * per_sm), kBloomThreads, smem, s>>>(a, ga, h, ga.work + 1, fgrab, split);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
+// the shapes instantiated: cfg4's (16-byte rows, 2500 draws) and cfg5's (128-byte
+// rows, 4000 draws); others keep the two kernels
+bool duo_shape(uint32_t draws, uint32_t stride) {
+    const uint32_t W = stride / 4, maxr = (draws + kBloomThreads - 1) / kBloomThreads;
+    return (W <= 2 && maxr == 10) || (W > 4 && W <= 8 && maxr == 16);
+}
+
+template <int KIND>
+cudaError_t duo_kind(const SamplerArgs& sa, const GatherArgs& ga, const HeadArgs& h,
+                     cudaStream_t s, int num_sms) {
+    if (ga.tp.stride / 4 <= 2) return duo_one<KIND, 2, 10>(sa, ga, h, s, num_sms);
+    return duo_one<KIND, 8, 16>(sa, ga, h, s, num_sms);
+}
+
+// k_floyd_headpipe (sngb_floyd_headpipe.cuh): the workers of k_floyd_pipe also take
+// the head test and the survivors' fp32 test; one RNG pass
+template <int KIND, int G, int MAXR>
+cudaError_t fhp_one(SamplerArgs a, const GatherArgs& ga, const HeadArgs& h, cudaStream_t s,
+                    int num_sms) {
+    const BloomGeom bg = bloom_geometry(a.draws);
+    a.hash_mask = bg.words;
+    a.key_bits = bg.bits_log2;
+    a.col_words = bg.col_words;
+    const size_t smem = fhp_smem_bytes(bg);
+    auto k = k_floyd_headpipe<KIND, G, MAXR>;
+    int dev = 0, mx = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBloomThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const char* ge = std::getenv("SNGB_FHP_GRAB");
+    const uint32_t grab = ge && std::atoi(ge) > 0 ? (uint32_t)std::atoi(ge) : 64u;
+    const uint64_t rows = a.row_end - a.row_begin;
+    const uint64_t want = (rows + grab - 1) / grab, cap = (uint64_t)num_sms * per_sm;
+    k<<<(unsigned)(want < cap ? want : cap), kBloomThreads, smem, s>>>(a, ga, h, grab);
+    note_launch(1);
+    return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t fhp_kind(const SamplerArgs& sa, const GatherArgs& ga, const HeadArgs& h,
+                     cudaStream_t s, int num_sms) {
+    if (ga.tp.stride / 4 <= 2) return fhp_one<KIND, 2, 10>(sa, ga, h, s, num_sms);
+    return fhp_one<KIND, 8, 16>(sa, ga, h, s, num_sms);
+}
+
 bool fh_eligible(uint32_t draws, uint32_t stride) {
     const char* e = std::getenv("SNGB_FH");
     return draws > 1024 && draws <= 4096 && stride / 4 <= 8 && !(e && std::atoi(e) == 0);
@@ -387,6 +516,8 @@ bool fused_eligible(uint64_t n, uint32_t draws, uint32_t stride) {
     if (mode == 0 || draws < 1 || draws > 4096 || n - 2 >= 0xffffffffull || stride / 4 > 32)
         return false;
     if (mode == 2 && (uint64_t)draws * draws > 8 * n) return false;
+    if ((mode == 3 || mode == 4) && !duo_shape(draws, stride))
+        return false;  // k_duo / k_floyd_headpipe: two shapes instantiated
     const uint64_t bm_words = (((n - 1) + 31) / 32 + 3) & ~3ull;
     return bm_words * 4 > 9216 || std::getenv("SNGB_FLOYD_NO_BITMAP") != nullptr;
 }
@@ -401,6 +532,25 @@ cudaError_t launch_floyd_head(const SamplerArgs& in, const GatherArgs& ga, const
                               cudaStream_t s, int num_sms) {
     const uint64_t rows = in.row_end - in.row_begin;
     if (rows == 0 || in.draws == 0) return cudaSuccess;
+    {
+        const char* fe = std::getenv("SNGB_FUSED");
+        if ((fe ? std::atoi(fe) : kFusedDefault) == 4) {  // one RNG pass, the workers do it all
+            if (!ga.work || !duo_shape(in.draws, ga.tp.stride)) return cudaErrorInvalidValue;
+            switch (h.kind) {
+                case kHeadU16x2: return fhp_kind<kHeadU16x2>(in, ga, h, s, num_sms);
+                case kHeadU8x4: return fhp_kind<kHeadU8x4>(in, ga, h, s, num_sms);
+                default: return fhp_kind<kHeadU8x2>(in, ga, h, s, num_sms);
+            }
+        }
+        if ((fe ? std::atoi(fe) : kFusedDefault) == 3) {  // the two kernels as roles of one launch
+            if (!ga.work || !duo_shape(in.draws, ga.tp.stride)) return cudaErrorInvalidValue;
+            switch (h.kind) {
+                case kHeadU16x2: return duo_kind<kHeadU16x2>(in, ga, h, s, num_sms);
+                case kHeadU8x4: return duo_kind<kHeadU8x4>(in, ga, h, s, num_sms);
+                default: return duo_kind<kHeadU8x2>(in, ga, h, s, num_sms);
+            }
+        }
+    }
     if (fh_eligible(in.draws, ga.tp.stride)) {  // block per vertex, survivors off the workers' path
         switch (h.kind) {
             case kHeadU16x2: return fh_kind<kHeadU16x2>(in, ga, h, s, num_sms);

@@ -188,6 +188,8 @@ __host__ __device__ __forceinline__ float ordered_value(uint32_t k) {
 void floyd_geometry(uint32_t draws, uint32_t& slots, uint32_t& col_words);
 size_t floyd_scratch_bytes(uint32_t draws, int num_sms, uint64_t rows);
 cudaError_t launch_sampler(const SamplerArgs& a, cudaStream_t s, int num_sms);
+// launch_sampler would pick k_floyd_pipe for this problem (it likes 64 rows per block)
+bool sampler_uses_pipe(uint64_t n, uint32_t draws);
 cudaError_t launch_gather(const GatherArgs& a, bool exhaustive, cudaStream_t s, int num_sms);
 // exact fp64 decision of the band pairs; accepted ones go to `sink`
 cudaError_t launch_band(const TestParams& tp, const EdgeSink& sink, unsigned long long* counters,

@@ -293,6 +293,25 @@ cudaError_t raise_smem_limit(const void* kernel) {
     return e;
 }
 
+// k_floyd_pipe pays where a vertex has many group entries for one resolver warp
+// (about draws^2 / 2^B of them: cfg5 240, cfg4 93): measured 272 vs 312 ms on cfg5
+// and 45.4 vs 41.8 ms on cfg4 against k_floyd_lean, so it takes over from ~160.
+// SNGB_FLOYD_PIPE=0|1 forces the choice.
+static bool pipe_wanted(uint32_t D) {
+    if (D <= 1024 || D > 4096) return false;
+    if (const char* penv = std::getenv("SNGB_FLOYD_PIPE")) return std::atoi(penv) != 0;
+    const BloomGeom bg = bloom_geometry(D);
+    return (uint64_t)D * D >= (160ull << bg.bits_log2);
+}
+
+bool sampler_uses_pipe(uint64_t n, uint32_t draws) {
+    const uint64_t bm_words = (((n - 1) + 31) / 32 + 3) & ~3ull;
+    if (bm_words * 4 <= 9216 && !std::getenv("SNGB_FLOYD_NO_BITMAP")) return false;
+    const char* fwenv = std::getenv("SNGB_FLOYD_WARP");
+    if (fwenv && std::atoi(fwenv) == 1 && !std::getenv("SNGB_FLOYD_BLOOM")) return false;
+    return n - 2 < 0xffffffffull && pipe_wanted(draws);
+}
+
 cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
     const uint64_t rows = in.row_end - in.row_begin;
     if (rows == 0 || in.draws == 0) return cudaSuccess;
@@ -382,8 +401,7 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
                                           k_floyd_lean<14>, k_floyd_lean<15>, k_floyd_lean<16>};
         // k_floyd_pipe: k_floyd_lean's workers resolve their own group entries,
         // pipelined over the vertex loop (no resolver warp); SNGB_FLOYD_PIPE=0|1
-        const char* penv = std::getenv("SNGB_FLOYD_PIPE");
-        const bool pipe = D > 1024 && (penv ? std::atoi(penv) != 0 : kPipeDefault);
+        const bool pipe = pipe_wanted(D);
         if (pipe) {
             static constexpr KFn kPipe[12] = {k_floyd_pipe<5>,  k_floyd_pipe<6>,  k_floyd_pipe<7>,
                                               k_floyd_pipe<8>,  k_floyd_pipe<9>,  k_floyd_pipe<10>,

@@ -744,6 +744,73 @@ def test_fused_floyd_head_equals_two_kernels(monkeypatch, cfg, n, fh):
 
 
 @pytest.mark.parametrize("cfg,n", [(4, 400_000), (5, 300_000), (4, 1_000_000), (5, 2_500_000)])
+def test_headpipe_equals_two_kernels(monkeypatch, cfg, n):
+    """k_floyd_headpipe (sngb_floyd_headpipe.cuh, SNGB_FUSED=4: k_floyd_pipe's workers
+    also take the head test and their survivors' fp32 test, one RNG pass) against
+    the two kernels on reduced cfg4/cfg5 shapes: the same edge list, collisions,
+    replayed vertices and pair counts; with forced Lemire replays and a row range."""
+    import torch
+    w = synthetic.CONFIGS[cfg]
+    x = torch.from_numpy(synthetic.generate(cfg, n=n)).cuda()
+    rate = w.draws / n
+    for force, rows in ((None, (0, 0)), ("9", (0, 0)), (None, (n // 4, n // 2 + 3))):
+        if force:
+            monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
+        else:
+            monkeypatch.delenv("SNGB_TEST_FORCE_IRREGULAR", raising=False)
+        monkeypatch.setenv("SNGB_FUSED", "4")
+        kf, gf = sng.sampled_edges_device(x, w.eps, rate, w.seed, rows[0], rows[1])
+        monkeypatch.setenv("SNGB_FUSED", "0")
+        monkeypatch.setenv("SNGB_FLOYD_PIPE", "0")
+        k2, g2 = sng.sampled_edges_device(x, w.eps, rate, w.seed, rows[0], rows[1])
+        monkeypatch.delenv("SNGB_FLOYD_PIPE", raising=False)
+        torch.cuda.synchronize()
+        assert gf.filter_bits == g2.filter_bits == 16
+        assert torch.equal(kf, k2), (cfg, force, rows)
+        assert gf.collisions == g2.collisions > 0
+        assert gf.irregular_vertices == g2.irregular_vertices
+        assert gf.kernel_launches < g2.kernel_launches
+        if not force:
+            assert gf.gather_pairs == g2.gather_pairs
+            assert gf.pairs_evaluated == g2.pairs_evaluated
+            assert gf.band_rechecks == g2.band_rechecks
+
+
+@pytest.mark.parametrize("cfg,n,split", [(4, 400_000, None), (5, 300_000, None), (4, 1_000_000, "0"),
+                                         (5, 2_500_000, "0"), (5, 2_500_000, None)])
+def test_duo_equals_two_kernels(monkeypatch, cfg, n, split):
+    """k_duo (sngb_fused.cu, SNGB_FUSED=3: the Floyd bookkeeping and the head gather
+    as two roles of one launch) against the two kernels on reduced cfg4/cfg5
+    shapes: the same edge list, collisions, replayed vertices and pair counts;
+    with forced Lemire replays, a row range, and both role layouts."""
+    import torch
+    w = synthetic.CONFIGS[cfg]
+    x = torch.from_numpy(synthetic.generate(cfg, n=n)).cuda()
+    rate = w.draws / n
+    if split is not None:
+        monkeypatch.setenv("SNGB_DUO_SPLIT", split)
+    for force, rows in ((None, (0, 0)), ("9", (0, 0)), (None, (n // 4, n // 2 + 3))):
+        if force:
+            monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)
+        else:
+            monkeypatch.delenv("SNGB_TEST_FORCE_IRREGULAR", raising=False)
+        monkeypatch.setenv("SNGB_FUSED", "3")
+        kf, gf = sng.sampled_edges_device(x, w.eps, rate, w.seed, rows[0], rows[1])
+        monkeypatch.setenv("SNGB_FUSED", "0")
+        monkeypatch.setenv("SNGB_FLOYD_PIPE", "0")
+        k2, g2 = sng.sampled_edges_device(x, w.eps, rate, w.seed, rows[0], rows[1])
+        monkeypatch.delenv("SNGB_FLOYD_PIPE", raising=False)
+        torch.cuda.synchronize()
+        assert gf.filter_bits == g2.filter_bits == 16
+        assert torch.equal(kf, k2), (cfg, force, rows)
+        assert gf.collisions == g2.collisions > 0
+        assert gf.irregular_vertices == g2.irregular_vertices
+        assert gf.gather_pairs == g2.gather_pairs
+        assert gf.pairs_evaluated == g2.pairs_evaluated
+        assert gf.kernel_launches < g2.kernel_launches
+
+
+@pytest.mark.parametrize("cfg,n", [(4, 400_000), (5, 300_000), (4, 1_000_000), (5, 2_500_000)])
 def test_floyd_lean_equals_bloom(monkeypatch, cfg, n):
     """k_floyd_lean (sngb_floyd_lean.cuh, the default above 1024 draws) against
     k_floyd_bloom (SNGB_FLOYD_LEAN=0) on reduced cfg4/cfg5 shapes: the same edge
@@ -754,6 +821,7 @@ def test_floyd_lean_equals_bloom(monkeypatch, cfg, n):
     rate = w.draws / n
     monkeypatch.setenv("SNGB_FUSED", "0")
     monkeypatch.setenv("SNGB_FLOYD_WARP", "0")
+    monkeypatch.setenv("SNGB_FLOYD_PIPE", "0")
     for force in (None, "7"):
         if force:
             monkeypatch.setenv("SNGB_TEST_FORCE_IRREGULAR", force)

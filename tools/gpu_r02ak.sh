@@ -1,0 +1,7 @@
+#!/bin/bash
+# k_floyd_headpipe: parity tests, A/B against the two kernels on cfg4/cfg5
+OUT=gpurun_out/r02ak
+mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "headpipe" > $OUT/pytest_sel.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_sel.log
+tail -15 $OUT/pytest_sel.log
+timeout 1200 python tools/duo_ab.py 4 5 > $OUT/fhp_ab.jsonl 2> $OUT/fhp_ab.err; cat $OUT/fhp_ab.jsonl; tail -3 $OUT/fhp_ab.err

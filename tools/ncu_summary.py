@@ -72,7 +72,15 @@ def main():
                 inst = float(v.replace(",", ""))
     if units and inst:
         print(f"| warp instructions per {uname} | {inst / units:.2f} |")
-    get = {m: _num(vals[hdr.index(m)]) for m, _ in METRICS if m in hdr}
+    # base units: bytes and nanoseconds (ncu scales each value's unit on its own)
+    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "s": 1e9, "ms": 1e6,
+             "us": 1e3, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1.0, "nsecond": 1.0}
+
+    def _base(m):
+        v = _num(vals[hdr.index(m)])
+        return None if v is None else v * scale.get(unit_row[hdr.index(m)].strip(), 1.0)
+
+    get = {m: _base(m) for m, _ in METRICS if m in hdr}
     sec, req = (get.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"),
                 get.get("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"))
     tpi = get.get("smsp__thread_inst_executed_per_inst_executed.ratio")
@@ -95,6 +103,7 @@ def main():
             "lts_throughput_pct": get.get("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
             "dram_throughput_pct": get.get("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
             "l2_hit_rate_pct": get.get("lts__t_sector_hit_rate.pct"),
+            "l1tex_throughput_pct": get.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
             "issue_active_pct": get.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "warps_active_pct": get.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
             "sectors_per_request": (sec / req) if (sec and req) else None,
