@@ -87,6 +87,8 @@ DevCtx& get_ctx(int dev, int slot) {
         CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->qev, cudaEventDisableTiming));
+        for (auto& e : c->sh_g) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : c->sh_f) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->pev, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->up_start, cudaEventDisableTiming));
         for (auto& e : c->up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -452,7 +454,11 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
     // generated once) when the head filter runs; the head plan decides, so the
     // sampler launch is held back until then
     const bool fuse_try = head_try && !exhaustive && fused_eligible(n, draws, stride);
-    const bool side_pre = !exhaustive && !fuse_try && !h_src && (q8_try || head_try) &&
+    // shared draws: the head gather writes its draws, k_floyd_pipe reads them (the
+    // sampler launch is held back until the head plan is known, as for fuse_try)
+    const bool share_try =
+        head_try && !exhaustive && !fuse_try && share_eligible(n, (uint32_t)draws);
+    const bool side_pre = !exhaustive && !fuse_try && !share_try && !h_src && (q8_try || head_try) &&
                           !(stride <= 64 && (re - rb) >= 10000 && draws <= 1024) &&  // not overlap
                           env_u64("SNGB_OVERLAP", 2) != 1 && env_u64("SNGB_SIDE_PRE", 1) != 0;
     if (side_pre) CK(cudaEventRecord(c.fork, s));
@@ -503,8 +509,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         const bool overlap =
             !exhaustive && (ov == 1 || (ov == 2 && stride <= 64 && (re - rb) >= 10000));
         // host upload: the sampler reads no points, so it also runs while they arrive
-        const bool side =
-            !exhaustive && !fuse_try && (overlap || side_pre || (h_src && attempt == 0));
+        const bool side = !exhaustive && !fuse_try && !share_try &&
+                          (overlap || side_pre || (h_src && attempt == 0));
         if (pre_partners && attempt == 0) {  // before the sampler on the side stream
             c.partners.ensure((re - rb) * draws * 4ull);
             c.poff.ensure((re - rb) * (chunks + 1) * 4ull);
@@ -539,7 +545,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
             sa.counters = dc;
             return sa;
         };
-        if (!exhaustive && !fuse_try) {
+        if (!exhaustive && !fuse_try && !share_try) {
             SamplerArgs sa = make_sa();
             if (side) {
                 // the Floyd bookkeeping needs no point data: run it on the side
@@ -665,6 +671,8 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
         if (side_pre) CK(cudaStreamWaitEvent(s, c.join, 0));  // gather after the sampler
         const bool fused = fuse_try && head_on;
         if (fuse_try && !head_on) CK(launch_sampler(make_sa(), s, c.num_sms));  // unfused after all
+        const bool share = share_try && head_on && gphases == 1;
+        if (share_try && !share) CK(launch_sampler(make_sa(), s, c.num_sms));  // no head filter after all
         tm.mark(E_SAMPLED);
         GatherArgs ga{};
         ga.tp = tp;
@@ -767,6 +775,57 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 ga.work = c.work.as<unsigned long long>() + work_slot++;
                 ++work_slot;  // k_duo's Floyd chunk counter (ga.work + 1)
                 CK(launch_floyd_head(make_sa(), ga, hp.args, gs, c.num_sms));
+            } else if (share) {
+                // Row chunks through a bounded draw buffer: the gather of chunk k on this
+                // stream writes buffer k & 1, the Floyd pass of chunk k on the side stream
+                // reads it while the gather of chunk k + 1 runs (two buffers, events).
+                const uint64_t rows = re - rb, per_row = draws * 4ull;
+                size_t free_b = 0, total_b = 0;
+                CK(cudaMemGetInfo(&free_b, &total_b));
+                uint64_t budget = env_u64("SNGB_TBUF_MB", 4096) << 20;  // per buffer
+                budget = std::min<uint64_t>(budget, (free_b + c.tbuf.bytes) / 4);
+                uint64_t crow = std::max<uint64_t>(budget / per_row, 1024);
+                crow = std::max<uint64_t>(crow, (rows + 199) / 200);  // <= 200 chunks (work slots)
+                crow = std::min<uint64_t>(crow, rows);
+                const uint64_t nchunks = (rows + crow - 1) / crow;
+                const uint32_t nbuf = nchunks > 1 ? 2 : 1;
+                c.tbuf.ensure(nbuf * crow * per_row);
+                c.tflags.ensure(nbuf * crow);
+                const bool serial = env_u64("SNGB_SHARE_SERIAL", 0) == 1;
+                cudaStream_t fs = serial ? gs : c.side;
+                for (uint64_t k = 0; k < nchunks; ++k) {
+                    const uint32_t b = (uint32_t)(k & (nbuf - 1));
+                    const uint64_t r0 = rb + k * crow, r1 = std::min<uint64_t>(re, r0 + crow);
+                    if (k >= 2 && !serial) CK(cudaStreamWaitEvent(gs, c.sh_f[b], 0));
+                    ga.tbuf = c.tbuf.as<uint32_t>() + (uint64_t)b * crow * draws;
+                    ga.tflags = c.tflags.as<unsigned char>() + (uint64_t)b * crow;
+                    ga.tbuf_row0 = r0;
+                    gather(r0, r1, 0, (uint32_t)n);
+                    SamplerArgs sa = make_sa();
+                    sa.row_begin = r0;
+                    sa.row_end = r1;
+                    sa.tbuf = ga.tbuf;
+                    sa.tflags = ga.tflags;
+                    sa.tbuf_row0 = r0;
+                    sa.rows_per_block = (uint32_t)env_u64("SNGB_SAMPLER_RPB", 16);
+                    if (!serial) {
+                        CK(cudaEventRecord(c.sh_g[b], gs));
+                        CK(cudaStreamWaitEvent(fs, c.sh_g[b], 0));
+                    }
+                    if (k == 0 && !serial) {
+                        tm.mark_on(E_SIDE0, fs);
+                        tm.side = true;
+                    }
+                    CK(launch_sampler(sa, fs, c.num_sms));
+                    if (!serial) CK(cudaEventRecord(c.sh_f[b], fs));
+                }
+                ga.tbuf = nullptr;
+                ga.tflags = nullptr;
+                if (!serial) {
+                    tm.mark_on(E_SIDE1, fs);
+                    CK(cudaEventRecord(c.join, fs));
+                    CK(cudaStreamWaitEvent(s, c.join, 0));  // extras need every Floyd pass
+                }
             } else {
                 for (uint32_t ph = 0; ph < gphases; ++ph) gather(rb, re, part(ph), part(ph + 1));
             }

@@ -53,7 +53,7 @@ inline size_t pipe_smem_bytes(const BloomGeom& g) {
 // The vertices first, first + stride, ... (nv of them) of one block; `smem` is
 // pipe_smem_bytes() of dynamic shared memory.  Called once per block by
 // k_floyd_pipe and once per claimed chunk by k_duo (sngb_fused.cu).
-template <int MAXR>
+template <int MAXR, bool SHT = false>
 __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned char* smem,
                                                const uint64_t first, const uint64_t stride,
                                                const uint32_t nv) {
@@ -175,7 +175,6 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
         uint32_t tr[MAXR];
         uint32_t tmax = 0;
         bool fired = false;
-        uint64_t key = 0;
         uint32_t sa = 0;
         if (has_v) {
             {  // clear the other parity's filters (last used by vertex s - 1)
@@ -187,30 +186,49 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
                     so[w] = z4;
                 }
             }
-            key = vertex_key(a.seed_mixed, u);
-            const uint64_t z0 = key + (uint64_t)(tid + 1) * kGamma;  // stream_at(key, i + 1)
             const uint32_t fa = smem_addr(filt + par * WB);
             sa = smem_addr(shared_bits + par * WB);
-            uint32_t smin = 0xffffffffu;
+            if constexpr (SHT) {
+                // shared draws: the head gather wrote t_i (and whether the stream met the
+                // Lemire pre-condition or the test hook) for this row
+                const uint32_t* tv = a.tbuf + (u - a.tbuf_row0) * D + tid;
 #pragma unroll
-            for (int r = 0; r < MAXR; ++r) {
-                uint32_t slo;
-                const uint32_t t = lemire32_slo(mix(z0 + (uint64_t)r * dz), b0 + kT * r, slo);
-                tr[r] = t;
-                if (r < MAXR - 1 || in_tail) {
-                    smin = min(smin, slo);
-                    tmax = max(tmax, t);
-                    const uint32_t off = (t >> 3) & wmask, bit = 1u << (t & 31);
-                    red_or_sh(sa + off, atom_or_sh(fa + off, bit) & bit);
-                }
-            }
-            fired = hook_thread && (u % a.force_mod) == 0;
-            if (smin == 0u) {  // rare (2^-32 per draw): the exact pre-condition, lo < bound
-#pragma unroll 1
+                for (int r = 0; r < MAXR; ++r)
+                    tr[r] = (r < MAXR - 1 || in_tail) ? __ldcs(tv + kT * r) : 0u;
+                fired = tid == 0 && a.tflags[u - a.tbuf_row0] != 0;
+#pragma unroll
                 for (int r = 0; r < MAXR; ++r) {
-                    bool fi;
-                    lemire32(mix(z0 + (uint64_t)r * dz), b0 + kT * r, fi);
-                    fired |= fi && (r < MAXR - 1 || in_tail);
+                    const uint32_t t = tr[r];
+                    if (r < MAXR - 1 || in_tail) {
+                        tmax = max(tmax, t);
+                        const uint32_t off = (t >> 3) & wmask, bit = 1u << (t & 31);
+                        red_or_sh(sa + off, atom_or_sh(fa + off, bit) & bit);
+                    }
+                }
+            } else {
+                const uint64_t key = vertex_key(a.seed_mixed, u);
+                const uint64_t z0 = key + (uint64_t)(tid + 1) * kGamma;  // stream_at(key, i + 1)
+                uint32_t smin = 0xffffffffu;
+#pragma unroll
+                for (int r = 0; r < MAXR; ++r) {
+                    uint32_t slo;
+                    const uint32_t t = lemire32_slo(mix(z0 + (uint64_t)r * dz), b0 + kT * r, slo);
+                    tr[r] = t;
+                    if (r < MAXR - 1 || in_tail) {
+                        smin = min(smin, slo);
+                        tmax = max(tmax, t);
+                        const uint32_t off = (t >> 3) & wmask, bit = 1u << (t & 31);
+                        red_or_sh(sa + off, atom_or_sh(fa + off, bit) & bit);
+                    }
+                }
+                fired = hook_thread && (u % a.force_mod) == 0;
+                if (smin == 0u) {  // rare (2^-32 per draw): the exact pre-condition, lo < bound
+#pragma unroll 1
+                    for (int r = 0; r < MAXR; ++r) {
+                        bool fi;
+                        lemire32(mix(z0 + (uint64_t)r * dz), b0 + kT * r, fi);
+                        fired |= fi && (r < MAXR - 1 || in_tail);
+                    }
                 }
             }
         }
@@ -250,7 +268,7 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
             __syncthreads();
             if (tid == 0) {
                 ++nrep;
-                ncol += bloom_replay(key, u, a.n, base, filt, 4 * WB, xs);
+                ncol += bloom_replay(vertex_key(a.seed_mixed, u), u, a.n, base, filt, 4 * WB, xs);
                 s_cc[par] = s_ovf[par] = 0;
             }
             if (tid < kW) s_wc[par][tid] = 0;
@@ -309,11 +327,11 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
     }
 }
 
-template <int MAXR>
+template <int MAXR, bool SHT>
 __global__ void __launch_bounds__(kBloomThreads, 4) k_floyd_pipe(const SamplerArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint64_t first = a.row_begin + blockIdx.x;
     const uint32_t nv =
         first < a.row_end ? (uint32_t)((a.row_end - first + gridDim.x - 1) / gridDim.x) : 0u;
-    floyd_pipe_run<MAXR>(a, smem, first, gridDim.x, nv);
+    floyd_pipe_run<MAXR, SHT>(a, smem, first, gridDim.x, nv);
 }

@@ -13,6 +13,9 @@
 #include "sngb_internal.cuh"
 #include "sngb_rng.cuh"
 
+#ifndef SNGB_SHARE_DRAWS
+#define SNGB_SHARE_DRAWS 0  // see sngb_internal.cuh: the shared-draws experiment (build flag)
+#endif
 #ifndef SNGB_HEAD_UF
 #define SNGB_HEAD_UF 2
 #endif
@@ -114,6 +117,10 @@ __device__ __forceinline__ void gather_head_body(const GatherArgs& a, const Head
         };
 
         uint32_t limit = a.draws;
+#if SNGB_SHARE_DRAWS
+        // shared draws: this row's slice of the draw buffer (streaming stores)
+        uint32_t* tb = a.tbuf ? a.tbuf + (u - a.tbuf_row0) * a.draws : nullptr;
+#endif
         uint64_t z = vertex_key(a.seed_mixed, u) + (uint64_t)(lane + 1) * kGamma;
         for (uint32_t i0 = 0; i0 < limit; i0 += 32 * R, z += (uint64_t)(32 * R) * kGamma) {
             // draws of this step, branch-free (the test hook resolved per vertex;
@@ -126,6 +133,9 @@ __device__ __forceinline__ void gather_head_body(const GatherArgs& a, const Head
                 bool fire;
                 const uint32_t t = lemire32(mix(z + (uint64_t)(32 * k) * kGamma), a.base + i + 1, fire);
                 const bool valid = i < limit;
+#if SNGB_SHARE_DRAWS
+                if (tb && i < a.draws) __stcs(tb + i, t);
+#endif
                 fires |= ((fire || i == hook) && valid) ? (1u << k) : 0u;
                 const uint32_t p = t + (t >= (uint32_t)u ? 1u : 0u);
                 pv[k] = valid ? p : (uint32_t)u;
@@ -167,6 +177,9 @@ __device__ __forceinline__ void gather_head_body(const GatherArgs& a, const Head
             }
         }
         if (qn) fp32_step(0, qn);
+#if SNGB_SHARE_DRAWS
+        if (a.tflags && lane == 0) a.tflags[u - a.tbuf_row0] = limit < a.draws ? 1 : 0;
+#endif
         __syncwarp();
     }
     stage.flush(a.sink, lane);

@@ -77,7 +77,8 @@ struct DevCtx {
     std::mutex mu;
     Buf pts, upload, keys, keys_alt, extras, scratch, counters, deg, core, parent, broot, first,
         flags, rank, temp, labels, roles, work, q8, upload64, rnorm, band, partners, poff, rstart,
-        colstats, perm;
+        colstats, perm, tbuf, tflags;
+    cudaEvent_t sh_g[2] = {}, sh_f[2] = {};  // shared draws: chunk gathered / chunk's Floyd pass done
     cudaEvent_t qev = nullptr;  // min/max of the points copied to the host (8-bit filter)
     cudaEvent_t pev = nullptr;  // bucketed partner lists ready (host-upload 8-bit schedule)
     unsigned long long* h_counters = nullptr;  // pinned mirror of the counter block
@@ -96,7 +97,7 @@ struct DevCtx {
                        &mg_bord, &mg_bordred})
             b->release();
         for (Buf* b : {&pts, &upload, &keys, &keys_alt, &extras, &scratch, &counters, &deg, &core,
-                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band, &partners, &poff, &rstart, &colstats, &perm})
+                       &parent, &broot, &first, &flags, &rank, &temp, &labels, &roles, &work, &q8, &upload64, &rnorm, &band, &partners, &poff, &rstart, &colstats, &perm, &tbuf, &tflags})
             b->release();
     }
 };

@@ -95,6 +95,14 @@ struct GatherArgs {
     const uint32_t* poff;
     uint64_t partners_row0;
     uint32_t nbuckets, blo, bhi;
+    // Shared draws (head gather -> k_floyd_pipe; only in builds with -DSNGB_SHARE_DRAWS=1:
+    // measured no faster, DESIGN 5b): the gather also writes every draw
+    // value t_i of row u to tbuf[(u - tbuf_row0) * draws + i] and whether the row's
+    // stream met the Lemire pre-condition to tflags[u - tbuf_row0], so the Floyd
+    // bookkeeping reads them instead of regenerating each draw.  null: off
+    uint32_t* tbuf;
+    unsigned char* tflags;
+    uint64_t tbuf_row0;
 };
 
 // Test hook (env SNGB_TEST_FORCE_IRREGULAR=m): pretend the Lemire reject
@@ -118,6 +126,9 @@ struct SamplerArgs {
     uint32_t hash_shift;       // 32 - log2(slots)
     uint32_t col_words;        // u32 words of a draws-bit bitmap (multiple of 4)
     uint32_t key_bits;         // bits of a draw value t (fast path epoch tags)
+    const uint32_t* tbuf;           // shared draws written by the head gather (see GatherArgs)
+    const unsigned char* tflags;
+    uint64_t tbuf_row0;
     unsigned long long* scratch64;  // global tables when they do not fit shared memory
     unsigned long long* extras;  // (u << 32) | v ordered pairs to evaluate
     unsigned long long extras_capacity;
@@ -190,6 +201,8 @@ size_t floyd_scratch_bytes(uint32_t draws, int num_sms, uint64_t rows);
 cudaError_t launch_sampler(const SamplerArgs& a, cudaStream_t s, int num_sms);
 // launch_sampler would pick k_floyd_pipe for this problem (it likes 64 rows per block)
 bool sampler_uses_pipe(uint64_t n, uint32_t draws);
+// the head gather can hand its draws to k_floyd_pipe through global memory (SNGB_SHARE_T)
+bool share_eligible(uint64_t n, uint32_t draws);
 cudaError_t launch_gather(const GatherArgs& a, bool exhaustive, cudaStream_t s, int num_sms);
 // exact fp64 decision of the band pairs; accepted ones go to `sink`
 cudaError_t launch_band(const TestParams& tp, const EdgeSink& sink, unsigned long long* counters,

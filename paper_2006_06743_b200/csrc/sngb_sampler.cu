@@ -237,6 +237,9 @@ __global__ void __launch_bounds__(kFloydThreads) k_floyd(const SamplerArgs a) {
     }
 }
 
+#ifndef SNGB_SHARE_DRAWS
+#define SNGB_SHARE_DRAWS 0
+#endif
 #include "sngb_floyd_bitmap.cuh"
 #include "sngb_floyd_bloom.cuh"
 #include "sngb_floyd_warp.cuh"
@@ -310,6 +313,29 @@ bool sampler_uses_pipe(uint64_t n, uint32_t draws) {
     const char* fwenv = std::getenv("SNGB_FLOYD_WARP");
     if (fwenv && std::atoi(fwenv) == 1 && !std::getenv("SNGB_FLOYD_BLOOM")) return false;
     return n - 2 < 0xffffffffull && pipe_wanted(draws);
+}
+
+// Shared draws (builds with -DSNGB_SHARE_DRAWS=1, then SNGB_SHARE_T=1): wherever
+// launch_sampler would run the filter kernels on more than 1024 draws per vertex and
+// the head gather runs, the gather writes its draws and k_floyd_pipe reads them
+// (sngb_api.cu pipelines row chunks through a bounded buffer).  Bit-exact, and no
+// faster (cfg5 613 vs 606 ms: the stores cost the L1TEX-bound gather what the loads
+// save the sampler, profiles/r02_ab_share.jsonl), hence a build flag.
+bool share_eligible(uint64_t n, uint32_t draws) {
+#if !SNGB_SHARE_DRAWS
+    (void)n;
+    (void)draws;
+    return false;
+#endif
+    const char* se = std::getenv("SNGB_SHARE_T");
+    if (!se || std::atoi(se) == 0) return false;
+    // an explicit choice of Floyd kernel (A/B runs, the parity tests) keeps its own draws
+    if (std::getenv("SNGB_FLOYD_PIPE") || std::getenv("SNGB_FLOYD_LEAN")) return false;
+    if (draws <= 1024 || draws > 4096 || n - 2 >= 0xffffffffull) return false;
+    const uint64_t bm_words = (((n - 1) + 31) / 32 + 3) & ~3ull;
+    if (bm_words * 4 <= 9216 && !std::getenv("SNGB_FLOYD_NO_BITMAP")) return false;
+    const char* fwenv = std::getenv("SNGB_FLOYD_WARP");
+    return !(fwenv && std::atoi(fwenv) == 1 && !std::getenv("SNGB_FLOYD_BLOOM"));
 }
 
 cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
@@ -401,13 +427,24 @@ cudaError_t launch_sampler(const SamplerArgs& in, cudaStream_t s, int num_sms) {
                                           k_floyd_lean<14>, k_floyd_lean<15>, k_floyd_lean<16>};
         // k_floyd_pipe: k_floyd_lean's workers resolve their own group entries,
         // pipelined over the vertex loop (no resolver warp); SNGB_FLOYD_PIPE=0|1
-        const bool pipe = pipe_wanted(D);
+        const bool pipe = pipe_wanted(D) || a.tbuf;  // shared draws: k_floyd_pipe reads them
         if (pipe) {
-            static constexpr KFn kPipe[12] = {k_floyd_pipe<5>,  k_floyd_pipe<6>,  k_floyd_pipe<7>,
-                                              k_floyd_pipe<8>,  k_floyd_pipe<9>,  k_floyd_pipe<10>,
-                                              k_floyd_pipe<11>, k_floyd_pipe<12>, k_floyd_pipe<13>,
-                                              k_floyd_pipe<14>, k_floyd_pipe<15>, k_floyd_pipe<16>};
+            static constexpr KFn kPipe[12] = {
+                k_floyd_pipe<5, false>,  k_floyd_pipe<6, false>,  k_floyd_pipe<7, false>,
+                k_floyd_pipe<8, false>,  k_floyd_pipe<9, false>,  k_floyd_pipe<10, false>,
+                k_floyd_pipe<11, false>, k_floyd_pipe<12, false>, k_floyd_pipe<13, false>,
+                k_floyd_pipe<14, false>, k_floyd_pipe<15, false>, k_floyd_pipe<16, false>};
+#if SNGB_SHARE_DRAWS
+            static constexpr KFn kPipeT[12] = {
+                k_floyd_pipe<5, true>,  k_floyd_pipe<6, true>,  k_floyd_pipe<7, true>,
+                k_floyd_pipe<8, true>,  k_floyd_pipe<9, true>,  k_floyd_pipe<10, true>,
+                k_floyd_pipe<11, true>, k_floyd_pipe<12, true>, k_floyd_pipe<13, true>,
+                k_floyd_pipe<14, true>, k_floyd_pipe<15, true>, k_floyd_pipe<16, true>};
+            KFn kp = (a.tbuf ? kPipeT : kPipe)[(D + kBloomThreads - 1) / kBloomThreads - 5];
+#else
+            if (a.tbuf) return cudaErrorInvalidValue;  // built without the shared-draws kernels
             KFn kp = kPipe[(D + kBloomThreads - 1) / kBloomThreads - 5];
+#endif
             const size_t psmem = pipe_smem_bytes(bg);
             cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(kp));
             if (e != cudaSuccess) return e;
