@@ -146,27 +146,80 @@ def load_traffic(workload: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region.
+
+    NVML in-process (a 10 Hz thread; the GIL is released while the library call
+    runs): an `nvidia-smi -lms 100` child cost the large configs ~5 ms of GPU
+    stall per poll on some boxes (cfg4: an 88.0 ms step around an 82.9 ms call).
+    Falls back to that child process when NVML is not importable."""
 
     Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NVML_REASONS = ((0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"),
+                    (0x20, "sw_thermal_slowdown"), (0x4, "sw_power_cap"))
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, reasons bitmask) from NVML
+        self.mx = None
+        self.thread = None
+        self._stop = None
+        self.source = None
+
+    def _nvml_loop(self, nv, h):
+        while not self._stop.is_set():
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                     int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(h))))
+            except Exception:
+                pass
+            self._stop.wait(0.1)
 
     def start(self):
+        if os.environ.get("SNGB_BENCH_CLOCKS") != "smi":
+            try:
+                import threading
+
+                import pynvml as nv
+                nv.nvmlInit()
+                # NVML enumerates every GPU of the box: map the CUDA ordinal through its UUID
+                import torch
+                uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+                h = None
+                for i in range(nv.nvmlDeviceGetCount()):
+                    hi = nv.nvmlDeviceGetHandleByIndex(i)
+                    u = nv.nvmlDeviceGetUUID(hi)
+                    u = u.decode() if isinstance(u, bytes) else u
+                    if uuid in u:
+                        h = hi
+                        break
+                if h is None:
+                    h = nv.nvmlDeviceGetHandleByIndex(self.index)
+                self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+                self._stop = threading.Event()
+                self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+                self.thread.start()
+                self.source = "nvml"
+                return
+            except Exception:
+                self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "100", "-i", str(self.index)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi -lms 100"
         except Exception:
             self.proc = None
 
     def stop(self):
+        if self.thread:
+            self._stop.set()
+            self.thread.join(timeout=2)
+            return
         if not self.proc:
             return
         self.proc.terminate()
@@ -178,6 +231,14 @@ class ClockSampler:
         self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
+        if self.thread:
+            sms = [a for a, _ in self.samples]
+            bits = 0
+            for _, r in self.samples:
+                bits |= r
+            return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": self.mx,
+                    "reasons": sorted(nm for b, nm in self.NVML_REASONS if bits & b),
+                    "samples": len(sms), "source": self.source}
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -194,7 +255,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sms)}
+                "reasons": sorted(reasons), "samples": len(sms), "source": self.source}
 
 
 def _workload_config(w, n_gpus: int, extra: dict | None = None) -> dict:

@@ -555,11 +555,12 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 // gather starts while it runs: cfg5 e2e 614 vs 943 ms persistent; 32
                 // rows per block there, 625 vs 639 ms with 8)
                 // (k_floyd_pipe: 64 rows per block, two drain steps each; cfg5 602 vs
-                // 609 ms with 8, 630 ms persistent)
+                // 609 ms with 8, 630 ms persistent.  k_floyd_lean likes them too now that
+                // it gains nothing beside the gather: cfg4 82.8 vs 84.7 ms with 8,
+                // profiles/r02_lean_rpb_cfg4.jsonl)
                 sa.rows_per_block = (uint32_t)env_u64(
-                    "SNGB_SAMPLER_RPB", sampler_uses_pipe(n, (uint32_t)draws)
-                                            ? 64
-                                            : (h_src ? 32 : (overlap ? (draws > 1024 ? 8 : 32) : 0)));
+                    "SNGB_SAMPLER_RPB",
+                    draws > 1024 && draws <= 4096 ? 64 : (h_src ? 32 : (overlap ? 32 : 0)));
                 if (!(side_pre && attempt == 0)) CK(cudaEventRecord(c.fork, s));
                 CK(cudaStreamWaitEvent(c.side, c.fork, 0));
                 tm.mark_on(E_SIDE0, c.side);
@@ -568,7 +569,7 @@ int build_graph(DevCtx& c, cudaStream_t s, Timer& tm, const float* d_pts, uint64
                 tm.side = true;
                 CK(cudaEventRecord(c.join, c.side));
             } else {
-                if (sampler_uses_pipe(n, (uint32_t)draws))
+                if (sampler_uses_pipe(n, (uint32_t)draws) || (draws > 1024 && draws <= 4096))
                     sa.rows_per_block = (uint32_t)env_u64("SNGB_SAMPLER_RPB", 64);
                 CK(launch_sampler(sa, s, c.num_sms));
             }
