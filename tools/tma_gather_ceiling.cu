@@ -196,6 +196,68 @@ __global__ void __launch_bounds__(256) k_bulk(const uint16_t* __restrict__ tab, 
 }
 
 
+// Mixed: every lane keeps S gather4 stages in flight AND does UN LDG lookups per
+// stage wait.  If the TMA unit's path to L2 were independent of the LSU / L1TEX tag
+// stage the two rates would add (1.0 + 0.6 per SM-cycle).
+template <int S, int UN>
+__global__ void __launch_bounds__(256) k_mix(const __grid_constant__ CUtensorMap tm,
+                                             const uint16_t* __restrict__ tab, uint32_t rows16,
+                                             uint32_t iters, uint32_t* sink) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) unsigned long long mb[8][S];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned char* buf = sm + (size_t)w * S * 4096;
+    if (lane == 0)
+        for (int s = 0; s < S; ++s) mbar_init(smem_u32(&mb[w][s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    uint32_t acc = 0;
+    uint32_t sub[S];
+    auto issue = [&](uint32_t it, int s) {
+        uint32_t r[4], sb = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t h = hash32(gid * 0x9E3779B1u + it * 4 + k);
+            const uint32_t e = (uint32_t)(((uint64_t)h * (rows16 * 8ull)) >> 32);
+            r[k] = e >> 3;
+            sb |= (e & 7u) << (3 * k);
+        }
+        sub[s] = sb;
+        const uint32_t mbar = smem_u32(&mb[w][s]);
+        if (lane == 0) mbar_expect_tx(mbar, 2048);
+        __syncwarp();
+        g4(smem_u32(buf + s * 4096 + lane * 128), &tm, mbar, 0, r[0], r[1], r[2], r[3]);
+    };
+#pragma unroll
+    for (int s = 0; s < S; ++s) issue(s, s);
+    uint32_t ph = 0;
+    for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            uint16_t v[UN];
+#pragma unroll
+            for (int k = 0; k < UN; ++k) {  // the LDG lookups ride on the stage's latency
+                const uint32_t h = hash32(~gid * 0x85EBCA6Bu + (it * S + s) * UN + k);
+                v[k] = __ldg(tab + (uint32_t)(((uint64_t)h * (rows16 * 8ull)) >> 32));
+            }
+            mbar_wait(smem_u32(&mb[w][s]), ph);
+            const uint16_t* st = reinterpret_cast<const uint16_t*>(buf + s * 4096 + lane * 128);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc ^= st[k * 8 + ((sub[s] >> (3 * k)) & 7u)];
+#pragma unroll
+            for (int k = 0; k < UN; ++k) acc ^= v[k];
+            __syncwarp();
+            issue((it + 1) * S + s, s);
+        }
+        ph ^= 1u;
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_wait(smem_u32(&mb[w][s]), ph);
+    if (acc == 0x7fffu && gid == 0u) sink[0] = acc;
+}
+
+
 // Wide rows (the 8-bit gather's heads: the first 256 B of random 800-B rows,
 // cfg2's 56 MB table).  ldg: half a warp per row (16 lanes x 16 B), UN rows
 // in flight per half warp.  g4w: lanes 0..7 each issue one gather4 (4 rows x
@@ -345,6 +407,29 @@ static int wide(int sms, int clk, PFN_cuTensorMapEncodeTiled_v12000 encode, uint
     return 0;
 }
 
+template <int S, int UN>
+static int run_mix(const CUtensorMap& tm, const uint16_t* tab, uint32_t rows16, int sms, int clk,
+                   unsigned long long mb, uint32_t* sink) {
+    for (int bpsm : {2, 4, 8}) {
+        const int grid = sms * bpsm;
+        const double threads = (double)grid * 256;
+        const size_t smem = (size_t)8 * S * 4096;
+        const uint32_t it = 64;
+        cudaFuncSetAttribute(k_mix<S, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        double ms = time_ms([&] { k_mix<S, UN><<<grid, 256, smem>>>(tm, tab, rows16, it, sink); });
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            printf("{\"case\": \"mix\", \"error\": \"%s\"}\n", cudaGetErrorString(e));
+            return 1;
+        }
+        const double rps = threads * (double)it * S * (4.0 + UN) / (ms * 1e-3);
+        printf("{\"case\": \"mix_g4_ldg\", \"table_mb\": %llu, \"bpsm\": %d, \"stages\": %d, \"ldg_per_stage\": %d, \"rows_per_s\": %.4g, \"per_sm_cycle\": %.3f}\n",
+               mb, bpsm, S, UN, rps, rps / (sms * (clk * 1e3)));
+        fflush(stdout);
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
     int sms = 0, clk = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -357,6 +442,7 @@ int main(int argc, char** argv) {
     uint32_t* sink;
     CK(cudaMalloc(&sink, 4));
     if (argc > 1 && argv[1][0] == 'w') return wide(sms, clk, encode, sink);
+    const bool mixed = argc > 1 && argv[1][0] == 'm';
     for (uint64_t mb : {2ull, 40ull, 80ull, 400ull}) {
         const uint64_t heads = mb * 1000000ull / 2;  // u16 heads
         const uint32_t rows16 = (uint32_t)(heads / 8);
@@ -374,6 +460,15 @@ int main(int argc, char** argv) {
         if (cr != CUDA_SUCCESS) {
             fprintf(stderr, "encode failed %d\n", (int)cr);
             return 1;
+        }
+        if (mixed) {
+            if (run_mix<2, 4>(tm, tab, rows16, sms, clk, mb, sink)) return 1;
+            if (run_mix<2, 8>(tm, tab, rows16, sms, clk, mb, sink)) return 1;
+            if (run_mix<2, 16>(tm, tab, rows16, sms, clk, mb, sink)) return 1;
+            if (run_mix<4, 4>(tm, tab, rows16, sms, clk, mb, sink)) return 1;
+            if (run_mix<4, 8>(tm, tab, rows16, sms, clk, mb, sink)) return 1;
+            CK(cudaFree(tab));
+            continue;
         }
         for (int bpsm : {2, 4, 8}) {
             const int grid = sms * bpsm;
