@@ -42,6 +42,18 @@ constexpr int kPipeSlots = 1 << kPipeHashLog2;
 constexpr uint32_t kPipeMaxGroup = 384;  // entries per vertex the 512-slot hash takes
 constexpr uint32_t kPipeNone = 0xffffffffu;
 
+// shared-memory access at a compile-time byte offset from a 32-bit shared address
+template <uint32_t OFF>
+__device__ __forceinline__ void pipe_red_or_off(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
+}
+template <uint32_t OFF>
+__device__ __forceinline__ uint32_t pipe_ld_off(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF) : "memory");
+    return v;
+}
+
 inline size_t pipe_smem_bytes(const BloomGeom& g) {
     return 4ull * g.words * 4                          // filter + shared-bit filter, x2 parity
            + 2ull * g.col_words * 4                    // collided bitmaps, x2 parity
@@ -59,7 +71,11 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
                                                const uint32_t nv) {
     constexpr int kT = kBloomThreads;
     constexpr int kW = kT / 32;
-    const uint32_t WB = a.hash_mask;  // filter words (2^B / 32)
+    // filter words (2^B / 32): bloom_geometry gives B = 15 up to 2048 draws (MAXR <= 8) and
+    // B = 16 above, so the table size and the distance between a vertex's filter and
+    // its shared-bit filter are compile-time constants (immediate offsets, no add)
+    constexpr uint32_t WB = MAXR >= 9 ? 2048u : 1024u;
+    constexpr uint32_t kShOff = 2 * WB * 4;  // bytes from filt[par] to shared_bits[par]
     const uint32_t W = a.col_words;
     uint32_t* filt = reinterpret_cast<uint32_t*>(smem);          // [2][WB]
     uint32_t* shared_bits = filt + 2 * WB;                         // [2][WB]
@@ -69,6 +85,7 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
     uint32_t* clist = reinterpret_cast<uint32_t*>(glist + 2 * kW * kPipeSeg);  // [2][kChainCap]
     unsigned long long* htab =
         reinterpret_cast<unsigned long long*>(clist + 2 * kChainCap);  // [2][kPipeSlots]
+    __shared__ unsigned long long s_key[2];  // [parity] the vertex's stream key (thread 0 computes it)
     __shared__ uint32_t s_wc[2][kW];  // [parity][warp] group entries
     __shared__ uint32_t s_ng[2];      // [parity] group entries of the vertex
     __shared__ uint32_t s_cc[2];      // [parity] chain candidates
@@ -88,12 +105,13 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
     for (uint32_t s = tid; s < 2 * kPipeSlots; s += kT) htab[s] = ~0ull;
     if (tid < 2 * kW) (&s_wc[0][0])[tid] = 0;
     if (tid < 2) s_ng[tid] = s_cc[tid] = s_ovf[tid] = 0;
+    if (tid == 0) s_key[0] = vertex_key(a.seed_mixed, first);  // vertex 0; vertex s + 1 in step s
     __syncthreads();
 
     const uint64_t dz = (uint64_t)kT * kGamma;  // counter step between a thread's draws
     // MAXR = ceil(D / kT): slots r < MAXR - 1 are full, the last one holds D - kT (MAXR - 1) draws
     const bool in_tail = (uint32_t)tid < D - kT * (MAXR - 1);
-    const uint32_t wmask = (WB - 1) << 2;          // byte offset of t's filter word
+    constexpr uint32_t wmask = (WB - 1) << 2;      // byte offset of t's filter word
     const uint32_t b0 = base + (uint32_t)tid + 1;  // Lemire bound of slot 0: j + 1
     const bool hook_thread = a.force_mod != 0 && (D / 2) % kT == (uint32_t)tid;
     const uint32_t lt = (1u << lane) - 1u;
@@ -175,7 +193,7 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
         uint32_t tr[MAXR];
         uint32_t tmax = 0;
         bool fired = false;
-        uint32_t sa = 0;
+        uint32_t fa = 0;
         if (has_v) {
             {  // clear the other parity's filters (last used by vertex s - 1)
                 uint4* fo = reinterpret_cast<uint4*>(filt + (par ^ 1u) * WB);
@@ -186,8 +204,7 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
                     so[w] = z4;
                 }
             }
-            const uint32_t fa = smem_addr(filt + par * WB);
-            sa = smem_addr(shared_bits + par * WB);
+            fa = smem_addr(filt + par * WB);
             if constexpr (SHT) {
                 // shared draws: the head gather wrote t_i (and whether the stream met the
                 // Lemire pre-condition or the test hook) for this row
@@ -202,11 +219,11 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
                     if (r < MAXR - 1 || in_tail) {
                         tmax = max(tmax, t);
                         const uint32_t off = (t >> 3) & wmask, bit = 1u << (t & 31);
-                        red_or_sh(sa + off, atom_or_sh(fa + off, bit) & bit);
+                        pipe_red_or_off<kShOff>(fa + off, atom_or_sh(fa + off, bit) & bit);
                     }
                 }
             } else {
-                const uint64_t key = vertex_key(a.seed_mixed, u);
+                const uint64_t key = s_key[par];  // vertex_key(a.seed_mixed, u)
                 const uint64_t z0 = key + (uint64_t)(tid + 1) * kGamma;  // stream_at(key, i + 1)
                 uint32_t smin = 0xffffffffu;
 #pragma unroll
@@ -218,7 +235,7 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
                         smin = min(smin, slo);
                         tmax = max(tmax, t);
                         const uint32_t off = (t >> 3) & wmask, bit = 1u << (t & 31);
-                        red_or_sh(sa + off, atom_or_sh(fa + off, bit) & bit);
+                        pipe_red_or_off<kShOff>(fa + off, atom_or_sh(fa + off, bit) & bit);
                     }
                 }
                 fired = hook_thread && (u % a.force_mod) == 0;
@@ -233,6 +250,7 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
             }
         }
         const bool any_fired = __syncthreads_or(fired);
+        if (tid == 0 && s + 1 < nv) s_key[par ^ 1u] = vertex_key(a.seed_mixed, u + stride);
 
         // ---- B: vertex s - 1: collided entries ----
         if (has_prev) {
@@ -287,7 +305,8 @@ __device__ __forceinline__ void floyd_pipe_run(const SamplerArgs& a, unsigned ch
                 for (int r = 0; r < MAXR; ++r) {
                     const uint32_t t = tr[r];
                     const uint32_t off = (t >> 3) & wmask, bit = 1u << (t & 31);
-                    const bool hit = (ld_sh(sa + off) & bit) && (r < MAXR - 1 || in_tail);
+                    const bool hit =
+                        (pipe_ld_off<kShOff>(fa + off) & bit) && (r < MAXR - 1 || in_tail);
                     const uint32_t m = __ballot_sync(kFull, hit);
                     const uint32_t pos = wpos + __popc(m & lt);
                     if (hit && pos < kPipeSeg)
