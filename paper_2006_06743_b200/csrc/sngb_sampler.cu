@@ -301,13 +301,15 @@ cudaError_t raise_smem_limit(const void* kernel) {
 // the final kernels (profiles/r02_pipe_threshold.jsonl, n = 4 M, 64 rows per block):
 // k_floyd_lean is ahead at 1100 draws (37 entries: 15.8 vs 17.6 ms) and 2100 (67:
 // 26.7 vs 27.2), k_floyd_pipe at 1500 (69: 20.7 vs 21.4), 2048 (128: 27.0 vs 31.4),
-// 2600 (103: 32.7 vs 33.7) and everywhere above (4096: 57.0 vs 63.1), so it takes
-// over from 68 entries.  SNGB_FLOYD_PIPE=0|1 forces the choice.
+// 2600 (103: 32.7 vs 33.7) and everywhere above (4096: 57.0 vs 63.1).  Between 68
+// and 100 entries the two are within 3 % either way (cfg4, 95: 38.1 vs 38.4 ms on
+// the device, but 85.5 vs 83.5 ms through the host call), so it takes over from 100.
+// SNGB_FLOYD_PIPE=0|1 forces the choice.
 static bool pipe_wanted(uint32_t D) {
     if (D <= 1024 || D > 4096) return false;
     if (const char* penv = std::getenv("SNGB_FLOYD_PIPE")) return std::atoi(penv) != 0;
     const BloomGeom bg = bloom_geometry(D);
-    return (uint64_t)D * D >= (68ull << bg.bits_log2);
+    return (uint64_t)D * D >= (100ull << bg.bits_log2);
 }
 
 bool sampler_uses_pipe(uint64_t n, uint32_t draws) {
