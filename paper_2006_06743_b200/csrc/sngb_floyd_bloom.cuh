@@ -138,6 +138,18 @@ __device__ __forceinline__ uint32_t ld_sh(uint32_t addr) {
     return v;
 }
 
+// shared-memory access at a compile-time byte offset from a 32-bit shared address
+template <uint32_t OFF>
+__device__ __forceinline__ void pipe_red_or_off(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
+}
+template <uint32_t OFF>
+__device__ __forceinline__ uint32_t pipe_ld_off(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF) : "memory");
+    return v;
+}
+
 constexpr int kBarWorkers = 1;  // 256 worker threads
 constexpr int kBarReady = 2;    // + parity: lists of a vertex are complete (288)
 constexpr int kBarFree = 4;     // + parity: resolver is done with that parity (288)

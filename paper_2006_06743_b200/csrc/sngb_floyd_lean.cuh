@@ -34,7 +34,11 @@ template <int MAXR>
 __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_lean(const SamplerArgs a) {
     constexpr int kT = kBloomThreads;
     extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t WB = a.hash_mask;  // filter words (2^B / 32)
+    // filter words (2^B / 32): bloom_geometry gives B = 15 up to 2048 draws (MAXR <= 8) and
+    // B = 16 above -- a compile-time constant, so a draw's shared-bit word is its filter
+    // word plus an immediate offset (as k_floyd_pipe)
+    constexpr uint32_t WB = MAXR >= 9 ? 2048u : 1024u;
+    constexpr uint32_t kShOff = 2 * WB * 4;  // bytes from filt[par] to shared_bits[par]
     const uint32_t W = a.col_words;
     uint32_t* filt = reinterpret_cast<uint32_t*>(smem);          // [2][WB]
     uint32_t* shared_bits = filt + 2 * WB;                         // [2][WB]
@@ -45,6 +49,7 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_lean(con
     unsigned long long* htab =
         reinterpret_cast<unsigned long long*>(clist + 2 * kChainCap);  // [kHashSlots]
     __shared__ uint32_t s_cnt[2][2];  // [parity][group, chain]
+    __shared__ unsigned long long s_key;  // the next vertex's stream key (worker thread 0 computes it)
 
     const int tid = threadIdx.x, lane = tid & 31;
     const bool resolver = tid >= kT;
@@ -55,6 +60,7 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_lean(con
     for (uint32_t s = tid; s < 4 * WB + W; s += kBloomBlock) filt[s] = 0;
     for (uint32_t s = tid; s < kHashSlots; s += kBloomBlock) htab[s] = ~0ull;
     if (tid < 4) (&s_cnt[0][0])[tid] = 0;
+    if (tid == 0) s_key = vertex_key(a.seed_mixed, a.row_begin + blockIdx.x);
     __syncthreads();
 
     if (resolver) {
@@ -65,7 +71,7 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_lean(con
         // MAXR = ceil(D / kT): slots r < MAXR - 1 are full, the last one holds
         // D - kT (MAXR - 1) draws
         const bool in_tail = (uint32_t)tid < D - kT * (MAXR - 1);
-        const uint32_t wmask = (WB - 1) << 2;       // byte offset of t's filter word
+        constexpr uint32_t wmask = (WB - 1) << 2;   // byte offset of t's filter word
         const uint32_t b0 = base + (uint32_t)tid + 1;  // Lemire bound of slot 0: j + 1
         // test hook (see test_fire): the thread and slot of draw D / 2
         const bool hook_thread = a.force_mod != 0 && (D / 2) % kT == (uint32_t)tid;
@@ -84,9 +90,9 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_lean(con
                     so[w] = z4;
                 }
             }
-            const uint64_t key = vertex_key(a.seed_mixed, u);
+            const uint64_t key = s_key;  // vertex_key(a.seed_mixed, u), written one vertex ahead
             const uint64_t z0 = key + (uint64_t)(tid + 1) * kGamma;  // stream_at(key, i + 1)
-            const uint32_t fa = smem_addr(filt + par * WB), sa = smem_addr(shared_bits + par * WB);
+            const uint32_t fa = smem_addr(filt + par * WB);
 
             uint32_t tr[MAXR];
             uint32_t smin = 0xffffffffu, tmax = 0;
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_lean(con
                 const uint32_t off = (t >> 3) & wmask, bit = 1u << (t & 31);
                 // the shared-bit mark is an unconditional OR of (old & bit): a
                 // predicated red compiles to a branch + reconvergence (3 issue slots)
-                red_or_sh(sa + off, atom_or_sh(fa + off, bit) & bit);
+                pipe_red_or_off<kShOff>(fa + off, atom_or_sh(fa + off, bit) & bit);
             };
 #pragma unroll
             for (int r = 0; r < MAXR; ++r) {
@@ -142,7 +148,11 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_lean(con
                 bar_sync(kBarWorkers, kT);
                 bar_arrive(kBarReady + par, kBloomBlock);
             };
-            if (bar_or(kBarWorkers, kT, fired)) {
+            const bool any_fired = bar_or(kBarWorkers, kT, fired);
+            // every worker has read s_key: the next vertex's key (read after this vertex's
+            // last worker barrier)
+            if (tid == 0) s_key = vertex_key(a.seed_mixed, u + gridDim.x);
+            if (any_fired) {
                 replay();
                 continue;
             }
@@ -151,7 +161,7 @@ __global__ void __launch_bounds__(kBloomBlock, SNGB_BLOOM_MINB) k_floyd_lean(con
             for (int r = 0; r < MAXR; ++r) {
                 const uint32_t t = tr[r];
                 const uint32_t off = (t >> 3) & wmask, bit = 1u << (t & 31);
-                const bool hit = (ld_sh(sa + off) & bit) && (r < MAXR - 1 || in_tail);
+                const bool hit = (pipe_ld_off<kShOff>(fa + off) & bit) && (r < MAXR - 1 || in_tail);
                 if (hit) {
                     const uint32_t p = atomicAdd(&cnt[0], 1u);
                     if (p < kGroupCap) gl[p] = ((unsigned long long)t << 32) | ((uint32_t)tid + kT * r);

@@ -42,18 +42,6 @@ constexpr int kPipeSlots = 1 << kPipeHashLog2;
 constexpr uint32_t kPipeMaxGroup = 384;  // entries per vertex the 512-slot hash takes
 constexpr uint32_t kPipeNone = 0xffffffffu;
 
-// shared-memory access at a compile-time byte offset from a 32-bit shared address
-template <uint32_t OFF>
-__device__ __forceinline__ void pipe_red_or_off(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.or.b32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
-}
-template <uint32_t OFF>
-__device__ __forceinline__ uint32_t pipe_ld_off(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF) : "memory");
-    return v;
-}
-
 inline size_t pipe_smem_bytes(const BloomGeom& g) {
     return 4ull * g.words * 4                          // filter + shared-bit filter, x2 parity
            + 2ull * g.col_words * 4                    // collided bitmaps, x2 parity

@@ -299,17 +299,15 @@ cudaError_t raise_smem_limit(const void* kernel) {
 // k_floyd_pipe pays where a vertex has many group entries for one resolver warp
 // (about draws^2 / 2^B of them: cfg5 240, cfg4 93).  A sweep over the draw count on
 // the final kernels (profiles/r02_pipe_threshold.jsonl, n = 4 M, 64 rows per block):
-// k_floyd_lean is ahead at 1100 draws (37 entries: 15.8 vs 17.6 ms) and 2100 (67:
-// 26.7 vs 27.2), k_floyd_pipe at 1500 (69: 20.7 vs 21.4), 2048 (128: 27.0 vs 31.4),
-// 2600 (103: 32.7 vs 33.7) and everywhere above (4096: 57.0 vs 63.1).  Between 68
-// and 100 entries the two are within 3 % either way (cfg4, 95: 38.1 vs 38.4 ms on
-// the device, but 85.5 vs 83.5 ms through the host call), so it takes over from 100.
-// SNGB_FLOYD_PIPE=0|1 forces the choice.
+// k_floyd_lean is ahead up to 2600 draws at B = 16 (103 entries: 32.4 vs 32.8 ms; 2100:
+// 25.4 vs 27.2; 1500 at B = 15: 20.6 vs 20.7), k_floyd_pipe at 2048 draws (B = 15, 128
+// entries: 27.0 vs 30.6 ms), 3000 (137: 36.6 vs 38.9) and everywhere above (4096: 56.6
+// vs 62.8), so it takes over from 120 entries.  SNGB_FLOYD_PIPE=0|1 forces the choice.
 static bool pipe_wanted(uint32_t D) {
     if (D <= 1024 || D > 4096) return false;
     if (const char* penv = std::getenv("SNGB_FLOYD_PIPE")) return std::atoi(penv) != 0;
     const BloomGeom bg = bloom_geometry(D);
-    return (uint64_t)D * D >= (100ull << bg.bits_log2);
+    return (uint64_t)D * D >= (120ull << bg.bits_log2);
 }
 
 bool sampler_uses_pipe(uint64_t n, uint32_t draws) {
