@@ -1,7 +1,7 @@
 #!/bin/bash
 # r02 round check on the k_floyd_pipe tree: GPU suite, smoke, default bench (cfg5) + reference arm,
 # launch list of the bench command, ncu --set full of the two cfg5 kernels.
-OUT=gpurun_out/r02ax
+OUT=gpurun_out/r02az
 mkdir -p $OUT
 (time timeout 1500 python -m pytest tests -q -m gpu -x) > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 tail -4 $OUT/pytest_gpu.log
