@@ -693,7 +693,10 @@ def main():
     # each fetched sector that is algorithmic bytes.
     rng_peak = None
     try:
-        for ln in open(os.path.join(ROOT, "profiles", "r01_microbench.jsonl")):
+        mb_path = os.path.join(ROOT, "profiles", "r02_microbench.jsonl")  # the current draw code
+        if not os.path.exists(mb_path):
+            mb_path = os.path.join(ROOT, "profiles", "r01_microbench.jsonl")
+        for ln in open(mb_path):
             rec = json.loads(ln)
             if rec.get("bench") == "rng_draw":
                 rng_peak = rec["draws_per_s"]
@@ -703,7 +706,7 @@ def main():
         draws_s = gather_pairs / (g_ms / 1e3)
         roofline["rng"] = {"draws_per_s": draws_s, "ceiling_draws_per_s": rng_peak,
                            "frac": (draws_s / rng_peak) if rng_peak else None,
-                           "source": "profiles/r01_microbench.jsonl rng_draw (one SplitMix64 + "
+                           "source": "profiles/" + os.path.basename(mb_path) + " rng_draw (one SplitMix64 + "
                                      "Lemire draw per lane, no memory traffic)"}
     if not q8 and not head and 4 * d < 32:
         row = 8 if d <= 2 else 16

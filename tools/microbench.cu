@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <vector>
 
+#include "../paper_2006_06743_b200/csrc/sngb_rng.cuh"
+
 #define CK(x)                                                                                 \
     do {                                                                                      \
         cudaError_t e = (x);                                                                  \
@@ -60,11 +62,9 @@ __global__ void k_smem(unsigned long long* sink, uint32_t words_per_warp_log2) {
     if (acc == 0x12345678u) sink[0] = acc;
 }
 
-__device__ __forceinline__ uint64_t mix(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-    return z ^ (z >> 31);
-}
+// the product's draw: sngb::mix (sngb_rng.cuh; its 64-bit constant multiplies are one
+// IMAD.WIDE and two chained IMADs since round 2)
+using sngb::mix;
 
 __global__ void k_rng(unsigned long long* sink, uint32_t draws) {
     const uint64_t key = mix(blockIdx.x * 1024ull + threadIdx.x);
