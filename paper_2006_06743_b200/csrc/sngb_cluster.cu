@@ -222,8 +222,12 @@ __global__ void k_first(uint64_t n, const uint8_t* __restrict__ core,
         if (core[v]) {
             if (parent[v] == (uint32_t)v) atomicMin(&first[v], (uint32_t)v);
         } else {
+            // first[r] only decreases, so a (possibly stale) value <= v means the atomic
+            // could not change it: on cfg5 a cluster's hundreds of thousands of border
+            // vertices otherwise queue on one address (k_first 1.4 ms)
             const uint32_t r = broot[v];
-            if (r != kNone) atomicMin(&first[r], (uint32_t)v);
+            if (r != kNone && *(volatile uint32_t*)&first[r] > (uint32_t)v)
+                atomicMin(&first[r], (uint32_t)v);
         }
     }
 }
